@@ -1,0 +1,127 @@
+/* sthk.h -- C ABI of the B200 spatiotemporal-Hawkes likelihood engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj):
+ *
+ *   hawkes::logLikelihood(const EventSet&, const Params&, const Backend&,
+ *                         bool keepPerEvent) -> LikelihoodResult
+ *       include/sthawkes/likelihood.hpp:24-26, src/likelihood.cpp:10-55
+ *   hawkes::logLikelihoodBatch(...)      likelihood.hpp:28-31, likelihood.cpp:57-75
+ *
+ * The reference's own plugin slot (pairReduce + PairReduceSpec,
+ * backend.hpp:65-88,170-192) carries host-side callables that
+ * capture host pointers, so a device engine plugs in one level up, at
+ * logLikelihood. The reference API is stateless; this engine is stateful
+ * (events stay resident in HBM across evaluations), and the C++ adapter
+ * (paper_2005_10123_b200/adapter/hawkes_b200_adapter.cpp)
+ * restores the stateless reference signature on top of it.
+ *
+ * Conventions
+ *   Status codes: every entry point is noexcept and returns STHK_OK or one of
+ *     the errors below; the message is available from sthk_last_error().
+ *     A numerically degenerate evaluation (some lambda_i <= 0 or non-finite,
+ *     likelihood.cpp:36-39,47-54) is NOT an error: status STHK_OK with
+ *     *valid = 0, *loglik = -inf and grad[] = NaN.
+ *   Params order is hawkes::Params order (types.hpp:51-57):
+ *     p[0]=mu0 p[1]=tauX p[2]=tauT p[3]=theta p[4]=omega p[5]=h.
+ *   Ownership: the engine owns all device memory; the caller owns every host
+ *     buffer passed in; no host pointer is retained after a call returns.
+ *   Threading: one handle must not be used from two threads at once.
+ *   Determinism: results are bitwise identical for identical (events,
+ *     params), and independent of the number of devices / ranks.
+ */
+#ifndef STHK_H
+#define STHK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STHK_OK 0
+#define STHK_EINVAL 1     /* invalid argument (maps to std::invalid_argument) */
+#define STHK_ENOTLOADED 2 /* evaluation before sthk_load_events / set_params */
+#define STHK_ECUDA 3      /* CUDA runtime error (maps to std::runtime_error) */
+#define STHK_ENCCL 4      /* NCCL error */
+
+#define STHK_NCCL_ID_BYTES 128
+
+typedef struct sthk_engine sthk_engine;
+
+/* Engine over n_devices GPUs driven from this process (n_devices >= 1).
+ * Target rows are partitioned across the devices; one NCCL all-reduce
+ * combines the per-block partial sums. */
+int sthk_create(const int* device_ids, int n_devices, sthk_engine** out);
+
+/* One-process-per-GPU engine: this process owns `device` and is `rank` of
+ * `world`; `nccl_id` is the STHK_NCCL_ID_BYTES blob from
+ * sthk_nccl_unique_id() on rank 0, broadcast by the caller. */
+int sthk_nccl_unique_id(void* nccl_id);
+int sthk_create_rank(int device, int rank, int world, const void* nccl_id,
+                     sthk_engine** out);
+
+int sthk_destroy(sthk_engine* e);
+
+/* Copies n events (time-sorted SoA, km / days) to every device.
+ * Validation and messages follow the EventSet constructor (types.hpp:85-109):
+ * n >= 1, finite entries, t >= 0, t nondecreasing, window_end finite and
+ * >= t[n-1]. Replaces any previously loaded set. */
+int sthk_load_events(sthk_engine* e, const double* x, const double* y,
+                     const double* t, int64_t n, double window_end);
+
+/* Validates like Params::validate (types.hpp:59-72). */
+int sthk_set_params(sthk_engine* e, const double* params6);
+
+/* Synchronous evaluations with the current params.
+ * per_event (nullable, length n): log(lambda_i) - Lambda_i, 0 for degenerate
+ * rows (likelihood.cpp:25,41). grad6 receives d loglik / d params in Params
+ * order. */
+int sthk_loglik(sthk_engine* e, double* loglik, int* valid, double* per_event);
+int sthk_loglik_grad(sthk_engine* e, double* loglik, int* valid, double* grad6,
+                     double* per_event);
+
+/* Batch over P parameter vectors (params: P x 6, row-major), elementwise
+ * identical to P single calls (logLikelihoodBatch, likelihood.cpp:57-75).
+ * grad (nullable): P x 6. */
+int sthk_loglik_batch(sthk_engine* e, const double* params, int64_t P,
+                      double* loglik, int* valid, double* grad);
+
+/* Asynchronous pair: enqueue one evaluation of the current params on the
+ * engine's stream(s); sthk_result() waits for and returns the latest one. */
+int sthk_enqueue(sthk_engine* e, int want_grad, int want_per_event);
+int sthk_result(sthk_engine* e, double* loglik, int* valid, double* grad6,
+                double* per_event);
+
+/* Introspection for benchmarks / tests. */
+typedef struct sthk_stats {
+  int64_t n;                 /* events loaded */
+  int64_t pairs_bg;          /* background pairs evaluated (tile granularity) */
+  int64_t pairs_tr;          /* trigger pairs evaluated (tile granularity) */
+  int64_t pairs_any;         /* pairs with either term evaluated */
+  int64_t pairs_dense;       /* n * n */
+  double pair_kernel_ms;     /* device time of the last pair kernel(s), max over
+                                local devices; 0 unless timing is enabled */
+  double eval_ms;            /* device time of the last whole evaluation */
+  int32_t source_chunk;      /* sources per work item (SC) of the last eval */
+  int32_t work_items;        /* live (row tile, chunk) items of the last eval */
+  int32_t n_devices;         /* devices driven by this handle */
+  int32_t rank, world;       /* rank-mode coordinates (0, 1 otherwise) */
+} sthk_stats;
+
+int sthk_set_timing(sthk_engine* e, int enable);
+int sthk_get_stats(sthk_engine* e, sthk_stats* out);
+/* cudaStream_t of local device slot `slot` (for event-based timing). */
+int sthk_get_stream(sthk_engine* e, int slot, void** stream);
+/* Debug/testing knob: 0 = exact tile culling on (default), 1 = evaluate the
+ * dense pair set (results are bitwise identical either way). */
+int sthk_set_dense(sthk_engine* e, int dense);
+
+const char* sthk_last_error(const sthk_engine* e);
+const char* sthk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STHK_H */

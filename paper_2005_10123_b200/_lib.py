@@ -1,0 +1,83 @@
+"""ctypes binding of include/sthk.h and include/sthk_sim.h (libsthk.so)."""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_uint64, c_void_p
+
+STHK_OK = 0
+STHK_EINVAL = 1
+STHK_ENOTLOADED = 2
+STHK_ECUDA = 3
+STHK_ENCCL = 4
+NCCL_ID_BYTES = 128
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "libsthk.so")
+
+
+class StatsStruct(ctypes.Structure):
+    _fields_ = [
+        ("n", c_int64),
+        ("pairs_bg", c_int64),
+        ("pairs_tr", c_int64),
+        ("pairs_any", c_int64),
+        ("pairs_dense", c_int64),
+        ("pair_kernel_ms", c_double),
+        ("eval_ms", c_double),
+        ("source_chunk", ctypes.c_int32),
+        ("work_items", ctypes.c_int32),
+        ("n_devices", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+    ]
+
+
+# (name, restype, argtypes) for every entry point declared in include/*.h
+_DPTR = POINTER(c_double)
+_IPTR = POINTER(c_int)
+SIGNATURES = [
+    ("sthk_create", c_int, [POINTER(c_int), c_int, POINTER(c_void_p)]),
+    ("sthk_nccl_unique_id", c_int, [c_void_p]),
+    ("sthk_create_rank", c_int, [c_int, c_int, c_int, c_void_p, POINTER(c_void_p)]),
+    ("sthk_destroy", c_int, [c_void_p]),
+    ("sthk_load_events", c_int, [c_void_p, _DPTR, _DPTR, _DPTR, c_int64, c_double]),
+    ("sthk_set_params", c_int, [c_void_p, _DPTR]),
+    ("sthk_loglik", c_int, [c_void_p, _DPTR, _IPTR, _DPTR]),
+    ("sthk_loglik_grad", c_int, [c_void_p, _DPTR, _IPTR, _DPTR, _DPTR]),
+    ("sthk_loglik_batch", c_int, [c_void_p, _DPTR, c_int64, _DPTR, _IPTR, _DPTR]),
+    ("sthk_enqueue", c_int, [c_void_p, c_int, c_int]),
+    ("sthk_result", c_int, [c_void_p, _DPTR, _IPTR, _DPTR, _DPTR]),
+    ("sthk_set_timing", c_int, [c_void_p, c_int]),
+    ("sthk_get_stats", c_int, [c_void_p, POINTER(StatsStruct)]),
+    ("sthk_get_stream", c_int, [c_void_p, c_int, POINTER(c_void_p)]),
+    ("sthk_set_dense", c_int, [c_void_p, c_int]),
+    ("sthk_last_error", c_char_p, [c_void_p]),
+    ("sthk_version", c_char_p, []),
+    ("sthk_sim_cloud", c_int, [c_int64, _DPTR, c_uint64, _DPTR, _DPTR, _DPTR, _DPTR]),
+    ("sthk_sim_cluster", c_int,
+     [_DPTR, _DPTR, c_double, c_uint64, c_int64, _DPTR, _DPTR, _DPTR, _IPTR, POINTER(c_int64)]),
+]
+
+
+def load_library() -> ctypes.CDLL:
+    """Load the in-tree libsthk.so (fails loudly if it was not built)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = lib_path()
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build the CUDA engine first "
+            "(python -c 'import __graft_entry__ as g; g.build()')")
+    lib = ctypes.CDLL(path)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib

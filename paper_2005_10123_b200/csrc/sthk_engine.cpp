@@ -1,0 +1,707 @@
+// Host engine behind the sthk.h C ABI: device-resident event sets, per-eval
+// planning (exact culling windows, chunk size, cost-balanced row partition),
+// kernel sequencing on one CUDA stream per device, and the single NCCL
+// all-reduce that combines per-block partials across devices / ranks.
+//
+// Reference behaviour mirrored here (file:line under /root/reference/proj):
+//   Params::validate         include/sthawkes/types.hpp:59-72 (same message)
+//   EventSet validation      include/sthawkes/types.hpp:85-109 (same messages)
+//   logLikelihood            src/likelihood.cpp:10-55 (valid/-inf semantics,
+//                            per-event terms 0 on degenerate rows)
+//   logLikelihoodBatch       src/likelihood.cpp:57-75 (elementwise identical)
+//   pairReduceRun            include/sthawkes/backend.hpp:142-166 (contiguous
+//                            target blocks -> here contiguous 1024-row blocks
+//                            per device, partials combined in block order)
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "../../include/sthk.h"
+#include "sthk_kernels.cuh"
+
+namespace {
+
+using sthk::kNOut;
+using sthk::kRB;
+using sthk::kTM;
+using sthk::kTS;
+
+struct InvalidArg : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NcclErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NotLoaded : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaErr(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+void ckn(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    throw NcclErr(std::string(what) + ": " + ncclGetErrorString(r));
+  }
+}
+
+template <typename T>
+void dev_grow(T*& p, size_t& cap, size_t need) {
+  if (need <= cap && p) return;
+  if (p) ck(cudaFree(p), "cudaFree");
+  p = nullptr;
+  const size_t bytes = std::max<size_t>(need, 1) * sizeof(T);
+  ck(cudaMalloc(reinterpret_cast<void**>(&p), bytes), "cudaMalloc");
+  cap = need;
+}
+
+struct Slot {
+  int dev = 0;
+  int sms = 148;
+  int occ_grad = 1, occ_val = 1;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  double *x = nullptr, *y = nullptr, *t = nullptr;
+  size_t x_cap = 0, y_cap = 0, t_cap = 0;
+  int2* ranges = nullptr;
+  size_t ranges_cap = 0;
+  int* counts = nullptr;
+  size_t counts_cap = 0;
+  int2* items = nullptr;
+  size_t items_cap = 0;
+  int* scalars = nullptr;  // [0] n_items, [1] work counter
+  double* partial = nullptr;
+  size_t partial_cap = 0;
+  double* block_partial = nullptr;
+  size_t bp_cap = 0;
+  double* out = nullptr;  // kNOut
+  double* per_event = nullptr;
+  size_t pe_cap = 0;
+  unsigned long long* pair_counts = nullptr;
+  double* h_out = nullptr;                 // pinned kNOut
+  unsigned long long* h_counts = nullptr;  // pinned 3
+  double* h_per_event = nullptr;           // pinned
+  size_t h_pe_cap = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int row0 = 0, row1 = 0;  // rows of the last enqueued eval
+};
+
+}  // namespace
+
+struct sthk_engine {
+  std::vector<Slot> slots;
+  bool rank_mode = false;
+  int rank = 0, world = 1;
+  std::vector<double> ht;  // host copy of times (planning)
+  int64_t n = 0, npad = 0;
+  double window_end = 0;
+  double p[6] = {0, 0, 0, 0, 0, 0};
+  bool loaded = false, has_params = false;
+  bool timing = false, dense = false;
+  std::string err;
+  bool pending = false, last_grad = false, last_pe = false;
+  int last_sc = 0, last_items_est = 0;
+};
+
+namespace {
+
+constexpr int kItemsTarget = 4096;
+
+void set_dev(const Slot& s) { ck(cudaSetDevice(s.dev), "cudaSetDevice"); }
+
+void init_slot(Slot& s, int dev) {
+  s.dev = dev;
+  set_dev(s);
+  ck(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
+  for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
+  ck(cudaMalloc(&s.scalars, 2 * sizeof(int)), "cudaMalloc");
+  ck(cudaMalloc(&s.out, kNOut * sizeof(double)), "cudaMalloc");
+  ck(cudaMalloc(&s.pair_counts, 3 * sizeof(unsigned long long)), "cudaMalloc");
+  ck(cudaMallocHost(&s.h_out, kNOut * sizeof(double)), "cudaMallocHost");
+  ck(cudaMallocHost(&s.h_counts, 3 * sizeof(unsigned long long)), "cudaMallocHost");
+  s.occ_grad = sthk::pair_kernel_occupancy(true);
+  s.occ_val = sthk::pair_kernel_occupancy(false);
+  ck(cudaGetLastError(), "occupancy");
+}
+
+void free_slot(Slot& s) {
+  cudaSetDevice(s.dev);
+  if (s.stream) cudaStreamSynchronize(s.stream);
+  if (s.comm) ncclCommDestroy(s.comm);
+  for (void* p : {static_cast<void*>(s.x), static_cast<void*>(s.y), static_cast<void*>(s.t),
+                  static_cast<void*>(s.ranges), static_cast<void*>(s.counts),
+                  static_cast<void*>(s.items), static_cast<void*>(s.scalars),
+                  static_cast<void*>(s.partial), static_cast<void*>(s.block_partial),
+                  static_cast<void*>(s.out), static_cast<void*>(s.per_event),
+                  static_cast<void*>(s.pair_counts)}) {
+    if (p) cudaFree(p);
+  }
+  for (void* p : {static_cast<void*>(s.h_out), static_cast<void*>(s.h_counts),
+                  static_cast<void*>(s.h_per_event)}) {
+    if (p) cudaFreeHost(p);
+  }
+  for (auto& e : s.ev) {
+    if (e) cudaEventDestroy(e);
+  }
+  if (s.stream) cudaStreamDestroy(s.stream);
+}
+
+// Params::validate, types.hpp:59-72.
+void validate_params(const double* p) {
+  auto pos = [](double v) { return std::isfinite(v) && v > 0.0; };
+  if (!(pos(p[0]) && pos(p[1]) && pos(p[2]) && pos(p[4]) && pos(p[5]) &&
+        std::isfinite(p[3]) && p[3] >= 0.0)) {
+    throw InvalidArg(
+        "Params: mu0, tauX, tauT, omega, h must be positive and finite; "
+        "theta must be nonnegative and finite");
+  }
+}
+
+// EventSet constructor checks, types.hpp:85-109.
+void validate_events(const double* x, const double* y, const double* t, int64_t n,
+                     double window_end) {
+  if (n < 1) throw InvalidArg("EventSet: need at least one event");
+  if (!x || !y || !t) throw InvalidArg("EventSet: coordinate/time length mismatch");
+  if (n > (int64_t{1} << 30)) throw InvalidArg("sthk: at most 2^30 events supported");
+  for (int64_t i = 0; i < n; ++i) {
+    if (!std::isfinite(x[i]) || !std::isfinite(y[i]) || !std::isfinite(t[i])) {
+      throw InvalidArg("EventSet: non-finite entry at index " + std::to_string(i));
+    }
+    if (t[i] < 0.0) throw InvalidArg("EventSet: negative time at index " + std::to_string(i));
+    if (i > 0 && t[i] < t[i - 1]) {
+      throw InvalidArg("EventSet: times not sorted at index " + std::to_string(i));
+    }
+  }
+  if (!std::isfinite(window_end) || window_end < t[n - 1]) {
+    throw InvalidArg("EventSet: windowEnd precedes last event");
+  }
+}
+
+struct EvalPlan {
+  sthk::PairConsts k;
+  int sc = 0;
+  int nchunks = 0;
+  std::vector<int> cuts;  // shard row boundaries (size shards+1)
+};
+
+// Culling windows: background term is exactly 0 when |dt| > dB, trigger term
+// when dt > dT (fexp flushes below -708.40; we cut at -709).
+void culling_windows(const double* p, double& dB, double& dT) {
+  dB = p[2] * std::sqrt(2.0 * sthk::kCullExponent) * (1.0 + 1e-9);
+  dT = sthk::kCullExponent / p[4] * (1.0 + 1e-9);
+}
+
+int64_t lb(const std::vector<double>& t, int64_t n, double v) {
+  return std::lower_bound(t.begin(), t.begin() + n, v) - t.begin();
+}
+int64_t ub(const std::vector<double>& t, int64_t n, double v) {
+  return std::upper_bound(t.begin(), t.begin() + n, v) - t.begin();
+}
+
+EvalPlan make_plan(const sthk_engine& e, int shards) {
+  EvalPlan pl;
+  const double* p = e.p;
+  double dB, dT;
+  culling_windows(p, dB, dT);
+  pl.k.cx = -0.5 / (p[1] * p[1]);
+  pl.k.ct = -0.5 / (p[2] * p[2]);
+  pl.k.ch = -0.5 / (p[5] * p[5]);
+  pl.k.nom = -p[4];
+  const double inf = std::numeric_limits<double>::infinity();
+  pl.k.dB = e.dense ? inf : dB;
+  pl.k.dT = e.dense ? inf : dT;
+
+  // Chunk size from the (culled) mean live width of sampled tiles. Depends
+  // only on (events, params): identical on every rank and device count.
+  const int64_t n = e.n;
+  const int64_t ntiles = (n + kTM - 1) / kTM;
+  const int samples = static_cast<int>(std::min<int64_t>(ntiles, 64));
+  double wsum = 0.0;
+  for (int s = 0; s < samples; ++s) {
+    const int64_t tile = samples == 1 ? 0 : (ntiles - 1) * s / (samples - 1);
+    const int64_t first = tile * kTM, last = std::min(first + kTM, n) - 1;
+    const int64_t lo = std::min(lb(e.ht, n, e.ht[first] - std::max(dB, dT)), first);
+    const int64_t hi = std::max(ub(e.ht, n, e.ht[last] + dB), last + 1);
+    wsum += static_cast<double>(hi - lo);
+  }
+  const double wmean = wsum / samples;
+  double sc = wmean * static_cast<double>(ntiles) / kItemsTarget;
+  sc = std::ceil(sc / kTS) * kTS;
+  sc = std::max<double>(sc, 4 * kTS);
+  sc = std::min<double>(sc, static_cast<double>(e.npad));
+  pl.sc = static_cast<int>(sc);
+  pl.nchunks = static_cast<int>((n + pl.sc - 1) / pl.sc);
+
+  // Cost-balanced partition of 1024-row blocks across shards (background
+  // window is two-sided, trigger one-sided: cost ~ live source width).
+  const int64_t nb = (n + kRB - 1) / kRB;
+  pl.cuts.assign(shards + 1, 0);
+  pl.cuts[shards] = static_cast<int>(n);
+  if (shards > 1) {
+    std::vector<double> cost(nb);
+    double tot = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t first = b * kRB, last = std::min(first + kRB, n) - 1;
+      const double w = e.dense ? static_cast<double>(n)
+                               : static_cast<double>(ub(e.ht, n, e.ht[last] + dB) -
+                                                     lb(e.ht, n, e.ht[first] - std::max(dB, dT)));
+      cost[b] = w * static_cast<double>(last - first + 1);
+      tot += cost[b];
+    }
+    double run = 0;
+    int64_t b = 0;
+    for (int s = 1; s < shards; ++s) {
+      const double target = tot * s / shards;
+      while (b < nb && run + 0.5 * cost[b] < target) run += cost[b++];
+      pl.cuts[s] = static_cast<int>(std::min<int64_t>(b * kRB, n));
+    }
+  }
+  return pl;
+}
+
+void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
+  if (!e.loaded) throw NotLoaded("sthk: no events loaded");
+  if (!e.has_params) throw NotLoaded("sthk: no parameters set");
+  const int shards = e.rank_mode ? e.world : static_cast<int>(e.slots.size());
+  const EvalPlan pl = make_plan(e, shards);
+  e.last_sc = pl.sc;
+  const int NS = grad ? sthk::kNSumGrad : sthk::kNSumVal;
+  const int64_t ntiles_total = (e.n + kTM - 1) / kTM;
+  const int nb_total = static_cast<int>((e.n + kRB - 1) / kRB);
+  const double* p = e.p;
+  const double kPi = 3.14159265358979323846;
+
+  for (size_t si = 0; si < e.slots.size(); ++si) {
+    Slot& s = e.slots[si];
+    const int shard = e.rank_mode ? e.rank : static_cast<int>(si);
+    s.row0 = pl.cuts[shard];
+    s.row1 = pl.cuts[shard + 1];
+    set_dev(s);
+    const int tile0 = s.row0 / kTM;
+    const int tile1 = static_cast<int>((s.row1 + kTM - 1) / kTM);
+    const int ntiles = std::max(tile1 - tile0, 0);
+    dev_grow(s.ranges, s.ranges_cap, static_cast<size_t>(ntiles_total));
+    dev_grow(s.counts, s.counts_cap, static_cast<size_t>(std::max(ntiles, 1)));
+    dev_grow(s.items, s.items_cap, static_cast<size_t>(std::max(ntiles, 1)) * pl.nchunks);
+    dev_grow(s.partial, s.partial_cap, static_cast<size_t>(pl.nchunks) * NS * e.npad);
+    dev_grow(s.block_partial, s.bp_cap, static_cast<size_t>(nb_total) * kNOut);
+    if (want_pe) dev_grow(s.per_event, s.pe_cap, static_cast<size_t>(e.npad));
+
+    cudaStream_t st = s.stream;
+    if (e.timing) ck(cudaEventRecord(s.ev[0], st), "event");
+    ck(cudaMemsetAsync(s.pair_counts, 0, 3 * sizeof(unsigned long long), st), "memset");
+    if (shards > 1) {
+      ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
+    }
+    if (ntiles == 0) {
+      // an empty shard still takes part in the collective
+      ck(cudaMemsetAsync(s.scalars, 0, 2 * sizeof(int), st), "memset");
+    } else {
+      sthk::PlanArgs pa{};
+      pa.t = s.t;
+      pa.n = e.n;
+      pa.tile0 = tile0;
+      pa.tile1 = tile1;
+      pa.dB = pl.k.dB;
+      pa.dT = pl.k.dT;
+      pa.dense = e.dense ? 1 : 0;
+      pa.sc = pl.sc;
+      pa.nchunks = pl.nchunks;
+      pa.ranges = s.ranges;
+      pa.counts = s.counts;
+      pa.items = s.items;
+      pa.n_items = s.scalars;
+      pa.work_counter = s.scalars + 1;
+      ck(sthk::launch_plan(pa, st), "plan");
+
+      sthk::PairArgs qa{};
+      qa.x = s.x;
+      qa.y = s.y;
+      qa.t = s.t;
+      qa.n = e.n;
+      qa.npad = e.npad;
+      qa.k = pl.k;
+      qa.sc = pl.sc;
+      qa.ranges = s.ranges;
+      qa.items = s.items;
+      qa.n_items = s.scalars;
+      qa.work_counter = s.scalars + 1;
+      qa.partial = s.partial;
+      qa.pair_counts = s.pair_counts;
+      const int grid = s.sms * (grad ? s.occ_grad : s.occ_val);
+      if (e.timing) ck(cudaEventRecord(s.ev[1], st), "event");
+      ck(sthk::launch_pairs(qa, grad, grid, st), "pair kernel");
+      if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
+
+      sthk::FinArgs fa{};
+      fa.t = s.t;
+      fa.n = e.n;
+      fa.npad = e.npad;
+      fa.row0 = s.row0;
+      fa.row1 = s.row1;
+      fa.window_end = e.window_end;
+      fa.mu0 = p[0];
+      fa.tauX = p[1];
+      fa.tauT = p[2];
+      fa.theta = p[3];
+      fa.omega = p[4];
+      fa.h = p[5];
+      // HawkesPairTerm constants, kernels.hpp:78-84
+      fa.bgNorm = std::pow(2.0 * kPi, -1.5) / (p[1] * p[1] * p[2]);
+      fa.trNorm = p[3] * p[4] / (2.0 * kPi * p[5] * p[5]);
+      fa.cT = p[4] / (2.0 * kPi * p[5] * p[5]);
+      fa.sc = pl.sc;
+      fa.nchunks = pl.nchunks;
+      fa.dense = e.dense ? 1 : 0;
+      fa.ranges = s.ranges;
+      fa.partial = s.partial;
+      fa.per_event = want_pe ? s.per_event : nullptr;
+      fa.block_partial = s.block_partial;
+      ck(sthk::launch_finalize(fa, grad, st), "finalize");
+    }
+  }
+
+  if (shards > 1) {
+    ckn(ncclGroupStart(), "ncclGroupStart");
+    for (Slot& s : e.slots) {
+      ckn(ncclAllReduce(s.block_partial, s.block_partial, static_cast<size_t>(nb_total) * kNOut,
+                        ncclDouble, ncclSum, s.comm, s.stream),
+          "ncclAllReduce");
+    }
+    ckn(ncclGroupEnd(), "ncclGroupEnd");
+  }
+
+  for (Slot& s : e.slots) {
+    set_dev(s);
+    cudaStream_t st = s.stream;
+    ck(sthk::launch_final_sum(s.block_partial, nb_total, s.out, st), "final sum");
+    ck(cudaMemcpyAsync(s.h_out, s.out, kNOut * sizeof(double), cudaMemcpyDeviceToHost, st),
+       "D2H");
+    ck(cudaMemcpyAsync(s.h_counts, s.pair_counts, 3 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st),
+       "D2H");
+    if (want_pe && s.row1 > s.row0) {
+      if (s.h_pe_cap < static_cast<size_t>(e.npad)) {
+        if (s.h_per_event) ck(cudaFreeHost(s.h_per_event), "cudaFreeHost");
+        ck(cudaMallocHost(&s.h_per_event, sizeof(double) * e.npad), "cudaMallocHost");
+        s.h_pe_cap = static_cast<size_t>(e.npad);
+      }
+      ck(cudaMemcpyAsync(s.h_per_event + s.row0, s.per_event + s.row0,
+                         sizeof(double) * (s.row1 - s.row0), cudaMemcpyDeviceToHost, st),
+         "D2H");
+    }
+    if (e.timing) ck(cudaEventRecord(s.ev[3], st), "event");
+  }
+  e.pending = true;
+  e.last_grad = grad;
+  e.last_pe = want_pe;
+}
+
+void collect(sthk_engine& e, double* loglik, int* valid, double* grad6, double* per_event) {
+  if (!e.pending) throw NotLoaded("sthk: no evaluation enqueued");
+  for (Slot& s : e.slots) {
+    set_dev(s);
+    ck(cudaStreamSynchronize(s.stream), "evaluation");
+  }
+  e.pending = false;
+  const double* o = e.slots[0].h_out;
+  const bool ok = o[7] == 0.0 && std::isfinite(o[0]);
+  if (valid) *valid = ok ? 1 : 0;
+  if (loglik) *loglik = ok ? o[0] : -std::numeric_limits<double>::infinity();
+  if (grad6) {
+    for (int k = 0; k < 6; ++k) {
+      grad6[k] = (ok && e.last_grad) ? o[1 + k] : std::numeric_limits<double>::quiet_NaN();
+    }
+  }
+  if (per_event && e.last_pe) {
+    for (Slot& s : e.slots) {
+      if (s.row1 > s.row0) {
+        std::memcpy(per_event + s.row0, s.h_per_event + s.row0,
+                    sizeof(double) * (s.row1 - s.row0));
+      }
+    }
+  }
+}
+
+int fail(sthk_engine* e, int code, const char* msg) {
+  if (e) e->err = msg;
+  return code;
+}
+
+template <typename F>
+int guarded(sthk_engine* e, F&& f) {
+  if (!e) return STHK_EINVAL;
+  try {
+    f();
+    e->err.clear();
+    return STHK_OK;
+  } catch (const InvalidArg& x) {
+    return fail(e, STHK_EINVAL, x.what());
+  } catch (const NotLoaded& x) {
+    return fail(e, STHK_ENOTLOADED, x.what());
+  } catch (const NcclErr& x) {
+    return fail(e, STHK_ENCCL, x.what());
+  } catch (const CudaErr& x) {
+    return fail(e, STHK_ECUDA, x.what());
+  } catch (const std::exception& x) {
+    return fail(e, STHK_ECUDA, x.what());
+  }
+}
+
+thread_local std::string g_create_err;
+
+}  // namespace
+
+extern "C" {
+
+const char* sthk_version(void) { return "sthk 0.1 (sm_100a, fp64)"; }
+
+const char* sthk_last_error(const sthk_engine* e) {
+  return e ? e->err.c_str() : g_create_err.c_str();
+}
+
+int sthk_create(const int* device_ids, int n_devices, sthk_engine** out) {
+  if (!out || n_devices < 1 || !device_ids) {
+    g_create_err = "sthk_create: need n_devices >= 1";
+    return STHK_EINVAL;
+  }
+  *out = nullptr;
+  auto e = std::make_unique<sthk_engine>();
+  try {
+    int count = 0;
+    ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    for (int i = 0; i < n_devices; ++i) {
+      if (device_ids[i] < 0 || device_ids[i] >= count) {
+        g_create_err = "sthk_create: device id out of range";
+        return STHK_EINVAL;
+      }
+    }
+    e->slots.resize(n_devices);
+    for (int i = 0; i < n_devices; ++i) init_slot(e->slots[i], device_ids[i]);
+    if (n_devices > 1) {
+      std::vector<ncclComm_t> comms(n_devices);
+      ckn(ncclCommInitAll(comms.data(), n_devices, device_ids), "ncclCommInitAll");
+      for (int i = 0; i < n_devices; ++i) e->slots[i].comm = comms[i];
+    }
+  } catch (const NcclErr& x) {
+    g_create_err = x.what();
+    for (auto& s : e->slots) free_slot(s);
+    return STHK_ENCCL;
+  } catch (const std::exception& x) {
+    g_create_err = x.what();
+    for (auto& s : e->slots) free_slot(s);
+    return STHK_ECUDA;
+  }
+  *out = e.release();
+  return STHK_OK;
+}
+
+int sthk_nccl_unique_id(void* nccl_id) {
+  if (!nccl_id) return STHK_EINVAL;
+  ncclUniqueId id;
+  const ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    g_create_err = ncclGetErrorString(r);
+    return STHK_ENCCL;
+  }
+  static_assert(sizeof(ncclUniqueId) == STHK_NCCL_ID_BYTES, "nccl id size");
+  std::memcpy(nccl_id, &id, sizeof(id));
+  return STHK_OK;
+}
+
+int sthk_create_rank(int device, int rank, int world, const void* nccl_id,
+                     sthk_engine** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_id)) {
+    g_create_err = "sthk_create_rank: invalid rank/world";
+    return STHK_EINVAL;
+  }
+  *out = nullptr;
+  auto e = std::make_unique<sthk_engine>();
+  e->rank_mode = true;
+  e->rank = rank;
+  e->world = world;
+  try {
+    e->slots.resize(1);
+    init_slot(e->slots[0], device);
+    if (world > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      ckn(ncclCommInitRank(&e->slots[0].comm, world, id, rank), "ncclCommInitRank");
+    }
+  } catch (const NcclErr& x) {
+    g_create_err = x.what();
+    for (auto& s : e->slots) free_slot(s);
+    return STHK_ENCCL;
+  } catch (const std::exception& x) {
+    g_create_err = x.what();
+    for (auto& s : e->slots) free_slot(s);
+    return STHK_ECUDA;
+  }
+  *out = e.release();
+  return STHK_OK;
+}
+
+int sthk_destroy(sthk_engine* e) {
+  if (!e) return STHK_EINVAL;
+  for (auto& s : e->slots) free_slot(s);
+  delete e;
+  return STHK_OK;
+}
+
+int sthk_load_events(sthk_engine* e, const double* x, const double* y, const double* t,
+                     int64_t n, double window_end) {
+  return guarded(e, [&] {
+    validate_events(x, y, t, n, window_end);
+    if (e->pending) collect(*e, nullptr, nullptr, nullptr, nullptr);
+    const int64_t npad = (n + kTM - 1) / kTM * kTM;
+    e->ht.assign(t, t + n);
+    for (auto& v : e->ht) v = v + 0.0;  // canonicalise -0.0 (mask compares bits)
+    std::vector<double> hx(npad, 0.0), hy(npad, 0.0), htp(npad, e->ht[n - 1]);
+    std::memcpy(hx.data(), x, sizeof(double) * n);
+    std::memcpy(hy.data(), y, sizeof(double) * n);
+    std::memcpy(htp.data(), e->ht.data(), sizeof(double) * n);
+    for (Slot& s : e->slots) {
+      set_dev(s);
+      dev_grow(s.x, s.x_cap, static_cast<size_t>(npad));
+      dev_grow(s.y, s.y_cap, static_cast<size_t>(npad));
+      dev_grow(s.t, s.t_cap, static_cast<size_t>(npad));
+      ck(cudaMemcpyAsync(s.x, hx.data(), sizeof(double) * npad, cudaMemcpyHostToDevice, s.stream),
+         "H2D");
+      ck(cudaMemcpyAsync(s.y, hy.data(), sizeof(double) * npad, cudaMemcpyHostToDevice, s.stream),
+         "H2D");
+      ck(cudaMemcpyAsync(s.t, htp.data(), sizeof(double) * npad, cudaMemcpyHostToDevice, s.stream),
+         "H2D");
+      ck(cudaStreamSynchronize(s.stream), "H2D");
+    }
+    e->n = n;
+    e->npad = npad;
+    e->window_end = window_end;
+    e->loaded = true;
+  });
+}
+
+int sthk_set_params(sthk_engine* e, const double* params6) {
+  return guarded(e, [&] {
+    if (!params6) throw InvalidArg("sthk_set_params: null params");
+    validate_params(params6);
+    std::memcpy(e->p, params6, sizeof(e->p));
+    e->has_params = true;
+  });
+}
+
+int sthk_enqueue(sthk_engine* e, int want_grad, int want_per_event) {
+  return guarded(e, [&] {
+    if (e->pending) throw InvalidArg("sthk_enqueue: previous result not collected");
+    enqueue_eval(*e, want_grad != 0, want_per_event != 0);
+  });
+}
+
+int sthk_result(sthk_engine* e, double* loglik, int* valid, double* grad6, double* per_event) {
+  return guarded(e, [&] { collect(*e, loglik, valid, grad6, per_event); });
+}
+
+int sthk_loglik(sthk_engine* e, double* loglik, int* valid, double* per_event) {
+  return guarded(e, [&] {
+    if (e->pending) collect(*e, nullptr, nullptr, nullptr, nullptr);
+    enqueue_eval(*e, false, per_event != nullptr);
+    collect(*e, loglik, valid, nullptr, per_event);
+  });
+}
+
+int sthk_loglik_grad(sthk_engine* e, double* loglik, int* valid, double* grad6,
+                     double* per_event) {
+  return guarded(e, [&] {
+    if (e->pending) collect(*e, nullptr, nullptr, nullptr, nullptr);
+    enqueue_eval(*e, true, per_event != nullptr);
+    collect(*e, loglik, valid, grad6, per_event);
+  });
+}
+
+int sthk_loglik_batch(sthk_engine* e, const double* params, int64_t P, double* loglik,
+                      int* valid, double* grad) {
+  return guarded(e, [&] {
+    if (P < 1 || !params) throw InvalidArg("logLikelihoodBatch: empty parameter list");
+    for (int64_t i = 0; i < P; ++i) {
+      try {
+        validate_params(params + 6 * i);
+      } catch (const InvalidArg& x) {
+        throw InvalidArg("logLikelihoodBatch: entry " + std::to_string(i) + ": " + x.what());
+      }
+    }
+    if (e->pending) collect(*e, nullptr, nullptr, nullptr, nullptr);
+    double saved[6];
+    std::memcpy(saved, e->p, sizeof(saved));
+    const bool had = e->has_params;
+    for (int64_t i = 0; i < P; ++i) {
+      std::memcpy(e->p, params + 6 * i, sizeof(e->p));
+      e->has_params = true;
+      enqueue_eval(*e, grad != nullptr, false);
+      collect(*e, loglik + i, valid + i, grad ? grad + 6 * i : nullptr, nullptr);
+    }
+    std::memcpy(e->p, saved, sizeof(saved));
+    e->has_params = had;
+  });
+}
+
+int sthk_set_timing(sthk_engine* e, int enable) {
+  return guarded(e, [&] { e->timing = enable != 0; });
+}
+
+int sthk_set_dense(sthk_engine* e, int dense) {
+  return guarded(e, [&] { e->dense = dense != 0; });
+}
+
+int sthk_get_stream(sthk_engine* e, int slot, void** stream) {
+  return guarded(e, [&] {
+    if (slot < 0 || slot >= static_cast<int>(e->slots.size()) || !stream) {
+      throw InvalidArg("sthk_get_stream: bad slot");
+    }
+    *stream = e->slots[slot].stream;
+  });
+}
+
+int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
+  return guarded(e, [&] {
+    if (!out) throw InvalidArg("sthk_get_stats: null");
+    std::memset(out, 0, sizeof(*out));
+    out->n = e->n;
+    out->pairs_dense = e->n * e->n;
+    out->n_devices = static_cast<int>(e->slots.size());
+    out->rank = e->rank;
+    out->world = e->world;
+    out->source_chunk = e->last_sc;
+    for (Slot& s : e->slots) {
+      out->pairs_bg += static_cast<int64_t>(s.h_counts[0]);
+      out->pairs_tr += static_cast<int64_t>(s.h_counts[1]);
+      out->pairs_any += static_cast<int64_t>(s.h_counts[2]);
+      if (e->timing && s.row1 > s.row0) {
+        float a = 0, b = 0;
+        set_dev(s);
+        if (cudaEventElapsedTime(&a, s.ev[1], s.ev[2]) == cudaSuccess) {
+          out->pair_kernel_ms = std::max(out->pair_kernel_ms, static_cast<double>(a));
+        }
+        if (cudaEventElapsedTime(&b, s.ev[0], s.ev[3]) == cudaSuccess) {
+          out->eval_ms = std::max(out->eval_ms, static_cast<double>(b));
+        }
+      }
+    }
+    cudaGetLastError();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,432 @@
+// sm_100a kernels of the B200 spatiotemporal-Hawkes likelihood engine.
+//
+// One evaluation = plan -> pairs -> finalize -> [NCCL all-reduce] -> final sum.
+//
+//  plan_ranges / plan_items   per 128-row target tile, the live source range
+//                             [lo, hi) from a binary search on the sorted
+//                             times (exact underflow culling),
+//                             cut into (tile, chunk) work items.
+//  pair_kernel<GRAD>          the O(N^2) hot loop (reference: pairReduceBlock,
+//                             backend.hpp:95-137, with HawkesPairTerm,
+//                             kernels.hpp:76-106). Persistent CTAs pull work
+//                             items from an atomic counter; each CTA owns 128
+//                             targets in registers (one per thread) and
+//                             streams 128-source stages through shared memory
+//                             with double-buffered cp.async.bulk (TMA) copies.
+//                             Per stage a CTA-uniform mode is chosen from the
+//                             stage/tile time ranges: background on/off and
+//                             trigger none / unmasked / masked (the strict
+//                             t_src < t_tgt rule, kernels.hpp:44,99-100).
+//                             With GRAD the 4 extra gradient sums are fused
+//                             into the same pass.
+//  finalize_kernel<GRAD>      per row: sum chunk partials in chunk order,
+//                             lambda, compensator (kernels.hpp:54-65), log,
+//                             gradient terms, degenerate flag
+//                             (likelihood.cpp:34-43); then a fixed-order
+//                             block tree-reduction into per-1024-row partials.
+//  final_sum_kernel           fixed-order sum of the block partials.
+//
+// Determinism: every floating-point sum has a fixed order that depends only
+// on (events, params) -- not on scheduling, culling decisions or the number
+// of GPUs -- so results are bitwise reproducible.
+#include <cmath>
+
+#include "sthk_device.cuh"
+#include "sthk_kernels.cuh"
+
+namespace sthk {
+
+namespace {
+
+constexpr double kInvSqrt2 = 0.7071067811865475244;     // kernels.hpp:14
+constexpr double kInvSqrt2Pi = 0.3989422804014326779;   // kernels.hpp:13
+
+__device__ __forceinline__ int64_t lower_bound_t(const double* t, int64_t n, double v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (t[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int64_t upper_bound_t(const double* t, int64_t n, double v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (t[mid] <= v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// Plan
+// ---------------------------------------------------------------------------
+__global__ void plan_ranges_kernel(const PlanArgs a) {
+  const int tile = a.tile0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (tile >= a.tile1) return;
+  const int64_t first = static_cast<int64_t>(tile) * kTM;
+  const int64_t last = min(first + kTM, a.n) - 1;
+  int lo, hi;
+  if (a.dense) {
+    lo = 0;
+    hi = static_cast<int>(a.n);
+  } else {
+    const double tmin = a.t[first], tmax = a.t[last];
+    lo = static_cast<int>(lower_bound_t(a.t, a.n, tmin - fmax(a.dB, a.dT)));
+    hi = static_cast<int>(upper_bound_t(a.t, a.n, tmax + a.dB));
+    // the tile's own rows are always live (background self term)
+    lo = min(lo, static_cast<int>(first));
+    hi = max(hi, static_cast<int>(last + 1));
+  }
+  a.ranges[tile] = make_int2(lo, hi);
+  const int c0 = a.dense ? 0 : lo / a.sc;
+  const int c1 = a.dense ? a.nchunks - 1 : (hi - 1) / a.sc;
+  a.counts[tile - a.tile0] = c1 - c0 + 1;
+}
+
+// Single CTA: exclusive scan of per-tile item counts, then the item list in
+// (tile, chunk) order. Also resets the persistent kernel's work counter.
+__global__ void __launch_bounds__(1024) plan_items_kernel(const PlanArgs a) {
+  __shared__ int s_scan[1024];
+  __shared__ int s_carry;
+  const int tid = threadIdx.x;
+  const int ntiles = a.tile1 - a.tile0;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < ntiles; base += 1024) {
+    const int i = base + tid;
+    const int c = i < ntiles ? a.counts[i] : 0;
+    s_scan[tid] = c;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      const int v = tid >= off ? s_scan[tid - off] : 0;
+      __syncthreads();
+      s_scan[tid] += v;
+      __syncthreads();
+    }
+    const int excl = s_carry + s_scan[tid] - c;
+    if (i < ntiles) {
+      const int tile = a.tile0 + i;
+      const int2 rg = a.ranges[tile];
+      const int c0 = a.dense ? 0 : rg.x / a.sc;
+      for (int q = 0; q < c; ++q) a.items[excl + q] = make_int2(tile, c0 + q);
+    }
+    __syncthreads();
+    if (tid == 1023) s_carry += s_scan[1023];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *a.n_items = s_carry;
+    *a.work_counter = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pair kernel
+// ---------------------------------------------------------------------------
+// TR: 0 = no trigger term, 1 = trigger without mask (every source strictly
+// earlier than every target of the tile), 2 = trigger with the strict
+// t_src < t_tgt mask (kernels.hpp:99-100). Times are >= +0 (canonicalised on
+// load), so the mask compares their bit patterns as integers.
+template <bool GRAD, bool BG, int TR>
+__device__ __forceinline__ void stage_loop(const double* __restrict__ sx,
+                                           const double* __restrict__ sy,
+                                           const double* __restrict__ st, int cnt,
+                                           double xi, double yi, double ti,
+                                           const PairConsts& k,
+                                           const double* __restrict__ tab,
+                                           double* acc) {
+  const long long tib = __double_as_longlong(ti);
+#pragma unroll 4
+  for (int j = 0; j < cnt; ++j) {
+    const double sj = st[j];
+    const double dx = xi - sx[j];
+    const double dy = yi - sy[j];
+    const double dt = ti - sj;
+    const double r2 = fma(dx, dx, dy * dy);
+    if constexpr (BG) {
+      const double dt2 = dt * dt;
+      const double e = fexp(fma(k.cx, r2, k.ct * dt2), tab);
+      acc[0] += e;
+      if constexpr (GRAD) {
+        acc[1] = fma(e, r2, acc[1]);
+        acc[2] = fma(e, dt2, acc[2]);
+      }
+    }
+    if constexpr (TR != 0) {
+      double e = fexp(fma(k.nom, dt, k.ch * r2), tab);
+      if constexpr (TR == 2) e = (__double_as_longlong(sj) < tib) ? e : 0.0;
+      if constexpr (GRAD) {
+        acc[3] += e;
+        acc[4] = fma(e, dt, acc[4]);
+        acc[5] = fma(e, r2, acc[5]);
+      } else {
+        acc[1] += e;
+      }
+    }
+  }
+}
+
+template <bool GRAD>
+__global__ void __launch_bounds__(kTM, 4) pair_kernel(const PairArgs a) {
+  constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
+  __shared__ __align__(128) double s_src[2][3][kTS];
+  __shared__ double s_tab[64];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ int s_item[2];
+
+  const int tid = threadIdx.x;
+  if (tid < 64) s_tab[tid] = kExpTable[tid];
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int n_items = *a.n_items;
+  const int64_t n = a.n;
+  uint32_t phase = 0;
+  unsigned long long cBg = 0, cTr = 0, cAny = 0;
+
+  for (int iter = 0;; ++iter) {
+    if (tid == 0) s_item[iter & 1] = atomicAdd(a.work_counter, 1);
+    __syncthreads();
+    const int item = s_item[iter & 1];
+    if (item >= n_items) break;
+
+    const int2 it = a.items[item];
+    const int tile = it.x, chunk = it.y;
+    const int2 rg = a.ranges[tile];
+    const int64_t first = static_cast<int64_t>(tile) * kTM;
+    const int64_t row = first + tid;
+    const double xi = a.x[row], yi = a.y[row], ti = a.t[row];
+    const int64_t last = min(first + kTM, n) - 1;
+    const double tmin = a.t[first], tmax = a.t[last];
+    const int rows_real = static_cast<int>(last - first + 1);
+
+    int s_begin = max(rg.x, chunk * a.sc);
+    s_begin -= s_begin % kTS;
+    const int s_end = min(rg.y, (chunk + 1) * a.sc);
+    const int nst = (s_end - s_begin + kTS - 1) / kTS;
+
+    double acc[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) acc[q] = 0.0;
+
+    constexpr uint32_t kStageBytes = kTS * sizeof(double);
+    if (tid == 0 && nst > 0) {
+      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes);
+      tma_load_1d(s_src[0][0], a.x + s_begin, kStageBytes, &s_bar[0]);
+      tma_load_1d(s_src[0][1], a.y + s_begin, kStageBytes, &s_bar[0]);
+      tma_load_1d(s_src[0][2], a.t + s_begin, kStageBytes, &s_bar[0]);
+    }
+    for (int s = 0; s < nst; ++s) {
+      const int buf = s & 1;
+      // every thread is done with the other buffer (stage s-1) -> refill it
+      __syncthreads();
+      if (tid == 0 && s + 1 < nst) {
+        const int nb = buf ^ 1;
+        const int64_t s0n = s_begin + static_cast<int64_t>(s + 1) * kTS;
+        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes);
+        tma_load_1d(s_src[nb][0], a.x + s0n, kStageBytes, &s_bar[nb]);
+        tma_load_1d(s_src[nb][1], a.y + s0n, kStageBytes, &s_bar[nb]);
+        tma_load_1d(s_src[nb][2], a.t + s0n, kStageBytes, &s_bar[nb]);
+      }
+      mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+
+      const int64_t s0 = s_begin + static_cast<int64_t>(s) * kTS;
+      const int cnt = static_cast<int>(min(static_cast<int64_t>(kTS), n - s0));
+      const double* sx = s_src[buf][0];
+      const double* sy = s_src[buf][1];
+      const double* st = s_src[buf][2];
+      const double smin = st[0], smax = st[cnt - 1];
+
+      const bool bg = !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
+      int tr;
+      if (smin >= tmax || smax < tmin - a.k.dT) tr = 0;
+      else if (smax < tmin) tr = 1;
+      else tr = 2;
+
+      if (bg) {
+        if (tr == 0) stage_loop<GRAD, true, 0>(sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
+        else if (tr == 1) stage_loop<GRAD, true, 1>(sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
+        else stage_loop<GRAD, true, 2>(sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
+      } else {
+        if (tr == 1) stage_loop<GRAD, false, 1>(sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
+        else if (tr == 2) stage_loop<GRAD, false, 2>(sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
+      }
+      if (tid == 0) {
+        const unsigned long long pr = static_cast<unsigned long long>(cnt) * rows_real;
+        if (bg) cBg += pr;
+        if (tr) cTr += pr;
+        if (bg || tr) cAny += pr;
+      }
+    }
+
+    double* out = a.partial + static_cast<size_t>(chunk) * NS * a.npad + row;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) out[static_cast<size_t>(q) * a.npad] = acc[q];
+  }
+
+  if (tid == 0 && a.pair_counts) {
+    atomicAdd(&a.pair_counts[0], cBg);
+    atomicAdd(&a.pair_counts[1], cTr);
+    atomicAdd(&a.pair_counts[2], cAny);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Finalize: per-row lambda / compensator / log / gradient, block partials.
+// ---------------------------------------------------------------------------
+template <bool GRAD>
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) {
+  constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
+  __shared__ double s_red[kNOut][kFinThreads];
+  const int tid = threadIdx.x;
+  const int64_t base = static_cast<int64_t>(a.row0) + static_cast<int64_t>(blockIdx.x) * kRB;
+  double acc[kNOut];
+#pragma unroll
+  for (int q = 0; q < kNOut; ++q) acc[q] = 0.0;
+
+  for (int q = 0; q < kRB / kFinThreads; ++q) {
+    const int64_t r = base + q * kFinThreads + tid;
+    if (r >= a.row1) break;
+    const int2 rg = a.ranges[r / kTM];
+    const int c0 = a.dense ? 0 : rg.x / a.sc;
+    const int c1 = a.dense ? a.nchunks - 1 : (rg.y - 1) / a.sc;
+    double s[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) s[k] = 0.0;
+    for (int c = c0; c <= c1; ++c) {
+      const double* p = a.partial + static_cast<size_t>(c) * NS * a.npad + r;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) s[k] += p[static_cast<size_t>(k) * a.npad];
+    }
+    const double sB = s[0];
+    const double sT = GRAD ? s[3] : s[1];
+    const double B = a.bgNorm * sB;
+    const double Tr = a.trNorm * sT;
+    const double lam = a.mu0 * B + Tr;  // likelihood.cpp:35
+
+    const double ti = a.t[r];
+    const double D = a.window_end - ti;
+    // compensatorTerm, kernels.hpp:54-65; normalCdf = 0.5 erfc(-z/sqrt2)
+    const double Phi1 = 0.5 * erfc(-(D / a.tauT) * kInvSqrt2);
+    const double Phi0 = 0.5 * erfc(-(-ti / a.tauT) * kInvSqrt2);
+    const double em1 = expm1(-a.omega * D);
+    const double Lam = a.mu0 * (Phi1 - Phi0) + (-a.theta * em1);
+
+    if (!(lam > 0.0) || !isfinite(lam)) {  // likelihood.cpp:36-39
+      acc[7] += 1.0;
+      if (a.per_event) a.per_event[r] = 0.0;
+      continue;
+    }
+    const double term = log(lam) - Lam;
+    acc[0] += term;
+    if (a.per_event) a.per_event[r] = term;
+    if constexpr (GRAD) {
+      const double inv = 1.0 / lam;
+      const double tx3 = a.tauX * a.tauX * a.tauX;
+      const double tt3 = a.tauT * a.tauT * a.tauT;
+      const double h3 = a.h * a.h * a.h;
+      const double mb = a.mu0 * a.bgNorm;
+      // d lambda / d p
+      const double dl1 = mb * (-2.0 * sB / a.tauX + s[1] / tx3);
+      const double dl2 = mb * (-sB / a.tauT + s[2] / tt3);
+      const double dl3 = a.cT * sT;
+      const double dl4 = a.trNorm * (sT / a.omega - s[4]);
+      const double dl5 = a.trNorm * (-2.0 * sT / a.h + s[5] / h3);
+      // d Lambda / d p
+      const double z1 = D / a.tauT, z0 = ti / a.tauT;
+      const double phi1 = kInvSqrt2Pi * exp(-0.5 * z1 * z1);
+      const double phi0 = kInvSqrt2Pi * exp(-0.5 * z0 * z0);
+      const double dL2 = -a.mu0 * (phi1 * D + phi0 * ti) / (a.tauT * a.tauT);
+      acc[1] += B * inv - (Phi1 - Phi0);
+      acc[2] += dl1 * inv;
+      acc[3] += dl2 * inv - dL2;
+      acc[4] += dl3 * inv + em1;
+      acc[5] += dl4 * inv - a.theta * D * (em1 + 1.0);
+      acc[6] += dl5 * inv;
+    }
+  }
+
+#pragma unroll
+  for (int q = 0; q < kNOut; ++q) s_red[q][tid] = acc[q];
+  __syncthreads();
+  for (int w = kFinThreads / 2; w > 0; w >>= 1) {
+    if (tid < w) {
+#pragma unroll
+      for (int q = 0; q < kNOut; ++q) s_red[q][tid] += s_red[q][tid + w];
+    }
+    __syncthreads();
+  }
+  if (tid < kNOut) {
+    a.block_partial[(base / kRB) * kNOut + tid] = s_red[tid][0];
+  }
+}
+
+__global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict__ bp,
+                                                        int nblocks, double* out) {
+  __shared__ double s_red[kNOut][256];
+  const int tid = threadIdx.x;
+  double acc[kNOut];
+#pragma unroll
+  for (int q = 0; q < kNOut; ++q) acc[q] = 0.0;
+  for (int b = tid; b < nblocks; b += 256) {
+#pragma unroll
+    for (int q = 0; q < kNOut; ++q) acc[q] += bp[static_cast<size_t>(b) * kNOut + q];
+  }
+#pragma unroll
+  for (int q = 0; q < kNOut; ++q) s_red[q][tid] = acc[q];
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (tid < w) {
+#pragma unroll
+      for (int q = 0; q < kNOut; ++q) s_red[q][tid] += s_red[q][tid + w];
+    }
+    __syncthreads();
+  }
+  if (tid < kNOut) out[tid] = s_red[tid][0];
+}
+
+}  // namespace
+
+cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
+  const int ntiles = a.tile1 - a.tile0;
+  if (ntiles <= 0) return cudaSuccess;
+  plan_ranges_kernel<<<(ntiles + 255) / 256, 256, 0, stream>>>(a);
+  plan_items_kernel<<<1, 1024, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pairs(const PairArgs& a, bool grad, int grid, cudaStream_t stream) {
+  if (grad) pair_kernel<true><<<grid, kTM, 0, stream>>>(a);
+  else pair_kernel<false><<<grid, kTM, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream) {
+  const int nblocks = (a.row1 - a.row0 + kRB - 1) / kRB;
+  if (nblocks <= 0) return cudaSuccess;
+  if (grad) finalize_kernel<true><<<nblocks, kFinThreads, 0, stream>>>(a);
+  else finalize_kernel<false><<<nblocks, kFinThreads, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,
+                             cudaStream_t stream) {
+  final_sum_kernel<<<1, 256, 0, stream>>>(block_partial, nblocks, out);
+  return cudaGetLastError();
+}
+
+int pair_kernel_occupancy(bool grad) {
+  int occ = 0;
+  if (grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<true>, kTM, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<false>, kTM, 0);
+  return occ > 0 ? occ : 1;
+}
+
+}  // namespace sthk

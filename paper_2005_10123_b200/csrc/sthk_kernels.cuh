@@ -1,0 +1,93 @@
+// Kernel-side interface of the B200 Hawkes engine (shared by sthk_kernels.cu
+// and the host engine). Plain structs passed by value as kernel parameters.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace sthk {
+
+constexpr int kTM = 128;    // target rows per tile (= threads per pair CTA)
+constexpr int kTS = 128;    // sources per shared-memory stage
+constexpr int kRB = 1024;   // rows per reduction block (multi-GPU partition unit)
+constexpr int kFinThreads = 256;
+constexpr int kNSumGrad = 6;  // S_B, S_Br, S_Bt, S_T, S_Tt, S_Tr
+constexpr int kNSumVal = 2;   // S_B, S_T
+constexpr int kNOut = 8;      // loglik, 6 gradient terms, degenerate-row count
+
+// Exponent cut used for exact culling: every pair whose time-only exponent
+// bound is below this value has fexp(...) == +0 exactly (fexp flushes below
+// -708.40), so skipping it leaves every sum bitwise unchanged.
+constexpr double kCullExponent = 709.0;
+
+struct PairConsts {
+  double cx;    // -1/(2 tauX^2)
+  double ct;    // -1/(2 tauT^2)
+  double ch;    // -1/(2 h^2)
+  double nom;   // -omega
+  double dB;    // background live iff |dt| <= dB   (inf when dense)
+  double dT;    // trigger live iff 0 < dt <= dT    (inf when dense)
+};
+
+struct PlanArgs {
+  const double* t;
+  int64_t n;
+  int tile0, tile1;     // this shard's row tiles [tile0, tile1)
+  double dB, dT;
+  int dense;
+  int sc;               // sources per chunk (multiple of kTS)
+  int nchunks;          // ceil(n / sc)
+  int2* ranges;         // [ntiles] live source range [lo, hi) per row tile
+  int* counts;          // [ntiles] items per row tile (scratch)
+  int2* items;          // (row tile, chunk) work list
+  int* n_items;         // device scalar
+  int* work_counter;    // device scalar, reset here
+};
+
+struct PairArgs {
+  const double* x;
+  const double* y;
+  const double* t;
+  int64_t n;
+  int64_t npad;
+  PairConsts k;
+  int sc;
+  const int2* ranges;
+  const int2* items;
+  const int* n_items;
+  int* work_counter;
+  double* partial;      // [nchunks][nsum][npad]
+  unsigned long long* pair_counts;  // [3]: bg, tr, any (tile granularity)
+};
+
+struct FinArgs {
+  const double* t;
+  int64_t n;
+  int64_t npad;
+  int row0, row1;       // shard rows (row0 multiple of kRB)
+  double window_end;
+  // parameters and folded constants
+  double mu0, tauX, tauT, theta, omega, h;
+  double bgNorm;        // (2pi)^-1.5 / (tauX^2 tauT)       kernels.hpp:79
+  double trNorm;        // theta omega / (2 pi h^2)          kernels.hpp:82
+  double cT;            // omega / (2 pi h^2)  (d lambda / d theta)
+  int sc;
+  int nchunks;
+  int dense;
+  const int2* ranges;
+  const double* partial;
+  double* per_event;    // nullable
+  double* block_partial;  // [nblocks_total][kNOut]
+};
+
+// Launch wrappers (sthk_kernels.cu). All enqueue on `stream`.
+cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
+cudaError_t launch_pairs(const PairArgs& a, bool grad, int grid, cudaStream_t stream);
+cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream);
+cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,
+                             cudaStream_t stream);
+// Resident CTAs per SM of the pair kernel (for the persistent grid size).
+int pair_kernel_occupancy(bool grad);
+
+}  // namespace sthk

@@ -1,0 +1,239 @@
+"""Engine handle over the C ABI (include/sthk.h) and the reference-named
+entry points logLikelihood / logLikelihoodBatch (likelihood.hpp:24-31) plus
+logLikelihoodGradient (new; the reference has no gradient).
+
+Error mapping follows the C++ adapter: STHK_EINVAL ->
+ValueError (the reference's std::invalid_argument), anything else ->
+EngineError (std::runtime_error). A degenerate evaluation is not an error:
+it returns valid=False, logLik=-inf (likelihood.cpp:47-50).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from ctypes import byref, c_double, c_int, c_void_p
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .types import EventSet, LikelihoodResult, Params
+
+
+class EngineError(RuntimeError):
+    pass
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(c_double))
+
+
+class Engine:
+    """Stateful device engine: events stay resident in HBM across calls.
+
+    devices: local CUDA device ids driven from this process (rows are
+    partitioned across them, one NCCL all-reduce per evaluation).
+    rank/world/nccl_id: one-process-per-GPU mode (torchrun); pass the id
+    from Engine.nccl_unique_id() on rank 0 to every rank.
+    """
+
+    def __init__(self, devices: Sequence[int] = (0,), *, rank: Optional[int] = None,
+                 world: int = 1, nccl_id: Optional[bytes] = None):
+        self._lib = _lib.load_library()
+        self._h = c_void_p()
+        self._lock = threading.Lock()
+        self._events_key = None
+        self._n = 0
+        if rank is None:
+            ids = (c_int * len(devices))(*devices)
+            rc = self._lib.sthk_create(ids, len(devices), byref(self._h))
+        else:
+            buf = None
+            if world > 1:
+                if nccl_id is None or len(nccl_id) != _lib.NCCL_ID_BYTES:
+                    raise ValueError("nccl_id must be the 128-byte id from rank 0")
+                buf = ctypes.create_string_buffer(bytes(nccl_id), _lib.NCCL_ID_BYTES)
+            rc = self._lib.sthk_create_rank(int(devices[0]), int(rank), int(world),
+                                            buf, byref(self._h))
+        if rc != _lib.STHK_OK:
+            msg = self._lib.sthk_last_error(None).decode()
+            raise (ValueError if rc == _lib.STHK_EINVAL else EngineError)(
+                f"sthk_create failed ({rc}): {msg}")
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = _lib.load_library()
+        buf = ctypes.create_string_buffer(_lib.NCCL_ID_BYTES)
+        rc = lib.sthk_nccl_unique_id(buf)
+        if rc != _lib.STHK_OK:
+            raise EngineError(f"sthk_nccl_unique_id failed ({rc})")
+        return buf.raw
+
+    # -- lifecycle ---------------------------------------------------------
+    def close(self) -> None:
+        if self._h:
+            self._lib.sthk_destroy(self._h)
+            self._h = c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- helpers -----------------------------------------------------------
+    def _check(self, rc: int, what: str) -> None:
+        if rc == _lib.STHK_OK:
+            return
+        msg = self._lib.sthk_last_error(self._h).decode()
+        if rc == _lib.STHK_EINVAL:
+            raise ValueError(msg)
+        raise EngineError(f"{what} failed ({rc}): {msg}")
+
+    @property
+    def handle(self) -> c_void_p:
+        return self._h
+
+    # -- C ABI wrappers ----------------------------------------------------
+    def load_events(self, x, y, t, window_end: float) -> None:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        t = np.ascontiguousarray(t, dtype=np.float64)
+        n = t.size
+        if x.size != n or y.size != n:
+            raise ValueError("EventSet: coordinate/time length mismatch")
+        self._check(self._lib.sthk_load_events(self._h, _dptr(x), _dptr(y), _dptr(t), n,
+                                               float(window_end)), "sthk_load_events")
+        self._n = n
+        self._events_key = None
+
+    def load(self, events: EventSet) -> None:
+        """Load an EventSet unless it is already resident (identity cache)."""
+        key = (id(events), events.size(), events.windowEnd())
+        if self._events_key == key:
+            return
+        self.load_events(events.xs(), events.ys(), events.ts(), events.windowEnd())
+        self._events_key = key
+        self._events_ref = events  # keep alive so id() stays unique
+
+    def set_params(self, params) -> None:
+        p = params.as_array() if isinstance(params, Params) else np.asarray(params, np.float64)
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        self._check(self._lib.sthk_set_params(self._h, _dptr(p)), "sthk_set_params")
+
+    def loglik(self, per_event: bool = False):
+        ll, ok = c_double(), c_int()
+        pe = np.zeros(self._n) if per_event else None
+        self._check(self._lib.sthk_loglik(self._h, byref(ll), byref(ok),
+                                          _dptr(pe) if pe is not None else None), "sthk_loglik")
+        return ll.value, bool(ok.value), pe
+
+    def loglik_grad(self, per_event: bool = False):
+        ll, ok = c_double(), c_int()
+        g = np.zeros(6)
+        pe = np.zeros(self._n) if per_event else None
+        self._check(self._lib.sthk_loglik_grad(self._h, byref(ll), byref(ok), _dptr(g),
+                                               _dptr(pe) if pe is not None else None),
+                    "sthk_loglik_grad")
+        return ll.value, bool(ok.value), g, pe
+
+    def loglik_batch(self, params_list, grad: bool = False):
+        P = np.ascontiguousarray(np.asarray(params_list, dtype=np.float64).reshape(-1, 6))
+        m = P.shape[0]
+        ll = np.zeros(m)
+        ok = np.zeros(m, dtype=np.int32)
+        g = np.zeros((m, 6)) if grad else None
+        self._check(self._lib.sthk_loglik_batch(
+            self._h, _dptr(P) if m else None, m, _dptr(ll),
+            ok.ctypes.data_as(ctypes.POINTER(c_int)), _dptr(g) if grad else None),
+            "sthk_loglik_batch")
+        return ll, ok.astype(bool), g
+
+    def enqueue(self, grad: bool = True, per_event: bool = False) -> None:
+        self._check(self._lib.sthk_enqueue(self._h, int(grad), int(per_event)), "sthk_enqueue")
+
+    def result(self, per_event: bool = False):
+        ll, ok = c_double(), c_int()
+        g = np.zeros(6)
+        pe = np.zeros(self._n) if per_event else None
+        self._check(self._lib.sthk_result(self._h, byref(ll), byref(ok), _dptr(g),
+                                          _dptr(pe) if pe is not None else None), "sthk_result")
+        return ll.value, bool(ok.value), g, pe
+
+    def set_timing(self, on: bool) -> None:
+        self._check(self._lib.sthk_set_timing(self._h, int(on)), "sthk_set_timing")
+
+    def set_dense(self, on: bool) -> None:
+        self._check(self._lib.sthk_set_dense(self._h, int(on)), "sthk_set_dense")
+
+    def stats(self) -> dict:
+        s = _lib.StatsStruct()
+        self._check(self._lib.sthk_get_stats(self._h, byref(s)), "sthk_get_stats")
+        return {name: getattr(s, name) for name, _ in _lib.StatsStruct._fields_}
+
+    def stream(self, slot: int = 0) -> int:
+        p = c_void_p()
+        self._check(self._lib.sthk_get_stream(self._h, slot, byref(p)), "sthk_get_stream")
+        return p.value or 0
+
+
+_DEFAULT: Optional[Engine] = None
+_DEFAULT_LOCK = threading.Lock()
+
+
+def default_engine() -> Engine:
+    global _DEFAULT
+    with _DEFAULT_LOCK:
+        if _DEFAULT is None:
+            _DEFAULT = Engine((0,))
+        return _DEFAULT
+
+
+def logLikelihood(events: EventSet, params: Params, backend=None,
+                  keepPerEvent: bool = False, engine: Optional[Engine] = None) -> LikelihoodResult:
+    """likelihood.hpp:24-26. `backend` is accepted for signature parity and
+    ignored (the device engine replaces the reference's CPU backends)."""
+    params.validate()
+    eng = engine or default_engine()
+    with eng._lock:
+        eng.load(events)
+        eng.set_params(params)
+        ll, ok, pe = eng.loglik(per_event=keepPerEvent)
+    return LikelihoodResult(ll, ok, pe if keepPerEvent else np.zeros(0))
+
+
+def logLikelihoodGradient(events: EventSet, params: Params, backend=None,
+                          keepPerEvent: bool = False, engine: Optional[Engine] = None):
+    """Log-likelihood plus d logLik / d params in Params order
+    (mu0, tauX, tauT, theta, omega, h). grad is NaN when valid is False."""
+    params.validate()
+    eng = engine or default_engine()
+    with eng._lock:
+        eng.load(events)
+        eng.set_params(params)
+        ll, ok, g, pe = eng.loglik_grad(per_event=keepPerEvent)
+    return LikelihoodResult(ll, ok, pe if keepPerEvent else np.zeros(0)), g
+
+
+def logLikelihoodBatch(events: EventSet, paramsList, backend=None, keepPerEvent: bool = False,
+                       engine: Optional[Engine] = None):
+    """likelihood.cpp:57-75: elementwise identical to repeated calls."""
+    if len(paramsList) == 0:
+        raise ValueError("logLikelihoodBatch: empty parameter list")
+    out = []
+    for i, p in enumerate(paramsList):
+        try:
+            out.append(logLikelihood(events, p, backend, keepPerEvent, engine))
+        except ValueError as e:
+            raise ValueError(f"logLikelihoodBatch: entry {i}: {e}") from None
+    return out
+
+
+log_likelihood = logLikelihood
+log_likelihood_gradient = logLikelihoodGradient

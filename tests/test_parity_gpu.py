@@ -1,0 +1,98 @@
+"""GPU parity: the sm_100a engine vs the long-double oracle and the verbatim
+reference engine (oracle/_ref). Tolerances from BASELINE.json north_star:
+<= 1e-10 relative on loglik, <= 1e-8 per gradient component (scale-aware
+norm sum_i |d l_i / d p_k| near stationary points)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle_glue as og
+import paper_2005_10123_b200 as pk
+
+pytestmark = pytest.mark.gpu
+
+LL_TOL = 1e-10
+G_TOL = 1e-8
+
+
+def _rand_params(rng):
+    return pk.Params(rng.uniform(0.3, 2.0), rng.uniform(0.5, 2.0), rng.uniform(2.0, 20.0),
+                     rng.uniform(0.05, 0.8), rng.uniform(0.3, 3.0), rng.uniform(0.1, 1.0))
+
+
+def _check(engine, ev, p, ll_tol=LL_TOL, g_tol=G_TOL):
+    r, g = pk.logLikelihoodGradient(ev, p, engine=engine)
+    o = og.oracle_loglik_grad(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), p.as_array())
+    assert r.valid == o["valid"]
+    if not o["valid"]:
+        assert r.logLik == -math.inf
+        return r, g, o
+    assert abs(r.logLik - o["loglik"]) <= ll_tol * abs(o["loglik"]), (r.logLik, o["loglik"])
+    # scale-aware gradient norm (|grad| itself can be ~0 near the MLE)
+    scale = np.maximum(np.abs(o["grad"]), 1e-12 * max(1.0, abs(o["loglik"])))
+    err = np.abs(g - o["grad"]) / scale
+    assert np.all(err <= g_tol), (g, o["grad"], err)
+    return r, g, o
+
+
+def test_single_event_closed_form(engine):
+    # test_likelihood.cpp:42-56
+    ev = pk.EventSet([0.0], [0.0], [1.0], 1.0)
+    p = pk.Params(1, 1, 1, 1, 1, 1)
+    r = pk.logLikelihood(ev, p, engine=engine)
+    assert r.valid
+    assert abs(r.logLik - (-3.0981603456825612)) <= 1e-13
+
+
+def test_five_event_fixture(engine):
+    # test_likelihood.cpp:84-104
+    ev = pk.EventSet([0.1, 0.9, -0.4, 0.2, 1.1], [-0.2, 0.3, 0.5, 0.9, -0.8],
+                     [0.4, 1.1, 1.9, 3.0, 4.2], 5.0)
+    p = pk.Params(0.6, 0.9, 3.0, 0.5, 1.1, 0.35)
+    r, g, o = _check(engine, ev, p)
+    assert abs(r.logLik - (-19.396372326920137)) <= 1e-10 * 19.4
+
+
+def test_random_instances(engine):
+    # test_likelihood.cpp:106-121 shape: N in {2,3,10,100}, 8 reps each
+    rng = np.random.default_rng(2024)
+    inst = 0
+    for n in (2, 3, 10, 100):
+        for _ in range(8):
+            ev = pk.generateBenchmarkCloud(n, pk.SimWindow(0, 4, 0, 4, 60), 1000 + inst)
+            _check(engine, ev, _rand_params(rng))
+            inst += 1
+
+
+@pytest.mark.parametrize("n", [127, 128, 129, 1000, 4099])
+def test_tile_edges(engine, n):
+    ev = pk.generateBenchmarkCloud(n, pk.SimWindow(0, 4, 0, 4, 60), n)
+    _check(engine, ev, pk.Params(0.6, 0.9, 3.0, 0.5, 1.1, 0.35))
+
+
+def test_dc_shaped_culling_exact(engine):
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=6000)
+    for p in (pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695), pk.Params(1, 1.6, 14, 0.1, 1, 1)):
+        engine.load(ev)
+        engine.set_params(p)
+        engine.set_dense(False)
+        a = engine.loglik_grad()
+        engine.set_dense(True)
+        b = engine.loglik_grad()
+        engine.set_dense(False)
+        assert a[0] == b[0] and np.array_equal(a[2], b[2])
+        _check(engine, ev, p)
+
+
+def test_matches_reference_engine(engine):
+    if not og.ref_available():
+        pytest.skip("oracle/_ref not built")
+    ev = pk.generateBenchmarkCloud(1000, pk.SimWindow(0, 4, 0, 4, 60), 1000)
+    p = pk.Params(0.6, 0.9, 3.0, 0.5, 1.1, 0.35)
+    ref, ok, _ = og.ref_loglik(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), p.as_array(), 4, 8)
+    r = pk.logLikelihood(ev, p, engine=engine)
+    assert ok and r.valid
+    assert abs(r.logLik - ref) <= LL_TOL * abs(ref)
