@@ -44,7 +44,7 @@ double oracle_normal_cdf(double z) { return (double)cdfl((long double)z); }
 int oracle_loglik_grad(const double* x, const double* y, const double* t,
                        int64_t n, double window_end, const double* p,
                        int threads, double* loglik, int* valid, double* grad,
-                       double* per_event, double* sums) {
+                       double* per_event, double* sums, double* grad_abs) {
   if (!params_valid(p) || n < 1) return 1;
   const long double mu0 = p[0], tx = p[1], tt = p[2], th = p[3], om = p[4], h = p[5];
   const long double cB = powl(2.0L * kPiL, -1.5L) / (tx * tx * tt);
@@ -113,9 +113,14 @@ int oracle_loglik_grad(const double* x, const double* y, const double* t,
   }
 
   long double tot[7] = {0, 0, 0, 0, 0, 0, 0};
+  long double absum[6] = {0, 0, 0, 0, 0, 0};
   for (int64_t i = 0; i < n; ++i) {
     for (int k = 0; k < 7; ++k) tot[k] += row[8 * i + k];
+    for (int k = 0; k < 6; ++k) absum[k] += fabsl(row[8 * i + 1 + k]);
     if (per_event) per_event[i] = (double)row[8 * i];
+  }
+  if (grad_abs) {
+    for (int k = 0; k < 6; ++k) grad_abs[k] = (double)absum[k];
   }
   free(row);
   const int ok = !bad && isfinite((double)tot[0]);

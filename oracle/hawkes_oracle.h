@@ -19,11 +19,14 @@ extern "C" {
  *   per_event[n]    : log(lambda_i) - Lambda_i, 0 for degenerate rows (NULL ok).
  *   sums[6*n]       : per-row raw sums (S_B,S_Br,S_Bt,S_T,S_Tt,S_Tr), row-major
  *                     by row (NULL ok) -- for kernel-level diagnostics.
+ *   grad_abs[6]     : sum_i |d l_i / d p[k]|, the scale of each gradient
+ *                     component's summands (NULL ok); the parity tolerance
+ *                     near stationary points is relative to it.
  * threads <= 0 uses all OpenMP threads. Returns 0, or 1 on invalid params. */
 int oracle_loglik_grad(const double* x, const double* y, const double* t,
                        int64_t n, double window_end, const double* p,
                        int threads, double* loglik, int* valid, double* grad,
-                       double* per_event, double* sums);
+                       double* per_event, double* sums, double* grad_abs);
 
 /* Long-double Phi / phi (erfc-based), for known-answer checks. */
 double oracle_normal_cdf(double z);

@@ -45,7 +45,7 @@ def oracle_lib():
         lib = ctypes.CDLL(path)
         lib.oracle_loglik_grad.restype = c_int
         lib.oracle_loglik_grad.argtypes = [_D, _D, _D, c_int64, c_double, _D, c_int, _D,
-                                           POINTER(c_int), _D, _D, _D]
+                                           POINTER(c_int), _D, _D, _D, _D]
         lib.oracle_normal_cdf.restype = c_double
         lib.oracle_normal_cdf.argtypes = [c_double]
         _ORACLE = lib
@@ -93,11 +93,12 @@ def oracle_loglik_grad(x, y, t, window_end, params, threads=0, per_event=False, 
     g = np.zeros(6)
     pe = np.zeros(n) if per_event else None
     sm = np.zeros(6 * n) if sums else None
+    ga = np.zeros(6)
     rc = lib.oracle_loglik_grad(_d(x), _d(y), _d(t), n, float(window_end), _d(p), threads,
-                                byref(ll), byref(ok), _d(g), _d(pe), _d(sm))
+                                byref(ll), byref(ok), _d(g), _d(pe), _d(sm), _d(ga))
     if rc != 0:
         raise ValueError("oracle: invalid params")
-    return dict(loglik=ll.value, valid=bool(ok.value), grad=g, per_event=pe,
+    return dict(loglik=ll.value, valid=bool(ok.value), grad=g, grad_abs=ga, per_event=pe,
                 sums=None if sm is None else sm.reshape(n, 6))
 
 

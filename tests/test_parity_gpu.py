@@ -29,10 +29,16 @@ def _check(engine, ev, p, ll_tol=LL_TOL, g_tol=G_TOL):
         assert r.logLik == -math.inf
         return r, g, o
     assert abs(r.logLik - o["loglik"]) <= ll_tol * abs(o["loglik"]), (r.logLik, o["loglik"])
-    # scale-aware gradient norm (|grad| itself can be ~0 near the MLE)
-    scale = np.maximum(np.abs(o["grad"]), 1e-12 * max(1.0, abs(o["loglik"])))
+    # scale-aware gradient norm: |g_k - g_k^oracle| <= tol * sum_i |d l_i/d p_k|
+    # (|g_k| itself can be ~0 near a stationary point)
+    scale = np.maximum(o["grad_abs"], 1e-300)
     err = np.abs(g - o["grad"]) / scale
     assert np.all(err <= g_tol), (g, o["grad"], err)
+    # plain per-component relative error wherever the component is not
+    # dominated by cancellation (|g_k| >= 1e-6 sum_i |d l_i / d p_k|)
+    well = np.abs(o["grad"]) >= 1e-6 * o["grad_abs"]
+    rel = np.abs(g - o["grad"]) / np.maximum(np.abs(o["grad"]), 1e-300)
+    assert np.all(rel[well] <= g_tol), (g, o["grad"], rel)
     return r, g, o
 
 
