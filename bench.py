@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Benchmark: spatiotemporal-Hawkes log-likelihood + full 6-parameter gradient
+on B200 (BASELINE.json metric: "loglik+gradient evals/sec and
+pair-interactions/sec at N=85k, 1/2/4/8 B200 vs CPU").
+
+Workload (BASELINE.json configs[1], SURVEY.md §8 d1 "C2"): N=85,000
+DC-gunshot-shaped events from the reference's cluster simulator
+(simulateClusterProcess, Rng(2005), rate 0.053217 on 15x15 km x 4750 d,
+first 85,000 in time order), evaluated at Theta_post=(0.66, 1.6, 14, 0.344,
+1440, 0.0695). One step = one loglik+gradient evaluation (all N^2 pairs
+accounted for; provably-zero tiles skipped exactly). Theta_init from the MH
+sampler is reported as a secondary line.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): target rows are partitioned
+across ranks (cost-balanced, 1024-row blocks) and the block partials are
+combined with one NCCL all-reduce inside the engine: strong scaling of a
+single evaluation, timed as the max over ranks.
+
+--impl reference times the reference's own multithreaded SIMD CPU engine
+(hawkes::logLikelihood compiled verbatim from /root/reference into
+oracle/_ref) on all host cores, log-likelihood only (the reference has no
+gradient), on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+N_EVENTS = 85_000
+THETA_POST = [0.66, 1.6, 14.0, 0.344, 1440.0, 0.0695]
+THETA_INIT = [1.0, 1.6, 14.0, 0.1, 1.0, 1.0]
+SIM_TRUTH = [1.0, 1.6, 14.0, 0.344, 1440.0, 0.0695]
+SIM_WINDOW = (0.0, 15.0, 0.0, 15.0, 4750.0)
+SIM_RATE = 0.053217
+SIM_SEED = 2005
+METRIC = "loglik+gradient evals/sec and pair-interactions/sec at N=85k"
+# counted flops per evaluated pair (exp = 29 flops)
+FLOPS_ANY, FLOPS_BG_GRAD, FLOPS_TR_GRAD = 6, 38, 38
+NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 64 DFMA/clk x 2 x 1.965 GHz
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def make_workload():
+    import paper_2005_10123_b200 as pk
+    ev, _ = pk.simulateClusterProcess(pk.Params(*SIM_TRUTH), pk.SimWindow(*SIM_WINDOW), SIM_RATE,
+                                      SIM_SEED, keep=N_EVENTS)
+    return ev
+
+
+def config_dict(world):
+    return {
+        "workload": "C2: N=85,000 DC-shaped simulated events (simulateClusterProcess Rng(2005)), "
+                    "loglik + 6-parameter gradient, FP64",
+        "n_events": N_EVENTS,
+        "theta": THETA_POST,
+        "parallelism": f"row-partition x{world} + NCCL all-reduce" if world > 1 else "1 GPU",
+        "l2": "flushed between timed steps (256 MiB write); inputs (2 MB) are L2-resident within a step",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        self.path = f"/tmp/sthk_clocks_{os.getpid()}.csv"
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons, power = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the verbatim reference CPU engine on rank 0."""
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_glue as og
+    ev = make_workload()
+    cores = os.cpu_count() or 1
+    lanes = 8 if og.has_avx512() else 4
+    base = {"impl": "reference", "metric": METRIC, "unit": "evals/s", "n_gpus": world,
+            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(world), "vs_baseline": None}
+    if not og.ref_available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
+        return
+    x, y, t, T = ev.xs(), ev.ys(), ev.ts(), ev.windowEnd()
+    # bounded sample: full N=85k evaluations, step count capped at ~150 s
+    t0 = time.perf_counter()
+    og.ref_loglik(x, y, t, T, THETA_POST, threads=cores, lanes=lanes)
+    one = time.perf_counter() - t0
+    steps = max(3, min(args.steps, int(150.0 / max(one, 1e-3))))
+    warm = max(0, min(args.warmup, 1) - 1)  # the probe above is the first warm-up
+    for _ in range(warm):
+        og.ref_loglik(x, y, t, T, THETA_POST, threads=cores, lanes=lanes)
+    times, vals = [], []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        ll, ok, _ = og.ref_loglik(x, y, t, T, THETA_POST, threads=cores, lanes=lanes)
+        times.append(time.perf_counter() - t0)
+        vals.append(ll)
+    assert len(set(vals)) == 1, "reference drift across repeats (bench.cpp:39-43 guard)"
+    total = sum(times)
+    v = steps / total
+    sample = (f"{steps} full N=85,000 log-likelihood evaluations (reference threads{cores}+simd{lanes}, "
+              f"no gradient: the reference has none)")
+    out = dict(base)
+    out.update({
+        "value": v, "steps": steps, "warmup": warm + 1, "ms_per_step": 1e3 * total / steps,
+        "pair_interactions_per_s": v * N_EVENTS ** 2,
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "reference",
+                         "sample": sample, "hardware": og.ref_hardware()},
+        "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "loglik": vals[0], "steps_requested": args.steps,
+        "gpu_launches": 0,
+    })
+    print(json.dumps(out))
+
+
+def cpu_baseline_probe():
+    """Reference CPU engine on this host's cores, a bounded sample (rank 0, N=1)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_glue as og
+    if not og.ref_available():
+        return {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    ev = make_workload()
+    cores = os.cpu_count() or 1
+    lanes = 8 if og.has_avx512() else 4
+    x, y, t, T = ev.xs(), ev.ys(), ev.ts(), ev.windowEnd()
+    og.ref_loglik(x, y, t, T, THETA_POST, threads=cores, lanes=lanes)  # warm-up
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < 3 or (time.perf_counter() - t_start < 10.0 and len(times) < 10):
+        t0 = time.perf_counter()
+        og.ref_loglik(x, y, t, T, THETA_POST, threads=cores, lanes=lanes)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return {"value": 1.0 / med, "unit": "evals/s", "cores": cores, "kind": "reference",
+            "sample": f"{len(times)} full N=85,000 loglik evals (threads{cores}+simd{lanes}, "
+                      "median; loglik only, the reference has no gradient)",
+            "hardware": og.ref_hardware(), "s_per_eval": med}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2005_10123_b200 as pk
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        obj = [pk.Engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        eng = pk.Engine((local_rank,), rank=rank, world=world, nccl_id=obj[0])
+    else:
+        eng = pk.Engine((local_rank,))
+
+    ev = make_workload()
+    n = ev.size()
+    # pinned host copies for the end-to-end arm
+    hx = torch.from_numpy(np.array(ev.xs())).pin_memory()
+    hy = torch.from_numpy(np.array(ev.ys())).pin_memory()
+    ht = torch.from_numpy(np.array(ev.ts())).pin_memory()
+    eng.load_events(hx.numpy(), hy.numpy(), ht.numpy(), ev.windowEnd())
+    eng.set_timing(True)
+    stream = torch.cuda.ExternalStream(eng.stream(0))
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        tt = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    def timed_device(theta, steps, warmup):
+        eng.set_params(theta)
+        for _ in range(warmup):
+            eng.loglik_grad()
+        barrier()
+        pair_ms, evals_ms, dev_ms = [], [], []
+        st = None
+        for _ in range(steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()  # untimed L2 flush between steps
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            eng.set_params(theta)
+            eng.enqueue(grad=True)
+            with torch.cuda.stream(stream):
+                e1.record(stream)
+            res = eng.result()
+            e1.synchronize()
+            dev_ms.append(e0.elapsed_time(e1))
+            st = eng.stats()
+            pair_ms.append(st["pair_kernel_ms"])
+            evals_ms.append(st["eval_ms"])
+        barrier()
+        tot_ms = max_over_ranks(sum(dev_ms))
+        return dict(total_ms=tot_ms, pair_ms=statistics.mean(pair_ms),
+                    pair_ms_max=max_over_ranks(statistics.mean(pair_ms)),
+                    eval_ms=statistics.mean(evals_ms), stats=st, loglik=res[0], valid=res[1],
+                    grad=list(res[2]))
+
+    # FP64 roofline denominator, measured on this device
+    peak_best, peak_mean = eng_peak(pk, local_rank)
+
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    main_run = timed_device(THETA_POST, args.steps, args.warmup)
+    clocks = sampler.stop() if sampler else None
+    sec_run = timed_device(THETA_INIT, max(10, args.steps // 5), 3)
+
+    # end to end through the public API: pinned host inputs -> H2D -> eval -> D2H
+    def e2e(theta, steps):
+        for _ in range(2):
+            eng.load_events(hx.numpy(), hy.numpy(), ht.numpy(), ev.windowEnd())
+            eng.set_params(theta)
+            eng.loglik_grad()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            eng.load_events(hx.numpy(), hy.numpy(), ht.numpy(), ev.windowEnd())
+            eng.set_params(theta)
+            eng.loglik_grad()
+        el = time.perf_counter() - t0
+        barrier()
+        return max_over_ranks(el)
+
+    e2e_s = e2e(THETA_POST, args.steps)
+
+    if rank != 0:
+        eng.close()
+        dist.destroy_process_group()
+        return
+
+    K = args.steps
+    total_ms = main_run["total_ms"]
+    ms_step = total_ms / K
+    evals_s = 1e3 / ms_step
+    st = main_run["stats"]
+    # counts are this rank's pairs; flops of the local pair-kernel launch
+    flops_launch = (FLOPS_ANY * st["pairs_any"] + FLOPS_BG_GRAD * st["pairs_bg"]
+                    + FLOPS_TR_GRAD * st["pairs_tr"])
+    achieved = flops_launch / (main_run["pair_ms"] * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "pair_kernel_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    st2 = sec_run["stats"]
+    flops2 = (FLOPS_ANY * st2["pairs_any"] + FLOPS_BG_GRAD * st2["pairs_bg"]
+              + FLOPS_TR_GRAD * st2["pairs_tr"])
+    out = {
+        "metric": METRIC,
+        "value": evals_s,
+        "unit": "evals/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (reference simulator restated bit-exactly)",
+        "config": config_dict(world),
+        "pair_interactions_per_s": evals_s * float(n) * float(n),
+        "pairs_evaluated_per_eval": {"bg": st["pairs_bg"], "trigger": st["pairs_tr"],
+                                     "any": st["pairs_any"], "dense": st["pairs_dense"]},
+        "loglik": main_run["loglik"],
+        "grad": main_run["grad"],
+        "e2e": {"value": K / e2e_s, "unit": "evals/s",
+                "h2d_bytes_per_step": 3 * 8 * n,
+                "d2h_bytes_per_step": 8 * 8 + 3 * 8,
+                "path": "Engine.load_events(pinned x,y,t) + set_params + loglik_grad (C ABI)"},
+        "gpu_launches": 5 * K,
+        "roofline": {
+            "bound": "fp64",
+            "kernel": "pair_kernel<GRAD=true>",
+            "achieved": achieved,
+            "peak": peak_best,
+            "unit": "TFLOP/s",
+            "frac": achieved / peak_best if peak_best else None,
+            "peak_source": "measured in-run DFMA probe (sthk_measure_fp64_peak); "
+                           "MEASURED_PEAKS.json has no FP64 entry",
+            "frac_of_nominal_37.2": achieved / NOMINAL_FP64_TFLOPS,
+            "flops_per_launch": flops_launch,
+            "flop_model": "6*P_any + 38*P_bg + 38*P_tr (SURVEY.md §8 d3; exp counted as 29)",
+            "pair_kernel_ms": main_run["pair_ms"],
+            "pair_kernel_share_of_step": main_run["pair_ms"] / ms_step,
+            "traffic": traffic,
+        },
+        "secondary": {
+            "theta_init": {
+                "theta": THETA_INIT,
+                "evals_per_s": 1e3 * max(10, K // 5) / sec_run["total_ms"],
+                "pair_kernel_ms": sec_run["pair_ms"],
+                "roofline_achieved_tflops": flops2 / (sec_run["pair_ms"] * 1e-3) / 1e12,
+                "pairs_evaluated": {"bg": st2["pairs_bg"], "trigger": st2["pairs_tr"]},
+                "loglik": sec_run["loglik"],
+            },
+        },
+        "clocks": clocks,
+        "fp64_peak_tflops": {"best": peak_best, "mean": peak_mean},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline_probe()
+        out["cpu_baseline"] = cb
+        if cb.get("value"):
+            out["speedup_vs_cpu_baseline"] = {"value": evals_s / cb["value"],
+                                              "e2e": (K / e2e_s) / cb["value"]}
+    print(json.dumps(out))
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def eng_peak(pk, dev):
+    import ctypes
+    lib = pk.load_library()
+    best, mean = ctypes.c_double(), ctypes.c_double()
+    rc = lib.sthk_measure_fp64_peak(dev, 10, ctypes.byref(best), ctypes.byref(mean))
+    if rc != 0:
+        return None, None
+    return best.value, mean.value
+
+
+if __name__ == "__main__":
+    main()

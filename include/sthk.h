@@ -117,6 +117,11 @@ int sthk_get_stream(sthk_engine* e, int slot, void** stream);
  * dense pair set (results are bitwise identical either way). */
 int sthk_set_dense(sthk_engine* e, int dense);
 
+/* DFMA throughput probe on `device` (roofline denominator for the FP64
+ * pair kernels): best and mean TFLOP/s over `reps` timed launches. */
+int sthk_measure_fp64_peak(int device, int reps, double* tflops_best,
+                           double* tflops_mean);
+
 const char* sthk_last_error(const sthk_engine* e);
 const char* sthk_version(void);
 

@@ -17,7 +17,8 @@ _LIB = None
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "libsthk.so")
+    # STHK_LIB overrides the in-tree library (kernel-variant experiments only)
+    return os.environ.get("STHK_LIB") or os.path.join(_HERE, "libsthk.so")
 
 
 class StatsStruct(ctypes.Structure):
@@ -56,6 +57,7 @@ SIGNATURES = [
     ("sthk_get_stats", c_int, [c_void_p, POINTER(StatsStruct)]),
     ("sthk_get_stream", c_int, [c_void_p, c_int, POINTER(c_void_p)]),
     ("sthk_set_dense", c_int, [c_void_p, c_int]),
+    ("sthk_measure_fp64_peak", c_int, [c_int, c_int, _DPTR, _DPTR]),
     ("sthk_last_error", c_char_p, [c_void_p]),
     ("sthk_version", c_char_p, []),
     ("sthk_sim_cloud", c_int, [c_int64, _DPTR, c_uint64, _DPTR, _DPTR, _DPTR, _DPTR]),

@@ -77,6 +77,8 @@ struct Slot {
   ncclComm_t comm = nullptr;
   double *x = nullptr, *y = nullptr, *t = nullptr;
   size_t x_cap = 0, y_cap = 0, t_cap = 0;
+  double4* tile_box = nullptr;
+  size_t box_cap = 0;
   int2* ranges = nullptr;
   size_t ranges_cap = 0;
   int* counts = nullptr;
@@ -148,7 +150,7 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.items), static_cast<void*>(s.scalars),
                   static_cast<void*>(s.partial), static_cast<void*>(s.block_partial),
                   static_cast<void*>(s.out), static_cast<void*>(s.per_event),
-                  static_cast<void*>(s.pair_counts)}) {
+                  static_cast<void*>(s.pair_counts), static_cast<void*>(s.tile_box)}) {
     if (p) cudaFree(p);
   }
   for (void* p : {static_cast<void*>(s.h_out), static_cast<void*>(s.h_counts),
@@ -218,10 +220,12 @@ EvalPlan make_plan(const sthk_engine& e, int shards) {
   const double* p = e.p;
   double dB, dT;
   culling_windows(p, dB, dT);
-  pl.k.cx = -0.5 / (p[1] * p[1]);
-  pl.k.ct = -0.5 / (p[2] * p[2]);
-  pl.k.ch = -0.5 / (p[5] * p[5]);
-  pl.k.nom = -p[4];
+  // exponent constants in L units (x 256/ln2), see exp_l (sthk_device.cuh)
+  const long double L = 256.0L / 0.693147180559945309417232121458176568L;
+  pl.k.cxL = static_cast<double>(-0.5L * L / (static_cast<long double>(p[1]) * p[1]));
+  pl.k.ctL = static_cast<double>(-0.5L * L / (static_cast<long double>(p[2]) * p[2]));
+  pl.k.chL = static_cast<double>(-0.5L * L / (static_cast<long double>(p[5]) * p[5]));
+  pl.k.nomL = static_cast<double>(-L * p[4]);
   const double inf = std::numeric_limits<double>::infinity();
   pl.k.dB = e.dense ? inf : dB;
   pl.k.dT = e.dense ? inf : dT;
@@ -333,6 +337,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
       qa.x = s.x;
       qa.y = s.y;
       qa.t = s.t;
+      qa.tile_box = s.tile_box;
       qa.n = e.n;
       qa.npad = e.npad;
       qa.k = pl.k;
@@ -570,22 +575,29 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
     if (e->pending) collect(*e, nullptr, nullptr, nullptr, nullptr);
     const int64_t npad = (n + kTM - 1) / kTM * kTM;
     e->ht.assign(t, t + n);
-    for (auto& v : e->ht) v = v + 0.0;  // canonicalise -0.0 (mask compares bits)
-    std::vector<double> hx(npad, 0.0), hy(npad, 0.0), htp(npad, e->ht[n - 1]);
-    std::memcpy(hx.data(), x, sizeof(double) * n);
-    std::memcpy(hy.data(), y, sizeof(double) * n);
-    std::memcpy(htp.data(), e->ht.data(), sizeof(double) * n);
+    // Straight from the caller's buffers (pinned or pageable) to every
+    // device; the pad tail is zero and is never read as a source (stage
+    // loops are bounded by n) nor reported as a target.
+    const size_t bytes = sizeof(double) * static_cast<size_t>(n);
+    const size_t pad = sizeof(double) * static_cast<size_t>(npad - n);
     for (Slot& s : e->slots) {
       set_dev(s);
       dev_grow(s.x, s.x_cap, static_cast<size_t>(npad));
       dev_grow(s.y, s.y_cap, static_cast<size_t>(npad));
       dev_grow(s.t, s.t_cap, static_cast<size_t>(npad));
-      ck(cudaMemcpyAsync(s.x, hx.data(), sizeof(double) * npad, cudaMemcpyHostToDevice, s.stream),
-         "H2D");
-      ck(cudaMemcpyAsync(s.y, hy.data(), sizeof(double) * npad, cudaMemcpyHostToDevice, s.stream),
-         "H2D");
-      ck(cudaMemcpyAsync(s.t, htp.data(), sizeof(double) * npad, cudaMemcpyHostToDevice, s.stream),
-         "H2D");
+      ck(cudaMemcpyAsync(s.x, x, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
+      ck(cudaMemcpyAsync(s.y, y, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
+      ck(cudaMemcpyAsync(s.t, t, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
+      if (pad) {
+        ck(cudaMemsetAsync(s.x + n, 0, pad, s.stream), "memset");
+        ck(cudaMemsetAsync(s.y + n, 0, pad, s.stream), "memset");
+        ck(cudaMemsetAsync(s.t + n, 0, pad, s.stream), "memset");
+      }
+      dev_grow(s.tile_box, s.box_cap, static_cast<size_t>(npad / kTS));
+      ck(sthk::launch_tile_boxes(s.x, s.y, n, s.tile_box, s.stream), "tile boxes");
+    }
+    for (Slot& s : e->slots) {
+      set_dev(s);
       ck(cudaStreamSynchronize(s.stream), "H2D");
     }
     e->n = n;

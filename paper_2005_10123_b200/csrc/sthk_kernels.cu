@@ -34,6 +34,10 @@
 #include "sthk_device.cuh"
 #include "sthk_kernels.cuh"
 
+#ifndef STHK_PAIR_MINB
+#define STHK_PAIR_MINB 5  // resident pair CTAs per SM the register budget targets
+#endif
+
 namespace sthk {
 
 namespace {
@@ -127,17 +131,18 @@ __global__ void __launch_bounds__(1024) plan_items_kernel(const PlanArgs a) {
 // ---------------------------------------------------------------------------
 // TR: 0 = no trigger term, 1 = trigger without mask (every source strictly
 // earlier than every target of the tile), 2 = trigger with the strict
-// t_src < t_tgt mask (kernels.hpp:99-100). Times are >= +0 (canonicalised on
-// load), so the mask compares their bit patterns as integers.
-template <bool GRAD, bool BG, int TR>
+// t_src < t_tgt mask (kernels.hpp:99-100), applied as a select so masked-out
+// lanes (whose exponent may be positive) contribute exactly +0.
+// CHECK = false when the stage's exponent lower bound proves no pair can
+// underflow, so exp_l may skip its flush test.
+template <bool GRAD, bool BG, int TR, bool CHECK>
 __device__ __forceinline__ void stage_loop(const double* __restrict__ sx,
                                            const double* __restrict__ sy,
                                            const double* __restrict__ st, int cnt,
                                            double xi, double yi, double ti,
                                            const PairConsts& k,
-                                           const double* __restrict__ tab,
+                                           const uint2* __restrict__ tab,
                                            double* acc) {
-  const long long tib = __double_as_longlong(ti);
 #pragma unroll 4
   for (int j = 0; j < cnt; ++j) {
     const double sj = st[j];
@@ -147,7 +152,7 @@ __device__ __forceinline__ void stage_loop(const double* __restrict__ sx,
     const double r2 = fma(dx, dx, dy * dy);
     if constexpr (BG) {
       const double dt2 = dt * dt;
-      const double e = fexp(fma(k.cx, r2, k.ct * dt2), tab);
+      const double e = exp_l<CHECK>(fma(k.cxL, r2, k.ctL * dt2), tab);
       acc[0] += e;
       if constexpr (GRAD) {
         acc[1] = fma(e, r2, acc[1]);
@@ -155,8 +160,8 @@ __device__ __forceinline__ void stage_loop(const double* __restrict__ sx,
       }
     }
     if constexpr (TR != 0) {
-      double e = fexp(fma(k.nom, dt, k.ch * r2), tab);
-      if constexpr (TR == 2) e = (__double_as_longlong(sj) < tib) ? e : 0.0;
+      double e = exp_l<CHECK>(fma(k.nomL, dt, k.chL * r2), tab);
+      if constexpr (TR == 2) e = (sj < ti) ? e : 0.0;
       if constexpr (GRAD) {
         acc[3] += e;
         acc[4] = fma(e, dt, acc[4]);
@@ -168,16 +173,33 @@ __device__ __forceinline__ void stage_loop(const double* __restrict__ sx,
   }
 }
 
+template <bool GRAD, bool CHECK>
+__device__ __forceinline__ void stage_dispatch(bool bg, int tr, const double* sx,
+                                               const double* sy, const double* st, int cnt,
+                                               double xi, double yi, double ti,
+                                               const PairConsts& k, const uint2* tab,
+                                               double* acc) {
+  if (bg) {
+    if (tr == 0) stage_loop<GRAD, true, 0, CHECK>(sx, sy, st, cnt, xi, yi, ti, k, tab, acc);
+    else if (tr == 1) stage_loop<GRAD, true, 1, CHECK>(sx, sy, st, cnt, xi, yi, ti, k, tab, acc);
+    else stage_loop<GRAD, true, 2, CHECK>(sx, sy, st, cnt, xi, yi, ti, k, tab, acc);
+  } else {
+    if (tr == 1) stage_loop<GRAD, false, 1, CHECK>(sx, sy, st, cnt, xi, yi, ti, k, tab, acc);
+    else if (tr == 2) stage_loop<GRAD, false, 2, CHECK>(sx, sy, st, cnt, xi, yi, ti, k, tab, acc);
+  }
+}
+
 template <bool GRAD>
-__global__ void __launch_bounds__(kTM, 4) pair_kernel(const PairArgs a) {
+__global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArgs a) {
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   __shared__ __align__(128) double s_src[2][3][kTS];
-  __shared__ double s_tab[64];
+  __shared__ uint2 s_tab[256];
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ int s_item[2];
 
   const int tid = threadIdx.x;
-  if (tid < 64) s_tab[tid] = kExpTable[tid];
+  s_tab[tid] = kExpTable[tid];
+  s_tab[tid + kTM] = kExpTable[tid + kTM];
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
@@ -204,6 +226,7 @@ __global__ void __launch_bounds__(kTM, 4) pair_kernel(const PairArgs a) {
     const double xi = a.x[row], yi = a.y[row], ti = a.t[row];
     const int64_t last = min(first + kTM, n) - 1;
     const double tmin = a.t[first], tmax = a.t[last];
+    const double4 bt = a.tile_box[tile];
     const int rows_real = static_cast<int>(last - first + 1);
 
     int s_begin = max(rg.x, chunk * a.sc);
@@ -234,30 +257,32 @@ __global__ void __launch_bounds__(kTM, 4) pair_kernel(const PairArgs a) {
         tma_load_1d(s_src[nb][1], a.y + s0n, kStageBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][2], a.t + s0n, kStageBytes, &s_bar[nb]);
       }
-      mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
-      phase ^= 1u << buf;
-
       const int64_t s0 = s_begin + static_cast<int64_t>(s) * kTS;
       const int cnt = static_cast<int>(min(static_cast<int64_t>(kTS), n - s0));
-      const double* sx = s_src[buf][0];
-      const double* sy = s_src[buf][1];
-      const double* st = s_src[buf][2];
-      const double smin = st[0], smax = st[cnt - 1];
+      const double4 bs = a.tile_box[s0 / kTS];
+      const double smin = a.t[s0], smax = a.t[s0 + cnt - 1];
 
       const bool bg = !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
       int tr;
       if (smin >= tmax || smax < tmin - a.k.dT) tr = 0;
       else if (smax < tmin) tr = 1;
       else tr = 2;
+      // exponent lower bounds over the (tile, stage) box pair
+      const double dxm = fmax(bt.y - bs.x, bs.y - bt.x);
+      const double dym = fmax(bt.w - bs.z, bs.w - bt.z);
+      const double r2m = dxm * dxm + dym * dym;
+      const double dtm = fmax(tmax - smin, smax - tmin);
+      const bool safe = (!bg || a.k.cxL * r2m + a.k.ctL * (dtm * dtm) > kSafeExpL) &&
+                        (!tr || a.k.nomL * dtm + a.k.chL * r2m > kSafeExpL);
 
-      if (bg) {
-        if (tr == 0) stage_loop<GRAD, true, 0>(sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
-        else if (tr == 1) stage_loop<GRAD, true, 1>(sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
-        else stage_loop<GRAD, true, 2>(sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
-      } else {
-        if (tr == 1) stage_loop<GRAD, false, 1>(sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
-        else if (tr == 2) stage_loop<GRAD, false, 2>(sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
-      }
+      mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+
+      const double* sx = s_src[buf][0];
+      const double* sy = s_src[buf][1];
+      const double* st = s_src[buf][2];
+      if (safe) stage_dispatch<GRAD, false>(bg, tr, sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
+      else stage_dispatch<GRAD, true>(bg, tr, sx, sy, st, cnt, xi, yi, ti, a.k, s_tab, acc);
       if (tid == 0) {
         const unsigned long long pr = static_cast<unsigned long long>(cnt) * rows_real;
         if (bg) cBg += pr;
@@ -276,6 +301,24 @@ __global__ void __launch_bounds__(kTM, 4) pair_kernel(const PairArgs a) {
     atomicAdd(&a.pair_counts[1], cTr);
     atomicAdd(&a.pair_counts[2], cAny);
   }
+}
+
+// Per 128-event tile bounding box of the (x, y) coordinates (params
+// independent; computed once per load). Feeds the no-underflow proofs.
+__global__ void tile_box_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                int64_t n, double4* box) {
+  const int64_t tile = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t first = tile * kTS;
+  if (first >= n) return;
+  const int64_t last = min(first + kTS, n);
+  double x0 = x[first], x1 = x0, y0 = y[first], y1 = y0;
+  for (int64_t i = first + 1; i < last; ++i) {
+    x0 = fmin(x0, x[i]);
+    x1 = fmax(x1, x[i]);
+    y0 = fmin(y0, y[i]);
+    y1 = fmax(y1, y[i]);
+  }
+  box[tile] = make_double4(x0, x1, y0, y1);
 }
 
 // ---------------------------------------------------------------------------
@@ -348,7 +391,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
       acc[2] += dl1 * inv;
       acc[3] += dl2 * inv - dL2;
       acc[4] += dl3 * inv + em1;
-      acc[5] += dl4 * inv - a.theta * D * (em1 + 1.0);
+      // exp(-omega D) directly: 1 + expm1 cancels when omega D is large
+      acc[5] += dl4 * inv - a.theta * D * exp(-a.omega * D);
       acc[6] += dl5 * inv;
     }
   }
@@ -393,6 +437,13 @@ __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict
 }
 
 }  // namespace
+
+cudaError_t launch_tile_boxes(const double* x, const double* y, int64_t n, double4* box,
+                              cudaStream_t stream) {
+  const int64_t ntiles = (n + kTS - 1) / kTS;
+  tile_box_kernel<<<static_cast<unsigned>((ntiles + 127) / 128), 128, 0, stream>>>(x, y, n, box);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
   const int ntiles = a.tile1 - a.tile0;

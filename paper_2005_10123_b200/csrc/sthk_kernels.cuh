@@ -16,16 +16,19 @@ constexpr int kNSumGrad = 6;  // S_B, S_Br, S_Bt, S_T, S_Tt, S_Tr
 constexpr int kNSumVal = 2;   // S_B, S_T
 constexpr int kNOut = 8;      // loglik, 6 gradient terms, degenerate-row count
 
-// Exponent cut used for exact culling: every pair whose time-only exponent
-// bound is below this value has fexp(...) == +0 exactly (fexp flushes below
-// -708.40), so skipping it leaves every sum bitwise unchanged.
+// Exponent cut (natural units) used for exact culling: every pair whose
+// time-only exponent bound is below -kCullExponent has exp_l(...) == +0
+// exactly (exp_l flushes below -708.40), so skipping it leaves every sum
+// bitwise unchanged.
 constexpr double kCullExponent = 709.0;
 
+// Exponent constants are pre-multiplied by kExpL = 256/ln2 ("L units", see
+// exp_l in sthk_device.cuh).
 struct PairConsts {
-  double cx;    // -1/(2 tauX^2)
-  double ct;    // -1/(2 tauT^2)
-  double ch;    // -1/(2 h^2)
-  double nom;   // -omega
+  double cxL;   // -L/(2 tauX^2)
+  double ctL;   // -L/(2 tauT^2)
+  double chL;   // -L/(2 h^2)
+  double nomL;  // -L omega
   double dB;    // background live iff |dt| <= dB   (inf when dense)
   double dT;    // trigger live iff 0 < dt <= dT    (inf when dense)
 };
@@ -49,6 +52,7 @@ struct PairArgs {
   const double* x;
   const double* y;
   const double* t;
+  const double4* tile_box;  // per 128-event tile: xmin, xmax, ymin, ymax
   int64_t n;
   int64_t npad;
   PairConsts k;
@@ -82,6 +86,8 @@ struct FinArgs {
 };
 
 // Launch wrappers (sthk_kernels.cu). All enqueue on `stream`.
+cudaError_t launch_tile_boxes(const double* x, const double* y, int64_t n, double4* box,
+                              cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_pairs(const PairArgs& a, bool grad, int grid, cudaStream_t stream);
 cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream);

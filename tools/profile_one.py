@@ -1,0 +1,16 @@
+"""Short driver for ncu captures: C2 workload, a few loglik+grad evaluations."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2005_10123_b200 as pk  # noqa: E402
+
+theta = bench.THETA_INIT if "--init" in sys.argv else bench.THETA_POST
+ev = bench.make_workload()
+e = pk.Engine((0,))
+e.load(ev)
+e.set_params(theta)
+for _ in range(5):
+    r = e.loglik_grad()
+print("loglik", r[0])
