@@ -116,6 +116,18 @@ int sthk_get_stream(sthk_engine* e, int slot, void** stream);
 /* Debug/testing knob: 0 = exact tile culling on (default), 1 = evaluate the
  * dense pair set (results are bitwise identical either way). */
 int sthk_set_dense(sthk_engine* e, int dense);
+/* Testing knob for the multi-device partition on one device: split the rows
+ * into k cost-balanced shards run one after another on the single device and
+ * combined exactly as the NCCL path combines them (k = 1: off). Results must
+ * be bitwise identical for every k. Single-device handles only. */
+int sthk_set_virtual_shards(sthk_engine* e, int k);
+
+/* Host-only planning (no device): the cost-balanced row partition the engine
+ * uses for `shards` devices/ranks -- cuts[0..shards], multiples of 1024 rows,
+ * cuts[shards] = n -- and the source-chunk size. Identical on every rank for
+ * identical (times, params). */
+int sthk_plan_partition(const double* t, int64_t n, const double* params6,
+                        int shards, int dense, int* cuts, int* source_chunk);
 
 /* DFMA throughput probe on `device` (roofline denominator for the FP64
  * pair kernels): best and mean TFLOP/s over `reps` timed launches. */

@@ -57,7 +57,9 @@ SIGNATURES = [
     ("sthk_get_stats", c_int, [c_void_p, POINTER(StatsStruct)]),
     ("sthk_get_stream", c_int, [c_void_p, c_int, POINTER(c_void_p)]),
     ("sthk_set_dense", c_int, [c_void_p, c_int]),
+    ("sthk_set_virtual_shards", c_int, [c_void_p, c_int]),
     ("sthk_measure_fp64_peak", c_int, [c_int, c_int, _DPTR, _DPTR]),
+    ("sthk_plan_partition", c_int, [_DPTR, c_int64, _DPTR, c_int, c_int, _IPTR, _IPTR]),
     ("sthk_last_error", c_char_p, [c_void_p]),
     ("sthk_version", c_char_p, []),
     ("sthk_sim_cloud", c_int, [c_int64, _DPTR, c_uint64, _DPTR, _DPTR, _DPTR, _DPTR]),

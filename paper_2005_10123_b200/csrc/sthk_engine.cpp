@@ -99,7 +99,8 @@ struct Slot {
   double* h_per_event = nullptr;           // pinned
   size_t h_pe_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  int row0 = 0, row1 = 0;  // rows of the last enqueued eval
+  int row0 = 0, row1 = 0;  // rows of the last enqueued eval (first..last run)
+  std::vector<std::pair<int, int>> runs;  // row ranges run on this slot
 };
 
 }  // namespace
@@ -114,6 +115,7 @@ struct sthk_engine {
   double p[6] = {0, 0, 0, 0, 0, 0};
   bool loaded = false, has_params = false;
   bool timing = false, dense = false;
+  int virtual_shards = 1;  // testing: partition rows over k shards on one device
   std::string err;
   bool pending = false, last_grad = false, last_pe = false;
   int last_sc = 0, last_items_est = 0;
@@ -215,7 +217,14 @@ int64_t ub(const std::vector<double>& t, int64_t n, double v) {
   return std::upper_bound(t.begin(), t.begin() + n, v) - t.begin();
 }
 
-EvalPlan make_plan(const sthk_engine& e, int shards) {
+struct PlanInput {
+  const std::vector<double>& ht;
+  int64_t n, npad;
+  const double* p;
+  bool dense;
+};
+
+EvalPlan make_plan(const PlanInput& e, int shards) {
   EvalPlan pl;
   const double* p = e.p;
   double dB, dT;
@@ -281,8 +290,10 @@ EvalPlan make_plan(const sthk_engine& e, int shards) {
 void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
   if (!e.loaded) throw NotLoaded("sthk: no events loaded");
   if (!e.has_params) throw NotLoaded("sthk: no parameters set");
-  const int shards = e.rank_mode ? e.world : static_cast<int>(e.slots.size());
-  const EvalPlan pl = make_plan(e, shards);
+  const bool vshards = !e.rank_mode && e.slots.size() == 1 && e.virtual_shards > 1;
+  const int shards = vshards ? e.virtual_shards
+                             : (e.rank_mode ? e.world : static_cast<int>(e.slots.size()));
+  const EvalPlan pl = make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense}, shards);
   e.last_sc = pl.sc;
   const int NS = grad ? sthk::kNSumGrad : sthk::kNSumVal;
   const int64_t ntiles_total = (e.n + kTM - 1) / kTM;
@@ -290,14 +301,28 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
   const double* p = e.p;
   const double kPi = 3.14159265358979323846;
 
-  for (size_t si = 0; si < e.slots.size(); ++si) {
-    Slot& s = e.slots[si];
-    const int shard = e.rank_mode ? e.rank : static_cast<int>(si);
-    s.row0 = pl.cuts[shard];
-    s.row1 = pl.cuts[shard + 1];
+  // (slot, shard) runs: one per device, or every virtual shard on slot 0
+  std::vector<std::pair<int, int>> runs;
+  if (vshards) {
+    for (int k = 0; k < shards; ++k) runs.emplace_back(0, k);
+  } else {
+    for (int si = 0; si < static_cast<int>(e.slots.size()); ++si) {
+      runs.emplace_back(si, e.rank_mode ? e.rank : si);
+    }
+  }
+  for (Slot& s : e.slots) s.runs.clear();
+  for (const auto& run : runs) {
+    Slot& s = e.slots[run.first];
+    const int shard = run.second;
+    const bool first_run = s.runs.empty();
+    const int row0 = pl.cuts[shard];
+    const int row1 = pl.cuts[shard + 1];
+    s.runs.emplace_back(row0, row1);
+    if (first_run) s.row0 = row0;
+    s.row1 = row1;
     set_dev(s);
-    const int tile0 = s.row0 / kTM;
-    const int tile1 = static_cast<int>((s.row1 + kTM - 1) / kTM);
+    const int tile0 = row0 / kTM;
+    const int tile1 = static_cast<int>((row1 + kTM - 1) / kTM);
     const int ntiles = std::max(tile1 - tile0, 0);
     dev_grow(s.ranges, s.ranges_cap, static_cast<size_t>(ntiles_total));
     dev_grow(s.counts, s.counts_cap, static_cast<size_t>(std::max(ntiles, 1)));
@@ -307,10 +332,12 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
     if (want_pe) dev_grow(s.per_event, s.pe_cap, static_cast<size_t>(e.npad));
 
     cudaStream_t st = s.stream;
-    if (e.timing) ck(cudaEventRecord(s.ev[0], st), "event");
-    ck(cudaMemsetAsync(s.pair_counts, 0, 3 * sizeof(unsigned long long), st), "memset");
-    if (shards > 1) {
-      ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
+    if (first_run) {
+      if (e.timing) ck(cudaEventRecord(s.ev[0], st), "event");
+      ck(cudaMemsetAsync(s.pair_counts, 0, 3 * sizeof(unsigned long long), st), "memset");
+      if (shards > 1) {
+        ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
+      }
     }
     if (ntiles == 0) {
       // an empty shard still takes part in the collective
@@ -349,7 +376,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
       qa.partial = s.partial;
       qa.pair_counts = s.pair_counts;
       const int grid = s.sms * (grad ? s.occ_grad : s.occ_val);
-      if (e.timing) ck(cudaEventRecord(s.ev[1], st), "event");
+      if (e.timing && first_run) ck(cudaEventRecord(s.ev[1], st), "event");
       ck(sthk::launch_pairs(qa, grad, grid, st), "pair kernel");
       if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
 
@@ -357,8 +384,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
       fa.t = s.t;
       fa.n = e.n;
       fa.npad = e.npad;
-      fa.row0 = s.row0;
-      fa.row1 = s.row1;
+      fa.row0 = row0;
+      fa.row1 = row1;
       fa.window_end = e.window_end;
       fa.mu0 = p[0];
       fa.tauX = p[1];
@@ -381,7 +408,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
     }
   }
 
-  if (shards > 1) {
+  if (shards > 1 && !vshards) {
     ckn(ncclGroupStart(), "ncclGroupStart");
     for (Slot& s : e.slots) {
       ckn(ncclAllReduce(s.block_partial, s.block_partial, static_cast<size_t>(nb_total) * kNOut,
@@ -400,7 +427,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
     ck(cudaMemcpyAsync(s.h_counts, s.pair_counts, 3 * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, st),
        "D2H");
-    if (want_pe && s.row1 > s.row0) {
+    if (want_pe && s.row1 > s.row0) {  // runs on one slot are contiguous
       if (s.h_pe_cap < static_cast<size_t>(e.npad)) {
         if (s.h_per_event) ck(cudaFreeHost(s.h_per_event), "cudaFreeHost");
         ck(cudaMallocHost(&s.h_per_event, sizeof(double) * e.npad), "cudaMallocHost");
@@ -676,6 +703,33 @@ int sthk_set_timing(sthk_engine* e, int enable) {
 
 int sthk_set_dense(sthk_engine* e, int dense) {
   return guarded(e, [&] { e->dense = dense != 0; });
+}
+
+int sthk_plan_partition(const double* t, int64_t n, const double* params6, int shards,
+                        int dense, int* cuts, int* source_chunk) {
+  if (!t || n < 1 || !params6 || shards < 1 || !cuts) return STHK_EINVAL;
+  try {
+    validate_params(params6);
+    const std::vector<double> ht(t, t + n);
+    const int64_t npad = (n + kTM - 1) / kTM * kTM;
+    const EvalPlan pl = make_plan(PlanInput{ht, n, npad, params6, dense != 0}, shards);
+    for (int k = 0; k <= shards; ++k) cuts[k] = pl.cuts[k];
+    if (source_chunk) *source_chunk = pl.sc;
+    return STHK_OK;
+  } catch (const std::exception& x) {
+    g_create_err = x.what();
+    return STHK_EINVAL;
+  }
+}
+
+int sthk_set_virtual_shards(sthk_engine* e, int k) {
+  return guarded(e, [&] {
+    if (k < 1 || k > 4096) throw InvalidArg("sthk_set_virtual_shards: k must be in [1, 4096]");
+    if (e->rank_mode || e->slots.size() != 1) {
+      throw InvalidArg("sthk_set_virtual_shards: single-device handles only");
+    }
+    e->virtual_shards = k;
+  });
 }
 
 int sthk_get_stream(sthk_engine* e, int slot, void** stream) {

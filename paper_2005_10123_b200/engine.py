@@ -172,6 +172,9 @@ class Engine:
     def set_dense(self, on: bool) -> None:
         self._check(self._lib.sthk_set_dense(self._h, int(on)), "sthk_set_dense")
 
+    def set_virtual_shards(self, k: int) -> None:
+        self._check(self._lib.sthk_set_virtual_shards(self._h, int(k)), "sthk_set_virtual_shards")
+
     def stats(self) -> dict:
         s = _lib.StatsStruct()
         self._check(self._lib.sthk_get_stats(self._h, byref(s)), "sthk_get_stats")

@@ -102,3 +102,70 @@ def test_matches_reference_engine(engine):
     r = pk.logLikelihood(ev, p, engine=engine)
     assert ok and r.valid
     assert abs(r.logLik - ref) <= LL_TOL * abs(ref)
+
+
+@pytest.mark.parametrize("k", [2, 3, 8])
+def test_partition_bitwise_invariant(engine, k):
+    """Row partition across k shards (the multi-GPU split, run on one device
+    and combined as the NCCL path does) gives bitwise-identical results."""
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=20000)
+    engine.load(ev)
+    for p in (pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695), pk.Params(1, 1.6, 14, 0.1, 1, 1)):
+        engine.set_params(p)
+        engine.set_virtual_shards(1)
+        a = engine.loglik_grad(per_event=True)
+        engine.set_virtual_shards(k)
+        b = engine.loglik_grad(per_event=True)
+        engine.set_virtual_shards(1)
+        assert a[0] == b[0] and np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
+
+
+def test_per_event_sums_to_total(engine):
+    # test_likelihood.cpp:134-146
+    ev = pk.generateBenchmarkCloud(120, pk.SimWindow(0, 4, 0, 4, 60), 5)
+    r = pk.logLikelihood(ev, pk.Params(0.9, 1.1, 5.0, 0.4, 1.3, 0.5), keepPerEvent=True,
+                         engine=engine)
+    assert r.valid and r.perEvent.size == 120
+    assert abs(r.perEvent.sum() - r.logLik) <= 1e-12 * 120
+
+
+def test_underflow_invalid_and_invalid_params(engine):
+    # test_likelihood.cpp:148-175
+    ev = pk.EventSet([0.0, 1.0], [0.0, 0.0], [0.0, 1.0])
+    r, g = pk.logLikelihoodGradient(ev, pk.Params(5e-324, 1e120, 1e120, 0.0, 1.0, 1.0),
+                                    engine=engine)
+    assert not r.valid and r.logLik == -math.inf and np.all(np.isnan(g))
+    with pytest.raises(ValueError):
+        pk.logLikelihood(ev, pk.Params(omega=-1.0), engine=engine)
+
+
+def test_batch_bitwise_equals_single(engine):
+    # test_likelihood.cpp:224-247
+    ev = pk.generateBenchmarkCloud(100, pk.SimWindow(0, 4, 0, 4, 60), 55)
+    rng = np.random.default_rng(56)
+    plist = [_rand_params(rng) for _ in range(3)]
+    plist.append(plist[0])
+    engine.load(ev)
+    ll, ok, g = engine.loglik_batch([p.as_array() for p in plist], grad=True)
+    for i, p in enumerate(plist):
+        engine.set_params(p)
+        s = engine.loglik_grad()
+        assert ll[i] == s[0] and np.array_equal(g[i], s[2])
+    assert ll[0] == ll[3]
+    with pytest.raises(ValueError):
+        engine.loglik_batch(np.zeros((0, 6)))
+
+
+def test_ties_strict_time_rule(engine):
+    """Equal timestamps never excite each other (kernels.hpp:44): the C2
+    tie-stress variant (times floored to whole seconds), vs the oracle."""
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=3000)
+    t = np.floor(ev.ts() * 86400.0) / 86400.0
+    ev2 = pk.EventSet(ev.xs(), ev.ys(), t)
+    assert np.sum(np.diff(t) == 0) > 0
+    for p in (pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695), pk.Params(1, 1.6, 14, 0.1, 1, 1)):
+        _check(engine, ev2, p)
