@@ -96,7 +96,7 @@ int sthk_result(sthk_engine* e, double* loglik, int* valid, double* grad6,
 /* Introspection for benchmarks / tests. */
 typedef struct sthk_stats {
   int64_t n;                 /* events loaded */
-  int64_t pairs_bg;          /* background pairs evaluated (tile granularity) */
+  int64_t pairs_bg;          /* ordered background pairs covered (tile granularity) */
   int64_t pairs_tr;          /* trigger pairs evaluated (tile granularity) */
   int64_t pairs_any;         /* pairs with either term evaluated */
   int64_t pairs_dense;       /* n * n */
@@ -107,6 +107,10 @@ typedef struct sthk_stats {
   int32_t work_items;        /* live (row tile, chunk) items of the last eval */
   int32_t n_devices;         /* devices driven by this handle */
   int32_t rank, world;       /* rank-mode coordinates (0, 1 otherwise) */
+  int64_t exp_evals;         /* exps evaluated by the last pair kernel(s) (a
+                                symmetric background exp serves 2 ordered pairs) */
+  int32_t kernel_mode;       /* STHK_KERNEL_ROWS or STHK_KERNEL_SYM */
+  int32_t reserved;
 } sthk_stats;
 
 int sthk_set_timing(sthk_engine* e, int enable);
@@ -116,6 +120,14 @@ int sthk_get_stream(sthk_engine* e, int slot, void** stream);
 /* Debug/testing knob: 0 = exact tile culling on (default), 1 = evaluate the
  * dense pair set (results are bitwise identical either way). */
 int sthk_set_dense(sthk_engine* e, int dense);
+/* Pair-kernel variant. STHK_KERNEL_SYM (default) evaluates each background
+ * pair once and adds it to both events' sums (b_ij = b_ji); STHK_KERNEL_ROWS
+ * sweeps ordered pairs per target row. Both are deterministic; they agree to
+ * rounding (different summation grouping), not bitwise. */
+#define STHK_KERNEL_ROWS 0
+#define STHK_KERNEL_SYM 1
+int sthk_set_kernel(sthk_engine* e, int mode);
+
 /* Testing knob for the multi-device partition on one device: split the rows
  * into k cost-balanced shards run one after another on the single device and
  * combined exactly as the NCCL path combines them (k = 1: off). Results must

@@ -35,6 +35,9 @@ class StatsStruct(ctypes.Structure):
         ("n_devices", ctypes.c_int32),
         ("rank", ctypes.c_int32),
         ("world", ctypes.c_int32),
+        ("exp_evals", c_int64),
+        ("kernel_mode", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -58,6 +61,7 @@ SIGNATURES = [
     ("sthk_get_stream", c_int, [c_void_p, c_int, POINTER(c_void_p)]),
     ("sthk_set_dense", c_int, [c_void_p, c_int]),
     ("sthk_set_virtual_shards", c_int, [c_void_p, c_int]),
+    ("sthk_set_kernel", c_int, [c_void_p, c_int]),
     ("sthk_measure_fp64_peak", c_int, [c_int, c_int, _DPTR, _DPTR]),
     ("sthk_plan_partition", c_int, [_DPTR, c_int64, _DPTR, c_int, c_int, _IPTR, _IPTR]),
     ("sthk_last_error", c_char_p, [c_void_p]),

@@ -139,6 +139,42 @@ __device__ __forceinline__ double exp_l(double x, const uint2* __restrict__ tab)
 }
 
 // ---------------------------------------------------------------------------
+// Deterministic fixed-point accumulation.
+//
+// Partial sums (always >= 0: every summand is e, e*r^2, e*dt^2, e*dt with
+// dt > 0) are converted to a two-word fixed-point number -- hi in units of
+// 2^-40, lo holding the exact remainder in units of 2^-80 -- and added with
+// 64-bit integer atomics. Integer addition is associative, so the totals are
+// bitwise independent of the order in which CTAs, devices or ranks add their
+// contributions; the representation error is <= 2^-81 per conversion (far
+// below the rounding of the double partial itself). Callers normalise each
+// sum to O(1) per pair first (|total| < 2^23).
+// ---------------------------------------------------------------------------
+constexpr double kFxHi = 0x1p40;
+constexpr double kFxHiInv = 0x1p-40;
+constexpr double kFxLo = 0x1p80;
+constexpr double kFxLoInv = 0x1p-80;
+
+__device__ __forceinline__ void fx_add(unsigned long long* hi, unsigned long long* lo, double v) {
+  const long long h = __double2ll_rn(v * kFxHi);
+  // exact: either v*2^40 >= 2^53 (already an integer, remainder 0) or
+  // h*2^-40 is exact and within a factor 2 of v (Sterbenz)
+  const double rem = fma(static_cast<double>(h), -kFxHiInv, v);
+  const long long l = __double2ll_rn(rem * kFxLo);
+  if (h != 0) atomicAdd(hi, static_cast<unsigned long long>(h));
+  if (l != 0) atomicAdd(lo, static_cast<unsigned long long>(l));
+}
+
+__device__ __forceinline__ double fx_value(unsigned long long hi, unsigned long long lo) {
+  long long H = static_cast<long long>(hi);
+  long long L = static_cast<long long>(lo);
+  const long long carry = L >> 40;  // floor(L / 2^40)
+  H += carry;
+  L -= carry * (1LL << 40);  // now 0 <= L < 2^40
+  return fma(static_cast<double>(H), kFxHiInv, static_cast<double>(L) * kFxLoInv);
+}
+
+// ---------------------------------------------------------------------------
 // TMA bulk copy (cp.async.bulk, SASS UBLKCP) + mbarrier helpers.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {

@@ -72,7 +72,7 @@ void dev_grow(T*& p, size_t& cap, size_t need) {
 struct Slot {
   int dev = 0;
   int sms = 148;
-  int occ_grad = 1, occ_val = 1;
+  int occ[2][2] = {{1, 1}, {1, 1}};  // [mode][grad]
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   double *x = nullptr, *y = nullptr, *t = nullptr;
@@ -86,8 +86,12 @@ struct Slot {
   int2* items = nullptr;
   size_t items_cap = 0;
   int* scalars = nullptr;  // [0] n_items, [1] work counter
-  double* partial = nullptr;
-  size_t partial_cap = 0;
+  unsigned long long* fx = nullptr;  // fixed-point background sums [6][npad]
+  size_t fx_cap = 0;
+  double* tpart = nullptr;           // trigger partials [nchunks][3][npad]
+  size_t tpart_cap = 0;
+  int2* crange = nullptr;
+  size_t crange_cap = 0;
   double* block_partial = nullptr;
   size_t bp_cap = 0;
   double* out = nullptr;  // kNOut
@@ -95,7 +99,7 @@ struct Slot {
   size_t pe_cap = 0;
   unsigned long long* pair_counts = nullptr;
   double* h_out = nullptr;                 // pinned kNOut
-  unsigned long long* h_counts = nullptr;  // pinned 3
+  unsigned long long* h_counts = nullptr;  // pinned kNCounts
   double* h_per_event = nullptr;           // pinned
   size_t h_pe_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -115,6 +119,7 @@ struct sthk_engine {
   double p[6] = {0, 0, 0, 0, 0, 0};
   bool loaded = false, has_params = false;
   bool timing = false, dense = false;
+  int mode = sthk::kSym;   // pair-kernel variant (sthk_set_kernel)
   int virtual_shards = 1;  // testing: partition rows over k shards on one device
   std::string err;
   bool pending = false, last_grad = false, last_pe = false;
@@ -135,11 +140,14 @@ void init_slot(Slot& s, int dev) {
   for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
   ck(cudaMalloc(&s.scalars, 2 * sizeof(int)), "cudaMalloc");
   ck(cudaMalloc(&s.out, kNOut * sizeof(double)), "cudaMalloc");
-  ck(cudaMalloc(&s.pair_counts, 3 * sizeof(unsigned long long)), "cudaMalloc");
+  ck(cudaMalloc(&s.pair_counts, sthk::kNCounts * sizeof(unsigned long long)), "cudaMalloc");
   ck(cudaMallocHost(&s.h_out, kNOut * sizeof(double)), "cudaMallocHost");
-  ck(cudaMallocHost(&s.h_counts, 3 * sizeof(unsigned long long)), "cudaMallocHost");
-  s.occ_grad = sthk::pair_kernel_occupancy(true);
-  s.occ_val = sthk::pair_kernel_occupancy(false);
+  ck(cudaMallocHost(&s.h_counts, sthk::kNCounts * sizeof(unsigned long long)),
+     "cudaMallocHost");
+  for (int m = 0; m < 2; ++m) {
+    s.occ[m][1] = sthk::pair_kernel_occupancy(true, m);
+    s.occ[m][0] = sthk::pair_kernel_occupancy(false, m);
+  }
   ck(cudaGetLastError(), "occupancy");
 }
 
@@ -150,7 +158,8 @@ void free_slot(Slot& s) {
   for (void* p : {static_cast<void*>(s.x), static_cast<void*>(s.y), static_cast<void*>(s.t),
                   static_cast<void*>(s.ranges), static_cast<void*>(s.counts),
                   static_cast<void*>(s.items), static_cast<void*>(s.scalars),
-                  static_cast<void*>(s.partial), static_cast<void*>(s.block_partial),
+                  static_cast<void*>(s.fx), static_cast<void*>(s.block_partial),
+                  static_cast<void*>(s.tpart), static_cast<void*>(s.crange),
                   static_cast<void*>(s.out), static_cast<void*>(s.per_event),
                   static_cast<void*>(s.pair_counts), static_cast<void*>(s.tile_box)}) {
     if (p) cudaFree(p);
@@ -222,6 +231,7 @@ struct PlanInput {
   int64_t n, npad;
   const double* p;
   bool dense;
+  bool sym;
 };
 
 EvalPlan make_plan(const PlanInput& e, int shards) {
@@ -249,7 +259,7 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
     const int64_t tile = samples == 1 ? 0 : (ntiles - 1) * s / (samples - 1);
     const int64_t first = tile * kTM, last = std::min(first + kTM, n) - 1;
     const int64_t lo = std::min(lb(e.ht, n, e.ht[first] - std::max(dB, dT)), first);
-    const int64_t hi = std::max(ub(e.ht, n, e.ht[last] + dB), last + 1);
+    const int64_t hi = e.sym ? last + 1 : std::max(ub(e.ht, n, e.ht[last] + dB), last + 1);
     wsum += static_cast<double>(hi - lo);
   }
   const double wmean = wsum / samples;
@@ -270,9 +280,9 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
     double tot = 0;
     for (int64_t b = 0; b < nb; ++b) {
       const int64_t first = b * kRB, last = std::min(first + kRB, n) - 1;
-      const double w = e.dense ? static_cast<double>(n)
-                               : static_cast<double>(ub(e.ht, n, e.ht[last] + dB) -
-                                                     lb(e.ht, n, e.ht[first] - std::max(dB, dT)));
+      const int64_t lo = e.dense ? 0 : lb(e.ht, n, e.ht[first] - std::max(dB, dT));
+      const int64_t hi = e.sym ? last + 1 : (e.dense ? n : ub(e.ht, n, e.ht[last] + dB));
+      const double w = static_cast<double>(std::max<int64_t>(hi - lo, 1));
       cost[b] = w * static_cast<double>(last - first + 1);
       tot += cost[b];
     }
@@ -287,127 +297,168 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   return pl;
 }
 
+// fxq: per-sum normalisation applied before fixed-point conversion so every
+// accumulated sum is O(1) per pair (S_B, S_Br/2tauX^2, S_Bt/2tauT^2, S_T,
+// omega S_Tt, S_Tr/2h^2).
+void fixed_point_scales(const double* p, double* q) {
+  q[0] = 1.0;
+  q[1] = 0.5 / (p[1] * p[1]);
+  q[2] = 0.5 / (p[2] * p[2]);
+  q[3] = 1.0;
+  q[4] = p[4];
+  q[5] = 0.5 / (p[5] * p[5]);
+}
+
+constexpr int kFxRows = 2 * 3;  // fixed-point words per event (3 background sums)
+
 void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
   if (!e.loaded) throw NotLoaded("sthk: no events loaded");
   if (!e.has_params) throw NotLoaded("sthk: no parameters set");
   const bool vshards = !e.rank_mode && e.slots.size() == 1 && e.virtual_shards > 1;
   const int shards = vshards ? e.virtual_shards
                              : (e.rank_mode ? e.world : static_cast<int>(e.slots.size()));
-  const EvalPlan pl = make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense}, shards);
+  const bool sym = e.mode == sthk::kSym;
+  const EvalPlan pl = make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym}, shards);
   e.last_sc = pl.sc;
-  const int NS = grad ? sthk::kNSumGrad : sthk::kNSumVal;
   const int64_t ntiles_total = (e.n + kTM - 1) / kTM;
   const int nb_total = static_cast<int>((e.n + kRB - 1) / kRB);
   const double* p = e.p;
   const double kPi = 3.14159265358979323846;
+  double fxq[sthk::kNSumGrad];
+  fixed_point_scales(p, fxq);
 
   // (slot, shard) runs: one per device, or every virtual shard on slot 0
-  std::vector<std::pair<int, int>> runs;
+  struct Run {
+    int slot, row0, row1;
+  };
+  std::vector<Run> runs;
   if (vshards) {
-    for (int k = 0; k < shards; ++k) runs.emplace_back(0, k);
+    for (int k = 0; k < shards; ++k) runs.push_back({0, pl.cuts[k], pl.cuts[k + 1]});
   } else {
     for (int si = 0; si < static_cast<int>(e.slots.size()); ++si) {
-      runs.emplace_back(si, e.rank_mode ? e.rank : si);
+      const int shard = e.rank_mode ? e.rank : si;
+      runs.push_back({si, pl.cuts[shard], pl.cuts[shard + 1]});
     }
   }
   for (Slot& s : e.slots) s.runs.clear();
-  for (const auto& run : runs) {
-    Slot& s = e.slots[run.first];
-    const int shard = run.second;
+
+  // phase 1: zero the accumulators, plan and run the pair kernel per run
+  for (const Run& run : runs) {
+    Slot& s = e.slots[run.slot];
     const bool first_run = s.runs.empty();
-    const int row0 = pl.cuts[shard];
-    const int row1 = pl.cuts[shard + 1];
-    s.runs.emplace_back(row0, row1);
-    if (first_run) s.row0 = row0;
-    s.row1 = row1;
+    s.runs.emplace_back(run.row0, run.row1);
+    if (first_run) s.row0 = run.row0;
+    s.row1 = run.row1;
     set_dev(s);
-    const int tile0 = row0 / kTM;
-    const int tile1 = static_cast<int>((row1 + kTM - 1) / kTM);
+    const int tile0 = run.row0 / kTM;
+    const int tile1 = static_cast<int>((run.row1 + kTM - 1) / kTM);
     const int ntiles = std::max(tile1 - tile0, 0);
     dev_grow(s.ranges, s.ranges_cap, static_cast<size_t>(ntiles_total));
     dev_grow(s.counts, s.counts_cap, static_cast<size_t>(std::max(ntiles, 1)));
     dev_grow(s.items, s.items_cap, static_cast<size_t>(std::max(ntiles, 1)) * pl.nchunks);
-    dev_grow(s.partial, s.partial_cap, static_cast<size_t>(pl.nchunks) * NS * e.npad);
+    dev_grow(s.fx, s.fx_cap, static_cast<size_t>(kFxRows) * e.npad);
+    dev_grow(s.tpart, s.tpart_cap, static_cast<size_t>(pl.nchunks) * 3 * e.npad);
+    dev_grow(s.crange, s.crange_cap, static_cast<size_t>(ntiles_total));
     dev_grow(s.block_partial, s.bp_cap, static_cast<size_t>(nb_total) * kNOut);
     if (want_pe) dev_grow(s.per_event, s.pe_cap, static_cast<size_t>(e.npad));
 
     cudaStream_t st = s.stream;
     if (first_run) {
       if (e.timing) ck(cudaEventRecord(s.ev[0], st), "event");
-      ck(cudaMemsetAsync(s.pair_counts, 0, 3 * sizeof(unsigned long long), st), "memset");
+      ck(cudaMemsetAsync(s.pair_counts, 0, sthk::kNCounts * sizeof(unsigned long long), st),
+         "memset");
+      ck(cudaMemsetAsync(s.fx, 0, sizeof(unsigned long long) * kFxRows * e.npad, st), "memset");
       if (shards > 1) {
         ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
       }
     }
-    if (ntiles == 0) {
-      // an empty shard still takes part in the collective
-      ck(cudaMemsetAsync(s.scalars, 0, 2 * sizeof(int), st), "memset");
-    } else {
-      sthk::PlanArgs pa{};
-      pa.t = s.t;
-      pa.n = e.n;
-      pa.tile0 = tile0;
-      pa.tile1 = tile1;
-      pa.dB = pl.k.dB;
-      pa.dT = pl.k.dT;
-      pa.dense = e.dense ? 1 : 0;
-      pa.sc = pl.sc;
-      pa.nchunks = pl.nchunks;
-      pa.ranges = s.ranges;
-      pa.counts = s.counts;
-      pa.items = s.items;
-      pa.n_items = s.scalars;
-      pa.work_counter = s.scalars + 1;
-      ck(sthk::launch_plan(pa, st), "plan");
+    if (ntiles == 0) continue;
+    sthk::PlanArgs pa{};
+    pa.t = s.t;
+    pa.n = e.n;
+    pa.tile0 = tile0;
+    pa.tile1 = tile1;
+    pa.dB = pl.k.dB;
+    pa.dT = pl.k.dT;
+    pa.dense = e.dense ? 1 : 0;
+    pa.sym = sym ? 1 : 0;
+    pa.sc = pl.sc;
+    pa.nchunks = pl.nchunks;
+    pa.ranges = s.ranges;
+    pa.crange = s.crange;
+    pa.counts = s.counts;
+    pa.items = s.items;
+    pa.n_items = s.scalars;
+    pa.work_counter = s.scalars + 1;
+    ck(sthk::launch_plan(pa, st), "plan");
 
-      sthk::PairArgs qa{};
-      qa.x = s.x;
-      qa.y = s.y;
-      qa.t = s.t;
-      qa.tile_box = s.tile_box;
-      qa.n = e.n;
-      qa.npad = e.npad;
-      qa.k = pl.k;
-      qa.sc = pl.sc;
-      qa.ranges = s.ranges;
-      qa.items = s.items;
-      qa.n_items = s.scalars;
-      qa.work_counter = s.scalars + 1;
-      qa.partial = s.partial;
-      qa.pair_counts = s.pair_counts;
-      const int grid = s.sms * (grad ? s.occ_grad : s.occ_val);
-      if (e.timing && first_run) ck(cudaEventRecord(s.ev[1], st), "event");
-      ck(sthk::launch_pairs(qa, grad, grid, st), "pair kernel");
-      if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
-
-      sthk::FinArgs fa{};
-      fa.t = s.t;
-      fa.n = e.n;
-      fa.npad = e.npad;
-      fa.row0 = row0;
-      fa.row1 = row1;
-      fa.window_end = e.window_end;
-      fa.mu0 = p[0];
-      fa.tauX = p[1];
-      fa.tauT = p[2];
-      fa.theta = p[3];
-      fa.omega = p[4];
-      fa.h = p[5];
-      // HawkesPairTerm constants, kernels.hpp:78-84
-      fa.bgNorm = std::pow(2.0 * kPi, -1.5) / (p[1] * p[1] * p[2]);
-      fa.trNorm = p[3] * p[4] / (2.0 * kPi * p[5] * p[5]);
-      fa.cT = p[4] / (2.0 * kPi * p[5] * p[5]);
-      fa.sc = pl.sc;
-      fa.nchunks = pl.nchunks;
-      fa.dense = e.dense ? 1 : 0;
-      fa.ranges = s.ranges;
-      fa.partial = s.partial;
-      fa.per_event = want_pe ? s.per_event : nullptr;
-      fa.block_partial = s.block_partial;
-      ck(sthk::launch_finalize(fa, grad, st), "finalize");
-    }
+    sthk::PairArgs qa{};
+    qa.x = s.x;
+    qa.y = s.y;
+    qa.t = s.t;
+    qa.tile_box = s.tile_box;
+    qa.n = e.n;
+    qa.npad = e.npad;
+    qa.k = pl.k;
+    qa.sc = pl.sc;
+    qa.ranges = s.ranges;
+    qa.items = s.items;
+    qa.n_items = s.scalars;
+    qa.work_counter = s.scalars + 1;
+    qa.fx = s.fx;
+    qa.tpart = s.tpart;
+    for (int k = 0; k < sthk::kNSumGrad; ++k) qa.fxq[k] = fxq[k];
+    qa.pair_counts = s.pair_counts;
+    const int grid = s.sms * s.occ[e.mode][grad ? 1 : 0];
+    if (e.timing && first_run) ck(cudaEventRecord(s.ev[1], st), "event");
+    ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
+    if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
   }
 
+  // phase 2: symmetric mode adds column sums to rows other devices own
+  if (sym && shards > 1 && !vshards) {
+    ckn(ncclGroupStart(), "ncclGroupStart");
+    for (Slot& s : e.slots) {
+      ckn(ncclAllReduce(s.fx, s.fx, static_cast<size_t>(kFxRows) * e.npad, ncclUint64, ncclSum,
+                        s.comm, s.stream),
+          "ncclAllReduce(fx)");
+    }
+    ckn(ncclGroupEnd(), "ncclGroupEnd");
+  }
+
+  // phase 3: per-row finalize into 1024-row block partials
+  for (const Run& run : runs) {
+    if (run.row1 <= run.row0) continue;
+    Slot& s = e.slots[run.slot];
+    set_dev(s);
+    sthk::FinArgs fa{};
+    fa.t = s.t;
+    fa.n = e.n;
+    fa.npad = e.npad;
+    fa.row0 = run.row0;
+    fa.row1 = run.row1;
+    fa.window_end = e.window_end;
+    fa.mu0 = p[0];
+    fa.tauX = p[1];
+    fa.tauT = p[2];
+    fa.theta = p[3];
+    fa.omega = p[4];
+    fa.h = p[5];
+    // HawkesPairTerm constants, kernels.hpp:78-84
+    fa.bgNorm = std::pow(2.0 * kPi, -1.5) / (p[1] * p[1] * p[2]);
+    fa.trNorm = p[3] * p[4] / (2.0 * kPi * p[5] * p[5]);
+    fa.cT = p[4] / (2.0 * kPi * p[5] * p[5]);
+    fa.fx = s.fx;
+    fa.tpart = s.tpart;
+    fa.crange = s.crange;
+    for (int k = 0; k < sthk::kNSumGrad; ++k) fa.fxq[k] = fxq[k];
+    fa.per_event = want_pe ? s.per_event : nullptr;
+    fa.block_partial = s.block_partial;
+    ck(sthk::launch_finalize(fa, grad, s.stream), "finalize");
+  }
+
+  // phase 4: exact combination of the block partials (each block has one
+  // non-zero contributor), then the fixed-order final sum on every device
   if (shards > 1 && !vshards) {
     ckn(ncclGroupStart(), "ncclGroupStart");
     for (Slot& s : e.slots) {
@@ -424,7 +475,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
     ck(sthk::launch_final_sum(s.block_partial, nb_total, s.out, st), "final sum");
     ck(cudaMemcpyAsync(s.h_out, s.out, kNOut * sizeof(double), cudaMemcpyDeviceToHost, st),
        "D2H");
-    ck(cudaMemcpyAsync(s.h_counts, s.pair_counts, 3 * sizeof(unsigned long long),
+    ck(cudaMemcpyAsync(s.h_counts, s.pair_counts, sthk::kNCounts * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, st),
        "D2H");
     if (want_pe && s.row1 > s.row0) {  // runs on one slot are contiguous
@@ -712,7 +763,7 @@ int sthk_plan_partition(const double* t, int64_t n, const double* params6, int s
     validate_params(params6);
     const std::vector<double> ht(t, t + n);
     const int64_t npad = (n + kTM - 1) / kTM * kTM;
-    const EvalPlan pl = make_plan(PlanInput{ht, n, npad, params6, dense != 0}, shards);
+    const EvalPlan pl = make_plan(PlanInput{ht, n, npad, params6, dense != 0, true}, shards);
     for (int k = 0; k <= shards; ++k) cuts[k] = pl.cuts[k];
     if (source_chunk) *source_chunk = pl.sc;
     return STHK_OK;
@@ -720,6 +771,15 @@ int sthk_plan_partition(const double* t, int64_t n, const double* params6, int s
     g_create_err = x.what();
     return STHK_EINVAL;
   }
+}
+
+int sthk_set_kernel(sthk_engine* e, int mode) {
+  return guarded(e, [&] {
+    if (mode != sthk::kRows && mode != sthk::kSym) {
+      throw InvalidArg("sthk_set_kernel: mode must be 0 (rows) or 1 (symmetric)");
+    }
+    e->mode = mode;
+  });
 }
 
 int sthk_set_virtual_shards(sthk_engine* e, int k) {
@@ -751,10 +811,12 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
     out->rank = e->rank;
     out->world = e->world;
     out->source_chunk = e->last_sc;
+    out->kernel_mode = e->mode;
     for (Slot& s : e->slots) {
       out->pairs_bg += static_cast<int64_t>(s.h_counts[0]);
       out->pairs_tr += static_cast<int64_t>(s.h_counts[1]);
       out->pairs_any += static_cast<int64_t>(s.h_counts[2]);
+      out->exp_evals += static_cast<int64_t>(s.h_counts[3]);
       if (e->timing && s.row1 > s.row0) {
         float a = 0, b = 0;
         set_dev(s);

@@ -83,9 +83,12 @@ __global__ void plan_ranges_kernel(const PlanArgs a) {
     lo = min(lo, static_cast<int>(first));
     hi = max(hi, static_cast<int>(last + 1));
   }
+  // symmetric mode: later tiles reach this one through their column sums
+  if (a.sym) hi = static_cast<int>(last + 1);
   a.ranges[tile] = make_int2(lo, hi);
   const int c0 = a.dense ? 0 : lo / a.sc;
-  const int c1 = a.dense ? a.nchunks - 1 : (hi - 1) / a.sc;
+  const int c1 = (hi - 1) / a.sc;
+  a.crange[tile] = make_int2(c0, c1);
   a.counts[tile - a.tile0] = c1 - c0 + 1;
 }
 
@@ -112,8 +115,7 @@ __global__ void __launch_bounds__(1024) plan_items_kernel(const PlanArgs a) {
     const int excl = s_carry + s_scan[tid] - c;
     if (i < ntiles) {
       const int tile = a.tile0 + i;
-      const int2 rg = a.ranges[tile];
-      const int c0 = a.dense ? 0 : rg.x / a.sc;
+      const int c0 = a.crange[tile].x;
       for (int q = 0; q < c; ++q) a.items[excl + q] = make_int2(tile, c0 + q);
     }
     __syncthreads();
@@ -187,6 +189,27 @@ __device__ __forceinline__ void stage_dispatch(bool bg, int tr, const double* sx
     if (tr == 1) stage_loop<GRAD, false, 1, CHECK>(sx, sy, st, cnt, xi, yi, ti, k, tab, acc);
     else if (tr == 2) stage_loop<GRAD, false, 2, CHECK>(sx, sy, st, cnt, xi, yi, ti, k, tab, acc);
   }
+}
+
+// Item-end row output. Background sums (which also receive column
+// contributions in kSym mode; S_B >= 1 always, the self term) go to the
+// fixed-point accumulators; trigger sums, which are row-only and may be
+// arbitrarily small, keep full relative precision as double partials per
+// (chunk, row), summed in chunk order by finalize.
+template <bool GRAD>
+__device__ __forceinline__ void store_row_sums(const PairArgs& a, int chunk, int64_t row,
+                                               const double* acc) {
+  constexpr int NB = GRAD ? 3 : 1;  // background sums
+  constexpr int NT = GRAD ? 3 : 1;  // trigger sums
+  if (row >= a.n) return;
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    fx_add(a.fx + static_cast<size_t>(2 * q) * a.npad + row,
+           a.fx + static_cast<size_t>(2 * q + 1) * a.npad + row, acc[q] * a.fxq[q]);
+  }
+  double* out = a.tpart + static_cast<size_t>(chunk) * NT * a.npad + row;
+#pragma unroll
+  for (int q = 0; q < NT; ++q) out[static_cast<size_t>(q) * a.npad] = acc[NB + q];
 }
 
 template <bool GRAD>
@@ -291,15 +314,320 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
       }
     }
 
-    double* out = a.partial + static_cast<size_t>(chunk) * NS * a.npad + row;
-#pragma unroll
-    for (int q = 0; q < NS; ++q) out[static_cast<size_t>(q) * a.npad] = acc[q];
+    store_row_sums<GRAD>(a, chunk, row, acc);
   }
 
   if (tid == 0 && a.pair_counts) {
     atomicAdd(&a.pair_counts[0], cBg);
     atomicAdd(&a.pair_counts[1], cTr);
     atomicAdd(&a.pair_counts[2], cAny);
+    atomicAdd(&a.pair_counts[3], cBg + cTr);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Symmetric-background pair kernel (kSym)
+// ---------------------------------------------------------------------------
+// A CTA owns a 128-row target tile I; lane l of every warp holds rows
+// l + 32q (q < 4) in registers, and warp w sweeps columns 32w..32w+31 of each
+// 128-source stage, so each thread evaluates a 4-row x 32-column block per
+// stage with the column's coordinates broadcast from shared memory.
+//   * J < I ("sym" stages): every background exp is added to its row sums
+//     and to its column's sums (b_ij = b_ji); the 4-row column partials are
+//     reduce-scattered across the warp with shuffles once per 4 columns and
+//     flushed to the fixed-point column accumulators once per stage. The
+//     trigger term (t_j < t_i) only feeds rows.
+//   * J == I ("diag" stage): all ordered pairs of the tile, rows only.
+// Row partials of the 4 warps are combined in a fixed order at item end.
+constexpr int kSymR = 4;  // rows per thread
+
+template <bool GRAD, bool SYM, bool BG, int TR, bool CHECK, bool VALID>
+__device__ __forceinline__ void sym_block(const double* __restrict__ sx,
+                                          const double* __restrict__ sy,
+                                          const double* __restrict__ st, int col0, int cnt,
+                                          const double (&xi)[kSymR], const double (&yi)[kSymR],
+                                          const double (&ti)[kSymR], const bool (&rv)[kSymR],
+                                          const PairConsts& k, const uint2* __restrict__ tab,
+                                          double (&racc)[kSymR][GRAD ? kNSumGrad : kNSumVal],
+                                          double* __restrict__ s_col) {
+  constexpr int NSC = GRAD ? 3 : 1;
+  constexpr int T0 = GRAD ? 3 : 1;
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int g = 0; g < 8; ++g) {
+    double cp[4][NSC];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = col0 + 4 * g + q;
+      const double xj = sx[j], yj = sy[j], tj = st[j];
+      bool cv = true;
+      if constexpr (VALID) cv = j < cnt;
+#pragma unroll
+      for (int r = 0; r < kSymR; ++r) {
+        const double dx = xi[r] - xj;
+        const double dy = yi[r] - yj;
+        const double dt = ti[r] - tj;
+        const double r2 = fma(dx, dx, dy * dy);
+        if constexpr (BG) {
+          const double dt2 = dt * dt;
+          double e = exp_l<CHECK>(fma(k.cxL, r2, k.ctL * dt2), tab);
+          if constexpr (VALID) e = (cv && rv[r]) ? e : 0.0;
+          racc[r][0] += e;
+          if constexpr (GRAD) {
+            racc[r][1] = fma(e, r2, racc[r][1]);
+            racc[r][2] = fma(e, dt2, racc[r][2]);
+          }
+          if constexpr (SYM) {
+            if (r == 0) {
+              cp[q][0] = e;
+              if constexpr (GRAD) {
+                cp[q][1] = e * r2;
+                cp[q][2] = e * dt2;
+              }
+            } else {
+              cp[q][0] += e;
+              if constexpr (GRAD) {
+                cp[q][1] = fma(e, r2, cp[q][1]);
+                cp[q][2] = fma(e, dt2, cp[q][2]);
+              }
+            }
+          }
+        }
+        if constexpr (TR != 0) {
+          double e = exp_l<CHECK>(fma(k.nomL, dt, k.chL * r2), tab);
+          if constexpr (TR == 2) e = (tj < ti[r]) ? e : 0.0;
+          if constexpr (VALID) e = (cv && rv[r]) ? e : 0.0;
+          racc[r][T0] += e;
+          if constexpr (GRAD) {
+            racc[r][4] = fma(e, dt, racc[r][4]);
+            racc[r][5] = fma(e, r2, racc[r][5]);
+          }
+        }
+      }
+    }
+    if constexpr (SYM && BG) {
+      // reduce-scatter the 4 x NSC column partials over the 32 lanes:
+      // xor 16 halves the columns, xor 8 halves again, xor 4/2/1 finish.
+      const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0;
+      double v2[2][NSC];
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+#pragma unroll
+        for (int c = 0; c < NSC; ++c) {
+          const double send = b4 ? cp[qq][c] : cp[2 + qq][c];
+          const double keep = b4 ? cp[2 + qq][c] : cp[qq][c];
+          v2[qq][c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+      }
+      double v1[NSC];
+#pragma unroll
+      for (int c = 0; c < NSC; ++c) {
+        const double send = b3 ? v2[0][c] : v2[1][c];
+        const double keep = b3 ? v2[1][c] : v2[0][c];
+        v1[c] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+#pragma unroll
+      for (int off = 4; off > 0; off >>= 1) {
+#pragma unroll
+        for (int c = 0; c < NSC; ++c) v1[c] += __shfl_xor_sync(0xffffffffu, v1[c], off);
+      }
+      if ((lane & 7) == 0) {
+        const int q = (b4 ? 2 : 0) + (b3 ? 1 : 0);
+#pragma unroll
+        for (int c = 0; c < NSC; ++c) s_col[(col0 + 4 * g + q) * NSC + c] = v1[c];
+      }
+    }
+  }
+}
+
+template <bool GRAD, bool SYM, bool CHECK, bool VALID>
+__device__ __forceinline__ void sym_dispatch(bool bg, int tr, const double* sx, const double* sy,
+                                             const double* st, int col0, int cnt,
+                                             const double (&xi)[kSymR], const double (&yi)[kSymR],
+                                             const double (&ti)[kSymR], const bool (&rv)[kSymR],
+                                             const PairConsts& k, const uint2* tab,
+                                             double (&racc)[kSymR][GRAD ? kNSumGrad : kNSumVal],
+                                             double* s_col) {
+#define STHK_SYM_CALL(B, T) \
+  sym_block<GRAD, SYM, B, T, CHECK, VALID>(sx, sy, st, col0, cnt, xi, yi, ti, rv, k, tab, racc, s_col)
+  if (bg) {
+    if (tr == 0) STHK_SYM_CALL(true, 0);
+    else if (tr == 1) STHK_SYM_CALL(true, 1);
+    else STHK_SYM_CALL(true, 2);
+  } else {
+    if (tr == 1) STHK_SYM_CALL(false, 1);
+    else if (tr == 2) STHK_SYM_CALL(false, 2);
+  }
+#undef STHK_SYM_CALL
+}
+
+template <bool GRAD>
+__global__ void __launch_bounds__(kTM, 3) sym_kernel(const PairArgs a) {
+  constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
+  constexpr int NSC = GRAD ? 3 : 1;
+  __shared__ __align__(128) double s_src[2][3][kTS];
+  __shared__ uint2 s_tab[256];
+  __shared__ double s_col[kTS * NSC];
+  __shared__ double s_red[4][NS][kTM];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ int s_item[2];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  s_tab[tid] = kExpTable[tid];
+  s_tab[tid + kTM] = kExpTable[tid + kTM];
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int n_items = *a.n_items;
+  const int64_t n = a.n;
+  uint32_t phase = 0;
+  unsigned long long cBg = 0, cTr = 0, cAny = 0, cExp = 0;
+
+  for (int iter = 0;; ++iter) {
+    if (tid == 0) s_item[iter & 1] = atomicAdd(a.work_counter, 1);
+    __syncthreads();
+    const int item = s_item[iter & 1];
+    if (item >= n_items) break;
+
+    const int2 it = a.items[item];
+    const int tile = it.x, chunk = it.y;
+    const int2 rg = a.ranges[tile];
+    const int64_t first = static_cast<int64_t>(tile) * kTM;
+    const int64_t last = min(first + kTM, n) - 1;
+    const int rows_real = static_cast<int>(last - first + 1);
+    const double tmin = a.t[first], tmax = a.t[last];
+    const double4 bt = a.tile_box[tile];
+    double xi[kSymR], yi[kSymR], ti[kSymR];
+    bool rv[kSymR];
+#pragma unroll
+    for (int r = 0; r < kSymR; ++r) {
+      const int64_t row = first + lane + 32 * r;
+      xi[r] = a.x[row];
+      yi[r] = a.y[row];
+      ti[r] = a.t[row];
+      rv[r] = row < n;
+    }
+    double racc[kSymR][NS];
+#pragma unroll
+    for (int r = 0; r < kSymR; ++r) {
+#pragma unroll
+      for (int q = 0; q < NS; ++q) racc[r][q] = 0.0;
+    }
+
+    int s_begin = max(rg.x, chunk * a.sc);
+    s_begin -= s_begin % kTS;
+    const int s_end = min(rg.y, (chunk + 1) * a.sc);
+    const int nst = (s_end - s_begin + kTS - 1) / kTS;
+
+    constexpr uint32_t kStageBytes = kTS * sizeof(double);
+    if (tid == 0 && nst > 0) {
+      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes);
+      tma_load_1d(s_src[0][0], a.x + s_begin, kStageBytes, &s_bar[0]);
+      tma_load_1d(s_src[0][1], a.y + s_begin, kStageBytes, &s_bar[0]);
+      tma_load_1d(s_src[0][2], a.t + s_begin, kStageBytes, &s_bar[0]);
+    }
+    for (int s = 0; s < nst; ++s) {
+      const int buf = s & 1;
+      // every thread is done with stage s-1 (its buffer and s_col)
+      __syncthreads();
+      if (tid == 0 && s + 1 < nst) {
+        const int nb = buf ^ 1;
+        const int64_t s0n = s_begin + static_cast<int64_t>(s + 1) * kTS;
+        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes);
+        tma_load_1d(s_src[nb][0], a.x + s0n, kStageBytes, &s_bar[nb]);
+        tma_load_1d(s_src[nb][1], a.y + s0n, kStageBytes, &s_bar[nb]);
+        tma_load_1d(s_src[nb][2], a.t + s0n, kStageBytes, &s_bar[nb]);
+      }
+      const int64_t s0 = s_begin + static_cast<int64_t>(s) * kTS;
+      const int cnt = static_cast<int>(min(static_cast<int64_t>(kTS), n - s0));
+      const bool diag = s0 == first;
+      const double4 bs = a.tile_box[s0 / kTS];
+      const double smin = a.t[s0], smax = a.t[s0 + cnt - 1];
+
+      const bool bg = !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
+      int tr;
+      if (smin >= tmax || smax < tmin - a.k.dT) tr = 0;
+      else if (smax < tmin) tr = 1;
+      else tr = 2;
+      const double dxm = fmax(bt.y - bs.x, bs.y - bt.x);
+      const double dym = fmax(bt.w - bs.z, bs.w - bt.z);
+      const double r2m = dxm * dxm + dym * dym;
+      const double dtm = fmax(tmax - smin, smax - tmin);
+      const bool safe = (!bg || a.k.cxL * r2m + a.k.ctL * (dtm * dtm) > kSafeExpL) &&
+                        (!tr || a.k.nomL * dtm + a.k.chL * r2m > kSafeExpL);
+
+      mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+
+      const double* sx = s_src[buf][0];
+      const double* sy = s_src[buf][1];
+      const double* st = s_src[buf][2];
+      const int col0 = warp * 32;
+      if (diag) {
+        sym_dispatch<GRAD, false, true, true>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
+                                              a.k, s_tab, racc, s_col);
+      } else if (rows_real < kTM) {
+        sym_dispatch<GRAD, true, true, true>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv, a.k,
+                                             s_tab, racc, s_col);
+      } else if (safe) {
+        sym_dispatch<GRAD, true, false, false>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
+                                               a.k, s_tab, racc, s_col);
+      } else {
+        sym_dispatch<GRAD, true, true, false>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
+                                              a.k, s_tab, racc, s_col);
+      }
+      if (!diag && bg) {
+        // column sums of source tile J: one fixed-point flush per column
+        __syncthreads();
+        const int64_t col = s0 + tid;
+#pragma unroll
+        for (int c = 0; c < NSC; ++c) {
+          fx_add(a.fx + static_cast<size_t>(2 * c) * a.npad + col,
+                 a.fx + static_cast<size_t>(2 * c + 1) * a.npad + col,
+                 s_col[tid * NSC + c] * a.fxq[c]);
+        }
+      }
+      if (tid == 0) {
+        const unsigned long long pr = static_cast<unsigned long long>(cnt) * rows_real;
+        if (diag) {
+          if (bg) cBg += pr;
+          if (tr) cTr += pr;
+          if (bg || tr) cAny += pr;
+          cExp += (bg ? pr : 0) + (tr ? pr : 0);
+        } else {
+          if (bg) cBg += 2 * pr;
+          if (tr) cTr += pr;
+          cAny += bg ? 2 * pr : (tr ? pr : 0);
+          cExp += (bg ? pr : 0) + (tr ? pr : 0);
+        }
+      }
+    }
+
+    // combine the 4 warps' row partials in a fixed order, then flush
+#pragma unroll
+    for (int r = 0; r < kSymR; ++r) {
+#pragma unroll
+      for (int q = 0; q < NS; ++q) s_red[warp][q][lane + 32 * r] = racc[r][q];
+    }
+    __syncthreads();
+    double v[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      v[q] = ((s_red[0][q][tid] + s_red[1][q][tid]) + s_red[2][q][tid]) + s_red[3][q][tid];
+    }
+    store_row_sums<GRAD>(a, chunk, first + tid, v);
+  }
+
+  if (tid == 0 && a.pair_counts) {
+    atomicAdd(&a.pair_counts[0], cBg);
+    atomicAdd(&a.pair_counts[1], cTr);
+    atomicAdd(&a.pair_counts[2], cAny);
+    atomicAdd(&a.pair_counts[3], cExp);
   }
 }
 
@@ -337,16 +665,21 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
   for (int q = 0; q < kRB / kFinThreads; ++q) {
     const int64_t r = base + q * kFinThreads + tid;
     if (r >= a.row1) break;
-    const int2 rg = a.ranges[r / kTM];
-    const int c0 = a.dense ? 0 : rg.x / a.sc;
-    const int c1 = a.dense ? a.nchunks - 1 : (rg.y - 1) / a.sc;
+    constexpr int NB = GRAD ? 3 : 1;
     double s[NS];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) s[k] = 0.0;
-    for (int c = c0; c <= c1; ++c) {
-      const double* p = a.partial + static_cast<size_t>(c) * NS * a.npad + r;
+    for (int k = 0; k < NB; ++k) {
+      s[k] = fx_value(a.fx[static_cast<size_t>(2 * k) * a.npad + r],
+                      a.fx[static_cast<size_t>(2 * k + 1) * a.npad + r]) /
+             a.fxq[k];
+    }
+    const int2 cr = a.crange[r / kTM];
 #pragma unroll
-      for (int k = 0; k < NS; ++k) s[k] += p[static_cast<size_t>(k) * a.npad];
+    for (int k = NB; k < NS; ++k) s[k] = 0.0;
+    for (int c = cr.x; c <= cr.y; ++c) {
+      const double* p = a.tpart + static_cast<size_t>(c) * (NS - NB) * a.npad + r;
+#pragma unroll
+      for (int k = NB; k < NS; ++k) s[k] += p[static_cast<size_t>(k - NB) * a.npad];
     }
     const double sB = s[0];
     const double sT = GRAD ? s[3] : s[1];
@@ -453,9 +786,14 @@ cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_pairs(const PairArgs& a, bool grad, int grid, cudaStream_t stream) {
-  if (grad) pair_kernel<true><<<grid, kTM, 0, stream>>>(a);
-  else pair_kernel<false><<<grid, kTM, 0, stream>>>(a);
+cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaStream_t stream) {
+  if (mode == kSym) {
+    if (grad) sym_kernel<true><<<grid, kTM, 0, stream>>>(a);
+    else sym_kernel<false><<<grid, kTM, 0, stream>>>(a);
+  } else {
+    if (grad) pair_kernel<true><<<grid, kTM, 0, stream>>>(a);
+    else pair_kernel<false><<<grid, kTM, 0, stream>>>(a);
+  }
   return cudaGetLastError();
 }
 
@@ -473,10 +811,15 @@ cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* o
   return cudaGetLastError();
 }
 
-int pair_kernel_occupancy(bool grad) {
+int pair_kernel_occupancy(bool grad, int mode) {
   int occ = 0;
-  if (grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<true>, kTM, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<false>, kTM, 0);
+  if (mode == kSym) {
+    if (grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel<true>, kTM, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel<false>, kTM, 0);
+  } else {
+    if (grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<true>, kTM, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<false>, kTM, 0);
+  }
   return occ > 0 ? occ : 1;
 }
 

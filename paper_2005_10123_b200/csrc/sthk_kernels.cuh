@@ -9,18 +9,28 @@
 namespace sthk {
 
 constexpr int kTM = 128;    // target rows per tile (= threads per pair CTA)
-constexpr int kTS = 128;    // sources per shared-memory stage
+constexpr int kTS = 128;    // sources per shared-memory stage (= tile size)
 constexpr int kRB = 1024;   // rows per reduction block (multi-GPU partition unit)
 constexpr int kFinThreads = 256;
 constexpr int kNSumGrad = 6;  // S_B, S_Br, S_Bt, S_T, S_Tt, S_Tr
 constexpr int kNSumVal = 2;   // S_B, S_T
 constexpr int kNOut = 8;      // loglik, 6 gradient terms, degenerate-row count
+constexpr int kNCounts = 4;   // pair counters: bg, trigger, any (ordered), exps
 
 // Exponent cut (natural units) used for exact culling: every pair whose
 // time-only exponent bound is below -kCullExponent has exp_l(...) == +0
 // exactly (exp_l flushes below -708.40), so skipping it leaves every sum
 // bitwise unchanged.
 constexpr double kCullExponent = 709.0;
+
+// Pair-kernel variants.
+//  kRows: each CTA owns 128 target rows and sweeps every live source
+//         (ordered pairs; row sums only).
+//  kSym:  the background term is symmetric (b_ij = b_ji), so each CTA
+//         sweeps only the source tiles J <= I; for J < I every background exp
+//         is added to the row sums of I and the column sums of J. The
+//         trigger term stays one-directional (t_j < t_i implies j < i).
+enum PairMode : int { kRows = 0, kSym = 1 };
 
 // Exponent constants are pre-multiplied by kExpL = 256/ln2 ("L units", see
 // exp_l in sthk_device.cuh).
@@ -39,15 +49,21 @@ struct PlanArgs {
   int tile0, tile1;     // this shard's row tiles [tile0, tile1)
   double dB, dT;
   int dense;
+  int sym;              // kSym: the live range ends at the tile's own end
   int sc;               // sources per chunk (multiple of kTS)
   int nchunks;          // ceil(n / sc)
   int2* ranges;         // [ntiles] live source range [lo, hi) per row tile
+  int2* crange;         // [ntiles] chunk range [c0, c1] per row tile
   int* counts;          // [ntiles] items per row tile (scratch)
   int2* items;          // (row tile, chunk) work list
   int* n_items;         // device scalar
   int* work_counter;    // device scalar, reset here
 };
 
+// Background sums (k = 0..2: S_B, S_Br, S_Bt) are fixed point,
+// fx[(k * 2 + h) * npad + row], h = 0 hi / 1 lo, scaled by fxq[k] before
+// conversion so they are O(1) per pair; trigger sums are double partials
+// tpart[(chunk * NT + k) * npad + row].
 struct PairArgs {
   const double* x;
   const double* y;
@@ -61,8 +77,10 @@ struct PairArgs {
   const int2* items;
   const int* n_items;
   int* work_counter;
-  double* partial;      // [nchunks][nsum][npad]
-  unsigned long long* pair_counts;  // [3]: bg, tr, any (tile granularity)
+  unsigned long long* fx;
+  double fxq[kNSumGrad];
+  double* tpart;        // trigger partials [nchunks][3 or 1][npad]
+  unsigned long long* pair_counts;  // [kNCounts] (tile granularity)
 };
 
 struct FinArgs {
@@ -76,11 +94,10 @@ struct FinArgs {
   double bgNorm;        // (2pi)^-1.5 / (tauX^2 tauT)       kernels.hpp:79
   double trNorm;        // theta omega / (2 pi h^2)          kernels.hpp:82
   double cT;            // omega / (2 pi h^2)  (d lambda / d theta)
-  int sc;
-  int nchunks;
-  int dense;
-  const int2* ranges;
-  const double* partial;
+  const unsigned long long* fx;
+  double fxq[kNSumGrad];
+  const double* tpart;
+  const int2* crange;
   double* per_event;    // nullable
   double* block_partial;  // [nblocks_total][kNOut]
 };
@@ -89,11 +106,11 @@ struct FinArgs {
 cudaError_t launch_tile_boxes(const double* x, const double* y, int64_t n, double4* box,
                               cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
-cudaError_t launch_pairs(const PairArgs& a, bool grad, int grid, cudaStream_t stream);
+cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaStream_t stream);
 cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream);
 cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,
                              cudaStream_t stream);
-// Resident CTAs per SM of the pair kernel (for the persistent grid size).
-int pair_kernel_occupancy(bool grad);
+// Resident CTAs per SM of a pair kernel (for the persistent grid size).
+int pair_kernel_occupancy(bool grad, int mode);
 
 }  // namespace sthk

@@ -172,6 +172,10 @@ class Engine:
     def set_dense(self, on: bool) -> None:
         self._check(self._lib.sthk_set_dense(self._h, int(on)), "sthk_set_dense")
 
+    def set_kernel(self, mode: int) -> None:
+        """0 = rows (ordered pairs), 1 = symmetric background (default)."""
+        self._check(self._lib.sthk_set_kernel(self._h, int(mode)), "sthk_set_kernel")
+
     def set_virtual_shards(self, k: int) -> None:
         self._check(self._lib.sthk_set_virtual_shards(self._h, int(k)), "sthk_set_virtual_shards")
 

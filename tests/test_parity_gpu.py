@@ -169,3 +169,46 @@ def test_ties_strict_time_rule(engine):
     assert np.sum(np.diff(t) == 0) > 0
     for p in (pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695), pk.Params(1, 1.6, 14, 0.1, 1, 1)):
         _check(engine, ev2, p)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_both_kernels_vs_oracle(engine, mode):
+    """Rows kernel (ordered pairs) and symmetric-background kernel each match
+    the oracle on C1 and on DC-shaped data at both thetas."""
+    engine.set_kernel(mode)
+    try:
+        ev = pk.generateBenchmarkCloud(1000, pk.SimWindow(0, 4, 0, 4, 60), 1000)
+        _check(engine, ev, pk.Params(0.6, 0.9, 3.0, 0.5, 1.1, 0.35))
+        ev2, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                           pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                           keep=5000)
+        for p in (pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695), pk.Params(1, 1.6, 14, 0.1, 1, 1)):
+            _check(engine, ev2, p)
+        rng = np.random.default_rng(99)
+        for n in (1, 2, 7, 129, 300):
+            evr = pk.generateBenchmarkCloud(n, pk.SimWindow(0, 4, 0, 4, 60), 500 + n)
+            _check(engine, evr, _rand_params(rng))
+    finally:
+        engine.set_kernel(1)
+
+
+def test_kernel_modes_agree_and_cull_exact(engine):
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=30000)
+    engine.load(ev)
+    for p in (pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695), pk.Params(1, 1.6, 14, 0.1, 1, 1)):
+        engine.set_params(p)
+        res = {}
+        for mode in (0, 1):
+            engine.set_kernel(mode)
+            engine.set_dense(False)
+            a = engine.loglik_grad()
+            engine.set_dense(True)
+            b = engine.loglik_grad()
+            engine.set_dense(False)
+            assert a[0] == b[0] and np.array_equal(a[2], b[2])  # culling is exact
+            res[mode] = a
+        engine.set_kernel(1)
+        assert abs(res[0][0] - res[1][0]) <= 1e-13 * abs(res[0][0])
+        assert np.allclose(res[0][2], res[1][2], rtol=1e-11, atol=0)
