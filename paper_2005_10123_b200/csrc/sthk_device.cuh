@@ -138,6 +138,36 @@ __device__ __forceinline__ double exp_l(double x, const uint2* __restrict__ tab)
   return res;
 }
 
+// N independent exp_l evaluations written in lockstep (stage by stage), so
+// the dependent 8-instruction chains are interleaved in program order and the
+// FP64 pipe's latency is covered by N-way ILP even at low occupancy.
+template <bool CHECK, int N>
+__device__ __forceinline__ void exp_l_batch(const double (&x)[N], double (&out)[N],
+                                            const uint2* __restrict__ tab) {
+  double t[N], u[N], q[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) t[i] = x[i] + kRoundMagic;
+#pragma unroll
+  for (int i = 0; i < N; ++i) u[i] = x[i] - (t[i] - kRoundMagic);
+#pragma unroll
+  for (int i = 0; i < N; ++i) q[i] = fma(kE4, u[i], kE3);
+#pragma unroll
+  for (int i = 0; i < N; ++i) q[i] = fma(q[i], u[i], kE2);
+#pragma unroll
+  for (int i = 0; i < N; ++i) q[i] = fma(q[i], u[i], kE1);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const double p = q[i] * u[i];
+    const long long tb = __double_as_longlong(t[i]);
+    const int k = static_cast<int>(tb);
+    const uint2 tj = tab[k & 255];
+    const double ts =
+        __hiloint2double(static_cast<int>(tj.y) + (k << 12), static_cast<int>(tj.x));
+    const double res = fma(ts, p, ts);
+    out[i] = CHECK ? (tb < kFlushBits ? 0.0 : res) : res;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Deterministic fixed-point accumulation.
 //

@@ -340,74 +340,93 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
 //   * J == I ("diag" stage): all ordered pairs of the tile, rows only.
 // Row partials of the 4 warps are combined in a fixed order at item end.
 constexpr int kSymR = 4;  // rows per thread
+#ifndef STHK_SYM_G
+#define STHK_SYM_G 4      // columns per shuffle reduce-scatter group (2 or 4)
+#endif
+#ifndef STHK_SYM_MINB
+#define STHK_SYM_MINB 3   // resident sym CTAs per SM the register budget targets
+#endif
+constexpr int kSymG = STHK_SYM_G;
 
 template <bool GRAD, bool SYM, bool BG, int TR, bool CHECK, bool VALID>
-__device__ __forceinline__ void sym_block(const double* __restrict__ sx,
+__device__ __forceinline__ void sym_pairs(int g, const double* __restrict__ sx,
                                           const double* __restrict__ sy,
                                           const double* __restrict__ st, int col0, int cnt,
                                           const double (&xi)[kSymR], const double (&yi)[kSymR],
                                           const double (&ti)[kSymR], const bool (&rv)[kSymR],
                                           const PairConsts& k, const uint2* __restrict__ tab,
                                           double (&racc)[kSymR][GRAD ? kNSumGrad : kNSumVal],
-                                          double* __restrict__ s_col) {
-  constexpr int NSC = GRAD ? 3 : 1;
+                                          double (&cp)[kSymG][GRAD ? 3 : 1]) {
   constexpr int T0 = GRAD ? 3 : 1;
-  const int lane = threadIdx.x & 31;
-#pragma unroll 1
-  for (int g = 0; g < 8; ++g) {
-    double cp[4][NSC];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = col0 + 4 * g + q;
-      const double xj = sx[j], yj = sy[j], tj = st[j];
-      bool cv = true;
-      if constexpr (VALID) cv = j < cnt;
+  for (int q = 0; q < kSymG; ++q) {
+    const int j = col0 + kSymG * g + q;
+    const double xj = sx[j], yj = sy[j], tj = st[j];
+    bool cv = true;
+    if constexpr (VALID) cv = j < cnt;
+    // geometry for the 4 rows, then the exps in lockstep
+    double dt[kSymR], r2[kSymR], dt2[kSymR], arg[kSymR], e[kSymR];
+#pragma unroll
+    for (int r = 0; r < kSymR; ++r) {
+      const double dx = xi[r] - xj;
+      const double dy = yi[r] - yj;
+      dt[r] = ti[r] - tj;
+      r2[r] = fma(dx, dx, dy * dy);
+    }
+    if constexpr (BG) {
 #pragma unroll
       for (int r = 0; r < kSymR; ++r) {
-        const double dx = xi[r] - xj;
-        const double dy = yi[r] - yj;
-        const double dt = ti[r] - tj;
-        const double r2 = fma(dx, dx, dy * dy);
-        if constexpr (BG) {
-          const double dt2 = dt * dt;
-          double e = exp_l<CHECK>(fma(k.cxL, r2, k.ctL * dt2), tab);
-          if constexpr (VALID) e = (cv && rv[r]) ? e : 0.0;
-          racc[r][0] += e;
-          if constexpr (GRAD) {
-            racc[r][1] = fma(e, r2, racc[r][1]);
-            racc[r][2] = fma(e, dt2, racc[r][2]);
-          }
-          if constexpr (SYM) {
-            if (r == 0) {
-              cp[q][0] = e;
-              if constexpr (GRAD) {
-                cp[q][1] = e * r2;
-                cp[q][2] = e * dt2;
-              }
-            } else {
-              cp[q][0] += e;
-              if constexpr (GRAD) {
-                cp[q][1] = fma(e, r2, cp[q][1]);
-                cp[q][2] = fma(e, dt2, cp[q][2]);
-              }
-            }
-          }
+        dt2[r] = dt[r] * dt[r];
+        arg[r] = fma(k.cxL, r2[r], k.ctL * dt2[r]);
+      }
+      exp_l_batch<CHECK>(arg, e, tab);
+#pragma unroll
+      for (int r = 0; r < kSymR; ++r) {
+        if constexpr (VALID) e[r] = (cv && rv[r]) ? e[r] : 0.0;
+        racc[r][0] += e[r];
+        if constexpr (GRAD) {
+          racc[r][1] = fma(e[r], r2[r], racc[r][1]);
+          racc[r][2] = fma(e[r], dt2[r], racc[r][2]);
         }
-        if constexpr (TR != 0) {
-          double e = exp_l<CHECK>(fma(k.nomL, dt, k.chL * r2), tab);
-          if constexpr (TR == 2) e = (tj < ti[r]) ? e : 0.0;
-          if constexpr (VALID) e = (cv && rv[r]) ? e : 0.0;
-          racc[r][T0] += e;
-          if constexpr (GRAD) {
-            racc[r][4] = fma(e, dt, racc[r][4]);
-            racc[r][5] = fma(e, r2, racc[r][5]);
-          }
+      }
+      if constexpr (SYM) {
+        cp[q][0] = (e[0] + e[1]) + (e[2] + e[3]);
+        if constexpr (GRAD) {
+          cp[q][1] = fma(e[3], r2[3], fma(e[2], r2[2], fma(e[1], r2[1], e[0] * r2[0])));
+          cp[q][2] = fma(e[3], dt2[3], fma(e[2], dt2[2], fma(e[1], dt2[1], e[0] * dt2[0])));
         }
       }
     }
-    if constexpr (SYM && BG) {
-      // reduce-scatter the 4 x NSC column partials over the 32 lanes:
-      // xor 16 halves the columns, xor 8 halves again, xor 4/2/1 finish.
+    if constexpr (TR != 0) {
+#pragma unroll
+      for (int r = 0; r < kSymR; ++r) arg[r] = fma(k.nomL, dt[r], k.chL * r2[r]);
+      exp_l_batch<CHECK>(arg, e, tab);
+#pragma unroll
+      for (int r = 0; r < kSymR; ++r) {
+        if constexpr (TR == 2) e[r] = (tj < ti[r]) ? e[r] : 0.0;
+        if constexpr (VALID) e[r] = (cv && rv[r]) ? e[r] : 0.0;
+        racc[r][T0] += e[r];
+        if constexpr (GRAD) {
+          racc[r][4] = fma(e[r], dt[r], racc[r][4]);
+          racc[r][5] = fma(e[r], r2[r], racc[r][5]);
+        }
+      }
+    }
+  }
+}
+
+template <bool GRAD, bool SYM, bool BG>
+__device__ __forceinline__ void sym_reduce(int g, int col0, double (&cp)[kSymG][GRAD ? 3 : 1],
+                                           double* __restrict__ s_col) {
+  constexpr int NSC = GRAD ? 3 : 1;
+  const int lane = threadIdx.x & 31;
+  if constexpr (SYM && BG) {
+    // reduce-scatter the kSymG x NSC column partials over the 32 lanes:
+    // the first log2(kSymG) xor steps halve the columns a lane keeps, the
+    // remaining steps finish the butterfly. All lanes holding a column end
+    // with bitwise-identical totals (each add is commutative).
+    double v1[NSC];
+    if constexpr (kSymG == 4) {
       const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0;
       double v2[2][NSC];
 #pragma unroll
@@ -419,7 +438,6 @@ __device__ __forceinline__ void sym_block(const double* __restrict__ sx,
           v2[qq][c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
         }
       }
-      double v1[NSC];
 #pragma unroll
       for (int c = 0; c < NSC; ++c) {
         const double send = b3 ? v2[0][c] : v2[1][c];
@@ -434,9 +452,49 @@ __device__ __forceinline__ void sym_block(const double* __restrict__ sx,
       if ((lane & 7) == 0) {
         const int q = (b4 ? 2 : 0) + (b3 ? 1 : 0);
 #pragma unroll
-        for (int c = 0; c < NSC; ++c) s_col[(col0 + 4 * g + q) * NSC + c] = v1[c];
+        for (int c = 0; c < NSC; ++c) s_col[(col0 + kSymG * g + q) * NSC + c] = v1[c];
+      }
+    } else {
+      const bool b4 = (lane & 16) != 0;
+#pragma unroll
+      for (int c = 0; c < NSC; ++c) {
+        const double send = b4 ? cp[0][c] : cp[1][c];
+        const double keep = b4 ? cp[1][c] : cp[0][c];
+        v1[c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) {
+#pragma unroll
+        for (int c = 0; c < NSC; ++c) v1[c] += __shfl_xor_sync(0xffffffffu, v1[c], off);
+      }
+      if ((lane & 15) == 0) {
+        const int q = b4 ? 1 : 0;
+#pragma unroll
+        for (int c = 0; c < NSC; ++c) s_col[(col0 + kSymG * g + q) * NSC + c] = v1[c];
       }
     }
+  }
+}
+
+// One stage for one warp: 32 columns x this thread's 4 rows, in groups of
+// kSymG columns, each group's column partials reduce-scattered right away.
+// (Interleaving group g's reduction with group g+1's pair math doubles the
+// live registers and spills; measured slower.)
+template <bool GRAD, bool SYM, bool BG, int TR, bool CHECK, bool VALID>
+__device__ __forceinline__ void sym_block(const double* __restrict__ sx,
+                                          const double* __restrict__ sy,
+                                          const double* __restrict__ st, int col0, int cnt,
+                                          const double (&xi)[kSymR], const double (&yi)[kSymR],
+                                          const double (&ti)[kSymR], const bool (&rv)[kSymR],
+                                          const PairConsts& k, const uint2* __restrict__ tab,
+                                          double (&racc)[kSymR][GRAD ? kNSumGrad : kNSumVal],
+                                          double* __restrict__ s_col) {
+#pragma unroll 1
+  for (int g = 0; g < 32 / kSymG; ++g) {
+    double cp[kSymG][GRAD ? 3 : 1];
+    sym_pairs<GRAD, SYM, BG, TR, CHECK, VALID>(g, sx, sy, st, col0, cnt, xi, yi, ti, rv, k, tab,
+                                               racc, cp);
+    sym_reduce<GRAD, SYM, BG>(g, col0, cp, s_col);
   }
 }
 
@@ -450,6 +508,9 @@ __device__ __forceinline__ void sym_dispatch(bool bg, int tr, const double* sx, 
                                              double* s_col) {
 #define STHK_SYM_CALL(B, T) \
   sym_block<GRAD, SYM, B, T, CHECK, VALID>(sx, sy, st, col0, cnt, xi, yi, ti, rv, k, tab, racc, s_col)
+#ifdef STHK_SYM_NO_TRIGGER_EXPERIMENT
+  tr = 0;  // timing experiment only: drops the trigger term
+#endif
   if (bg) {
     if (tr == 0) STHK_SYM_CALL(true, 0);
     else if (tr == 1) STHK_SYM_CALL(true, 1);
@@ -462,7 +523,7 @@ __device__ __forceinline__ void sym_dispatch(bool bg, int tr, const double* sx, 
 }
 
 template <bool GRAD>
-__global__ void __launch_bounds__(kTM, 3) sym_kernel(const PairArgs a) {
+__global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs a) {
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   constexpr int NSC = GRAD ? 3 : 1;
   __shared__ __align__(128) double s_src[2][3][kTS];
