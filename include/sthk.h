@@ -107,8 +107,11 @@ typedef struct sthk_stats {
   int32_t work_items;        /* live (row tile, chunk) items of the last eval */
   int32_t n_devices;         /* devices driven by this handle */
   int32_t rank, world;       /* rank-mode coordinates (0, 1 otherwise) */
-  int64_t exp_evals;         /* exps evaluated by the last pair kernel(s) (a
-                                symmetric background exp serves 2 ordered pairs) */
+  /* work executed by the last pair kernel(s): in symmetric mode one
+   * background exp serves 2 ordered pairs (pairs_bg counts ordered pairs) */
+  int64_t exec_bg;           /* background exps evaluated */
+  int64_t exec_geom;         /* pair geometries (dx, dy, dt, r^2) evaluated */
+  int64_t exec_sym;          /* background pairs also accumulated into columns */
   int32_t kernel_mode;       /* STHK_KERNEL_ROWS or STHK_KERNEL_SYM */
   int32_t reserved;
 } sthk_stats;

@@ -35,7 +35,9 @@ class StatsStruct(ctypes.Structure):
         ("n_devices", ctypes.c_int32),
         ("rank", ctypes.c_int32),
         ("world", ctypes.c_int32),
-        ("exp_evals", c_int64),
+        ("exec_bg", c_int64),
+        ("exec_geom", c_int64),
+        ("exec_sym", c_int64),
         ("kernel_mode", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
     ]

@@ -816,7 +816,9 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
       out->pairs_bg += static_cast<int64_t>(s.h_counts[0]);
       out->pairs_tr += static_cast<int64_t>(s.h_counts[1]);
       out->pairs_any += static_cast<int64_t>(s.h_counts[2]);
-      out->exp_evals += static_cast<int64_t>(s.h_counts[3]);
+      out->exec_bg += static_cast<int64_t>(s.h_counts[3]);
+      out->exec_geom += static_cast<int64_t>(s.h_counts[4]);
+      out->exec_sym += static_cast<int64_t>(s.h_counts[5]);
       if (e->timing && s.row1 > s.row0) {
         float a = 0, b = 0;
         set_dev(s);

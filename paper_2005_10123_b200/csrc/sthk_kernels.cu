@@ -321,7 +321,8 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
     atomicAdd(&a.pair_counts[0], cBg);
     atomicAdd(&a.pair_counts[1], cTr);
     atomicAdd(&a.pair_counts[2], cAny);
-    atomicAdd(&a.pair_counts[3], cBg + cTr);
+    atomicAdd(&a.pair_counts[3], cBg);   // background exps executed
+    atomicAdd(&a.pair_counts[4], cAny);  // pair geometries executed
   }
 }
 
@@ -547,7 +548,9 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
   const int n_items = *a.n_items;
   const int64_t n = a.n;
   uint32_t phase = 0;
-  unsigned long long cBg = 0, cTr = 0, cAny = 0, cExp = 0;
+  // ordered pairs covered (bg, trigger, any) and work executed (background
+  // exps, pair geometries, symmetric pairs with a column accumulation)
+  unsigned long long cBg = 0, cTr = 0, cAny = 0, xBg = 0, xGeo = 0, xSym = 0;
 
   for (int iter = 0;; ++iter) {
     if (tid == 0) s_item[iter & 1] = atomicAdd(a.work_counter, 1);
@@ -659,12 +662,15 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
           if (bg) cBg += pr;
           if (tr) cTr += pr;
           if (bg || tr) cAny += pr;
-          cExp += (bg ? pr : 0) + (tr ? pr : 0);
+          if (bg) xBg += pr;
+          if (bg || tr) xGeo += pr;
         } else {
           if (bg) cBg += 2 * pr;
           if (tr) cTr += pr;
           cAny += bg ? 2 * pr : (tr ? pr : 0);
-          cExp += (bg ? pr : 0) + (tr ? pr : 0);
+          if (bg) xBg += pr;
+          if (bg) xSym += pr;
+          if (bg || tr) xGeo += pr;
         }
       }
     }
@@ -688,7 +694,9 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
     atomicAdd(&a.pair_counts[0], cBg);
     atomicAdd(&a.pair_counts[1], cTr);
     atomicAdd(&a.pair_counts[2], cAny);
-    atomicAdd(&a.pair_counts[3], cExp);
+    atomicAdd(&a.pair_counts[3], xBg);
+    atomicAdd(&a.pair_counts[4], xGeo);
+    atomicAdd(&a.pair_counts[5], xSym);
   }
 }
 

@@ -15,7 +15,9 @@ constexpr int kFinThreads = 256;
 constexpr int kNSumGrad = 6;  // S_B, S_Br, S_Bt, S_T, S_Tt, S_Tr
 constexpr int kNSumVal = 2;   // S_B, S_T
 constexpr int kNOut = 8;      // loglik, 6 gradient terms, degenerate-row count
-constexpr int kNCounts = 4;   // pair counters: bg, trigger, any (ordered), exps
+// pair counters: ordered pairs covered (bg, trigger, any), then work executed
+// (background exps, pair geometries, symmetric column accumulations)
+constexpr int kNCounts = 6;
 
 // Exponent cut (natural units) used for exact culling: every pair whose
 // time-only exponent bound is below -kCullExponent has exp_l(...) == +0
