@@ -241,6 +241,8 @@ def main():
     ht = torch.from_numpy(np.array(ev.ts())).pin_memory()
     eng.load_events(hx.numpy(), hy.numpy(), ht.numpy(), ev.windowEnd())
     eng.set_timing(True)
+    # every timed step is a full evaluation: no background-sum reuse
+    eng.set_background_cache(False)
     stream = torch.cuda.ExternalStream(eng.stream(0))
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
@@ -312,6 +314,30 @@ def main():
         return max_over_ranks(el)
 
     e2e_s = e2e(THETA_POST, args.steps)
+
+    # MH-chain-style steps (informational, not the headline): tauX/tauT fixed,
+    # one of (mu0, theta, omega, h) moves per step, background sums reused.
+    def mh_style(steps):
+        eng.set_background_cache(True)
+        rng = np.random.default_rng(1)
+        theta = list(THETA_POST)
+        eng.set_params(theta)
+        eng.loglik()
+        barrier()
+        t0 = time.perf_counter()
+        hits = 0
+        for _ in range(steps):
+            k = [0, 3, 4, 5][int(rng.integers(4))]
+            cand = list(theta)
+            cand[k] = theta[k] * float(np.exp(0.01 * rng.standard_normal()))
+            eng.set_params(cand)
+            eng.loglik()
+            hits += eng.stats()["cache_hit"]
+        el = time.perf_counter() - t0
+        eng.set_background_cache(False)
+        return max_over_ranks(el), hits
+
+    mh_s, mh_hits = mh_style(args.steps)
 
     if rank != 0:
         eng.close()
@@ -400,6 +426,12 @@ def main():
                 "pairs": {"ordered_bg": st2["pairs_bg"], "trigger": st2["pairs_tr"], "bg_exps_executed": st2["exec_bg"]},
                 "loglik": sec_run["loglik"],
             },
+        },
+        "mh_style_loglik": {
+            "evals_per_s": K / mh_s, "unit": "evals/s", "cache_hits": mh_hits, "steps": K,
+            "what": "wall-clock loglik (value) calls with one of mu0/theta/omega/h perturbed per "
+                    "step (tauX, tauT fixed as in the reference sampler): background sums reused, "
+                    "trigger band swept; bitwise identical to full evaluations",
         },
         "clocks": clocks,
         "fp64_peak_tflops": {"best": peak_best, "mean": peak_mean},

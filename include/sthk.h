@@ -113,7 +113,8 @@ typedef struct sthk_stats {
   int64_t exec_geom;         /* pair geometries (dx, dy, dt, r^2) evaluated */
   int64_t exec_sym;          /* background pairs also accumulated into columns */
   int32_t kernel_mode;       /* STHK_KERNEL_ROWS or STHK_KERNEL_SYM */
-  int32_t reserved;
+  int32_t cache_hit;         /* 1 if the last evaluation reused cached
+                                background sums (trigger-only sweep) */
 } sthk_stats;
 
 int sthk_set_timing(sthk_engine* e, int enable);
@@ -127,6 +128,13 @@ int sthk_set_dense(sthk_engine* e, int dense);
  * pair once and adds it to both events' sums (b_ij = b_ji); STHK_KERNEL_ROWS
  * sweeps ordered pairs per target row. Both are deterministic; they agree to
  * rounding (different summation grouping), not bitwise. */
+/* Background-sum cache (default on). The background sums depend only on the
+ * events, tauX and tauT, which the reference MH sampler keeps fixed for a
+ * whole chain (sampler.cpp:48-49); while they are unchanged an evaluation
+ * sweeps only the trigger band. Results are bitwise identical with the cache
+ * on or off (fixed chunk grid). Benchmarks of full evaluations turn it off. */
+int sthk_set_background_cache(sthk_engine* e, int enable);
+
 #define STHK_KERNEL_ROWS 0
 #define STHK_KERNEL_SYM 1
 int sthk_set_kernel(sthk_engine* e, int mode);

@@ -39,7 +39,7 @@ class StatsStruct(ctypes.Structure):
         ("exec_geom", c_int64),
         ("exec_sym", c_int64),
         ("kernel_mode", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("cache_hit", ctypes.c_int32),
     ]
 
 
@@ -64,6 +64,7 @@ SIGNATURES = [
     ("sthk_set_dense", c_int, [c_void_p, c_int]),
     ("sthk_set_virtual_shards", c_int, [c_void_p, c_int]),
     ("sthk_set_kernel", c_int, [c_void_p, c_int]),
+    ("sthk_set_background_cache", c_int, [c_void_p, c_int]),
     ("sthk_measure_fp64_peak", c_int, [c_int, c_int, _DPTR, _DPTR]),
     ("sthk_plan_partition", c_int, [_DPTR, c_int64, _DPTR, c_int, c_int, _IPTR, _IPTR]),
     ("sthk_last_error", c_char_p, [c_void_p]),

@@ -120,6 +120,16 @@ struct sthk_engine {
   bool loaded = false, has_params = false;
   bool timing = false, dense = false;
   int mode = sthk::kSym;   // pair-kernel variant (sthk_set_kernel)
+  // Background-sum cache: S_B (and S_Br, S_Bt) depend only on the events,
+  // tauX, tauT -- fixed for a whole MH chain (sampler.cpp:48-49) -- so while
+  // they are unchanged an evaluation sweeps only the trigger band. The
+  // fixed chunk grid makes the cached path bitwise identical to a fresh one.
+  bool bg_cache = true;
+  bool cache_valid = false, cache_grad = false, last_cache_hit = false;
+  uint64_t load_gen = 0, cache_gen = 0;
+  double cache_tx = 0, cache_tt = 0;
+  int cache_mode = -1;
+  bool cache_dense = false;
   int virtual_shards = 1;  // testing: partition rows over k shards on one device
   std::string err;
   bool pending = false, last_grad = false, last_pe = false;
@@ -128,7 +138,7 @@ struct sthk_engine {
 
 namespace {
 
-constexpr int kItemsTarget = 4096;
+constexpr int kChunksTarget = 48;  // source chunks across N (work-item granularity)
 
 void set_dev(const Slot& s) { ck(cudaSetDevice(s.dev), "cudaSetDevice"); }
 
@@ -234,6 +244,14 @@ struct PlanInput {
   bool sym;
 };
 
+int chunk_size(int64_t n, int64_t npad) {
+  int64_t sc = (n + kChunksTarget - 1) / kChunksTarget;
+  sc = (sc + kTS - 1) / kTS * kTS;
+  sc = std::max<int64_t>(sc, 4 * kTS);
+  sc = std::min<int64_t>(sc, npad);
+  return static_cast<int>(sc);
+}
+
 EvalPlan make_plan(const PlanInput& e, int shards) {
   EvalPlan pl;
   const double* p = e.p;
@@ -249,25 +267,13 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   pl.k.dB = e.dense ? inf : dB;
   pl.k.dT = e.dense ? inf : dT;
 
-  // Chunk size from the (culled) mean live width of sampled tiles. Depends
-  // only on (events, params): identical on every rank and device count.
+  // Chunk size: a function of N only (never of the parameters, the device
+  // count or the culling mode). Partial sums are grouped per (tile, chunk), so
+  // a fixed chunk grid makes every evaluation path -- fused, trigger-only
+  // over a cached background, culled or dense, 1..k devices -- produce the
+  // same partials and hence bitwise-identical results.
   const int64_t n = e.n;
-  const int64_t ntiles = (n + kTM - 1) / kTM;
-  const int samples = static_cast<int>(std::min<int64_t>(ntiles, 64));
-  double wsum = 0.0;
-  for (int s = 0; s < samples; ++s) {
-    const int64_t tile = samples == 1 ? 0 : (ntiles - 1) * s / (samples - 1);
-    const int64_t first = tile * kTM, last = std::min(first + kTM, n) - 1;
-    const int64_t lo = std::min(lb(e.ht, n, e.ht[first] - std::max(dB, dT)), first);
-    const int64_t hi = e.sym ? last + 1 : std::max(ub(e.ht, n, e.ht[last] + dB), last + 1);
-    wsum += static_cast<double>(hi - lo);
-  }
-  const double wmean = wsum / samples;
-  double sc = wmean * static_cast<double>(ntiles) / kItemsTarget;
-  sc = std::ceil(sc / kTS) * kTS;
-  sc = std::max<double>(sc, 4 * kTS);
-  sc = std::min<double>(sc, static_cast<double>(e.npad));
-  pl.sc = static_cast<int>(sc);
+  pl.sc = chunk_size(n, e.npad);
   pl.nchunks = static_cast<int>((n + pl.sc - 1) / pl.sc);
 
   // Cost-balanced partition of 1024-row blocks across shards (background
@@ -320,6 +326,11 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
   const bool sym = e.mode == sthk::kSym;
   const EvalPlan pl = make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym}, shards);
   e.last_sc = pl.sc;
+  const bool cached = e.bg_cache && e.cache_valid && e.cache_gen == e.load_gen &&
+                      e.cache_tx == e.p[1] && e.cache_tt == e.p[2] && e.cache_mode == e.mode &&
+                      e.cache_dense == e.dense && (e.cache_grad || !grad);
+  e.last_cache_hit = cached;
+  e.cache_valid = false;  // re-armed below once the sweep is enqueued
   const int64_t ntiles_total = (e.n + kTM - 1) / kTM;
   const int nb_total = static_cast<int>((e.n + kRB - 1) / kRB);
   const double* p = e.p;
@@ -367,7 +378,10 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
       if (e.timing) ck(cudaEventRecord(s.ev[0], st), "event");
       ck(cudaMemsetAsync(s.pair_counts, 0, sthk::kNCounts * sizeof(unsigned long long), st),
          "memset");
-      ck(cudaMemsetAsync(s.fx, 0, sizeof(unsigned long long) * kFxRows * e.npad, st), "memset");
+      if (!cached) {
+        ck(cudaMemsetAsync(s.fx, 0, sizeof(unsigned long long) * kFxRows * e.npad, st),
+           "memset");
+      }
       if (shards > 1) {
         ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
       }
@@ -382,6 +396,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
     pa.dT = pl.k.dT;
     pa.dense = e.dense ? 1 : 0;
     pa.sym = sym ? 1 : 0;
+    pa.trig_only = cached ? 1 : 0;
     pa.sc = pl.sc;
     pa.nchunks = pl.nchunks;
     pa.ranges = s.ranges;
@@ -407,8 +422,11 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
     qa.work_counter = s.scalars + 1;
     qa.fx = s.fx;
     qa.tpart = s.tpart;
+    qa.bg_off = cached ? 1 : 0;
     for (int k = 0; k < sthk::kNSumGrad; ++k) qa.fxq[k] = fxq[k];
     qa.pair_counts = s.pair_counts;
+    // a trigger-only sweep runs the same kernel with the background switched
+    // off, so its trigger partials are summed exactly as in a full sweep
     const int grid = s.sms * s.occ[e.mode][grad ? 1 : 0];
     if (e.timing && first_run) ck(cudaEventRecord(s.ev[1], st), "event");
     ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
@@ -416,7 +434,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
   }
 
   // phase 2: symmetric mode adds column sums to rows other devices own
-  if (sym && shards > 1 && !vshards) {
+  if (sym && !cached && shards > 1 && !vshards) {
     ckn(ncclGroupStart(), "ncclGroupStart");
     for (Slot& s : e.slots) {
       ckn(ncclAllReduce(s.fx, s.fx, static_cast<size_t>(kFxRows) * e.npad, ncclUint64, ncclSum,
@@ -493,6 +511,15 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
   e.pending = true;
   e.last_grad = grad;
   e.last_pe = want_pe;
+  if (!cached) {
+    e.cache_grad = grad;
+    e.cache_gen = e.load_gen;
+    e.cache_tx = e.p[1];
+    e.cache_tt = e.p[2];
+    e.cache_mode = e.mode;
+    e.cache_dense = e.dense;
+  }
+  e.cache_valid = true;
 }
 
 void collect(sthk_engine& e, double* loglik, int* valid, double* grad6, double* per_event) {
@@ -682,6 +709,8 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
     e->npad = npad;
     e->window_end = window_end;
     e->loaded = true;
+    e->load_gen += 1;
+    e->cache_valid = false;
   });
 }
 
@@ -773,6 +802,13 @@ int sthk_plan_partition(const double* t, int64_t n, const double* params6, int s
   }
 }
 
+int sthk_set_background_cache(sthk_engine* e, int enable) {
+  return guarded(e, [&] {
+    e->bg_cache = enable != 0;
+    if (!e->bg_cache) e->cache_valid = false;
+  });
+}
+
 int sthk_set_kernel(sthk_engine* e, int mode) {
   return guarded(e, [&] {
     if (mode != sthk::kRows && mode != sthk::kSym) {
@@ -812,6 +848,7 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
     out->world = e->world;
     out->source_chunk = e->last_sc;
     out->kernel_mode = e->mode;
+    out->cache_hit = e->last_cache_hit ? 1 : 0;
     for (Slot& s : e->slots) {
       out->pairs_bg += static_cast<int64_t>(s.h_counts[0]);
       out->pairs_tr += static_cast<int64_t>(s.h_counts[1]);

@@ -75,6 +75,10 @@ __global__ void plan_ranges_kernel(const PlanArgs a) {
   if (a.dense) {
     lo = 0;
     hi = static_cast<int>(a.n);
+  } else if (a.trig_only) {
+    lo = min(static_cast<int>(lower_bound_t(a.t, a.n, a.t[first] - a.dT)),
+             static_cast<int>(first));
+    hi = static_cast<int>(last + 1);
   } else {
     const double tmin = a.t[first], tmax = a.t[last];
     lo = static_cast<int>(lower_bound_t(a.t, a.n, tmin - fmax(a.dB, a.dT)));
@@ -84,7 +88,7 @@ __global__ void plan_ranges_kernel(const PlanArgs a) {
     hi = max(hi, static_cast<int>(last + 1));
   }
   // symmetric mode: later tiles reach this one through their column sums
-  if (a.sym) hi = static_cast<int>(last + 1);
+  if (a.sym || a.trig_only) hi = static_cast<int>(last + 1);
   a.ranges[tile] = make_int2(lo, hi);
   const int c0 = a.dense ? 0 : lo / a.sc;
   const int c1 = (hi - 1) / a.sc;
@@ -204,6 +208,7 @@ __device__ __forceinline__ void store_row_sums(const PairArgs& a, int chunk, int
   if (row >= a.n) return;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
+    if (a.bg_off) break;
     fx_add(a.fx + static_cast<size_t>(2 * q) * a.npad + row,
            a.fx + static_cast<size_t>(2 * q + 1) * a.npad + row, acc[q] * a.fxq[q]);
   }
@@ -285,7 +290,7 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
       const double4 bs = a.tile_box[s0 / kTS];
       const double smin = a.t[s0], smax = a.t[s0 + cnt - 1];
 
-      const bool bg = !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
+      const bool bg = !a.bg_off && !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
       int tr;
       if (smin >= tmax || smax < tmin - a.k.dT) tr = 0;
       else if (smax < tmin) tr = 1;
@@ -613,7 +618,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       const double4 bs = a.tile_box[s0 / kTS];
       const double smin = a.t[s0], smax = a.t[s0 + cnt - 1];
 
-      const bool bg = !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
+      const bool bg = !a.bg_off && !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
       int tr;
       if (smin >= tmax || smax < tmin - a.k.dT) tr = 0;
       else if (smax < tmin) tr = 1;
@@ -645,7 +650,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
         sym_dispatch<GRAD, true, true, false>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
                                               a.k, s_tab, racc, s_col);
       }
-      if (!diag && bg) {
+      if (!diag && bg) {  // (never in a trigger-only sweep)
         // column sums of source tile J: one fixed-point flush per column
         __syncthreads();
         const int64_t col = s0 + tid;

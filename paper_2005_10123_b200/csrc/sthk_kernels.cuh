@@ -52,6 +52,7 @@ struct PlanArgs {
   double dB, dT;
   int dense;
   int sym;              // kSym: the live range ends at the tile's own end
+  int trig_only;        // trigger-only sweep: [t_min - dT, tile end)
   int sc;               // sources per chunk (multiple of kTS)
   int nchunks;          // ceil(n / sc)
   int2* ranges;         // [ntiles] live source range [lo, hi) per row tile
@@ -82,6 +83,7 @@ struct PairArgs {
   unsigned long long* fx;
   double fxq[kNSumGrad];
   double* tpart;        // trigger partials [nchunks][3 or 1][npad]
+  int bg_off;           // trigger-only sweep (background sums come from a cache)
   unsigned long long* pair_counts;  // [kNCounts] (tile granularity)
 };
 

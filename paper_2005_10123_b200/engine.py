@@ -172,6 +172,11 @@ class Engine:
     def set_dense(self, on: bool) -> None:
         self._check(self._lib.sthk_set_dense(self._h, int(on)), "sthk_set_dense")
 
+    def set_background_cache(self, on: bool) -> None:
+        """Reuse background sums while events/tauX/tauT are unchanged (default on)."""
+        self._check(self._lib.sthk_set_background_cache(self._h, int(on)),
+                    "sthk_set_background_cache")
+
     def set_kernel(self, mode: int) -> None:
         """0 = rows (ordered pairs), 1 = symmetric background (default)."""
         self._check(self._lib.sthk_set_kernel(self._h, int(mode)), "sthk_set_kernel")

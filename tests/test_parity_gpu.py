@@ -212,3 +212,38 @@ def test_kernel_modes_agree_and_cull_exact(engine):
         engine.set_kernel(1)
         assert abs(res[0][0] - res[1][0]) <= 1e-13 * abs(res[0][0])
         assert np.allclose(res[0][2], res[1][2], rtol=1e-11, atol=0)
+
+
+def test_background_cache_bitwise_transparent(engine):
+    """Reusing background sums (tauX, tauT unchanged) gives bitwise the same
+    loglik / gradient / per-event terms as full evaluations."""
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=12000)
+    seq = [pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695), pk.Params(0.7, 1.6, 14, 0.344, 1440, 0.0695),
+           pk.Params(0.7, 1.6, 14, 0.2, 1440, 0.0695), pk.Params(0.7, 1.6, 14, 0.2, 3.0, 0.0695),
+           pk.Params(0.7, 1.6, 14, 0.2, 3.0, 0.5), pk.Params(0.7, 1.2, 14, 0.2, 3.0, 0.5),
+           pk.Params(0.7, 1.2, 14, 0.2, 1.0, 0.5)]
+    for mode in (1, 0):
+        engine.set_kernel(mode)
+        engine.load(ev)
+        outs = {}
+        for cache in (False, True):
+            engine.set_background_cache(cache)
+            res, hits = [], []
+            for grad in (True, False):
+                for p in seq:
+                    engine.set_params(p)
+                    r = engine.loglik_grad(per_event=True) if grad else engine.loglik(per_event=True)
+                    res.append(r)
+                    hits.append(engine.stats()["cache_hit"])
+            outs[cache] = (res, hits)
+        engine.set_background_cache(True)
+        engine.set_kernel(1)
+        for a, b in zip(outs[False][0], outs[True][0]):
+            assert a[0] == b[0]
+            assert np.array_equal(a[-1], b[-1])
+            if len(a) == 4:
+                assert np.array_equal(a[2], b[2])
+        # hits: tauX change at index 5 forces a full sweep; grad->value reuses
+        assert sum(outs[True][1]) >= 9 and sum(outs[False][1]) == 0
