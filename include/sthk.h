@@ -44,6 +44,8 @@ extern "C" {
 #define STHK_ENOTLOADED 2 /* evaluation before sthk_load_events / set_params */
 #define STHK_ECUDA 3      /* CUDA runtime error (maps to std::runtime_error) */
 #define STHK_ENCCL 4      /* NCCL error */
+#define STHK_ERANGE 5     /* excitation: a per-event rate underflowed to zero
+                             (excitation.cpp:52-55; maps to std::runtime_error) */
 
 #define STHK_NCCL_ID_BYTES 128
 
@@ -86,6 +88,13 @@ int sthk_loglik_grad(sthk_engine* e, double* loglik, int* valid, double* grad6,
  * grad (nullable): P x 6. */
 int sthk_loglik_batch(sthk_engine* e, const double* params, int64_t P,
                       double* loglik, int* valid, double* grad);
+
+/* Per-event split of the rate into background mu_i = mu0 * B_i and
+ * self-excitation xi_i = T_i with pi_i = xi_i / (mu_i + xi_i), for the
+ * current params (hawkes::excitationProbabilities, excitation.cpp:13-58).
+ * Each output (nullable, length n) is filled; if any rate underflowed, pi is
+ * 0 on those rows and STHK_ERANGE is returned. */
+int sthk_excitation(sthk_engine* e, double* mu, double* xi, double* pi);
 
 /* Asynchronous pair: enqueue one evaluation of the current params on the
  * engine's stream(s); sthk_result() waits for and returns the latest one. */

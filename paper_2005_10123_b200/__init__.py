@@ -16,6 +16,7 @@ built extension raises, and evaluating without a CUDA device fails loudly.
 from __future__ import annotations
 
 from ._lib import (
+    STHK_ERANGE,
     STHK_OK,
     STHK_EINVAL,
     STHK_ENOTLOADED,
@@ -36,6 +37,13 @@ from .engine import (
     log_likelihood_gradient,
 )
 from .simulate import SimWindow, generateBenchmarkCloud, simulateClusterProcess
+from .excitation import (
+    ExcitationVector,
+    PosteriorExcitation,
+    excitationProbabilities,
+    posteriorExcitation,
+    thinIndices,
+)
 
 __all__ = [
     "STHK_OK", "STHK_EINVAL", "STHK_ENOTLOADED", "STHK_ECUDA", "STHK_ENCCL",
@@ -45,4 +53,6 @@ __all__ = [
     "logLikelihood", "logLikelihoodBatch", "logLikelihoodGradient",
     "log_likelihood", "log_likelihood_gradient",
     "SimWindow", "generateBenchmarkCloud", "simulateClusterProcess",
+    "ExcitationVector", "PosteriorExcitation", "excitationProbabilities",
+    "posteriorExcitation", "thinIndices",
 ]

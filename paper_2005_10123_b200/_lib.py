@@ -10,6 +10,7 @@ STHK_EINVAL = 1
 STHK_ENOTLOADED = 2
 STHK_ECUDA = 3
 STHK_ENCCL = 4
+STHK_ERANGE = 5
 NCCL_ID_BYTES = 128
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -56,6 +57,7 @@ SIGNATURES = [
     ("sthk_loglik", c_int, [c_void_p, _DPTR, _IPTR, _DPTR]),
     ("sthk_loglik_grad", c_int, [c_void_p, _DPTR, _IPTR, _DPTR, _DPTR]),
     ("sthk_loglik_batch", c_int, [c_void_p, _DPTR, c_int64, _DPTR, _IPTR, _DPTR]),
+    ("sthk_excitation", c_int, [c_void_p, _DPTR, _DPTR, _DPTR]),
     ("sthk_enqueue", c_int, [c_void_p, c_int, c_int]),
     ("sthk_result", c_int, [c_void_p, _DPTR, _IPTR, _DPTR, _DPTR]),
     ("sthk_set_timing", c_int, [c_void_p, c_int]),

@@ -1,4 +1,5 @@
-// hawkes::logLikelihood / logLikelihoodBatch over the sthk C ABI.
+// hawkes::logLikelihood / logLikelihoodBatch / excitationProbabilities /
+// posteriorExcitation over the sthk C ABI.
 //
 // Behaviour kept from the reference (proj/src/likelihood.cpp:10-75):
 //   * params.validate() and backend.validate() run first and throw
@@ -9,6 +10,8 @@
 //     when requested, 0 on degenerate rows.
 //   * logLikelihoodBatch rethrows "logLikelihoodBatch: entry i: ...".
 // Engine errors other than invalid arguments become std::runtime_error.
+// Linked in place of likelihood.cpp and excitation.cpp
+// (excitation semantics: proj/src/excitation.cpp:13-130).
 //
 // State: one process-wide engine on the devices in $STHK_DEVICES (default
 // "0"), created on first use. The device copy of the events is cached; a call
@@ -24,6 +27,9 @@
 #include <string>
 #include <vector>
 
+#include <fstream>
+
+#include "sthawkes/excitation.hpp"
 #include "sthawkes_b200.hpp"
 #include "sthk.h"
 
@@ -151,6 +157,87 @@ std::vector<LikelihoodResult> logLikelihoodBatch(const EventSet& events,
     }
   }
   return results;
+}
+
+ExcitationVector excitationProbabilities(const EventSet& events, const Params& params,
+                                         const Backend& backend) {
+  params.validate();
+  backend.validate();
+  AdapterEngine& e = engine();
+  std::lock_guard<std::mutex> lock(e.mu);
+  e.ensureLoaded(events);
+  e.setParams(params);
+  const Index n = events.size();
+  ExcitationVector out;
+  out.pi.resize(n);
+  out.mu.resize(n);
+  out.xi.resize(n);
+  const int rc = sthk_excitation(e.h, out.mu.data(), out.xi.data(), out.pi.data());
+  if (rc == STHK_ERANGE) throw std::runtime_error(sthk_last_error(e.h));
+  e.check(rc);
+  return out;
+}
+
+std::vector<Index> thinIndices(Index total, Index keep) {
+  if (total < 1 || keep < 1) {
+    throw std::invalid_argument("thinIndices: need total >= 1 and keep >= 1");
+  }
+  const Index k = keep < total ? keep : total;
+  std::vector<Index> idx(static_cast<size_t>(k));
+  for (Index j = 0; j < k; ++j) idx[static_cast<size_t>(j)] = j * total / k;
+  return idx;
+}
+
+PosteriorExcitation posteriorExcitation(const EventSet& events, const std::vector<Params>& draws,
+                                        const Backend& backend,
+                                        const PosteriorExcitationOptions& options) {
+  if (draws.empty()) throw std::invalid_argument("posteriorExcitation: no draws");
+  if (options.thinTo < 1) {
+    throw std::invalid_argument("posteriorExcitation: thinTo must be >= 1");
+  }
+  const Index n = events.size();
+  PosteriorExcitation out;
+  out.drawIndices = thinIndices(static_cast<Index>(draws.size()), options.thinTo);
+  const Index kept = static_cast<Index>(out.drawIndices.size());
+  const bool keepRows = kept * n <= options.memoryCapEntries;
+  if (keepRows) out.perDraw.setZero(kept, n);
+  out.meanPi.setZero(n);
+
+  std::ofstream dump;
+  if (options.dumpPath) {
+    dump.open(*options.dumpPath);
+    if (!dump) {
+      throw std::runtime_error("posteriorExcitation: cannot open dump file " +
+                               *options.dumpPath);
+    }
+    dump << "# sthawkes pi draws v1, events=" << n << "\n";
+  }
+  char num[40];
+  for (Index j = 0; j < kept; ++j) {
+    const Index d = out.drawIndices[static_cast<size_t>(j)];
+    ExcitationVector ex;
+    try {
+      ex = excitationProbabilities(events, draws[static_cast<size_t>(d)], backend);
+    } catch (const std::exception& err) {
+      throw std::runtime_error("posteriorExcitation: draw " + std::to_string(d) + ": " +
+                               err.what());
+    }
+    out.meanPi += ex.pi;  // draw order, then one division (bitwise as the reference)
+    if (keepRows) out.perDraw.row(j) = ex.pi.transpose();
+    if (dump.is_open()) {
+      dump << d;
+      for (Index i = 0; i < n; ++i) {
+        std::snprintf(num, sizeof num, "%.17g", ex.pi[i]);
+        dump << '\t' << num;
+      }
+      dump << '\n';
+    }
+  }
+  out.meanPi /= static_cast<double>(kept);
+  if (dump.is_open() && !dump) {
+    throw std::runtime_error("posteriorExcitation: failed writing dump file");
+  }
+  return out;
 }
 
 }  // namespace hawkes

@@ -97,6 +97,10 @@ struct Slot {
   double* out = nullptr;  // kNOut
   double* per_event = nullptr;
   size_t pe_cap = 0;
+  double* ex = nullptr;  // excitation mu, xi, pi [3][npad]
+  size_t ex_cap = 0;
+  double* h_ex = nullptr;  // pinned
+  size_t h_ex_cap = 0;
   unsigned long long* pair_counts = nullptr;
   double* h_out = nullptr;                 // pinned kNOut
   unsigned long long* h_counts = nullptr;  // pinned kNCounts
@@ -132,7 +136,7 @@ struct sthk_engine {
   bool cache_dense = false;
   int virtual_shards = 1;  // testing: partition rows over k shards on one device
   std::string err;
-  bool pending = false, last_grad = false, last_pe = false;
+  bool pending = false, last_grad = false, last_pe = false, last_ex = false;
   int last_sc = 0, last_items_est = 0;
 };
 
@@ -170,12 +174,13 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.items), static_cast<void*>(s.scalars),
                   static_cast<void*>(s.fx), static_cast<void*>(s.block_partial),
                   static_cast<void*>(s.tpart), static_cast<void*>(s.crange),
+                  static_cast<void*>(s.ex),
                   static_cast<void*>(s.out), static_cast<void*>(s.per_event),
                   static_cast<void*>(s.pair_counts), static_cast<void*>(s.tile_box)}) {
     if (p) cudaFree(p);
   }
   for (void* p : {static_cast<void*>(s.h_out), static_cast<void*>(s.h_counts),
-                  static_cast<void*>(s.h_per_event)}) {
+                  static_cast<void*>(s.h_per_event), static_cast<void*>(s.h_ex)}) {
     if (p) cudaFreeHost(p);
   }
   for (auto& e : s.ev) {
@@ -317,7 +322,7 @@ void fixed_point_scales(const double* p, double* q) {
 
 constexpr int kFxRows = 2 * 3;  // fixed-point words per event (3 background sums)
 
-void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
+void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false) {
   if (!e.loaded) throw NotLoaded("sthk: no events loaded");
   if (!e.has_params) throw NotLoaded("sthk: no parameters set");
   const bool vshards = !e.rank_mode && e.slots.size() == 1 && e.virtual_shards > 1;
@@ -372,6 +377,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
     dev_grow(s.crange, s.crange_cap, static_cast<size_t>(ntiles_total));
     dev_grow(s.block_partial, s.bp_cap, static_cast<size_t>(nb_total) * kNOut);
     if (want_pe) dev_grow(s.per_event, s.pe_cap, static_cast<size_t>(e.npad));
+    if (want_ex) dev_grow(s.ex, s.ex_cap, static_cast<size_t>(3) * e.npad);
 
     cudaStream_t st = s.stream;
     if (first_run) {
@@ -471,6 +477,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
     fa.crange = s.crange;
     for (int k = 0; k < sthk::kNSumGrad; ++k) fa.fxq[k] = fxq[k];
     fa.per_event = want_pe ? s.per_event : nullptr;
+    fa.ex_out = want_ex ? s.ex : nullptr;
     fa.block_partial = s.block_partial;
     ck(sthk::launch_finalize(fa, grad, s.stream), "finalize");
   }
@@ -506,11 +513,24 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe) {
                          sizeof(double) * (s.row1 - s.row0), cudaMemcpyDeviceToHost, st),
          "D2H");
     }
+    if (want_ex && s.row1 > s.row0) {
+      if (s.h_ex_cap < static_cast<size_t>(3 * e.npad)) {
+        if (s.h_ex) ck(cudaFreeHost(s.h_ex), "cudaFreeHost");
+        ck(cudaMallocHost(&s.h_ex, sizeof(double) * 3 * e.npad), "cudaMallocHost");
+        s.h_ex_cap = static_cast<size_t>(3 * e.npad);
+      }
+      for (int k = 0; k < 3; ++k) {
+        ck(cudaMemcpyAsync(s.h_ex + k * e.npad + s.row0, s.ex + k * e.npad + s.row0,
+                           sizeof(double) * (s.row1 - s.row0), cudaMemcpyDeviceToHost, st),
+           "D2H");
+      }
+    }
     if (e.timing) ck(cudaEventRecord(s.ev[3], st), "event");
   }
   e.pending = true;
   e.last_grad = grad;
   e.last_pe = want_pe;
+  e.last_ex = want_ex;
   if (!cached) {
     e.cache_grad = grad;
     e.cache_gen = e.load_gen;
@@ -749,6 +769,30 @@ int sthk_loglik_grad(sthk_engine* e, double* loglik, int* valid, double* grad6,
     enqueue_eval(*e, true, per_event != nullptr);
     collect(*e, loglik, valid, grad6, per_event);
   });
+}
+
+int sthk_excitation(sthk_engine* e, double* mu, double* xi, double* pi) {
+  int degenerate = 0;
+  const int rc = guarded(e, [&] {
+    if (e->pending) collect(*e, nullptr, nullptr, nullptr, nullptr);
+    enqueue_eval(*e, false, false, true);
+    collect(*e, nullptr, nullptr, nullptr, nullptr);
+    double* outs[3] = {mu, xi, pi};
+    for (Slot& s : e->slots) {
+      if (s.row1 <= s.row0) continue;
+      for (int k = 0; k < 3; ++k) {
+        if (outs[k]) {
+          std::memcpy(outs[k] + s.row0, s.h_ex + k * e->npad + s.row0,
+                      sizeof(double) * (s.row1 - s.row0));
+        }
+      }
+    }
+    degenerate = e->slots[0].h_out[7] > 0.0;
+  });
+  if (rc == STHK_OK && degenerate) {
+    return fail(e, STHK_ERANGE, "excitationProbabilities: per-event rate underflowed to zero");
+  }
+  return rc;
 }
 
 int sthk_loglik_batch(sthk_engine* e, const double* params, int64_t P, double* loglik,

@@ -769,6 +769,11 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
     const double em1 = expm1(-a.omega * D);
     const double Lam = a.mu0 * (Phi1 - Phi0) + (-a.theta * em1);
 
+    if (a.ex_out) {  // excitation split, excitation.cpp:31-51
+      a.ex_out[r] = a.mu0 * B;
+      a.ex_out[a.npad + r] = Tr;
+      a.ex_out[2 * a.npad + r] = (!(lam > 0.0) || !isfinite(lam)) ? 0.0 : Tr / lam;
+    }
     if (!(lam > 0.0) || !isfinite(lam)) {  // likelihood.cpp:36-39
       acc[7] += 1.0;
       if (a.per_event) a.per_event[r] = 0.0;

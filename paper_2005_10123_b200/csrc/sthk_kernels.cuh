@@ -103,6 +103,7 @@ struct FinArgs {
   const double* tpart;
   const int2* crange;
   double* per_event;    // nullable
+  double* ex_out;       // nullable: excitation mu, xi, pi as [3][npad]
   double* block_partial;  // [nblocks_total][kNOut]
 };
 

@@ -94,6 +94,8 @@ class Engine:
         msg = self._lib.sthk_last_error(self._h).decode()
         if rc == _lib.STHK_EINVAL:
             raise ValueError(msg)
+        if rc == _lib.STHK_ERANGE:
+            raise EngineError(msg)
         raise EngineError(f"{what} failed ({rc}): {msg}")
 
     @property
@@ -154,6 +156,14 @@ class Engine:
             ok.ctypes.data_as(ctypes.POINTER(c_int)), _dptr(g) if grad else None),
             "sthk_loglik_batch")
         return ll, ok.astype(bool), g
+
+    def excitation(self):
+        """(mu, xi, pi) per event for the current params; raises EngineError
+        on an underflowed rate (the reference's std::runtime_error)."""
+        mu, xi, pi = np.zeros(self._n), np.zeros(self._n), np.zeros(self._n)
+        rc = self._lib.sthk_excitation(self._h, _dptr(mu), _dptr(xi), _dptr(pi))
+        self._check(rc, "sthk_excitation")
+        return mu, xi, pi
 
     def enqueue(self, grad: bool = True, per_event: bool = False) -> None:
         self._check(self._lib.sthk_enqueue(self._h, int(grad), int(per_event)), "sthk_enqueue")

@@ -34,6 +34,13 @@ def test_reference_likelihood_suite_on_b200():
     assert "11/11 passed" in out.stdout
 
 
+def test_reference_excitation_suite_on_b200():
+    out = subprocess.run([_exe("test_excitation_b200")], capture_output=True, text=True,
+                         timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "13/13 passed" in out.stdout
+
+
 def _chain(exe, *args):
     out = subprocess.run([exe, *args], capture_output=True, text=True, timeout=1200)
     assert out.returncode == 0, out.stderr[-2000:]

@@ -9,7 +9,7 @@ import pytest
 import oracle_glue as og
 
 SUITES = {"test_kernels": 24, "test_pack": 6, "test_likelihood": 11, "test_backends": 11,
-          "test_simulator": 12}
+          "test_simulator": 12, "test_excitation": 13}
 
 
 @pytest.mark.parametrize("suite", sorted(SUITES))
