@@ -337,7 +337,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
   e.last_cache_hit = cached;
   e.cache_valid = false;  // re-armed below once the sweep is enqueued
   const int64_t ntiles_total = (e.n + kTM - 1) / kTM;
-  const int nb_total = static_cast<int>((e.n + kRB - 1) / kRB);
+  const int nb_total = static_cast<int>((e.n + sthk::kFB - 1) / sthk::kFB);
   const double* p = e.p;
   const double kPi = 3.14159265358979323846;
   double fxq[sthk::kNSumGrad];
@@ -370,7 +370,6 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     const int tile1 = static_cast<int>((run.row1 + kTM - 1) / kTM);
     const int ntiles = std::max(tile1 - tile0, 0);
     dev_grow(s.ranges, s.ranges_cap, static_cast<size_t>(ntiles_total));
-    dev_grow(s.counts, s.counts_cap, static_cast<size_t>(std::max(ntiles, 1)));
     dev_grow(s.items, s.items_cap, static_cast<size_t>(std::max(ntiles, 1)) * pl.nchunks);
     dev_grow(s.fx, s.fx_cap, static_cast<size_t>(kFxRows) * e.npad);
     dev_grow(s.tpart, s.tpart_cap, static_cast<size_t>(pl.nchunks) * 3 * e.npad);
@@ -407,7 +406,6 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     pa.nchunks = pl.nchunks;
     pa.ranges = s.ranges;
     pa.crange = s.crange;
-    pa.counts = s.counts;
     pa.items = s.items;
     pa.n_items = s.scalars;
     pa.work_counter = s.scalars + 1;

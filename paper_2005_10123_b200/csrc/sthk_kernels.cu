@@ -66,9 +66,8 @@ __device__ __forceinline__ int64_t upper_bound_t(const double* t, int64_t n, dou
 // ---------------------------------------------------------------------------
 // Plan
 // ---------------------------------------------------------------------------
-__global__ void plan_ranges_kernel(const PlanArgs a) {
-  const int tile = a.tile0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (tile >= a.tile1) return;
+// Live source range [lo, hi) and chunk range [c0, c1] of one row tile.
+__device__ __forceinline__ void tile_plan(const PlanArgs& a, int tile, int2& rg, int2& cr) {
   const int64_t first = static_cast<int64_t>(tile) * kTM;
   const int64_t last = min(first + kTM, a.n) - 1;
   int lo, hi;
@@ -89,41 +88,54 @@ __global__ void plan_ranges_kernel(const PlanArgs a) {
   }
   // symmetric mode: later tiles reach this one through their column sums
   if (a.sym || a.trig_only) hi = static_cast<int>(last + 1);
-  a.ranges[tile] = make_int2(lo, hi);
-  const int c0 = a.dense ? 0 : lo / a.sc;
-  const int c1 = (hi - 1) / a.sc;
-  a.crange[tile] = make_int2(c0, c1);
-  a.counts[tile - a.tile0] = c1 - c0 + 1;
+  rg = make_int2(lo, hi);
+  cr = make_int2(a.dense ? 0 : lo / a.sc, (hi - 1) / a.sc);
 }
 
-// Single CTA: exclusive scan of per-tile item counts, then the item list in
-// (tile, chunk) order. Also resets the persistent kernel's work counter.
-__global__ void __launch_bounds__(1024) plan_items_kernel(const PlanArgs a) {
-  __shared__ int s_scan[1024];
+// Single CTA: per-tile ranges, an exclusive scan of the per-tile item counts
+// and the (tile, chunk) work list in tile order; resets the persistent pair
+// kernel's work counter.
+__global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
+  __shared__ int s_warp[32];
   __shared__ int s_carry;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ntiles = a.tile1 - a.tile0;
   if (tid == 0) s_carry = 0;
   __syncthreads();
   for (int base = 0; base < ntiles; base += 1024) {
     const int i = base + tid;
-    const int c = i < ntiles ? a.counts[i] : 0;
-    s_scan[tid] = c;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-      const int v = tid >= off ? s_scan[tid - off] : 0;
-      __syncthreads();
-      s_scan[tid] += v;
-      __syncthreads();
-    }
-    const int excl = s_carry + s_scan[tid] - c;
+    int c = 0;
+    int2 rg, cr;
     if (i < ntiles) {
-      const int tile = a.tile0 + i;
-      const int c0 = a.crange[tile].x;
-      for (int q = 0; q < c; ++q) a.items[excl + q] = make_int2(tile, c0 + q);
+      tile_plan(a, a.tile0 + i, rg, cr);
+      a.ranges[a.tile0 + i] = rg;
+      a.crange[a.tile0 + i] = cr;
+      c = cr.y - cr.x + 1;
+    }
+    // block-wide inclusive scan: warp shuffles, then the warp totals
+    int v = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= off) v += u;
+    }
+    if (lane == 31) s_warp[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      int w = s_warp[lane];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += u;
+      }
+      s_warp[lane] = w;
     }
     __syncthreads();
-    if (tid == 1023) s_carry += s_scan[1023];
+    const int incl = v + (warp > 0 ? s_warp[warp - 1] : 0);
+    const int excl = s_carry + incl - c;
+    for (int q = 0; q < c; ++q) a.items[excl + q] = make_int2(a.tile0 + i, cr.x + q);
+    __syncthreads();
+    if (tid == 1023) s_carry += incl;
     __syncthreads();
   }
   if (tid == 0) {
@@ -581,11 +593,18 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       ti[r] = a.t[row];
       rv[r] = row < n;
     }
+    // Background row sums live in registers for the whole item; the trigger
+    // row sums (rarely active) are parked in this thread's s_red slots
+    // between trigger stages so the background-only loops keep their
+    // registers for ILP.
+    constexpr int NB = GRAD ? 3 : 1;
     double racc[kSymR][NS];
 #pragma unroll
     for (int r = 0; r < kSymR; ++r) {
 #pragma unroll
       for (int q = 0; q < NS; ++q) racc[r][q] = 0.0;
+#pragma unroll
+      for (int q = NB; q < NS; ++q) s_red[warp][q][lane + 32 * r] = 0.0;
     }
 
     int s_begin = max(rg.x, chunk * a.sc);
@@ -637,6 +656,13 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       const double* sy = s_src[buf][1];
       const double* st = s_src[buf][2];
       const int col0 = warp * 32;
+      if (tr) {
+#pragma unroll
+        for (int r = 0; r < kSymR; ++r) {
+#pragma unroll
+          for (int q = NB; q < NS; ++q) racc[r][q] = s_red[warp][q][lane + 32 * r];
+        }
+      }
       if (diag) {
         sym_dispatch<GRAD, false, true, true>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
                                               a.k, s_tab, racc, s_col);
@@ -649,6 +675,13 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       } else {
         sym_dispatch<GRAD, true, true, false>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
                                               a.k, s_tab, racc, s_col);
+      }
+      if (tr) {
+#pragma unroll
+        for (int r = 0; r < kSymR; ++r) {
+#pragma unroll
+          for (int q = NB; q < NS; ++q) s_red[warp][q][lane + 32 * r] = racc[r][q];
+        }
       }
       if (!diag && bg) {  // (never in a trigger-only sweep)
         // column sums of source tile J: one fixed-point flush per column
@@ -684,7 +717,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
 #pragma unroll
     for (int r = 0; r < kSymR; ++r) {
 #pragma unroll
-      for (int q = 0; q < NS; ++q) s_red[warp][q][lane + 32 * r] = racc[r][q];
+      for (int q = 0; q < NB; ++q) s_red[warp][q][lane + 32 * r] = racc[r][q];
     }
     __syncthreads();
     double v[NS];
@@ -731,13 +764,13 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   __shared__ double s_red[kNOut][kFinThreads];
   const int tid = threadIdx.x;
-  const int64_t base = static_cast<int64_t>(a.row0) + static_cast<int64_t>(blockIdx.x) * kRB;
+  const int64_t base = static_cast<int64_t>(a.row0) + static_cast<int64_t>(blockIdx.x) * kFB;
   double acc[kNOut];
 #pragma unroll
   for (int q = 0; q < kNOut; ++q) acc[q] = 0.0;
 
-  for (int q = 0; q < kRB / kFinThreads; ++q) {
-    const int64_t r = base + q * kFinThreads + tid;
+  do {  // one row per thread; `continue` / `break` skip to the reduction
+    const int64_t r = base + tid;
     if (r >= a.row1) break;
     constexpr int NB = GRAD ? 3 : 1;
     double s[NS];
@@ -807,7 +840,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
       acc[5] += dl4 * inv - a.theta * D * exp(-a.omega * D);
       acc[6] += dl5 * inv;
     }
-  }
+  } while (false);
 
 #pragma unroll
   for (int q = 0; q < kNOut; ++q) s_red[q][tid] = acc[q];
@@ -820,7 +853,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
     __syncthreads();
   }
   if (tid < kNOut) {
-    a.block_partial[(base / kRB) * kNOut + tid] = s_red[tid][0];
+    a.block_partial[(base / kFB) * kNOut + tid] = s_red[tid][0];
   }
 }
 
@@ -860,8 +893,7 @@ cudaError_t launch_tile_boxes(const double* x, const double* y, int64_t n, doubl
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
   const int ntiles = a.tile1 - a.tile0;
   if (ntiles <= 0) return cudaSuccess;
-  plan_ranges_kernel<<<(ntiles + 255) / 256, 256, 0, stream>>>(a);
-  plan_items_kernel<<<1, 1024, 0, stream>>>(a);
+  plan_kernel<<<1, 1024, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -877,7 +909,7 @@ cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaS
 }
 
 cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream) {
-  const int nblocks = (a.row1 - a.row0 + kRB - 1) / kRB;
+  const int nblocks = (a.row1 - a.row0 + kFB - 1) / kFB;
   if (nblocks <= 0) return cudaSuccess;
   if (grad) finalize_kernel<true><<<nblocks, kFinThreads, 0, stream>>>(a);
   else finalize_kernel<false><<<nblocks, kFinThreads, 0, stream>>>(a);

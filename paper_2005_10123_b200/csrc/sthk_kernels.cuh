@@ -12,6 +12,7 @@ constexpr int kTM = 128;    // target rows per tile (= threads per pair CTA)
 constexpr int kTS = 128;    // sources per shared-memory stage (= tile size)
 constexpr int kRB = 1024;   // rows per reduction block (multi-GPU partition unit)
 constexpr int kFinThreads = 256;
+constexpr int kFB = kFinThreads;  // rows per finalize block / block partial
 constexpr int kNSumGrad = 6;  // S_B, S_Br, S_Bt, S_T, S_Tt, S_Tr
 constexpr int kNSumVal = 2;   // S_B, S_T
 constexpr int kNOut = 8;      // loglik, 6 gradient terms, degenerate-row count
@@ -57,7 +58,6 @@ struct PlanArgs {
   int nchunks;          // ceil(n / sc)
   int2* ranges;         // [ntiles] live source range [lo, hi) per row tile
   int2* crange;         // [ntiles] chunk range [c0, c1] per row tile
-  int* counts;          // [ntiles] items per row tile (scratch)
   int2* items;          // (row tile, chunk) work list
   int* n_items;         // device scalar
   int* work_counter;    // device scalar, reset here
@@ -104,7 +104,7 @@ struct FinArgs {
   const int2* crange;
   double* per_event;    // nullable
   double* ex_out;       // nullable: excitation mu, xi, pi as [3][npad]
-  double* block_partial;  // [nblocks_total][kNOut]
+  double* block_partial;  // [ceil(n / kFB)][kNOut]
 };
 
 // Launch wrappers (sthk_kernels.cu). All enqueue on `stream`.

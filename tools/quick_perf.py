@@ -14,6 +14,7 @@ ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
 e = pk.Engine((0,))
 e.load(ev)
 e.set_timing(True)
+e.set_background_cache(bool(int(os.environ.get("QP_CACHE", "0"))))
 modes = [int(m) for m in os.environ.get("QP_MODES", "0,1").split(",")]
 denses = [bool(int(d)) for d in os.environ.get("QP_DENSE", "0,1").split(",")]
 for name, p in [("post", [0.66, 1.6, 14, 0.344, 1440, 0.0695]), ("init", [1, 1.6, 14, 0.1, 1, 1])]:
