@@ -11,6 +11,7 @@ ev = bench.make_workload()
 e = pk.Engine((0,))
 e.load(ev)
 e.set_params(theta)
+e.set_background_cache(False)  # every launch a full sweep
 for _ in range(5):
     r = e.loglik_grad()
 print("loglik", r[0])
