@@ -166,6 +166,10 @@ int sthk_plan_partition(const double* t, int64_t n, const double* params6,
 int sthk_measure_fp64_peak(int device, int reps, double* tflops_best,
                            double* tflops_mean);
 
+/* Diagnostic: the pair kernels' device exp (exp_l) on n natural-unit
+ * exponents x <= 0 (accuracy tests against libm). */
+int sthk_debug_exp(int device, const double* x, int64_t n, double* out);
+
 const char* sthk_last_error(const sthk_engine* e);
 const char* sthk_version(void);
 

@@ -69,6 +69,7 @@ SIGNATURES = [
     ("sthk_set_background_cache", c_int, [c_void_p, c_int]),
     ("sthk_measure_fp64_peak", c_int, [c_int, c_int, _DPTR, _DPTR]),
     ("sthk_plan_partition", c_int, [_DPTR, c_int64, _DPTR, c_int, c_int, _IPTR, _IPTR]),
+    ("sthk_debug_exp", c_int, [c_int, _DPTR, c_int64, _DPTR]),
     ("sthk_last_error", c_char_p, [c_void_p]),
     ("sthk_version", c_char_p, []),
     ("sthk_sim_cloud", c_int, [c_int64, _DPTR, c_uint64, _DPTR, _DPTR, _DPTR, _DPTR]),

@@ -77,6 +77,8 @@ struct Slot {
   ncclComm_t comm = nullptr;
   double *x = nullptr, *y = nullptr, *t = nullptr;
   size_t x_cap = 0, y_cap = 0, t_cap = 0;
+  double *xs = nullptr, *ys = nullptr;  // kSym: x, y scaled by sqrt(-cxL) (per evaluation)
+  size_t xs_cap = 0, ys_cap = 0;
   double4* tile_box = nullptr;
   size_t box_cap = 0;
   int2* ranges = nullptr;
@@ -170,6 +172,7 @@ void free_slot(Slot& s) {
   if (s.stream) cudaStreamSynchronize(s.stream);
   if (s.comm) ncclCommDestroy(s.comm);
   for (void* p : {static_cast<void*>(s.x), static_cast<void*>(s.y), static_cast<void*>(s.t),
+                  static_cast<void*>(s.xs), static_cast<void*>(s.ys),
                   static_cast<void*>(s.ranges), static_cast<void*>(s.counts),
                   static_cast<void*>(s.items), static_cast<void*>(s.scalars),
                   static_cast<void*>(s.fx), static_cast<void*>(s.block_partial),
@@ -222,6 +225,7 @@ void validate_events(const double* x, const double* y, const double* t, int64_t 
 
 struct EvalPlan {
   sthk::PairConsts k;
+  double sx = 1.0;  // kSym coordinate scale sqrt(-cxL)
   int sc = 0;
   int nchunks = 0;
   std::vector<int> cuts;  // shard row boundaries (size shards+1)
@@ -262,11 +266,14 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   const double* p = e.p;
   double dB, dT;
   culling_windows(p, dB, dT);
-  // exponent constants in L units (x 256/ln2), see exp_l (sthk_device.cuh)
-  const long double L = 256.0L / 0.693147180559945309417232121458176568L;
+  // exponent constants in L units (x 2048/ln2), see exp_l (sthk_device.cuh)
+  const long double L = 2048.0L / 0.693147180559945309417232121458176568L;
   pl.k.cxL = static_cast<double>(-0.5L * L / (static_cast<long double>(p[1]) * p[1]));
   pl.k.ctL = static_cast<double>(-0.5L * L / (static_cast<long double>(p[2]) * p[2]));
   pl.k.chL = static_cast<double>(-0.5L * L / (static_cast<long double>(p[5]) * p[5]));
+  // symmetric kernel: coordinates scaled by sx so that r2 = sx^2 r^2 ~ -cxL r^2
+  pl.sx = std::sqrt(-pl.k.cxL);
+  pl.k.chS = pl.k.chL / (pl.sx * pl.sx);
   pl.k.nomL = static_cast<double>(-L * p[4]);
   const double inf = std::numeric_limits<double>::infinity();
   pl.k.dB = e.dense ? inf : dB;
@@ -387,6 +394,9 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
         ck(cudaMemsetAsync(s.fx, 0, sizeof(unsigned long long) * kFxRows * e.npad, st),
            "memset");
       }
+      if (sym && !cached) {  // (a cached sweep has the same tauX: scaled copies still valid)
+        ck(sthk::launch_scale_xy(s.x, s.y, e.n, pl.sx, s.xs, s.ys, st), "scale xy");
+      }
       if (shards > 1) {
         ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
       }
@@ -415,6 +425,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     qa.x = s.x;
     qa.y = s.y;
     qa.t = s.t;
+    qa.xs = s.xs;
+    qa.ys = s.ys;
     qa.tile_box = s.tile_box;
     qa.n = e.n;
     qa.npad = e.npad;
@@ -428,6 +440,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     qa.tpart = s.tpart;
     qa.bg_off = cached ? 1 : 0;
     for (int k = 0; k < sthk::kNSumGrad; ++k) qa.fxq[k] = fxq[k];
+    if (sym) qa.fxq[1] = fxq[1] / (pl.sx * pl.sx);  // S_Br accumulates sx^2 r^2
     qa.pair_counts = s.pair_counts;
     // a trigger-only sweep runs the same kernel with the background switched
     // off, so its trigger partials are summed exactly as in a full sweep
@@ -472,6 +485,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     fa.cT = p[4] / (2.0 * kPi * p[5] * p[5]);
     fa.fx = s.fx;
     fa.tpart = s.tpart;
+    fa.tr_r2_scale = sym ? 1.0 / (pl.sx * pl.sx) : 1.0;
     fa.crange = s.crange;
     for (int k = 0; k < sthk::kNSumGrad; ++k) fa.fxq[k] = fxq[k];
     fa.per_event = want_pe ? s.per_event : nullptr;
@@ -597,7 +611,25 @@ thread_local std::string g_create_err;
 
 extern "C" {
 
-const char* sthk_version(void) { return "sthk 0.1 (sm_100a, fp64)"; }
+int sthk_debug_exp(int device, const double* x, int64_t n, double* out) {
+  if (!x || !out || n < 0) return STHK_EINVAL;
+  if (n == 0) return STHK_OK;
+  if (cudaSetDevice(device) != cudaSuccess) return STHK_ECUDA;
+  double *dx = nullptr, *dy = nullptr;
+  const size_t bytes = sizeof(double) * static_cast<size_t>(n);
+  int rc = STHK_OK;
+  if (cudaMalloc(&dx, bytes) != cudaSuccess || cudaMalloc(&dy, bytes) != cudaSuccess ||
+      cudaMemcpy(dx, x, bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+      sthk::launch_exp_probe(dx, n, dy, nullptr) != cudaSuccess ||
+      cudaMemcpy(out, dy, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    rc = STHK_ECUDA;
+  }
+  if (dx) cudaFree(dx);
+  if (dy) cudaFree(dy);
+  return rc;
+}
+
+const char* sthk_version(void) { return "sthk 0.2 (sm_100a, fp64)"; }
 
 const char* sthk_last_error(const sthk_engine* e) {
   return e ? e->err.c_str() : g_create_err.c_str();
@@ -708,6 +740,10 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       dev_grow(s.x, s.x_cap, static_cast<size_t>(npad));
       dev_grow(s.y, s.y_cap, static_cast<size_t>(npad));
       dev_grow(s.t, s.t_cap, static_cast<size_t>(npad));
+      dev_grow(s.xs, s.xs_cap, static_cast<size_t>(npad));
+      dev_grow(s.ys, s.ys_cap, static_cast<size_t>(npad));
+      ck(cudaMemsetAsync(s.xs, 0, sizeof(double) * npad, s.stream), "memset");
+      ck(cudaMemsetAsync(s.ys, 0, sizeof(double) * npad, s.stream), "memset");
       ck(cudaMemcpyAsync(s.x, x, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
       ck(cudaMemcpyAsync(s.y, y, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
       ck(cudaMemcpyAsync(s.t, t, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");

@@ -233,13 +233,12 @@ template <bool GRAD>
 __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArgs a) {
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   __shared__ __align__(128) double s_src[2][3][kTS];
-  __shared__ uint2 s_tab[256];
+  extern __shared__ uint2 s_tab[];  // kExpTableSize entries (dynamic)
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ int s_item[2];
 
   const int tid = threadIdx.x;
-  s_tab[tid] = kExpTable[tid];
-  s_tab[tid + kTM] = kExpTable[tid + kTM];
+  for (int i = tid; i < kExpTableSize; i += kTM) s_tab[i] = kExpTable[i];
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
@@ -367,7 +366,7 @@ constexpr int kSymR = 4;  // rows per thread
 constexpr int kSymG = STHK_SYM_G;
 
 template <bool GRAD, bool SYM, bool BG, int TR, bool CHECK, bool VALID>
-__device__ __forceinline__ void sym_pairs(int g, const double* __restrict__ sx,
+__device__ __forceinline__ void sym_pairs(int g, int perm, const double* __restrict__ sx,
                                           const double* __restrict__ sy,
                                           const double* __restrict__ st, int col0, int cnt,
                                           const double (&xi)[kSymR], const double (&yi)[kSymR],
@@ -378,11 +377,14 @@ __device__ __forceinline__ void sym_pairs(int g, const double* __restrict__ sx,
   constexpr int T0 = GRAD ? 3 : 1;
 #pragma unroll
   for (int q = 0; q < kSymG; ++q) {
-    const int j = col0 + kSymG * g + q;
+    // lane-permuted column order: slot q of this lane is column q ^ perm, so
+    // the reduce-scatter below needs no lane-dependent selects
+    const int j = col0 + kSymG * g + (q ^ perm);
     const double xj = sx[j], yj = sy[j], tj = st[j];
     bool cv = true;
     if constexpr (VALID) cv = j < cnt;
-    // geometry for the 4 rows, then the exps in lockstep
+    // geometry for the 4 rows (coordinates pre-scaled so that r2 is
+    // -cxL * r^2), then the exps in lockstep
     double dt[kSymR], r2[kSymR], dt2[kSymR], arg[kSymR], e[kSymR];
 #pragma unroll
     for (int r = 0; r < kSymR; ++r) {
@@ -395,7 +397,7 @@ __device__ __forceinline__ void sym_pairs(int g, const double* __restrict__ sx,
 #pragma unroll
       for (int r = 0; r < kSymR; ++r) {
         dt2[r] = dt[r] * dt[r];
-        arg[r] = fma(k.cxL, r2[r], k.ctL * dt2[r]);
+        arg[r] = fma(k.ctL, dt2[r], -r2[r]);
       }
       exp_l_batch<CHECK>(arg, e, tab);
 #pragma unroll
@@ -417,7 +419,7 @@ __device__ __forceinline__ void sym_pairs(int g, const double* __restrict__ sx,
     }
     if constexpr (TR != 0) {
 #pragma unroll
-      for (int r = 0; r < kSymR; ++r) arg[r] = fma(k.nomL, dt[r], k.chL * r2[r]);
+      for (int r = 0; r < kSymR; ++r) arg[r] = fma(k.nomL, dt[r], k.chS * r2[r]);
       exp_l_batch<CHECK>(arg, e, tab);
 #pragma unroll
       for (int r = 0; r < kSymR; ++r) {
@@ -433,62 +435,51 @@ __device__ __forceinline__ void sym_pairs(int g, const double* __restrict__ sx,
   }
 }
 
+// Reduce-scatter of the kSymG x NSC column partials over the 32 lanes. Slot
+// q of a lane holds column q ^ perm, where perm takes its bits from lane bits
+// 4 (and 3): the first xor steps then always keep the low slots and send the
+// high ones, and the remaining steps finish the butterfly. Every lane ends
+// with the total of column `perm` (all copies bitwise identical: each add is
+// commutative); one lane per column writes it.
 template <bool GRAD, bool SYM, bool BG>
-__device__ __forceinline__ void sym_reduce(int g, int col0, double (&cp)[kSymG][GRAD ? 3 : 1],
+__device__ __forceinline__ void sym_reduce(int g, int perm, int col0,
+                                           double (&cp)[kSymG][GRAD ? 3 : 1],
                                            double* __restrict__ s_col) {
   constexpr int NSC = GRAD ? 3 : 1;
   const int lane = threadIdx.x & 31;
   if constexpr (SYM && BG) {
-    // reduce-scatter the kSymG x NSC column partials over the 32 lanes:
-    // the first log2(kSymG) xor steps halve the columns a lane keeps, the
-    // remaining steps finish the butterfly. All lanes holding a column end
-    // with bitwise-identical totals (each add is commutative).
     double v1[NSC];
     if constexpr (kSymG == 4) {
-      const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0;
       double v2[2][NSC];
 #pragma unroll
       for (int qq = 0; qq < 2; ++qq) {
 #pragma unroll
         for (int c = 0; c < NSC; ++c) {
-          const double send = b4 ? cp[qq][c] : cp[2 + qq][c];
-          const double keep = b4 ? cp[2 + qq][c] : cp[qq][c];
-          v2[qq][c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+          v2[qq][c] = cp[qq][c] + __shfl_xor_sync(0xffffffffu, cp[2 + qq][c], 16);
         }
       }
 #pragma unroll
-      for (int c = 0; c < NSC; ++c) {
-        const double send = b3 ? v2[0][c] : v2[1][c];
-        const double keep = b3 ? v2[1][c] : v2[0][c];
-        v1[c] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
+      for (int c = 0; c < NSC; ++c) v1[c] = v2[0][c] + __shfl_xor_sync(0xffffffffu, v2[1][c], 8);
 #pragma unroll
       for (int off = 4; off > 0; off >>= 1) {
 #pragma unroll
         for (int c = 0; c < NSC; ++c) v1[c] += __shfl_xor_sync(0xffffffffu, v1[c], off);
       }
       if ((lane & 7) == 0) {
-        const int q = (b4 ? 2 : 0) + (b3 ? 1 : 0);
 #pragma unroll
-        for (int c = 0; c < NSC; ++c) s_col[(col0 + kSymG * g + q) * NSC + c] = v1[c];
+        for (int c = 0; c < NSC; ++c) s_col[(col0 + kSymG * g + perm) * NSC + c] = v1[c];
       }
     } else {
-      const bool b4 = (lane & 16) != 0;
 #pragma unroll
-      for (int c = 0; c < NSC; ++c) {
-        const double send = b4 ? cp[0][c] : cp[1][c];
-        const double keep = b4 ? cp[1][c] : cp[0][c];
-        v1[c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-      }
+      for (int c = 0; c < NSC; ++c) v1[c] = cp[0][c] + __shfl_xor_sync(0xffffffffu, cp[1][c], 16);
 #pragma unroll
       for (int off = 8; off > 0; off >>= 1) {
 #pragma unroll
         for (int c = 0; c < NSC; ++c) v1[c] += __shfl_xor_sync(0xffffffffu, v1[c], off);
       }
       if ((lane & 15) == 0) {
-        const int q = b4 ? 1 : 0;
 #pragma unroll
-        for (int c = 0; c < NSC; ++c) s_col[(col0 + kSymG * g + q) * NSC + c] = v1[c];
+        for (int c = 0; c < NSC; ++c) s_col[(col0 + kSymG * g + perm) * NSC + c] = v1[c];
       }
     }
   }
@@ -507,12 +498,14 @@ __device__ __forceinline__ void sym_block(const double* __restrict__ sx,
                                           const PairConsts& k, const uint2* __restrict__ tab,
                                           double (&racc)[kSymR][GRAD ? kNSumGrad : kNSumVal],
                                           double* __restrict__ s_col) {
+  const int lane = threadIdx.x & 31;
+  const int perm = kSymG == 4 ? (((lane >> 4) & 1) << 1) | ((lane >> 3) & 1) : (lane >> 4) & 1;
 #pragma unroll 1
   for (int g = 0; g < 32 / kSymG; ++g) {
     double cp[kSymG][GRAD ? 3 : 1];
-    sym_pairs<GRAD, SYM, BG, TR, CHECK, VALID>(g, sx, sy, st, col0, cnt, xi, yi, ti, rv, k, tab,
-                                               racc, cp);
-    sym_reduce<GRAD, SYM, BG>(g, col0, cp, s_col);
+    sym_pairs<GRAD, SYM, BG, TR, CHECK, VALID>(g, perm, sx, sy, st, col0, cnt, xi, yi, ti, rv, k,
+                                               tab, racc, cp);
+    sym_reduce<GRAD, SYM, BG>(g, perm, col0, cp, s_col);
   }
 }
 
@@ -545,7 +538,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   constexpr int NSC = GRAD ? 3 : 1;
   __shared__ __align__(128) double s_src[2][3][kTS];
-  __shared__ uint2 s_tab[256];
+  extern __shared__ uint2 s_tab[];  // kExpTableSize entries (dynamic)
   __shared__ double s_col[kTS * NSC];
   __shared__ double s_red[4][NS][kTM];
   __shared__ __align__(8) uint64_t s_bar[2];
@@ -553,8 +546,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  s_tab[tid] = kExpTable[tid];
-  s_tab[tid + kTM] = kExpTable[tid + kTM];
+  for (int i = tid; i < kExpTableSize; i += kTM) s_tab[i] = kExpTable[i];
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
@@ -588,8 +580,8 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
 #pragma unroll
     for (int r = 0; r < kSymR; ++r) {
       const int64_t row = first + lane + 32 * r;
-      xi[r] = a.x[row];
-      yi[r] = a.y[row];
+      xi[r] = a.xs[row];
+      yi[r] = a.ys[row];
       ti[r] = a.t[row];
       rv[r] = row < n;
     }
@@ -615,8 +607,8 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
     constexpr uint32_t kStageBytes = kTS * sizeof(double);
     if (tid == 0 && nst > 0) {
       mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes);
-      tma_load_1d(s_src[0][0], a.x + s_begin, kStageBytes, &s_bar[0]);
-      tma_load_1d(s_src[0][1], a.y + s_begin, kStageBytes, &s_bar[0]);
+      tma_load_1d(s_src[0][0], a.xs + s_begin, kStageBytes, &s_bar[0]);
+      tma_load_1d(s_src[0][1], a.ys + s_begin, kStageBytes, &s_bar[0]);
       tma_load_1d(s_src[0][2], a.t + s_begin, kStageBytes, &s_bar[0]);
     }
     for (int s = 0; s < nst; ++s) {
@@ -627,8 +619,8 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
         const int nb = buf ^ 1;
         const int64_t s0n = s_begin + static_cast<int64_t>(s + 1) * kTS;
         mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes);
-        tma_load_1d(s_src[nb][0], a.x + s0n, kStageBytes, &s_bar[nb]);
-        tma_load_1d(s_src[nb][1], a.y + s0n, kStageBytes, &s_bar[nb]);
+        tma_load_1d(s_src[nb][0], a.xs + s0n, kStageBytes, &s_bar[nb]);
+        tma_load_1d(s_src[nb][1], a.ys + s0n, kStageBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][2], a.t + s0n, kStageBytes, &s_bar[nb]);
       }
       const int64_t s0 = s_begin + static_cast<int64_t>(s) * kTS;
@@ -756,6 +748,29 @@ __global__ void tile_box_kernel(const double* __restrict__ x, const double* __re
   box[tile] = make_double4(x0, x1, y0, y1);
 }
 
+// Spatial coordinates pre-scaled by sx = sqrt(-cxL) for the symmetric
+// kernel, so that its squared distance is already the background exponent's
+// spatial part (one multiply less per pair). Time is not scaled: the strict
+// t_j < t_i rule and the trigger's small dt need the raw times.
+__global__ void scale_xy_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                int64_t n, double sx, double* __restrict__ xs,
+                                double* __restrict__ ys) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  xs[i] = x[i] * sx;
+  ys[i] = y[i] * sx;
+}
+
+// exp_l on a vector of natural-unit exponents (accuracy tests; the argument
+// is scaled to L units by one multiply, as the pair kernels' constants are).
+__global__ void exp_probe_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+  extern __shared__ uint2 s_tab[];
+  for (int i = threadIdx.x; i < kExpTableSize; i += blockDim.x) s_tab[i] = kExpTable[i];
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = exp_l<true>(x[i] * kExpL, s_tab);
+}
+
 // ---------------------------------------------------------------------------
 // Finalize: per-row lambda / compensator / log / gradient, block partials.
 // ---------------------------------------------------------------------------
@@ -788,6 +803,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
 #pragma unroll
       for (int k = NB; k < NS; ++k) s[k] += p[static_cast<size_t>(k - NB) * a.npad];
     }
+    if constexpr (GRAD) s[5] *= a.tr_r2_scale;  // kSym: sum of e * (-cxL) r^2
     const double sB = s[0];
     const double sT = GRAD ? s[3] : s[1];
     const double B = a.bgNorm * sB;
@@ -890,6 +906,19 @@ cudaError_t launch_tile_boxes(const double* x, const double* y, int64_t n, doubl
   return cudaGetLastError();
 }
 
+cudaError_t launch_scale_xy(const double* x, const double* y, int64_t n, double sx, double* xs,
+                            double* ys, cudaStream_t stream) {
+  scale_xy_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(x, y, n, sx, xs,
+                                                                               ys);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exp_probe(const double* x, int64_t n, double* out, cudaStream_t stream) {
+  exp_probe_kernel<<<static_cast<unsigned>((n + 255) / 256), 256,
+                     sizeof(uint2) * kExpTableSize, stream>>>(x, n, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
   const int ntiles = a.tile1 - a.tile0;
   if (ntiles <= 0) return cudaSuccess;
@@ -897,13 +926,31 @@ cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+constexpr size_t kTabBytes = sizeof(uint2) * kExpTableSize;
+
+// The exp table lives in dynamic shared memory (static + dynamic > 48 KB
+// needs the opt-in attribute); set once per device before the first launch.
+cudaError_t prepare_pair_kernels() {
+  cudaError_t err = cudaSuccess;
+  auto set = [&](const void* f) {
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(kTabBytes));
+    if (e != cudaSuccess) err = e;
+  };
+  set(reinterpret_cast<const void*>(&sym_kernel<true>));
+  set(reinterpret_cast<const void*>(&sym_kernel<false>));
+  set(reinterpret_cast<const void*>(&pair_kernel<true>));
+  set(reinterpret_cast<const void*>(&pair_kernel<false>));
+  return err;
+}
+
 cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaStream_t stream) {
   if (mode == kSym) {
-    if (grad) sym_kernel<true><<<grid, kTM, 0, stream>>>(a);
-    else sym_kernel<false><<<grid, kTM, 0, stream>>>(a);
+    if (grad) sym_kernel<true><<<grid, kTM, kTabBytes, stream>>>(a);
+    else sym_kernel<false><<<grid, kTM, kTabBytes, stream>>>(a);
   } else {
-    if (grad) pair_kernel<true><<<grid, kTM, 0, stream>>>(a);
-    else pair_kernel<false><<<grid, kTM, 0, stream>>>(a);
+    if (grad) pair_kernel<true><<<grid, kTM, kTabBytes, stream>>>(a);
+    else pair_kernel<false><<<grid, kTM, kTabBytes, stream>>>(a);
   }
   return cudaGetLastError();
 }
@@ -924,12 +971,13 @@ cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* o
 
 int pair_kernel_occupancy(bool grad, int mode) {
   int occ = 0;
+  if (prepare_pair_kernels() != cudaSuccess) return 1;
   if (mode == kSym) {
-    if (grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel<true>, kTM, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel<false>, kTM, 0);
+    if (grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel<true>, kTM, kTabBytes);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel<false>, kTM, kTabBytes);
   } else {
-    if (grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<true>, kTM, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<false>, kTM, 0);
+    if (grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<true>, kTM, kTabBytes);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<false>, kTM, kTabBytes);
   }
   return occ > 0 ? occ : 1;
 }

@@ -35,12 +35,13 @@ constexpr double kCullExponent = 709.0;
 //         trigger term stays one-directional (t_j < t_i implies j < i).
 enum PairMode : int { kRows = 0, kSym = 1 };
 
-// Exponent constants are pre-multiplied by kExpL = 256/ln2 ("L units", see
+// Exponent constants are pre-multiplied by kExpL = 2048/ln2 ("L units", see
 // exp_l in sthk_device.cuh).
 struct PairConsts {
   double cxL;   // -L/(2 tauX^2)
   double ctL;   // -L/(2 tauT^2)
   double chL;   // -L/(2 h^2)
+  double chS;   // chL / sx^2: trigger spatial constant on pre-scaled coordinates (kSym)
   double nomL;  // -L omega
   double dB;    // background live iff |dt| <= dB   (inf when dense)
   double dT;    // trigger live iff 0 < dt <= dT    (inf when dense)
@@ -71,6 +72,8 @@ struct PairArgs {
   const double* x;
   const double* y;
   const double* t;
+  const double* xs;         // kSym: x, y pre-scaled by sx = sqrt(-cxL) (r2 = -cxL r^2)
+  const double* ys;
   const double4* tile_box;  // per 128-event tile: xmin, xmax, ymin, ymax
   int64_t n;
   int64_t npad;
@@ -101,6 +104,7 @@ struct FinArgs {
   const unsigned long long* fx;
   double fxq[kNSumGrad];
   const double* tpart;
+  double tr_r2_scale;   // 1 (kRows) or 1/sx^2 (kSym: trigger r^2 sums on scaled coordinates)
   const int2* crange;
   double* per_event;    // nullable
   double* ex_out;       // nullable: excitation mu, xi, pi as [3][npad]
@@ -110,7 +114,10 @@ struct FinArgs {
 // Launch wrappers (sthk_kernels.cu). All enqueue on `stream`.
 cudaError_t launch_tile_boxes(const double* x, const double* y, int64_t n, double4* box,
                               cudaStream_t stream);
+cudaError_t launch_scale_xy(const double* x, const double* y, int64_t n, double sx, double* xs,
+                            double* ys, cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
+cudaError_t launch_exp_probe(const double* x, int64_t n, double* out, cudaStream_t stream);
 cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaStream_t stream);
 cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream);
 cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,

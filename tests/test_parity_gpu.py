@@ -247,3 +247,34 @@ def test_background_cache_bitwise_transparent(engine):
                 assert np.array_equal(a[2], b[2])
         # hits: tauX change at index 5 forces a full sweep; grad->value reuses
         assert sum(outs[True][1]) >= 9 and sum(outs[False][1]) == 0
+
+
+def _ulp_err(got, want):
+    return np.abs(got - want) / np.spacing(np.abs(want))
+
+
+def test_exp_l_accuracy(engine):
+    """The pair kernels' exp (2048-entry table + degree-3 polynomial, sthk_device.cuh)
+    against an extended-precision exp: <= 2 ulp (the reference's Pack exp bound,
+    test_pack.cpp:21-46) over the live range, exact +0 below -708.40 (the flush the
+    exact culling relies on), 1 at 0."""
+    import ctypes
+    lib = pk.load_library()
+    rng = np.random.default_rng(7)
+    x = np.concatenate([-rng.uniform(0, 708.3, 200_000), -rng.uniform(0, 1e-3, 20_000),
+                        -np.logspace(-12, 2.85, 20_000), [0.0, -708.3, -708.41, -745.0, -1e6]])
+    out = np.empty_like(x)
+    dp = ctypes.POINTER(ctypes.c_double)
+    rc = lib.sthk_debug_exp(0, x.ctypes.data_as(dp), x.size, out.ctypes.data_as(dp))
+    assert rc == 0
+    live = x >= -708.3
+    want = np.exp(x[live].astype(np.longdouble)).astype(np.float64)
+    # one extra rounding: the argument is scaled to L units (x * 2048/ln2)
+    # in double, an error of ~|x| * 2^-53 relative, i.e. up to ~700 * 1.1e-16
+    arg_err = np.abs(x[live]) * 2.0 ** -53 / np.spacing(1.0) * 2
+    err = _ulp_err(out[live], want)
+    assert np.all(err <= 2.0 + arg_err), float(np.max(err - arg_err))
+    small = live & (x > -1.0)
+    assert np.max(_ulp_err(out[small], np.exp(x[small].astype(np.longdouble)).astype(np.float64))) <= 2.0
+    assert out[x.size - 5] == 1.0
+    assert np.all(out[x < -708.41] == 0.0)
