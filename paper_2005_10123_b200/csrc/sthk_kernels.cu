@@ -229,11 +229,14 @@ __device__ __forceinline__ void store_row_sums(const PairArgs& a, int chunk, int
   for (int q = 0; q < NT; ++q) out[static_cast<size_t>(q) * a.npad] = acc[NB + q];
 }
 
+constexpr uint32_t kBoxBytes = sizeof(double4);
+
 template <bool GRAD>
 __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArgs a) {
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   __shared__ __align__(128) double s_src[2][3][kTS];
   extern __shared__ uint2 s_tab[];  // kExpTableSize entries (dynamic)
+  __shared__ __align__(32) double4 s_box[2];  // bounding box of the staged source tile
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ int s_item[2];
 
@@ -279,7 +282,8 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
 
     constexpr uint32_t kStageBytes = kTS * sizeof(double);
     if (tid == 0 && nst > 0) {
-      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes);
+      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes + kBoxBytes);
+      tma_load_1d(&s_box[0], a.tile_box + s_begin / kTS, kBoxBytes, &s_bar[0]);
       tma_load_1d(s_src[0][0], a.x + s_begin, kStageBytes, &s_bar[0]);
       tma_load_1d(s_src[0][1], a.y + s_begin, kStageBytes, &s_bar[0]);
       tma_load_1d(s_src[0][2], a.t + s_begin, kStageBytes, &s_bar[0]);
@@ -291,15 +295,19 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
       if (tid == 0 && s + 1 < nst) {
         const int nb = buf ^ 1;
         const int64_t s0n = s_begin + static_cast<int64_t>(s + 1) * kTS;
-        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes);
+        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes + kBoxBytes);
+        tma_load_1d(&s_box[nb], a.tile_box + s0n / kTS, kBoxBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][0], a.x + s0n, kStageBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][1], a.y + s0n, kStageBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][2], a.t + s0n, kStageBytes, &s_bar[nb]);
       }
       const int64_t s0 = s_begin + static_cast<int64_t>(s) * kTS;
       const int cnt = static_cast<int>(min(static_cast<int64_t>(kTS), n - s0));
-      const double4 bs = a.tile_box[s0 / kTS];
-      const double smin = a.t[s0], smax = a.t[s0 + cnt - 1];
+      mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+      // stage metadata from the staged copy (no global-memory round trip)
+      const double4 bs = s_box[buf];
+      const double smin = s_src[buf][2][0], smax = s_src[buf][2][cnt - 1];
 
       const bool bg = !a.bg_off && !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
       int tr;
@@ -314,8 +322,6 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
       const bool safe = (!bg || a.k.cxL * r2m + a.k.ctL * (dtm * dtm) > kSafeExpL) &&
                         (!tr || a.k.nomL * dtm + a.k.chL * r2m > kSafeExpL);
 
-      mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
-      phase ^= 1u << buf;
 
       const double* sx = s_src[buf][0];
       const double* sy = s_src[buf][1];
@@ -541,6 +547,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
   extern __shared__ uint2 s_tab[];  // kExpTableSize entries (dynamic)
   __shared__ double s_col[kTS * NSC];
   __shared__ double s_red[4][NS][kTM];
+  __shared__ __align__(32) double4 s_box[2];  // bounding box of the staged source tile
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ int s_item[2];
 
@@ -606,7 +613,8 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
 
     constexpr uint32_t kStageBytes = kTS * sizeof(double);
     if (tid == 0 && nst > 0) {
-      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes);
+      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes + kBoxBytes);
+      tma_load_1d(&s_box[0], a.tile_box + s_begin / kTS, kBoxBytes, &s_bar[0]);
       tma_load_1d(s_src[0][0], a.xs + s_begin, kStageBytes, &s_bar[0]);
       tma_load_1d(s_src[0][1], a.ys + s_begin, kStageBytes, &s_bar[0]);
       tma_load_1d(s_src[0][2], a.t + s_begin, kStageBytes, &s_bar[0]);
@@ -618,7 +626,8 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       if (tid == 0 && s + 1 < nst) {
         const int nb = buf ^ 1;
         const int64_t s0n = s_begin + static_cast<int64_t>(s + 1) * kTS;
-        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes);
+        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes + kBoxBytes);
+        tma_load_1d(&s_box[nb], a.tile_box + s0n / kTS, kBoxBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][0], a.xs + s0n, kStageBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][1], a.ys + s0n, kStageBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][2], a.t + s0n, kStageBytes, &s_bar[nb]);
@@ -626,8 +635,11 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       const int64_t s0 = s_begin + static_cast<int64_t>(s) * kTS;
       const int cnt = static_cast<int>(min(static_cast<int64_t>(kTS), n - s0));
       const bool diag = s0 == first;
-      const double4 bs = a.tile_box[s0 / kTS];
-      const double smin = a.t[s0], smax = a.t[s0 + cnt - 1];
+      mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+      // stage metadata from the staged copy (no global-memory round trip)
+      const double4 bs = s_box[buf];
+      const double smin = s_src[buf][2][0], smax = s_src[buf][2][cnt - 1];
 
       const bool bg = !a.bg_off && !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
       int tr;
@@ -641,8 +653,6 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       const bool safe = (!bg || a.k.cxL * r2m + a.k.ctL * (dtm * dtm) > kSafeExpL) &&
                         (!tr || a.k.nomL * dtm + a.k.chL * r2m > kSafeExpL);
 
-      mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
-      phase ^= 1u << buf;
 
       const double* sx = s_src[buf][0];
       const double* sy = s_src[buf][1];
