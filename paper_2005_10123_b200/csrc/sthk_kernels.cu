@@ -92,55 +92,79 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, int tile, int2& rg,
   cr = make_int2(a.dense ? 0 : lo / a.sc, (hi - 1) / a.sc);
 }
 
-// Single CTA: per-tile ranges, an exclusive scan of the per-tile item counts
-// and the (tile, chunk) work list in tile order; resets the persistent pair
-// kernel's work counter.
+// Number of 128-source stages of work item (tile, chunk) -- the same bounds
+// the pair kernels compute.
+__device__ __forceinline__ int item_stages(const PlanArgs& a, int2 rg, int chunk) {
+  int s_begin = max(rg.x, chunk * a.sc);
+  s_begin -= s_begin % kTS;
+  const int s_end = min(rg.y, (chunk + 1) * a.sc);
+  return max((s_end - s_begin + kTS - 1) / kTS, 0);
+}
+
+constexpr int kPlanBins = 1024;  // item-size classes (stages, clamped)
+
+// Single CTA: per-tile ranges, then the (tile, chunk) work list ordered by
+// decreasing item size (a counting sort on the stage count), so the
+// persistent pair kernel hands out the long items first and ends on short
+// ones (less idle time in the tail); resets the pair kernel's work counter.
+// The order only affects scheduling: every partial has a fixed destination
+// and integer (fixed-point) accumulation, so results do not depend on it.
 __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
+  __shared__ int s_hist[kPlanBins];
   __shared__ int s_warp[32];
-  __shared__ int s_carry;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ntiles = a.tile1 - a.tile0;
-  if (tid == 0) s_carry = 0;
+  for (int b = tid; b < kPlanBins; b += 1024) s_hist[b] = 0;
   __syncthreads();
-  for (int base = 0; base < ntiles; base += 1024) {
-    const int i = base + tid;
-    int c = 0;
+  // pass 1: ranges and the item-size histogram
+  for (int i = tid; i < ntiles; i += 1024) {
     int2 rg, cr;
-    if (i < ntiles) {
-      tile_plan(a, a.tile0 + i, rg, cr);
-      a.ranges[a.tile0 + i] = rg;
-      a.crange[a.tile0 + i] = cr;
-      c = cr.y - cr.x + 1;
+    tile_plan(a, a.tile0 + i, rg, cr);
+    a.ranges[a.tile0 + i] = rg;
+    a.crange[a.tile0 + i] = cr;
+    for (int c = cr.x; c <= cr.y; ++c) {
+      atomicAdd(&s_hist[min(item_stages(a, rg, c), kPlanBins - 1)], 1);
     }
-    // block-wide inclusive scan: warp shuffles, then the warp totals
-    int v = c;
+  }
+  __syncthreads();
+  // exclusive scan over the bins in decreasing size: bin b starts after all
+  // larger bins (thread t owns bin kPlanBins - 1 - t)
+  const int bin = kPlanBins - 1 - tid;
+  const int c = s_hist[bin];
+  int v = c;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, off);
+    if (lane >= off) v += u;
+  }
+  if (lane == 31) s_warp[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    int w = s_warp[lane];
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, v, off);
-      if (lane >= off) v += u;
+      const int u = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += u;
     }
-    if (lane == 31) s_warp[warp] = v;
-    __syncthreads();
-    if (warp == 0) {
-      int w = s_warp[lane];
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, w, off);
-        if (lane >= off) w += u;
-      }
-      s_warp[lane] = w;
-    }
-    __syncthreads();
-    const int incl = v + (warp > 0 ? s_warp[warp - 1] : 0);
-    const int excl = s_carry + incl - c;
-    for (int q = 0; q < c; ++q) a.items[excl + q] = make_int2(a.tile0 + i, cr.x + q);
-    __syncthreads();
-    if (tid == 1023) s_carry += incl;
-    __syncthreads();
+    s_warp[lane] = w;
   }
-  if (tid == 0) {
-    *a.n_items = s_carry;
+  __syncthreads();
+  const int incl = v + (warp > 0 ? s_warp[warp - 1] : 0);
+  if (tid == 1023) {
+    *a.n_items = incl;
     *a.work_counter = 0;
+  }
+  __syncthreads();
+  s_hist[bin] = incl - c;  // start offset of the bin
+  __syncthreads();
+  // pass 2: place every item
+  for (int i = tid; i < ntiles; i += 1024) {
+    const int tile = a.tile0 + i;
+    const int2 rg = a.ranges[tile], cr = a.crange[tile];
+    for (int ch = cr.x; ch <= cr.y; ++ch) {
+      const int pos = atomicAdd(&s_hist[min(item_stages(a, rg, ch), kPlanBins - 1)], 1);
+      a.items[pos] = make_int2(tile, ch);
+    }
   }
 }
 
@@ -230,24 +254,31 @@ __device__ __forceinline__ void store_row_sums(const PairArgs& a, int chunk, int
 }
 
 constexpr uint32_t kBoxBytes = sizeof(double4);
+constexpr uint32_t kTabBytes = sizeof(uint2) * kExpTableSize;
 
 template <bool GRAD>
 __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArgs a) {
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   __shared__ __align__(128) double s_src[2][3][kTS];
-  extern __shared__ uint2 s_tab[];  // kExpTableSize entries (dynamic)
+  extern __shared__ __align__(128) uint2 s_tab[];  // kExpTableSize entries (dynamic)
   __shared__ __align__(32) double4 s_box[2];  // bounding box of the staged source tile
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ int s_item[2];
 
   const int tid = threadIdx.x;
-  for (int i = tid; i < kExpTableSize; i += kTM) s_tab[i] = kExpTable[i];
+  __shared__ __align__(8) uint64_t s_tbar;
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
+    mbar_init(&s_tbar, 1);
     mbar_fence_init();
   }
   __syncthreads();
+  if (tid == 0) {  // the exp table: one 16 KB bulk copy (L2-resident source)
+    mbar_arrive_expect_tx(&s_tbar, kTabBytes);
+    tma_load_1d(s_tab, kExpTable, kTabBytes, &s_tbar);
+  }
+  mbar_wait(&s_tbar, 0);
 
   const int n_items = *a.n_items;
   const int64_t n = a.n;
@@ -544,7 +575,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   constexpr int NSC = GRAD ? 3 : 1;
   __shared__ __align__(128) double s_src[2][3][kTS];
-  extern __shared__ uint2 s_tab[];  // kExpTableSize entries (dynamic)
+  extern __shared__ __align__(128) uint2 s_tab[];  // kExpTableSize entries (dynamic)
   __shared__ double s_col[kTS * NSC];
   __shared__ double s_red[4][NS][kTM];
   __shared__ __align__(32) double4 s_box[2];  // bounding box of the staged source tile
@@ -553,13 +584,19 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kExpTableSize; i += kTM) s_tab[i] = kExpTable[i];
+  __shared__ __align__(8) uint64_t s_tbar;
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
+    mbar_init(&s_tbar, 1);
     mbar_fence_init();
   }
   __syncthreads();
+  if (tid == 0) {  // the exp table: one 16 KB bulk copy (L2-resident source)
+    mbar_arrive_expect_tx(&s_tbar, kTabBytes);
+    tma_load_1d(s_tab, kExpTable, kTabBytes, &s_tbar);
+  }
+  mbar_wait(&s_tbar, 0);
 
   const int n_items = *a.n_items;
   const int64_t n = a.n;
@@ -935,8 +972,6 @@ cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
   plan_kernel<<<1, 1024, 0, stream>>>(a);
   return cudaGetLastError();
 }
-
-constexpr size_t kTabBytes = sizeof(uint2) * kExpTableSize;
 
 // The exp table lives in dynamic shared memory (static + dynamic > 48 KB
 // needs the opt-in attribute); set once per device before the first launch.
