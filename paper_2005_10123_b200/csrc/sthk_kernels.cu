@@ -45,20 +45,38 @@ namespace {
 constexpr double kInvSqrt2 = 0.7071067811865475244;     // kernels.hpp:14
 constexpr double kInvSqrt2Pi = 0.3989422804014326779;   // kernels.hpp:13
 
-__device__ __forceinline__ int64_t lower_bound_t(const double* t, int64_t n, double v) {
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (t[mid] < v) lo = mid + 1; else hi = mid;
-  }
-  return lo;
+// Sorted-time searches in two levels: kPivots evenly spaced pivots
+// piv[k] = t[k * stride] in shared memory narrow the range to one stride,
+// then a binary search over global memory finishes it (log2(stride) dependent
+// loads instead of log2(n)). STRICT: first i with t[i] >= v (lower bound),
+// else first i with t[i] > v (upper bound).
+constexpr int kPivots = 1024;
+
+struct Pivots {
+  const double* piv;  // shared memory, np entries
+  int np;
+  int64_t stride;
+};
+
+template <bool STRICT>
+__device__ __forceinline__ bool before(double tv, double v) {
+  return STRICT ? (tv < v) : (tv <= v);
 }
 
-__device__ __forceinline__ int64_t upper_bound_t(const double* t, int64_t n, double v) {
-  int64_t lo = 0, hi = n;
+template <bool STRICT>
+__device__ __forceinline__ int64_t bound_t(const double* t, int64_t n, double v, const Pivots& p) {
+  // last pivot k with piv[k] "before" v (pivots are sorted)
+  int klo = 0, khi = p.np;  // answer k = (first pivot not before v) - 1
+  while (klo < khi) {
+    const int mid = (klo + khi) >> 1;
+    if (before<STRICT>(p.piv[mid], v)) klo = mid + 1; else khi = mid;
+  }
+  if (klo == 0) return 0;  // t[0] is not before v
+  int64_t lo = static_cast<int64_t>(klo - 1) * p.stride + 1;
+  int64_t hi = min(static_cast<int64_t>(klo) * p.stride, n);
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
-    if (t[mid] <= v) lo = mid + 1; else hi = mid;
+    if (before<STRICT>(t[mid], v)) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
@@ -67,7 +85,8 @@ __device__ __forceinline__ int64_t upper_bound_t(const double* t, int64_t n, dou
 // Plan
 // ---------------------------------------------------------------------------
 // Live source range [lo, hi) and chunk range [c0, c1] of one row tile.
-__device__ __forceinline__ void tile_plan(const PlanArgs& a, int tile, int2& rg, int2& cr) {
+__device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, int tile, int2& rg,
+                                          int2& cr) {
   const int64_t first = static_cast<int64_t>(tile) * kTM;
   const int64_t last = min(first + kTM, a.n) - 1;
   int lo, hi;
@@ -75,13 +94,13 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, int tile, int2& rg,
     lo = 0;
     hi = static_cast<int>(a.n);
   } else if (a.trig_only) {
-    lo = min(static_cast<int>(lower_bound_t(a.t, a.n, a.t[first] - a.dT)),
+    lo = min(static_cast<int>(bound_t<true>(a.t, a.n, a.t[first] - a.dT, pv)),
              static_cast<int>(first));
     hi = static_cast<int>(last + 1);
   } else {
     const double tmin = a.t[first], tmax = a.t[last];
-    lo = static_cast<int>(lower_bound_t(a.t, a.n, tmin - fmax(a.dB, a.dT)));
-    hi = static_cast<int>(upper_bound_t(a.t, a.n, tmax + a.dB));
+    lo = static_cast<int>(bound_t<true>(a.t, a.n, tmin - fmax(a.dB, a.dT), pv));
+    hi = static_cast<int>(bound_t<false>(a.t, a.n, tmax + a.dB, pv));
     // the tile's own rows are always live (background self term)
     lo = min(lo, static_cast<int>(first));
     hi = max(hi, static_cast<int>(last + 1));
@@ -112,14 +131,20 @@ constexpr int kPlanBins = 1024;  // item-size classes (stages, clamped)
 __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   __shared__ int s_hist[kPlanBins];
   __shared__ int s_warp[32];
+  __shared__ double s_piv[kPivots];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ntiles = a.tile1 - a.tile0;
   for (int b = tid; b < kPlanBins; b += 1024) s_hist[b] = 0;
+  Pivots pv;
+  pv.stride = (a.n + kPivots - 1) / kPivots;
+  pv.np = static_cast<int>((a.n + pv.stride - 1) / pv.stride);
+  pv.piv = s_piv;
+  for (int k = tid; k < pv.np; k += 1024) s_piv[k] = a.t[k * pv.stride];
   __syncthreads();
   // pass 1: ranges and the item-size histogram
   for (int i = tid; i < ntiles; i += 1024) {
     int2 rg, cr;
-    tile_plan(a, a.tile0 + i, rg, cr);
+    tile_plan(a, pv, a.tile0 + i, rg, cr);
     a.ranges[a.tile0 + i] = rg;
     a.crange[a.tile0 + i] = cr;
     for (int c = cr.x; c <= cr.y; ++c) {
