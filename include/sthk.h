@@ -124,6 +124,8 @@ typedef struct sthk_stats {
   int32_t kernel_mode;       /* STHK_KERNEL_ROWS or STHK_KERNEL_SYM */
   int32_t cache_hit;         /* 1 if the last evaluation reused cached
                                 background sums (trigger-only sweep) */
+  int32_t trigger_cache_hit; /* 1 if it also reused the trigger sums (only mu0 /
+                                theta changed: no pair sweep at all) */
 } sthk_stats;
 
 int sthk_set_timing(sthk_engine* e, int enable);
@@ -137,11 +139,15 @@ int sthk_set_dense(sthk_engine* e, int dense);
  * pair once and adds it to both events' sums (b_ij = b_ji); STHK_KERNEL_ROWS
  * sweeps ordered pairs per target row. Both are deterministic; they agree to
  * rounding (different summation grouping), not bitwise. */
-/* Background-sum cache (default on). The background sums depend only on the
+/* Sweep caches (default on). The background sums depend only on the
  * events, tauX and tauT, which the reference MH sampler keeps fixed for a
  * whole chain (sampler.cpp:48-49); while they are unchanged an evaluation
- * sweeps only the trigger band. Results are bitwise identical with the cache
- * on or off (fixed chunk grid). Benchmarks of full evaluations turn it off. */
+ * sweeps only the trigger band. The trigger sums depend only on the events,
+ * omega and h; while those are unchanged too (an MH move of mu0 or theta) an
+ * evaluation runs no pair sweep at all, only the per-event finalize. The
+ * work plan (live ranges, work list) is reused while the culling windows are
+ * unchanged. Results are bitwise identical with the caches on or off (fixed
+ * chunk grid, same kernels). Benchmarks of full evaluations turn them off. */
 int sthk_set_background_cache(sthk_engine* e, int enable);
 
 #define STHK_KERNEL_ROWS 0

@@ -41,6 +41,7 @@ class StatsStruct(ctypes.Structure):
         ("exec_sym", c_int64),
         ("kernel_mode", ctypes.c_int32),
         ("cache_hit", ctypes.c_int32),
+        ("trigger_cache_hit", ctypes.c_int32),
     ]
 
 

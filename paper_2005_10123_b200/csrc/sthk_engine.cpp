@@ -87,7 +87,7 @@ struct Slot {
   size_t counts_cap = 0;
   int2* items = nullptr;
   size_t items_cap = 0;
-  int* scalars = nullptr;  // [0] n_items, [1] work counter
+  int* scalars = nullptr;  // [0] n_items, [1] work counter, [2] pair CTAs done, [3] finalize blocks done
   unsigned long long* fx = nullptr;  // fixed-point background sums [6][npad]
   size_t fx_cap = 0;
   double* tpart = nullptr;           // trigger partials [nchunks][3][npad]
@@ -110,6 +110,11 @@ struct Slot {
   size_t h_pe_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int row0 = 0, row1 = 0;  // rows of the last enqueued eval (first..last run)
+  // plan cache (with the sweep caches on): the last plan's inputs; the plan
+  // is a function of (times, culling windows, mode, rows, chunking) only
+  bool plan_valid = false;
+  double plan_dB = 0, plan_dT = 0;
+  int plan_key[6] = {0, 0, 0, 0, 0, 0};  // tile0, tile1, sc, dense, sym, trig_only
   std::vector<std::pair<int, int>> runs;  // row ranges run on this slot
 };
 
@@ -132,6 +137,11 @@ struct sthk_engine {
   // fixed chunk grid makes the cached path bitwise identical to a fresh one.
   bool bg_cache = true;
   bool cache_valid = false, cache_grad = false, last_cache_hit = false;
+  // Trigger-sum cache (same switch): with the background cached, the trigger
+  // partials of the last sweep stay valid while omega and h are unchanged,
+  // so an evaluation that moves only mu0 / theta is a finalize pass.
+  bool tr_cache_valid = false, tr_cache_grad = false, last_tr_cache_hit = false;
+  double tr_cache_omega = 0, tr_cache_h = 0;
   uint64_t load_gen = 0, cache_gen = 0;
   double cache_tx = 0, cache_tt = 0;
   int cache_mode = -1;
@@ -154,7 +164,8 @@ void init_slot(Slot& s, int dev) {
   ck(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
   ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
   for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
-  ck(cudaMalloc(&s.scalars, 2 * sizeof(int)), "cudaMalloc");
+  ck(cudaMalloc(&s.scalars, 4 * sizeof(int)), "cudaMalloc");
+  ck(cudaMemset(s.scalars, 0, 4 * sizeof(int)), "memset");
   ck(cudaMalloc(&s.out, kNOut * sizeof(double)), "cudaMalloc");
   ck(cudaMalloc(&s.pair_counts, sthk::kNCounts * sizeof(unsigned long long)), "cudaMalloc");
   ck(cudaMallocHost(&s.h_out, kNOut * sizeof(double)), "cudaMallocHost");
@@ -341,8 +352,12 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
   const bool cached = e.bg_cache && e.cache_valid && e.cache_gen == e.load_gen &&
                       e.cache_tx == e.p[1] && e.cache_tt == e.p[2] && e.cache_mode == e.mode &&
                       e.cache_dense == e.dense && (e.cache_grad || !grad);
+  const bool tr_cached = cached && e.tr_cache_valid && e.tr_cache_omega == e.p[4] &&
+                         e.tr_cache_h == e.p[5] && e.tr_cache_grad == grad;  // (tpart layout)
   e.last_cache_hit = cached;
+  e.last_tr_cache_hit = tr_cached;
   e.cache_valid = false;  // re-armed below once the sweep is enqueued
+  e.tr_cache_valid = false;
   const int64_t ntiles_total = (e.n + kTM - 1) / kTM;
   const int nb_total = static_cast<int>((e.n + sthk::kFB - 1) / sthk::kFB);
   const double* p = e.p;
@@ -388,8 +403,10 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     cudaStream_t st = s.stream;
     if (first_run) {
       if (e.timing) ck(cudaEventRecord(s.ev[0], st), "event");
-      ck(cudaMemsetAsync(s.pair_counts, 0, sthk::kNCounts * sizeof(unsigned long long), st),
-         "memset");
+      if (e.timing) {  // pair counters feed the stats / roofline only
+        ck(cudaMemsetAsync(s.pair_counts, 0, sthk::kNCounts * sizeof(unsigned long long), st),
+           "memset");
+      }
       if (!cached) {
         ck(cudaMemsetAsync(s.fx, 0, sizeof(unsigned long long) * kFxRows * e.npad, st),
            "memset");
@@ -402,6 +419,11 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       }
     }
     if (ntiles == 0) continue;
+    if (tr_cached) {  // every pair sum is cached: finalize only
+      if (e.timing && first_run) ck(cudaEventRecord(s.ev[1], st), "event");
+      if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
+      continue;
+    }
     sthk::PlanArgs pa{};
     pa.t = s.t;
     pa.n = e.n;
@@ -419,7 +441,16 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     pa.items = s.items;
     pa.n_items = s.scalars;
     pa.work_counter = s.scalars + 1;
-    ck(sthk::launch_plan(pa, st), "plan");
+    const int key[6] = {tile0, tile1, pl.sc, pa.dense, pa.sym, pa.trig_only};
+    const bool plan_hit = e.bg_cache && !vshards && s.plan_valid && s.plan_dB == pa.dB &&
+                          s.plan_dT == pa.dT && std::equal(key, key + 6, s.plan_key);
+    if (!plan_hit) {  // (the work counter is re-armed by the last pair CTA)
+      ck(sthk::launch_plan(pa, st), "plan");
+      s.plan_valid = e.bg_cache && !vshards;
+      s.plan_dB = pa.dB;
+      s.plan_dT = pa.dT;
+      std::copy(key, key + 6, s.plan_key);
+    }
 
     sthk::PairArgs qa{};
     qa.x = s.x;
@@ -436,12 +467,13 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     qa.items = s.items;
     qa.n_items = s.scalars;
     qa.work_counter = s.scalars + 1;
+    qa.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 2);
     qa.fx = s.fx;
     qa.tpart = s.tpart;
     qa.bg_off = cached ? 1 : 0;
     for (int k = 0; k < sthk::kNSumGrad; ++k) qa.fxq[k] = fxq[k];
     if (sym) qa.fxq[1] = fxq[1] / (pl.sx * pl.sx);  // S_Br accumulates sx^2 r^2
-    qa.pair_counts = s.pair_counts;
+    qa.pair_counts = e.timing ? s.pair_counts : nullptr;
     // a trigger-only sweep runs the same kernel with the background switched
     // off, so its trigger partials are summed exactly as in a full sweep
     const int grid = s.sms * s.occ[e.mode][grad ? 1 : 0];
@@ -491,6 +523,10 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     fa.per_event = want_pe ? s.per_event : nullptr;
     fa.ex_out = want_ex ? s.ex : nullptr;
     fa.block_partial = s.block_partial;
+    // one shard on this slot and no collective: the final sum rides along
+    fa.fused_out = (shards == 1) ? s.out : nullptr;
+    fa.nblocks_total = nb_total;
+    fa.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 3);
     ck(sthk::launch_finalize(fa, grad, s.stream), "finalize");
   }
 
@@ -509,12 +545,18 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
   for (Slot& s : e.slots) {
     set_dev(s);
     cudaStream_t st = s.stream;
-    ck(sthk::launch_final_sum(s.block_partial, nb_total, s.out, st), "final sum");
+    if (shards > 1) {
+      ck(sthk::launch_final_sum(s.block_partial, nb_total, s.out, st), "final sum");
+    }
     ck(cudaMemcpyAsync(s.h_out, s.out, kNOut * sizeof(double), cudaMemcpyDeviceToHost, st),
        "D2H");
-    ck(cudaMemcpyAsync(s.h_counts, s.pair_counts, sthk::kNCounts * sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, st),
-       "D2H");
+    if (e.timing) {
+      ck(cudaMemcpyAsync(s.h_counts, s.pair_counts, sthk::kNCounts * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, st),
+         "D2H");
+    } else {
+      std::fill(s.h_counts, s.h_counts + sthk::kNCounts, 0ULL);
+    }
     if (want_pe && s.row1 > s.row0) {  // runs on one slot are contiguous
       if (s.h_pe_cap < static_cast<size_t>(e.npad)) {
         if (s.h_per_event) ck(cudaFreeHost(s.h_per_event), "cudaFreeHost");
@@ -552,6 +594,12 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     e.cache_dense = e.dense;
   }
   e.cache_valid = true;
+  if (!tr_cached) {
+    e.tr_cache_grad = grad;
+    e.tr_cache_omega = e.p[4];
+    e.tr_cache_h = e.p[5];
+  }
+  e.tr_cache_valid = e.bg_cache;
 }
 
 void collect(sthk_engine& e, double* loglik, int* valid, double* grad6, double* per_event) {
@@ -765,6 +813,8 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
     e->loaded = true;
     e->load_gen += 1;
     e->cache_valid = false;
+    e->tr_cache_valid = false;
+    for (Slot& s : e->slots) s.plan_valid = false;
   });
 }
 
@@ -883,7 +933,11 @@ int sthk_plan_partition(const double* t, int64_t n, const double* params6, int s
 int sthk_set_background_cache(sthk_engine* e, int enable) {
   return guarded(e, [&] {
     e->bg_cache = enable != 0;
-    if (!e->bg_cache) e->cache_valid = false;
+    if (!e->bg_cache) {
+      e->cache_valid = false;
+      e->tr_cache_valid = false;
+      for (Slot& s : e->slots) s.plan_valid = false;
+    }
   });
 }
 
@@ -927,6 +981,7 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
     out->source_chunk = e->last_sc;
     out->kernel_mode = e->mode;
     out->cache_hit = e->last_cache_hit ? 1 : 0;
+    out->trigger_cache_hit = e->last_tr_cache_hit ? 1 : 0;
     for (Slot& s : e->slots) {
       out->pairs_bg += static_cast<int64_t>(s.h_counts[0]);
       out->pairs_tr += static_cast<int64_t>(s.h_counts[1]);

@@ -395,6 +395,13 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
     store_row_sums<GRAD>(a, chunk, row, acc);
   }
 
+  if (tid == 0) {  // the last CTA out re-arms the work counter for the next launch
+    __threadfence();
+    if (atomicAdd(a.done_counter, 1u) == gridDim.x - 1) {
+      *a.work_counter = 0;
+      *a.done_counter = 0u;
+    }
+  }
   if (tid == 0 && a.pair_counts) {
     atomicAdd(&a.pair_counts[0], cBg);
     atomicAdd(&a.pair_counts[1], cTr);
@@ -792,6 +799,13 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
     store_row_sums<GRAD>(a, chunk, first + tid, v);
   }
 
+  if (tid == 0) {  // the last CTA out re-arms the work counter for the next launch
+    __threadfence();
+    if (atomicAdd(a.done_counter, 1u) == gridDim.x - 1) {
+      *a.work_counter = 0;
+      *a.done_counter = 0u;
+    }
+  }
   if (tid == 0 && a.pair_counts) {
     atomicAdd(&a.pair_counts[0], cBg);
     atomicAdd(&a.pair_counts[1], cTr);
@@ -806,18 +820,27 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
 // independent; computed once per load). Feeds the no-underflow proofs.
 __global__ void tile_box_kernel(const double* __restrict__ x, const double* __restrict__ y,
                                 int64_t n, double4* box) {
-  const int64_t tile = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // one warp per tile: 4 coalesced loads per lane, then a shuffle min/max
+  const int lane = threadIdx.x & 31;
+  const int64_t tile = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t first = tile * kTS;
   if (first >= n) return;
   const int64_t last = min(first + kTS, n);
   double x0 = x[first], x1 = x0, y0 = y[first], y1 = y0;
-  for (int64_t i = first + 1; i < last; ++i) {
+  for (int64_t i = first + lane; i < last; i += 32) {
     x0 = fmin(x0, x[i]);
     x1 = fmax(x1, x[i]);
     y0 = fmin(y0, y[i]);
     y1 = fmax(y1, y[i]);
   }
-  box[tile] = make_double4(x0, x1, y0, y1);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+    x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+    y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, off));
+    y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, off));
+  }
+  if (lane == 0) box[tile] = make_double4(x0, x1, y0, y1);
 }
 
 // Spatial coordinates pre-scaled by sx = sqrt(-cxL) for the symmetric
@@ -846,6 +869,31 @@ __global__ void exp_probe_kernel(const double* __restrict__ x, int64_t n, double
 // ---------------------------------------------------------------------------
 // Finalize: per-row lambda / compensator / log / gradient, block partials.
 // ---------------------------------------------------------------------------
+// Fixed-order sum of the block partials by one 256-thread block: thread t
+// sums blocks t, t+256, ... in order, then a fixed tree over the threads.
+__device__ __forceinline__ void final_sum_block(const double* __restrict__ bp, int nblocks,
+                                                double* out, double (*s_red)[256]) {
+  const int tid = threadIdx.x;
+  double acc[kNOut];
+#pragma unroll
+  for (int q = 0; q < kNOut; ++q) acc[q] = 0.0;
+  for (int b = tid; b < nblocks; b += 256) {
+#pragma unroll
+    for (int q = 0; q < kNOut; ++q) acc[q] += bp[static_cast<size_t>(b) * kNOut + q];
+  }
+#pragma unroll
+  for (int q = 0; q < kNOut; ++q) s_red[q][tid] = acc[q];
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (tid < w) {
+#pragma unroll
+      for (int q = 0; q < kNOut; ++q) s_red[q][tid] += s_red[q][tid + w];
+    }
+    __syncthreads();
+  }
+  if (tid < kNOut) out[tid] = s_red[tid][0];
+}
+
 template <bool GRAD>
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) {
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
@@ -943,30 +991,26 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
   if (tid < kNOut) {
     a.block_partial[(base / kFB) * kNOut + tid] = s_red[tid][0];
   }
+  if (a.fused_out) {  // single shard: the last block to finish does the final sum
+    __shared__ bool s_last;
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      s_last = atomicAdd(a.done_counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      final_sum_block(a.block_partial, a.nblocks_total, a.fused_out, s_red);
+      if (tid == 0) *a.done_counter = 0u;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict__ bp,
                                                         int nblocks, double* out) {
   __shared__ double s_red[kNOut][256];
-  const int tid = threadIdx.x;
-  double acc[kNOut];
-#pragma unroll
-  for (int q = 0; q < kNOut; ++q) acc[q] = 0.0;
-  for (int b = tid; b < nblocks; b += 256) {
-#pragma unroll
-    for (int q = 0; q < kNOut; ++q) acc[q] += bp[static_cast<size_t>(b) * kNOut + q];
-  }
-#pragma unroll
-  for (int q = 0; q < kNOut; ++q) s_red[q][tid] = acc[q];
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (tid < w) {
-#pragma unroll
-      for (int q = 0; q < kNOut; ++q) s_red[q][tid] += s_red[q][tid + w];
-    }
-    __syncthreads();
-  }
-  if (tid < kNOut) out[tid] = s_red[tid][0];
+  final_sum_block(bp, nblocks, out, s_red);
 }
 
 }  // namespace
@@ -974,7 +1018,7 @@ __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict
 cudaError_t launch_tile_boxes(const double* x, const double* y, int64_t n, double4* box,
                               cudaStream_t stream) {
   const int64_t ntiles = (n + kTS - 1) / kTS;
-  tile_box_kernel<<<static_cast<unsigned>((ntiles + 127) / 128), 128, 0, stream>>>(x, y, n, box);
+  tile_box_kernel<<<static_cast<unsigned>((ntiles + 7) / 8), 256, 0, stream>>>(x, y, n, box);
   return cudaGetLastError();
 }
 
@@ -1028,6 +1072,7 @@ cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaS
 cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream) {
   const int nblocks = (a.row1 - a.row0 + kFB - 1) / kFB;
   if (nblocks <= 0) return cudaSuccess;
+  static_assert(kFinThreads == 256, "fused final sum uses the 256-thread final_sum_block");
   if (grad) finalize_kernel<true><<<nblocks, kFinThreads, 0, stream>>>(a);
   else finalize_kernel<false><<<nblocks, kFinThreads, 0, stream>>>(a);
   return cudaGetLastError();

@@ -83,6 +83,7 @@ struct PairArgs {
   const int2* items;
   const int* n_items;
   int* work_counter;
+  unsigned int* done_counter;  // CTAs finished (the last one re-arms work_counter)
   unsigned long long* fx;
   double fxq[kNSumGrad];
   double* tpart;        // trigger partials [nchunks][3 or 1][npad]
@@ -109,6 +110,11 @@ struct FinArgs {
   double* per_event;    // nullable
   double* ex_out;       // nullable: excitation mu, xi, pi as [3][npad]
   double* block_partial;  // [ceil(n / kFB)][kNOut]
+  // single shard: fuse the final sum (the last block sums all nblocks_total
+  // block partials into fused_out); nullptr when a collective sits between
+  double* fused_out;
+  int nblocks_total;
+  unsigned int* done_counter;
 };
 
 // Launch wrappers (sthk_kernels.cu). All enqueue on `stream`.

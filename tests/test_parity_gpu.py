@@ -278,3 +278,43 @@ def test_exp_l_accuracy(engine):
     assert np.max(_ulp_err(out[small], np.exp(x[small].astype(np.longdouble)).astype(np.float64))) <= 2.0
     assert out[x.size - 5] == 1.0
     assert np.all(out[x < -708.41] == 0.0)
+
+
+def test_trigger_cache_and_plan_cache_bitwise_transparent(engine):
+    """MH-style moves with the sweep caches on: mu0 / theta moves reuse the
+    trigger sums too (finalize only), h moves reuse the work plan; every
+    result is bitwise the result of a full evaluation."""
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=9000)
+    base = [0.66, 1.6, 14, 0.344, 1440, 0.0695]
+    seq = []
+    rng = np.random.default_rng(3)
+    cur = list(base)
+    for _ in range(24):
+        k = [0, 3, 4, 5][int(rng.integers(4))]
+        cur = list(cur)
+        cur[k] *= float(np.exp(0.05 * rng.standard_normal()))
+        seq.append((pk.Params(*cur), bool(rng.integers(2))))
+    seq.append((pk.Params(*cur), True))   # repeat: grad after a possibly value-only sweep
+    seq.append((pk.Params(*cur), False))
+    engine.load(ev)
+    out = {}
+    for cache in (False, True):
+        engine.set_background_cache(cache)
+        res, hits = [], []
+        for p, grad in seq:
+            engine.set_params(p)
+            r = engine.loglik_grad(per_event=True) if grad else engine.loglik(per_event=True)
+            res.append(r)
+            st = engine.stats()
+            hits.append((st["cache_hit"], st["trigger_cache_hit"]))
+        out[cache] = (res, hits)
+    engine.set_background_cache(True)
+    for a, b in zip(out[False][0], out[True][0]):
+        assert a[0] == b[0]
+        assert np.array_equal(a[-1], b[-1])
+        if len(a) == 4:
+            assert np.array_equal(a[2], b[2])
+    assert sum(h[1] for h in out[False][1]) == 0
+    assert sum(h[1] for h in out[True][1]) >= 4
