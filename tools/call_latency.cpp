@@ -1,0 +1,49 @@
+// Per-call wall latency of the C ABI for MH-style moves at C2 (N=85k):
+// mu0 move (trigger cache hit: finalize only), h move (plan cached, trigger
+// sweep), omega move (plan + trigger sweep), full eval (caches off).
+#include <chrono>
+#include <cstdio>
+#include <vector>
+#include "../include/sthk.h"
+#include "../include/sthk_sim.h"
+int main() {
+  const int64_t cap = 90000;
+  std::vector<double> x(cap), y(cap), t(cap);
+  std::vector<int> par(cap);
+  int64_t cnt = 0;
+  const double truth[6] = {1, 1.6, 14, 0.344, 1440, 0.0695};
+  const double win[5] = {0, 15, 0, 15, 4750};
+  sthk_sim_cluster(truth, win, 0.053217, 2005, cap, x.data(), y.data(), t.data(), par.data(), &cnt);
+  const int64_t n = 85000;
+  sthk_engine* e = nullptr;
+  int dev = 0;
+  sthk_create(&dev, 1, &e);
+  sthk_load_events(e, x.data(), y.data(), t.data(), n, t[n - 1]);
+  double p[6] = {0.66, 1.6, 14, 0.344, 1440, 0.0695};
+  double ll; int valid;
+  sthk_set_params(e, p);
+  sthk_loglik(e, &ll, &valid, nullptr);
+  auto run = [&](const char* name, int k, double f) {
+    const int reps = 400;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < reps; ++i) {
+      p[k] *= (i & 1) ? 1.0 / f : f;
+      sthk_set_params(e, p);
+      sthk_loglik(e, &ll, &valid, nullptr);
+    }
+    double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() / reps;
+    sthk_stats st; sthk_get_stats(e, &st);
+    printf("%-28s %8.1f us/call  (cache_hit %d, trigger_cache_hit %d)\n", name, us, st.cache_hit, st.trigger_cache_hit);
+  };
+  run("mu0 move", 0, 1.01);
+  run("theta move", 3, 1.01);
+  run("h move", 5, 1.01);
+  run("omega move", 4, 1.01);
+  sthk_set_background_cache(e, 0);
+  run("mu0 move, caches off", 0, 1.01);
+  sthk_set_background_cache(e, 1);
+  // empty-ish: the same params (all caches hit)
+  run("no change", 0, 1.0);
+  sthk_destroy(e);
+  return 0;
+}
