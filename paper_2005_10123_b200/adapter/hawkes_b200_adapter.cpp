@@ -25,6 +25,7 @@
 // the very same three heap addresses with the same size and windowEnd that
 // also agrees at every sampled index; STHK_ADAPTER_FULL_CHECK=1 restores the
 // full comparison on every call.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -175,6 +176,40 @@ std::vector<LikelihoodResult> logLikelihoodBatch(const EventSet& events,
   }
   std::vector<LikelihoodResult> results;
   results.reserve(paramsList.size());
+  if (!keepPerEvent) {
+    // one engine call: entries validated in order (the reference's message
+    // for the first invalid one), evaluated grouped by (tauX, tauT, omega, h)
+    // so the exact sweep caches are shared across entries
+    for (size_t i = 0; i < paramsList.size(); ++i) {
+      try {
+        paramsList[i].validate();
+      } catch (const std::exception& ex) {
+        throw std::invalid_argument("logLikelihoodBatch: entry " + std::to_string(i) + ": " +
+                                    ex.what());
+      }
+    }
+    backend.validate();
+    AdapterEngine& e = engine();
+    std::lock_guard<std::mutex> lock(e.mu);
+    e.ensureLoaded(events);
+    const size_t P = paramsList.size();
+    std::vector<double> pv(6 * P), ll(P);
+    std::vector<int> ok(P);
+    for (size_t i = 0; i < P; ++i) {
+      const Params& p = paramsList[i];
+      const double v[6] = {p.mu0, p.tauX, p.tauT, p.theta, p.omega, p.h};
+      std::copy(v, v + 6, pv.begin() + static_cast<std::ptrdiff_t>(6 * i));
+    }
+    e.check(sthk_loglik_batch(e.h, pv.data(), static_cast<int64_t>(P), ll.data(), ok.data(),
+                              nullptr));
+    for (size_t i = 0; i < P; ++i) {
+      LikelihoodResult r;
+      r.valid = ok[i] != 0;
+      r.logLik = r.valid ? ll[i] : -std::numeric_limits<double>::infinity();
+      results.push_back(std::move(r));
+    }
+    return results;
+  }
   for (size_t i = 0; i < paramsList.size(); ++i) {
     try {
       results.push_back(logLikelihood(events, paramsList[i], backend, keepPerEvent));

@@ -894,7 +894,22 @@ int sthk_loglik_batch(sthk_engine* e, const double* params, int64_t P, double* l
     double saved[6];
     std::memcpy(saved, e->p, sizeof(saved));
     const bool had = e->has_params;
-    for (int64_t i = 0; i < P; ++i) {
+    // Evaluation order grouped by (tauX, tauT, omega, h): consecutive entries
+    // then reuse the cached background sums (same tauX, tauT) and trigger
+    // sums (same omega, h too), so a batch that varies mu0 / theta costs one
+    // sweep plus a finalize per entry. The caches are exact, so every result
+    // is bitwise the single-call result whatever the order.
+    std::vector<int64_t> order(static_cast<size_t>(P));
+    for (int64_t i = 0; i < P; ++i) order[static_cast<size_t>(i)] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+      const double* pa = params + 6 * a;
+      const double* pb = params + 6 * b;
+      for (int k : {1, 2, 4, 5}) {
+        if (pa[k] != pb[k]) return pa[k] < pb[k];
+      }
+      return false;
+    });
+    for (const int64_t i : order) {
       std::memcpy(e->p, params + 6 * i, sizeof(e->p));
       e->has_params = true;
       enqueue_eval(*e, grad != nullptr, false);

@@ -245,9 +245,22 @@ def logLikelihoodGradient(events: EventSet, params: Params, backend=None,
 
 def logLikelihoodBatch(events: EventSet, paramsList, backend=None, keepPerEvent: bool = False,
                        engine: Optional[Engine] = None):
-    """likelihood.cpp:57-75: elementwise identical to repeated calls."""
+    """likelihood.cpp:57-75: elementwise identical to repeated calls.
+    Without per-event terms the whole batch is one engine call, evaluated
+    grouped by (tauX, tauT, omega, h) so entries share the exact sweep caches."""
     if len(paramsList) == 0:
         raise ValueError("logLikelihoodBatch: empty parameter list")
+    if not keepPerEvent:
+        for i, p in enumerate(paramsList):
+            try:
+                p.validate()
+            except ValueError as e:
+                raise ValueError(f"logLikelihoodBatch: entry {i}: {e}") from None
+        eng = engine or default_engine()
+        with eng._lock:
+            eng.load(events)
+            ll, ok, _ = eng.loglik_batch([p.as_array() for p in paramsList])
+        return [LikelihoodResult(float(v), bool(o), np.zeros(0)) for v, o in zip(ll, ok)]
     out = []
     for i, p in enumerate(paramsList):
         try:

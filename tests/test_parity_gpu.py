@@ -318,3 +318,36 @@ def test_trigger_cache_and_plan_cache_bitwise_transparent(engine):
             assert np.array_equal(a[2], b[2])
     assert sum(h[1] for h in out[False][1]) == 0
     assert sum(h[1] for h in out[True][1]) >= 4
+
+
+def test_grouped_batch_shares_sweeps_bitwise(engine):
+    """f3: a profile/grid batch (mu0, theta varied over a few (omega, h)
+    pairs, shuffled) evaluated in one call is bitwise the single calls with
+    every cache off, for value and gradient batches."""
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=7000)
+    rng = np.random.default_rng(11)
+    plist = []
+    for om, h in [(1440.0, 0.0695), (500.0, 0.1), (1440.0, 0.2)]:
+        for _ in range(5):
+            plist.append([rng.uniform(0.3, 1.0), 1.6, 14.0, rng.uniform(0.1, 0.6), om, h])
+    plist.append([0.7, 1.3, 12.0, 0.3, 800.0, 0.08])
+    order = rng.permutation(len(plist))
+    plist = [plist[i] for i in order]
+    engine.load(ev)
+    engine.set_background_cache(True)
+    llb, okb, gb = engine.loglik_batch(plist, grad=True)
+    llv, okv, _ = engine.loglik_batch(plist)
+    engine.set_background_cache(False)
+    try:
+        for i, p in enumerate(plist):
+            engine.set_params(p)
+            s = engine.loglik_grad()
+            assert llb[i] == s[0] and np.array_equal(gb[i], s[2])
+            v = engine.loglik()
+            assert llv[i] == v[0]
+    finally:
+        engine.set_background_cache(True)
+    res = pk.logLikelihoodBatch(ev, [pk.Params(*p) for p in plist], engine=engine)
+    assert [r.logLik for r in res] == list(llv)
