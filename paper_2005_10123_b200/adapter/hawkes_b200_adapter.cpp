@@ -97,6 +97,7 @@ struct AdapterEngine {
         return;
       }
     }
+    n = -1;  // a failed load leaves the engine without events
     check(sthk_load_events(h, x, y, t, m, ev.windowEnd()));
     px = x;
     py = y;

@@ -87,7 +87,9 @@ struct Slot {
   size_t counts_cap = 0;
   int2* items = nullptr;
   size_t items_cap = 0;
-  int* scalars = nullptr;  // [0] n_items, [1] work counter, [2] pair CTAs done, [3] finalize blocks done
+  int* scalars = nullptr;  // [0] n_items, [1] work counter, [2] pair CTAs done, [3] finalize
+                           // blocks done, [4..5] first invalid event index (uint64)
+  unsigned long long* h_bad = nullptr;  // pinned
   unsigned long long* fx = nullptr;  // fixed-point background sums [6][npad]
   size_t fx_cap = 0;
   double* tpart = nullptr;           // trigger partials [nchunks][3][npad]
@@ -124,7 +126,8 @@ struct sthk_engine {
   std::vector<Slot> slots;
   bool rank_mode = false;
   int rank = 0, world = 1;
-  std::vector<double> ht;  // host copy of times (planning)
+  std::vector<double> ht;  // host copy of times (multi-shard planning only; lazy)
+  bool ht_valid = false;
   int64_t n = 0, npad = 0;
   double window_end = 0;
   double p[6] = {0, 0, 0, 0, 0, 0};
@@ -164,8 +167,9 @@ void init_slot(Slot& s, int dev) {
   ck(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
   ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
   for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
-  ck(cudaMalloc(&s.scalars, 4 * sizeof(int)), "cudaMalloc");
-  ck(cudaMemset(s.scalars, 0, 4 * sizeof(int)), "memset");
+  ck(cudaMalloc(&s.scalars, 6 * sizeof(int)), "cudaMalloc");
+  ck(cudaMemset(s.scalars, 0, 6 * sizeof(int)), "memset");
+  ck(cudaMallocHost(&s.h_bad, sizeof(unsigned long long)), "cudaMallocHost");
   ck(cudaMalloc(&s.out, kNOut * sizeof(double)), "cudaMalloc");
   ck(cudaMalloc(&s.pair_counts, sthk::kNCounts * sizeof(unsigned long long)), "cudaMalloc");
   ck(cudaMallocHost(&s.h_out, kNOut * sizeof(double)), "cudaMallocHost");
@@ -194,6 +198,7 @@ void free_slot(Slot& s) {
     if (p) cudaFree(p);
   }
   for (void* p : {static_cast<void*>(s.h_out), static_cast<void*>(s.h_counts),
+                  static_cast<void*>(s.h_bad),
                   static_cast<void*>(s.h_per_event), static_cast<void*>(s.h_ex)}) {
     if (p) cudaFreeHost(p);
   }
@@ -214,21 +219,26 @@ void validate_params(const double* p) {
   }
 }
 
-// EventSet constructor checks, types.hpp:85-109.
-void validate_events(const double* x, const double* y, const double* t, int64_t n,
-                     double window_end) {
+// EventSet constructor checks, types.hpp:85-109. The O(1) argument checks
+// run on the host; the per-event checks (finite, t >= 0, nondecreasing) run
+// on the device inside the tile-box pass over the uploaded copy, which
+// reports the first failing index; the message for it is rebuilt here in the
+// reference's order (non-finite, negative, unsorted), then windowEnd.
+void validate_event_args(const double* x, const double* y, const double* t, int64_t n) {
   if (n < 1) throw InvalidArg("EventSet: need at least one event");
   if (!x || !y || !t) throw InvalidArg("EventSet: coordinate/time length mismatch");
   if (n > (int64_t{1} << 30)) throw InvalidArg("sthk: at most 2^30 events supported");
-  for (int64_t i = 0; i < n; ++i) {
-    if (!std::isfinite(x[i]) || !std::isfinite(y[i]) || !std::isfinite(t[i])) {
-      throw InvalidArg("EventSet: non-finite entry at index " + std::to_string(i));
-    }
-    if (t[i] < 0.0) throw InvalidArg("EventSet: negative time at index " + std::to_string(i));
-    if (i > 0 && t[i] < t[i - 1]) {
-      throw InvalidArg("EventSet: times not sorted at index " + std::to_string(i));
-    }
+}
+
+[[noreturn]] void throw_event_error(const double* x, const double* y, const double* t, int64_t i) {
+  if (!std::isfinite(x[i]) || !std::isfinite(y[i]) || !std::isfinite(t[i])) {
+    throw InvalidArg("EventSet: non-finite entry at index " + std::to_string(i));
   }
+  if (t[i] < 0.0) throw InvalidArg("EventSet: negative time at index " + std::to_string(i));
+  throw InvalidArg("EventSet: times not sorted at index " + std::to_string(i));
+}
+
+void validate_window_end(const double* t, int64_t n, double window_end) {
   if (!std::isfinite(window_end) || window_end < t[n - 1]) {
     throw InvalidArg("EventSet: windowEnd precedes last event");
   }
@@ -347,6 +357,15 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
   const int shards = vshards ? e.virtual_shards
                              : (e.rank_mode ? e.world : static_cast<int>(e.slots.size()));
   const bool sym = e.mode == sthk::kSym;
+  if (shards > 1 && !e.ht_valid) {  // the cost-balanced partition needs the times on the host
+    Slot& s0 = e.slots[0];
+    set_dev(s0);
+    e.ht.resize(static_cast<size_t>(e.n));
+    ck(cudaMemcpyAsync(e.ht.data(), s0.t, sizeof(double) * e.n, cudaMemcpyDeviceToHost,
+                       s0.stream), "D2H");
+    ck(cudaStreamSynchronize(s0.stream), "D2H");
+    e.ht_valid = true;
+  }
   const EvalPlan pl = make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym}, shards);
   e.last_sc = pl.sc;
   const bool cached = e.bg_cache && e.cache_valid && e.cache_gen == e.load_gen &&
@@ -412,7 +431,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
            "memset");
       }
       if (sym && !cached) {  // (a cached sweep has the same tauX: scaled copies still valid)
-        ck(sthk::launch_scale_xy(s.x, s.y, e.n, pl.sx, s.xs, s.ys, st), "scale xy");
+        ck(sthk::launch_scale_xy(s.x, s.y, e.npad, pl.sx, s.xs, s.ys, st), "scale xy");
       }
       if (shards > 1) {
         ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
@@ -774,15 +793,17 @@ int sthk_destroy(sthk_engine* e) {
 int sthk_load_events(sthk_engine* e, const double* x, const double* y, const double* t,
                      int64_t n, double window_end) {
   return guarded(e, [&] {
-    validate_events(x, y, t, n, window_end);
+    validate_event_args(x, y, t, n);
     if (e->pending) collect(*e, nullptr, nullptr, nullptr, nullptr);
+    e->loaded = false;  // until the device-side checks pass
     const int64_t npad = (n + kTM - 1) / kTM * kTM;
-    e->ht.assign(t, t + n);
+    const bool multi = e->slots.size() > 1 || e->rank_mode;
+    if (multi) e->ht.assign(t, t + n);
+    e->ht_valid = multi;
     // Straight from the caller's buffers (pinned or pageable) to every
     // device; the pad tail is zero and is never read as a source (stage
     // loops are bounded by n) nor reported as a target.
     const size_t bytes = sizeof(double) * static_cast<size_t>(n);
-    const size_t pad = sizeof(double) * static_cast<size_t>(npad - n);
     for (Slot& s : e->slots) {
       set_dev(s);
       dev_grow(s.x, s.x_cap, static_cast<size_t>(npad));
@@ -790,23 +811,25 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       dev_grow(s.t, s.t_cap, static_cast<size_t>(npad));
       dev_grow(s.xs, s.xs_cap, static_cast<size_t>(npad));
       dev_grow(s.ys, s.ys_cap, static_cast<size_t>(npad));
-      ck(cudaMemsetAsync(s.xs, 0, sizeof(double) * npad, s.stream), "memset");
-      ck(cudaMemsetAsync(s.ys, 0, sizeof(double) * npad, s.stream), "memset");
       ck(cudaMemcpyAsync(s.x, x, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
       ck(cudaMemcpyAsync(s.y, y, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
       ck(cudaMemcpyAsync(s.t, t, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
-      if (pad) {
-        ck(cudaMemsetAsync(s.x + n, 0, pad, s.stream), "memset");
-        ck(cudaMemsetAsync(s.y + n, 0, pad, s.stream), "memset");
-        ck(cudaMemsetAsync(s.t + n, 0, pad, s.stream), "memset");
-      }
       dev_grow(s.tile_box, s.box_cap, static_cast<size_t>(npad / kTS));
-      ck(sthk::launch_tile_boxes(s.x, s.y, n, s.tile_box, s.stream), "tile boxes");
+      auto* bad = reinterpret_cast<unsigned long long*>(s.scalars + 4);
+      ck(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s.stream), "memset");
+      ck(sthk::launch_tile_boxes(s.x, s.y, s.t, n, npad, s.tile_box, bad, s.stream),
+         "tile boxes + checks");
+      ck(cudaMemcpyAsync(s.h_bad, bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                         s.stream),
+         "D2H");
     }
     for (Slot& s : e->slots) {
       set_dev(s);
       ck(cudaStreamSynchronize(s.stream), "H2D");
     }
+    const unsigned long long first_bad = *e->slots[0].h_bad;
+    if (first_bad != ~0ULL) throw_event_error(x, y, t, static_cast<int64_t>(first_bad));
+    validate_window_end(t, n, window_end);
     e->n = n;
     e->npad = npad;
     e->window_end = window_end;

@@ -818,8 +818,16 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
 
 // Per 128-event tile bounding box of the (x, y) coordinates (params
 // independent; computed once per load). Feeds the no-underflow proofs.
-__global__ void tile_box_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                                int64_t n, double4* box) {
+__global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
+                                double* __restrict__ t, int64_t n, int64_t npad, double4* box,
+                                unsigned long long* bad) {
+  // zero the pad tail [n, npad) of the coordinate arrays (never read as sources)
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid < npad - n) {
+    x[n + gid] = 0.0;
+    y[n + gid] = 0.0;
+    t[n + gid] = 0.0;
+  }
   // one warp per tile: 4 coalesced loads per lane, then a shuffle min/max
   const int lane = threadIdx.x & 31;
   const int64_t tile = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -827,11 +835,25 @@ __global__ void tile_box_kernel(const double* __restrict__ x, const double* __re
   if (first >= n) return;
   const int64_t last = min(first + kTS, n);
   double x0 = x[first], x1 = x0, y0 = y[first], y1 = y0;
+  int64_t first_bad = INT64_MAX;
   for (int64_t i = first + lane; i < last; i += 32) {
-    x0 = fmin(x0, x[i]);
-    x1 = fmax(x1, x[i]);
-    y0 = fmin(y0, y[i]);
-    y1 = fmax(y1, y[i]);
+    const double xv = x[i], yv = y[i], tv = t[i];
+    x0 = fmin(x0, xv);
+    x1 = fmax(x1, xv);
+    y0 = fmin(y0, yv);
+    y1 = fmax(y1, yv);
+    // EventSet checks (types.hpp:85-109): finite, t >= 0, nondecreasing
+    const double prev = i > 0 ? t[i - 1] : 0.0;
+    const bool ok = isfinite(xv) && isfinite(yv) && isfinite(tv) && tv >= prev;
+    if (!ok && i < first_bad) first_bad = i;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    first_bad = min(first_bad, static_cast<int64_t>(__shfl_xor_sync(0xffffffffu,
+                                                                    static_cast<long long>(first_bad), off)));
+  }
+  if (lane == 0 && first_bad != INT64_MAX) {
+    atomicMin(bad, static_cast<unsigned long long>(first_bad));
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -848,11 +870,11 @@ __global__ void tile_box_kernel(const double* __restrict__ x, const double* __re
 // spatial part (one multiply less per pair). Time is not scaled: the strict
 // t_j < t_i rule and the trigger's small dt need the raw times.
 __global__ void scale_xy_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                                int64_t n, double sx, double* __restrict__ xs,
+                                int64_t npad, double sx, double* __restrict__ xs,
                                 double* __restrict__ ys) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  xs[i] = x[i] * sx;
+  if (i >= npad) return;
+  xs[i] = x[i] * sx;  // (the pad tail of x, y is zero)
   ys[i] = y[i] * sx;
 }
 
@@ -1015,17 +1037,18 @@ __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict
 
 }  // namespace
 
-cudaError_t launch_tile_boxes(const double* x, const double* y, int64_t n, double4* box,
-                              cudaStream_t stream) {
+cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
+                              double4* box, unsigned long long* bad, cudaStream_t stream) {
   const int64_t ntiles = (n + kTS - 1) / kTS;
-  tile_box_kernel<<<static_cast<unsigned>((ntiles + 7) / 8), 256, 0, stream>>>(x, y, n, box);
+  tile_box_kernel<<<static_cast<unsigned>((ntiles + 7) / 8), 256, 0, stream>>>(x, y, t, n, npad,
+                                                                                box, bad);
   return cudaGetLastError();
 }
 
-cudaError_t launch_scale_xy(const double* x, const double* y, int64_t n, double sx, double* xs,
-                            double* ys, cudaStream_t stream) {
-  scale_xy_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(x, y, n, sx, xs,
-                                                                               ys);
+cudaError_t launch_scale_xy(const double* x, const double* y, int64_t npad, double sx,
+                            double* xs, double* ys, cudaStream_t stream) {
+  scale_xy_kernel<<<static_cast<unsigned>((npad + 255) / 256), 256, 0, stream>>>(x, y, npad, sx,
+                                                                                  xs, ys);
   return cudaGetLastError();
 }
 

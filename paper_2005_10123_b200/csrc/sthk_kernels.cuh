@@ -118,10 +118,13 @@ struct FinArgs {
 };
 
 // Launch wrappers (sthk_kernels.cu). All enqueue on `stream`.
-cudaError_t launch_tile_boxes(const double* x, const double* y, int64_t n, double4* box,
-                              cudaStream_t stream);
-cudaError_t launch_scale_xy(const double* x, const double* y, int64_t n, double sx, double* xs,
-                            double* ys, cudaStream_t stream);
+// Per-tile bounding boxes; also zeroes the pad tail [n, npad) of x, y, t and
+// runs the EventSet checks (finite, t >= 0, sorted): *bad = min(*bad, first
+// failing index) -- the caller initialises *bad to all ones.
+cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
+                              double4* box, unsigned long long* bad, cudaStream_t stream);
+cudaError_t launch_scale_xy(const double* x, const double* y, int64_t npad, double sx,
+                            double* xs, double* ys, cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_exp_probe(const double* x, int64_t n, double* out, cudaStream_t stream);
 cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaStream_t stream);

@@ -110,10 +110,10 @@ class Engine:
         n = t.size
         if x.size != n or y.size != n:
             raise ValueError("EventSet: coordinate/time length mismatch")
+        self._events_key = None  # (a failed load leaves the engine without events)
         self._check(self._lib.sthk_load_events(self._h, _dptr(x), _dptr(y), _dptr(t), n,
                                                float(window_end)), "sthk_load_events")
         self._n = n
-        self._events_key = None
 
     def load(self, events: EventSet) -> None:
         """Load an EventSet unless it is already resident (identity cache)."""

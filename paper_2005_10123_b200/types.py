@@ -54,14 +54,21 @@ class EventSet:
             raise ValueError("EventSet: need at least one event")
         if x.size != n or y.size != n:
             raise ValueError("EventSet: coordinate/time length mismatch")
-        bad = ~(np.isfinite(x) & np.isfinite(y) & np.isfinite(t))
-        if bad.any():
-            raise ValueError(f"EventSet: non-finite entry at index {int(np.argmax(bad))}")
-        if (t < 0).any():
-            raise ValueError(f"EventSet: negative time at index {int(np.argmax(t < 0))}")
-        dec = np.nonzero(t[1:] < t[:-1])[0]
-        if dec.size:
-            raise ValueError(f"EventSet: times not sorted at index {int(dec[0]) + 1}")
+        # the reference loop (types.hpp:90-104) stops at the first index with
+        # any failure and reports, at that index: non-finite, negative, unsorted
+        nonfinite = ~(np.isfinite(x) & np.isfinite(y) & np.isfinite(t))
+        with np.errstate(invalid="ignore"):
+            negative = t < 0
+            unsorted = np.zeros(n, dtype=bool)
+            unsorted[1:] = t[1:] < t[:-1]
+        fail = nonfinite | negative | unsorted
+        if fail.any():
+            i = int(np.argmax(fail))
+            if nonfinite[i]:
+                raise ValueError(f"EventSet: non-finite entry at index {i}")
+            if negative[i]:
+                raise ValueError(f"EventSet: negative time at index {i}")
+            raise ValueError(f"EventSet: times not sorted at index {i}")
         tmax = float(t[-1])
         we = tmax if windowEnd is None else float(windowEnd)
         if not math.isfinite(we) or we < tmax:

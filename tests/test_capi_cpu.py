@@ -63,3 +63,13 @@ def test_eventset_validation_messages():
         pk.EventSet([0, 1], [0, 1], [0.5, 1.0], 0.9)
     ev = pk.EventSet.sortedByTime([0, 1, 2], [0, 1, 2], [3.0, 1.0, 2.0])
     assert list(ev.ts()) == [1.0, 2.0, 3.0] and list(ev.xs()) == [1, 2, 0]
+
+
+def test_eventset_first_failure_in_reference_order():
+    # types.hpp:90-104 stops at the first index with any failure
+    with pytest.raises(ValueError, match="times not sorted at index 1"):
+        pk.EventSet([0, 1, 2], [0, 1, 2], [1.0, 0.5, float("nan")])
+    with pytest.raises(ValueError, match="non-finite entry at index 1"):
+        pk.EventSet([0, float("inf"), 2], [0, 1, 2], [1.0, 0.5, 0.2])
+    with pytest.raises(ValueError, match="negative time at index 1"):
+        pk.EventSet([0, 1], [0, 1], [1.0, -1.0])

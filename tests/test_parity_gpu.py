@@ -351,3 +351,26 @@ def test_grouped_batch_shares_sweeps_bitwise(engine):
         engine.set_background_cache(True)
     res = pk.logLikelihoodBatch(ev, [pk.Params(*p) for p in plist], engine=engine)
     assert [r.logLik for r in res] == list(llv)
+
+
+def test_engine_event_checks_match_reference_messages(engine):
+    """sthk_load_events runs the EventSet checks on the device (tile-box pass)
+    and reports the reference's message for the first failing index."""
+    cases = [
+        (([0, 1, 2], [0, 1, 2], [1.0, 0.5, np.nan], 5.0), "times not sorted at index 1"),
+        (([0, np.inf, 2], [0, 1, 2], [1.0, 0.5, 0.2], 5.0), "non-finite entry at index 1"),
+        (([0, 1], [0, 1], [1.0, -1.0], 5.0), "negative time at index 1"),
+        (([0, 1], [0, 1], [-1.0, 2.0], 5.0), "negative time at index 0"),
+        (([0, 1, 2], [0, 1, 2], [0.0, 1.0, 2.0], 1.5), "windowEnd precedes last event"),
+    ]
+    big_t = np.sort(np.random.default_rng(1).uniform(0, 100, 5000))
+    big_t[4321] = big_t[4320] - 1e-9
+    cases.append(((np.zeros(5000), np.zeros(5000), big_t, 200.0), "times not sorted at index 4321"))
+    for (x, y, t, we), msg in cases:
+        with pytest.raises(ValueError, match=msg):
+            engine.load_events(np.asarray(x, float), np.asarray(y, float), np.asarray(t, float), we)
+    # a failed load leaves the engine without events; a good load recovers
+    ev = pk.generateBenchmarkCloud(300, pk.SimWindow(0, 4, 0, 4, 60), 5)
+    engine.load(ev)
+    engine.set_params(pk.Params(0.6, 0.9, 3.0, 0.5, 1.1, 0.35))
+    assert engine.loglik()[1]
