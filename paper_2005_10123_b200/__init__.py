@@ -37,6 +37,16 @@ from .engine import (
     log_likelihood_gradient,
 )
 from .simulate import SimWindow, generateBenchmarkCloud, simulateClusterProcess
+from . import io
+from .io import (
+    EventFileSpec,
+    readEvents,
+    writeEvents,
+    deduplicate,
+    readChain,
+    writeChain,
+    loadRunConfig,
+)
 from .excitation import (
     ExcitationVector,
     PosteriorExcitation,
@@ -55,4 +65,6 @@ __all__ = [
     "SimWindow", "generateBenchmarkCloud", "simulateClusterProcess",
     "ExcitationVector", "PosteriorExcitation", "excitationProbabilities",
     "posteriorExcitation", "thinIndices",
+    "io", "EventFileSpec", "readEvents", "writeEvents", "deduplicate", "readChain",
+    "writeChain", "loadRunConfig",
 ]
