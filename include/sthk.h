@@ -126,6 +126,8 @@ typedef struct sthk_stats {
                                 background sums (trigger-only sweep) */
   int32_t trigger_cache_hit; /* 1 if it also reused the trigger sums (only mu0 /
                                 theta changed: no pair sweep at all) */
+  int64_t exec_far;          /* pairs evaluated in the FP32 far tier (every exponent
+                                provably < -40) */
 } sthk_stats;
 
 int sthk_set_timing(sthk_engine* e, int enable);
@@ -149,6 +151,11 @@ int sthk_set_dense(sthk_engine* e, int dense);
  * unchanged. Results are bitwise identical with the caches on or off (fixed
  * chunk grid, same kernels). Benchmarks of full evaluations turn them off. */
 int sthk_set_background_cache(sthk_engine* e, int enable);
+
+/* Far tier of the symmetric kernel (default on): stages whose every exponent
+ * is provably below -40 (terms < 4.3e-18 of the self term) run in FP32 on the
+ * MUFU/FP32 pipes; 0 = every pair in FP64 (testing / accuracy comparisons). */
+int sthk_set_far_tier(sthk_engine* e, int enable);
 
 #define STHK_KERNEL_ROWS 0
 #define STHK_KERNEL_SYM 1

@@ -79,6 +79,10 @@ struct Slot {
   size_t x_cap = 0, y_cap = 0, t_cap = 0;
   double *xs = nullptr, *ys = nullptr;  // kSym: x, y scaled by sqrt(-cxL) (per evaluation)
   size_t xs_cap = 0, ys_cap = 0;
+  float *xf = nullptr, *yf = nullptr, *tf = nullptr;  // kSym far tier: FP32 coordinates
+  size_t xf_cap = 0, yf_cap = 0, tf_cap = 0;
+  double4* h_box = nullptr;  // pinned: tile boxes (coordinate extents at load)
+  size_t h_box_cap = 0;
   double4* tile_box = nullptr;
   size_t box_cap = 0;
   int2* ranges = nullptr;
@@ -134,6 +138,9 @@ struct sthk_engine {
   bool loaded = false, has_params = false;
   bool timing = false, dense = false;
   int mode = sthk::kSym;   // pair-kernel variant (sthk_set_kernel)
+  bool far_tier = true;    // FP32 far tier of the symmetric kernel (sthk_set_far_tier)
+  double ext_x = 0, ext_y = 0;  // max |x - x[0]|, |y - y[0]| of the loaded set
+  double tile_tspan = 0;        // max time span of a 128-event tile
   // Background-sum cache: S_B (and S_Br, S_Bt) depend only on the events,
   // tauX, tauT -- fixed for a whole MH chain (sampler.cpp:48-49) -- so while
   // they are unchanged an evaluation sweeps only the trigger band. The
@@ -149,6 +156,7 @@ struct sthk_engine {
   double cache_tx = 0, cache_tt = 0;
   int cache_mode = -1;
   bool cache_dense = false;
+  bool cache_far = true;
   int virtual_shards = 1;  // testing: partition rows over k shards on one device
   std::string err;
   bool pending = false, last_grad = false, last_pe = false, last_ex = false;
@@ -158,6 +166,14 @@ struct sthk_engine {
 namespace {
 
 constexpr int kChunksTarget = 48;  // source chunks across N (work-item granularity)
+// Far tier: a stage runs in FP32 when every exponent on its bounding boxes is
+// below -kFarExponent (terms < 4.3e-18), and only if the FP32 coordinates
+// (space relative to event 0, time relative to each 128-event tile's first
+// event, in kernel units) stay within kFarCoordMax: a coordinate rounding of
+// <= 2.4e-4 units perturbs an exponent near the threshold by < 0.01 (log2),
+// i.e. < 1% of a term below 4.3e-18.
+constexpr double kFarExponent = 40.0;
+constexpr double kFarCoordMax = 4096.0;
 
 void set_dev(const Slot& s) { ck(cudaSetDevice(s.dev), "cudaSetDevice"); }
 
@@ -188,6 +204,7 @@ void free_slot(Slot& s) {
   if (s.comm) ncclCommDestroy(s.comm);
   for (void* p : {static_cast<void*>(s.x), static_cast<void*>(s.y), static_cast<void*>(s.t),
                   static_cast<void*>(s.xs), static_cast<void*>(s.ys),
+                  static_cast<void*>(s.xf), static_cast<void*>(s.yf), static_cast<void*>(s.tf),
                   static_cast<void*>(s.ranges), static_cast<void*>(s.counts),
                   static_cast<void*>(s.items), static_cast<void*>(s.scalars),
                   static_cast<void*>(s.fx), static_cast<void*>(s.block_partial),
@@ -198,7 +215,7 @@ void free_slot(Slot& s) {
     if (p) cudaFree(p);
   }
   for (void* p : {static_cast<void*>(s.h_out), static_cast<void*>(s.h_counts),
-                  static_cast<void*>(s.h_bad),
+                  static_cast<void*>(s.h_bad), static_cast<void*>(s.h_box),
                   static_cast<void*>(s.h_per_event), static_cast<void*>(s.h_ex)}) {
     if (p) cudaFreeHost(p);
   }
@@ -247,6 +264,7 @@ void validate_window_end(const double* t, int64_t n, double window_end) {
 struct EvalPlan {
   sthk::PairConsts k;
   double sx = 1.0;  // kSym coordinate scale sqrt(-cxL)
+  double sxf = 1.0, stf = 1.0;  // far-tier FP32 coordinate scales
   int sc = 0;
   int nchunks = 0;
   std::vector<int> cuts;  // shard row boundaries (size shards+1)
@@ -295,6 +313,17 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   // symmetric kernel: coordinates scaled by sx so that r2 = sx^2 r^2 ~ -cxL r^2
   pl.sx = std::sqrt(-pl.k.cxL);
   pl.k.chS = pl.k.chL / (pl.sx * pl.sx);
+  // far tier (FP32, log2 units): xf = (x - x0) sxf, tf = (t - t0) stf
+  const double kLn2 = 0.693147180559945309417232121458176568;
+  pl.sxf = 1.0 / (p[1] * std::sqrt(2.0 * kLn2));
+  pl.stf = 1.0 / (p[2] * std::sqrt(2.0 * kLn2));
+  pl.k.farL = -kFarExponent * static_cast<double>(L);
+  pl.k.fc1 = static_cast<float>(-p[4] / (pl.stf * kLn2));
+  pl.k.fc2 = static_cast<float>(-(p[1] * p[1]) / (p[5] * p[5]));
+  pl.k.fkr = pl.sx * pl.sx * 2.0 * p[1] * p[1] * kLn2;
+  pl.k.fkt1 = 1.0 / pl.stf;
+  pl.k.fkt2 = 1.0 / (pl.stf * pl.stf);
+  pl.k.fstf = pl.stf;
   pl.k.nomL = static_cast<double>(-L * p[4]);
   const double inf = std::numeric_limits<double>::infinity();
   pl.k.dB = e.dense ? inf : dB;
@@ -369,12 +398,14 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
   const EvalPlan pl = make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym}, shards);
   e.last_sc = pl.sc;
   const bool cached = e.bg_cache && e.cache_valid && e.cache_gen == e.load_gen &&
-                      e.cache_tx == e.p[1] && e.cache_tt == e.p[2] && e.cache_mode == e.mode &&
+                      e.cache_tx == e.p[1] && e.cache_tt == e.p[2] && e.cache_mode == e.mode && e.cache_far == e.far_tier &&
                       e.cache_dense == e.dense && (e.cache_grad || !grad);
   const bool tr_cached = cached && e.tr_cache_valid && e.tr_cache_omega == e.p[4] &&
                          e.tr_cache_h == e.p[5] && e.tr_cache_grad == grad;  // (tpart layout)
   e.last_cache_hit = cached;
   e.last_tr_cache_hit = tr_cached;
+  const bool far_on = sym && e.far_tier && e.ext_x * pl.sxf <= kFarCoordMax &&
+                      e.ext_y * pl.sxf <= kFarCoordMax && e.tile_tspan * pl.stf <= kFarCoordMax;
   e.cache_valid = false;  // re-armed below once the sweep is enqueued
   e.tr_cache_valid = false;
   const int64_t ntiles_total = (e.n + kTM - 1) / kTM;
@@ -430,8 +461,10 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
         ck(cudaMemsetAsync(s.fx, 0, sizeof(unsigned long long) * kFxRows * e.npad, st),
            "memset");
       }
-      if (sym && !cached) {  // (a cached sweep has the same tauX: scaled copies still valid)
-        ck(sthk::launch_scale_xy(s.x, s.y, e.npad, pl.sx, s.xs, s.ys, st), "scale xy");
+      if (sym && !cached) {  // (a cached sweep has the same tauX, tauT: copies still valid)
+        ck(sthk::launch_scale_xy(s.x, s.y, s.t, e.npad, pl.sx, s.xs, s.ys, pl.sxf, pl.stf,
+                                 far_on ? s.xf : nullptr, s.yf, s.tf, st),
+           "scale xy");
       }
       if (shards > 1) {
         ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
@@ -477,6 +510,10 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     qa.t = s.t;
     qa.xs = s.xs;
     qa.ys = s.ys;
+    qa.xf = s.xf;
+    qa.yf = s.yf;
+    qa.tf = s.tf;
+    qa.far_on = far_on ? 1 : 0;
     qa.tile_box = s.tile_box;
     qa.n = e.n;
     qa.npad = e.npad;
@@ -611,6 +648,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     e.cache_tt = e.p[2];
     e.cache_mode = e.mode;
     e.cache_dense = e.dense;
+    e.cache_far = e.far_tier;
   }
   e.cache_valid = true;
   if (!tr_cached) {
@@ -811,6 +849,9 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       dev_grow(s.t, s.t_cap, static_cast<size_t>(npad));
       dev_grow(s.xs, s.xs_cap, static_cast<size_t>(npad));
       dev_grow(s.ys, s.ys_cap, static_cast<size_t>(npad));
+      dev_grow(s.xf, s.xf_cap, static_cast<size_t>(npad));
+      dev_grow(s.yf, s.yf_cap, static_cast<size_t>(npad));
+      dev_grow(s.tf, s.tf_cap, static_cast<size_t>(npad));
       ck(cudaMemcpyAsync(s.x, x, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
       ck(cudaMemcpyAsync(s.y, y, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
       ck(cudaMemcpyAsync(s.t, t, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
@@ -822,6 +863,17 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       ck(cudaMemcpyAsync(s.h_bad, bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                          s.stream),
          "D2H");
+      if (&s == &e->slots[0]) {  // coordinate extents for the far-tier guard
+        const size_t nt = static_cast<size_t>(npad / kTS);
+        if (s.h_box_cap < nt) {
+          if (s.h_box) ck(cudaFreeHost(s.h_box), "cudaFreeHost");
+          ck(cudaMallocHost(&s.h_box, sizeof(double4) * nt), "cudaMallocHost");
+          s.h_box_cap = nt;
+        }
+        ck(cudaMemcpyAsync(s.h_box, s.tile_box, sizeof(double4) * nt, cudaMemcpyDeviceToHost,
+                           s.stream),
+           "D2H");
+      }
     }
     for (Slot& s : e->slots) {
       set_dev(s);
@@ -830,6 +882,23 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
     const unsigned long long first_bad = *e->slots[0].h_bad;
     if (first_bad != ~0ULL) throw_event_error(x, y, t, static_cast<int64_t>(first_bad));
     validate_window_end(t, n, window_end);
+    {
+      const Slot& s0 = e->slots[0];
+      const int64_t nt = (n + kTS - 1) / kTS;
+      double ex = 0, ey = 0;
+      for (int64_t k = 0; k < nt; ++k) {
+        const double4 b = s0.h_box[k];
+        ex = std::max({ex, std::fabs(b.x - x[0]), std::fabs(b.y - x[0])});
+        ey = std::max({ey, std::fabs(b.z - y[0]), std::fabs(b.w - y[0])});
+      }
+      e->ext_x = ex;
+      e->ext_y = ey;
+      double span = 0;
+      for (int64_t k = 0; k < nt; ++k) {
+        span = std::max(span, t[std::min(k * kTS + kTS, n) - 1] - t[k * kTS]);
+      }
+      e->tile_tspan = span;
+    }
     e->n = n;
     e->npad = npad;
     e->window_end = window_end;
@@ -979,6 +1048,10 @@ int sthk_set_background_cache(sthk_engine* e, int enable) {
   });
 }
 
+int sthk_set_far_tier(sthk_engine* e, int enable) {
+  return guarded(e, [&] { e->far_tier = enable != 0; });
+}
+
 int sthk_set_kernel(sthk_engine* e, int mode) {
   return guarded(e, [&] {
     if (mode != sthk::kRows && mode != sthk::kSym) {
@@ -1027,6 +1100,7 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
       out->exec_bg += static_cast<int64_t>(s.h_counts[3]);
       out->exec_geom += static_cast<int64_t>(s.h_counts[4]);
       out->exec_sym += static_cast<int64_t>(s.h_counts[5]);
+      out->exec_far += static_cast<int64_t>(s.h_counts[6]);
       if (e->timing && s.row1 > s.row0) {
         float a = 0, b = 0;
         set_dev(s);

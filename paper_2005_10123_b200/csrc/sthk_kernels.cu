@@ -578,6 +578,147 @@ __device__ __forceinline__ void sym_block(const double* __restrict__ sx,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Far tier (FP32): stages whose every pair has a background (and, if live,
+// trigger) exponent below -A (A = 40, e < 4.3e-18) on the tile/stage bounding
+// boxes. Their terms are below 2^-57 of the self term that every S_B holds,
+// so they are evaluated in FP32 (ex2.approx on the MUFU pipe, FP32 FMA pipe)
+// instead of FP64; the FP64 pipe keeps every term that can reach the sums'
+// precision. Relative error of a far term <= ~4% (FP32 coordinates, guarded
+// on the host), i.e. <= 2e-19 absolute per pair: far below the 1e-10 / 1e-8
+// tolerances. Coordinates: xf = (x - x0) sxf, tf = (t - t0) stf
+// with sxf = 1/(tauX sqrt(2 ln2)), stf = 1/(tauT sqrt(2 ln2)), so the
+// background exponent in log2 units is -(dxf^2 + dyf^2 + dtf^2).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float ex2f(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+template <bool GRAD, bool BG, bool TR>
+__device__ __forceinline__ void far_pairs(int g, int perm, const float* __restrict__ sx,
+                                          const float* __restrict__ sy,
+                                          const float* __restrict__ st, int col0,
+                                          const float (&xi)[kSymR], const float (&yi)[kSymR],
+                                          const float (&ti)[kSymR], float c1, float c2,
+                                          float (&rf)[kSymR][GRAD ? kNSumGrad : kNSumVal],
+                                          float (&cp)[kSymG][GRAD ? 3 : 1]) {
+  constexpr int T0 = GRAD ? 3 : 1;
+#pragma unroll
+  for (int q = 0; q < kSymG; ++q) {
+    const int j = col0 + kSymG * g + (q ^ perm);
+    const float xj = sx[j], yj = sy[j], tj = st[j];
+    float dt[kSymR], r2[kSymR], dt2[kSymR], e[kSymR];
+#pragma unroll
+    for (int r = 0; r < kSymR; ++r) {
+      const float dx = xi[r] - xj;
+      const float dy = yi[r] - yj;
+      dt[r] = ti[r] - tj;
+      r2[r] = fmaf(dx, dx, dy * dy);
+    }
+    if constexpr (BG) {
+#pragma unroll
+      for (int r = 0; r < kSymR; ++r) {
+        dt2[r] = dt[r] * dt[r];
+        e[r] = ex2f(-(r2[r] + dt2[r]));
+        rf[r][0] += e[r];
+        if constexpr (GRAD) {
+          rf[r][1] = fmaf(e[r], r2[r], rf[r][1]);
+          rf[r][2] = fmaf(e[r], dt2[r], rf[r][2]);
+        }
+      }
+      cp[q][0] = (e[0] + e[1]) + (e[2] + e[3]);
+      if constexpr (GRAD) {
+        cp[q][1] = fmaf(e[3], r2[3], fmaf(e[2], r2[2], fmaf(e[1], r2[1], e[0] * r2[0])));
+        cp[q][2] = fmaf(e[3], dt2[3], fmaf(e[2], dt2[2], fmaf(e[1], dt2[1], e[0] * dt2[0])));
+      }
+    }
+    if constexpr (TR) {  // unmasked: every source strictly earlier than every row
+#pragma unroll
+      for (int r = 0; r < kSymR; ++r) {
+        const float et = ex2f(fmaf(c1, dt[r], c2 * r2[r]));
+        rf[r][T0] += et;
+        if constexpr (GRAD) {
+          rf[r][4] = fmaf(et, dt[r], rf[r][4]);
+          rf[r][5] = fmaf(et, r2[r], rf[r][5]);
+        }
+      }
+    }
+  }
+}
+
+// One far stage for one warp: 32 columns x 4 rows in FP32, column partials
+// reduce-scattered with FP32 shuffles (lane-permuted order as in sym_reduce),
+// column totals stored to s_col in the FP64 path's units, row partials merged
+// into the FP64 row sums at the end.
+template <bool GRAD, bool BG, bool TR>
+__device__ __forceinline__ void far_block(const float* __restrict__ sx, const float* __restrict__ sy,
+                                          const float* __restrict__ st, int col0,
+                                          const float (&xi)[kSymR], const float (&yi)[kSymR],
+                                          const float (&ti)[kSymR], const PairConsts& k,
+                                          double (&racc)[kSymR][GRAD ? kNSumGrad : kNSumVal],
+                                          double* __restrict__ s_col) {
+  constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
+  constexpr int NSC = GRAD ? 3 : 1;
+  constexpr int T0 = GRAD ? 3 : 1;
+  const int lane = threadIdx.x & 31;
+  const int perm = (((lane >> 4) & 1) << 1) | ((lane >> 3) & 1);
+  static_assert(kSymG == 4, "far tier assumes 4-column groups");
+  float rf[kSymR][NS];
+#pragma unroll
+  for (int r = 0; r < kSymR; ++r) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) rf[r][q] = 0.0f;
+  }
+  const double cscale[3] = {1.0, k.fkr, k.fkt2};
+#pragma unroll 1
+  for (int g = 0; g < 32 / kSymG; ++g) {
+    float cp[kSymG][NSC];
+    far_pairs<GRAD, BG, TR>(g, perm, sx, sy, st, col0, xi, yi, ti, k.fc1, k.fc2, rf, cp);
+    if constexpr (BG) {
+      float v2[2][NSC], v1[NSC];
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+#pragma unroll
+        for (int c = 0; c < NSC; ++c) {
+          v2[qq][c] = cp[qq][c] + __shfl_xor_sync(0xffffffffu, cp[2 + qq][c], 16);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NSC; ++c) v1[c] = v2[0][c] + __shfl_xor_sync(0xffffffffu, v2[1][c], 8);
+#pragma unroll
+      for (int off = 4; off > 0; off >>= 1) {
+#pragma unroll
+        for (int c = 0; c < NSC; ++c) v1[c] += __shfl_xor_sync(0xffffffffu, v1[c], off);
+      }
+      if ((lane & 7) == 0) {
+#pragma unroll
+        for (int c = 0; c < NSC; ++c) {
+          s_col[(col0 + kSymG * g + perm) * NSC + c] = static_cast<double>(v1[c]) * cscale[c];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kSymR; ++r) {
+    if constexpr (BG) {
+      racc[r][0] += static_cast<double>(rf[r][0]);
+      if constexpr (GRAD) {
+        racc[r][1] = fma(static_cast<double>(rf[r][1]), k.fkr, racc[r][1]);
+        racc[r][2] = fma(static_cast<double>(rf[r][2]), k.fkt2, racc[r][2]);
+      }
+    }
+    if constexpr (TR) {
+      racc[r][T0] += static_cast<double>(rf[r][T0]);
+      if constexpr (GRAD) {
+        racc[r][4] = fma(static_cast<double>(rf[r][4]), k.fkt1, racc[r][4]);
+        racc[r][5] = fma(static_cast<double>(rf[r][5]), k.fkr, racc[r][5]);
+      }
+    }
+  }
+}
+
 template <bool GRAD, bool SYM, bool CHECK, bool VALID>
 __device__ __forceinline__ void sym_dispatch(bool bg, int tr, const double* sx, const double* sy,
                                              const double* st, int col0, int cnt,
@@ -607,6 +748,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   constexpr int NSC = GRAD ? 3 : 1;
   __shared__ __align__(128) double s_src[2][3][kTS];
+  __shared__ __align__(128) float s_srcf[2][3][kTS];  // far tier: FP32 copies of the stage
   extern __shared__ __align__(128) uint2 s_tab[];  // kExpTableSize entries (dynamic)
   __shared__ double s_col[kTS * NSC];
   __shared__ double s_red[4][NS][kTM];
@@ -635,7 +777,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
   uint32_t phase = 0;
   // ordered pairs covered (bg, trigger, any) and work executed (background
   // exps, pair geometries, symmetric pairs with a column accumulation)
-  unsigned long long cBg = 0, cTr = 0, cAny = 0, xBg = 0, xGeo = 0, xSym = 0;
+  unsigned long long cBg = 0, cTr = 0, cAny = 0, xBg = 0, xGeo = 0, xSym = 0, xFar = 0;
 
   for (int iter = 0;; ++iter) {
     if (tid == 0) s_item[iter & 1] = atomicAdd(a.work_counter, 1);
@@ -652,6 +794,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
     const double tmin = a.t[first], tmax = a.t[last];
     const double4 bt = a.tile_box[tile];
     double xi[kSymR], yi[kSymR], ti[kSymR];
+    float xfi[kSymR], yfi[kSymR], tfi[kSymR];
     bool rv[kSymR];
 #pragma unroll
     for (int r = 0; r < kSymR; ++r) {
@@ -660,6 +803,11 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       yi[r] = a.ys[row];
       ti[r] = a.t[row];
       rv[r] = row < n;
+      if (a.far_on) {
+        xfi[r] = a.xf[row];
+        yfi[r] = a.yf[row];
+        tfi[r] = a.tf[row];
+      }
     }
     // Background row sums live in registers for the whole item; the trigger
     // row sums (rarely active) are parked in this thread's s_red slots
@@ -681,9 +829,15 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
     const int nst = (s_end - s_begin + kTS - 1) / kTS;
 
     constexpr uint32_t kStageBytes = kTS * sizeof(double);
+    constexpr uint32_t kStageBytesF = kTS * sizeof(float);
     if (tid == 0 && nst > 0) {
-      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes + kBoxBytes);
+      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes + kBoxBytes + (a.far_on ? 3 * kStageBytesF : 0));
       tma_load_1d(&s_box[0], a.tile_box + s_begin / kTS, kBoxBytes, &s_bar[0]);
+      if (a.far_on) {
+        tma_load_1d(s_srcf[0][0], a.xf + s_begin, kStageBytesF, &s_bar[0]);
+        tma_load_1d(s_srcf[0][1], a.yf + s_begin, kStageBytesF, &s_bar[0]);
+        tma_load_1d(s_srcf[0][2], a.tf + s_begin, kStageBytesF, &s_bar[0]);
+      }
       tma_load_1d(s_src[0][0], a.xs + s_begin, kStageBytes, &s_bar[0]);
       tma_load_1d(s_src[0][1], a.ys + s_begin, kStageBytes, &s_bar[0]);
       tma_load_1d(s_src[0][2], a.t + s_begin, kStageBytes, &s_bar[0]);
@@ -695,8 +849,13 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       if (tid == 0 && s + 1 < nst) {
         const int nb = buf ^ 1;
         const int64_t s0n = s_begin + static_cast<int64_t>(s + 1) * kTS;
-        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes + kBoxBytes);
+        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes + kBoxBytes + (a.far_on ? 3 * kStageBytesF : 0));
         tma_load_1d(&s_box[nb], a.tile_box + s0n / kTS, kBoxBytes, &s_bar[nb]);
+        if (a.far_on) {
+          tma_load_1d(s_srcf[nb][0], a.xf + s0n, kStageBytesF, &s_bar[nb]);
+          tma_load_1d(s_srcf[nb][1], a.yf + s0n, kStageBytesF, &s_bar[nb]);
+          tma_load_1d(s_srcf[nb][2], a.tf + s0n, kStageBytesF, &s_bar[nb]);
+        }
         tma_load_1d(s_src[nb][0], a.xs + s0n, kStageBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][1], a.ys + s0n, kStageBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][2], a.t + s0n, kStageBytes, &s_bar[nb]);
@@ -721,7 +880,17 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       const double dtm = fmax(tmax - smin, smax - tmin);
       const bool safe = (!bg || a.k.cxL * r2m + a.k.ctL * (dtm * dtm) > kSafeExpL) &&
                         (!tr || a.k.nomL * dtm + a.k.chL * r2m > kSafeExpL);
-
+      // far tier: exponent UPPER bounds over the box pair (minimum distance
+      // and time gap) below farL for every live term
+      bool far = false;
+      if (a.far_on && !diag && rows_real == kTM && cnt == kTS && tr != 2 && (bg || tr)) {
+        const double gx = fmax(0.0, fmax(bs.x - bt.y, bt.x - bs.y));
+        const double gy = fmax(0.0, fmax(bs.z - bt.w, bt.z - bs.w));
+        const double r2g = gx * gx + gy * gy;
+        const double dtg = fmax(0.0, fmax(smin - tmax, tmin - smax));
+        far = (!bg || a.k.cxL * r2g + a.k.ctL * (dtg * dtg) < a.k.farL) &&
+              (!tr || a.k.nomL * dtg + a.k.chL * r2g < a.k.farL);
+      }
 
       const double* sx = s_src[buf][0];
       const double* sy = s_src[buf][1];
@@ -734,7 +903,20 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
           for (int q = NB; q < NS; ++q) racc[r][q] = s_red[warp][q][lane + 32 * r];
         }
       }
-      if (diag) {
+      if (far) {
+        const float* fx = s_srcf[buf][0];
+        const float* fy = s_srcf[buf][1];
+        const float* ft = s_srcf[buf][2];
+        // row times re-based onto the source tile's origin: one FP32 offset
+        // per stage (the tile-to-tile time gap, rounded once)
+        const float dtile = static_cast<float>((tmin - smin) * a.k.fstf);
+        float tfr[kSymR];
+#pragma unroll
+        for (int r = 0; r < kSymR; ++r) tfr[r] = tfi[r] + dtile;
+        if (bg && tr) far_block<GRAD, true, true>(fx, fy, ft, col0, xfi, yfi, tfr, a.k, racc, s_col);
+        else if (bg) far_block<GRAD, true, false>(fx, fy, ft, col0, xfi, yfi, tfr, a.k, racc, s_col);
+        else far_block<GRAD, false, true>(fx, fy, ft, col0, xfi, yfi, tfr, a.k, racc, s_col);
+      } else if (diag) {
         sym_dispatch<GRAD, false, true, true>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
                                               a.k, s_tab, racc, s_col);
       } else if (rows_real < kTM) {
@@ -767,6 +949,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       }
       if (tid == 0) {
         const unsigned long long pr = static_cast<unsigned long long>(cnt) * rows_real;
+        if (far) xFar += pr;
         if (diag) {
           if (bg) cBg += pr;
           if (tr) cTr += pr;
@@ -813,6 +996,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
     atomicAdd(&a.pair_counts[3], xBg);
     atomicAdd(&a.pair_counts[4], xGeo);
     atomicAdd(&a.pair_counts[5], xSym);
+    atomicAdd(&a.pair_counts[6], xFar);
   }
 }
 
@@ -870,12 +1054,22 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
 // spatial part (one multiply less per pair). Time is not scaled: the strict
 // t_j < t_i rule and the trigger's small dt need the raw times.
 __global__ void scale_xy_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                                int64_t npad, double sx, double* __restrict__ xs,
-                                double* __restrict__ ys) {
+                                const double* __restrict__ t, int64_t npad, double sx,
+                                double* __restrict__ xs, double* __restrict__ ys, double sxf,
+                                double stf, float* __restrict__ xf, float* __restrict__ yf,
+                                float* __restrict__ tf) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= npad) return;
-  xs[i] = x[i] * sx;  // (the pad tail of x, y is zero)
-  ys[i] = y[i] * sx;
+  const double xv = x[i], yv = y[i];  // (the pad tail of x, y, t is zero)
+  xs[i] = xv * sx;
+  ys[i] = yv * sx;
+  if (xf) {
+    // space relative to event 0; time relative to the first event of the
+    // event's own 128-tile (the kernel adds the tile-to-tile offset per stage)
+    xf[i] = static_cast<float>((xv - x[0]) * sxf);
+    yf[i] = static_cast<float>((yv - y[0]) * sxf);
+    tf[i] = static_cast<float>((t[i] - t[i - i % kTS]) * stf);
+  }
 }
 
 // exp_l on a vector of natural-unit exponents (accuracy tests; the argument
@@ -1045,10 +1239,11 @@ cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_
   return cudaGetLastError();
 }
 
-cudaError_t launch_scale_xy(const double* x, const double* y, int64_t npad, double sx,
-                            double* xs, double* ys, cudaStream_t stream) {
-  scale_xy_kernel<<<static_cast<unsigned>((npad + 255) / 256), 256, 0, stream>>>(x, y, npad, sx,
-                                                                                  xs, ys);
+cudaError_t launch_scale_xy(const double* x, const double* y, const double* t, int64_t npad,
+                            double sx, double* xs, double* ys, double sxf, double stf,
+                            float* xf, float* yf, float* tf, cudaStream_t stream) {
+  scale_xy_kernel<<<static_cast<unsigned>((npad + 255) / 256), 256, 0, stream>>>(
+      x, y, t, npad, sx, xs, ys, sxf, stf, xf, yf, tf);
   return cudaGetLastError();
 }
 

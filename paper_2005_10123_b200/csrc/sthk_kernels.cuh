@@ -18,7 +18,7 @@ constexpr int kNSumVal = 2;   // S_B, S_T
 constexpr int kNOut = 8;      // loglik, 6 gradient terms, degenerate-row count
 // pair counters: ordered pairs covered (bg, trigger, any), then work executed
 // (background exps, pair geometries, symmetric column accumulations)
-constexpr int kNCounts = 6;
+constexpr int kNCounts = 7;  // [6]: pairs evaluated in the FP32 far tier
 
 // Exponent cut (natural units) used for exact culling: every pair whose
 // time-only exponent bound is below -kCullExponent has exp_l(...) == +0
@@ -45,6 +45,15 @@ struct PairConsts {
   double nomL;  // -L omega
   double dB;    // background live iff |dt| <= dB   (inf when dense)
   double dT;    // trigger live iff 0 < dt <= dT    (inf when dense)
+  // far tier (kSym, FP32): a stage is far when every exponent on its box
+  // bounds is below farL (L units); FP32 coordinates xf, yf, tf (log2 units)
+  double farL;  // -A * kExpL, A = 40; +inf... disables (0 when off)
+  float fc1;    // trigger exponent, log2 units: fc1 * dtf + fc2 * r2f
+  float fc2;
+  double fkr;   // r2f -> r2 (kSym units, -cxL r^2)
+  double fkt1;  // dtf -> dt (days)
+  double fkt2;  // dtf^2 -> dt^2
+  double fstf;  // time scale of tf (tf = (t - t_tile0) * fstf)
 };
 
 struct PlanArgs {
@@ -74,6 +83,10 @@ struct PairArgs {
   const double* t;
   const double* xs;         // kSym: x, y pre-scaled by sx = sqrt(-cxL) (r2 = -cxL r^2)
   const double* ys;
+  const float* xf;          // kSym far tier: FP32 (x - x0) sxf, (y - y0) sxf, (t - t_tile0) stf
+  const float* yf;
+  const float* tf;
+  int far_on;               // far tier enabled for this evaluation
   const double4* tile_box;  // per 128-event tile: xmin, xmax, ymin, ymax
   int64_t n;
   int64_t npad;
@@ -123,8 +136,11 @@ struct FinArgs {
 // failing index) -- the caller initialises *bad to all ones.
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
                               double4* box, unsigned long long* bad, cudaStream_t stream);
-cudaError_t launch_scale_xy(const double* x, const double* y, int64_t npad, double sx,
-                            double* xs, double* ys, cudaStream_t stream);
+// kSym coordinates: xs, ys = (x, y) * sx; if xf: the far tier's FP32 copies
+// xf, yf = (x - x[0], y - y[0]) * sxf, tf = (t - t[tile start]) * stf.
+cudaError_t launch_scale_xy(const double* x, const double* y, const double* t, int64_t npad,
+                            double sx, double* xs, double* ys, double sxf, double stf,
+                            float* xf, float* yf, float* tf, cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_exp_probe(const double* x, int64_t n, double* out, cudaStream_t stream);
 cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaStream_t stream);

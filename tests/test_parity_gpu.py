@@ -374,3 +374,50 @@ def test_engine_event_checks_match_reference_messages(engine):
     engine.load(ev)
     engine.set_params(pk.Params(0.6, 0.9, 3.0, 0.5, 1.1, 0.35))
     assert engine.loglik()[1]
+
+
+def test_far_tier_matches_all_fp64(engine):
+    """The FP32 far tier (stages whose every exponent is provably < -40) changes
+    nothing the FP64 sums can see: far on vs far off (every pair in FP64) agree to
+    1e-13 on loglik and 1e-11 (scale-aware) on the gradient, at the C2 posterior and
+    at the sampler's initial point (ω = 1: far causal trigger stages), value and grad."""
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=30000)
+    engine.load(ev)
+    for theta in ([0.66, 1.6, 14, 0.344, 1440, 0.0695], [1, 1.6, 14, 0.1, 1, 1],
+                  [0.5, 0.7, 3.0, 0.3, 20.0, 0.3]):
+        engine.set_params(theta)
+        out = {}
+        for far in (1, 0):
+            engine.set_far_tier(bool(far))
+            engine.set_timing(True)
+            out[far] = (engine.loglik_grad(), engine.stats()["exec_far"], engine.loglik()[0])
+            engine.set_timing(False)
+        engine.set_far_tier(True)
+        (a, nfar, va), (b, nfar0, vb) = out[1], out[0]
+        assert nfar > 0 and nfar0 == 0, (theta, nfar)
+        assert abs(a[0] - b[0]) <= 1e-13 * abs(b[0]) and abs(va - vb) <= 1e-13 * abs(vb)
+        o = og.oracle_loglik_grad(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), np.array(theta))
+        assert np.all(np.abs(a[2] - b[2]) <= 1e-11 * o["grad_abs"]), (a[2], b[2])
+
+
+def test_far_tier_guard_off_for_extreme_coordinates(engine):
+    """FP32 coordinates must stay small in kernel units: a spatial extent of
+    ~1e4 tauX turns the far tier off (every pair FP64); a time span of ~500 tauT
+    keeps it on (times are tile-relative, only the 128-event tile span counts);
+    results match the oracle either way."""
+    rng = np.random.default_rng(4)
+    n = 12000
+    for xs, tspan, want_far in ((5.0, 1800.0, True), (3e4, 1800.0, False)):
+        t = np.sort(rng.uniform(0, tspan, n))
+        ev = pk.EventSet(rng.uniform(0, xs, n), rng.uniform(0, 5, n), t)
+        p = pk.Params(0.6, 0.9, 3.0, 0.3, 2.0, 0.3)
+        engine.load(ev)
+        engine.set_params(p)
+        engine.set_timing(True)
+        r = engine.loglik_grad()
+        assert (engine.stats()["exec_far"] > 0) == want_far
+        engine.set_timing(False)
+        o = og.oracle_loglik_grad(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), p.as_array())
+        assert abs(r[0] - o["loglik"]) <= 1e-10 * abs(o["loglik"])

@@ -15,6 +15,7 @@ e = pk.Engine((0,))
 e.load(ev)
 e.set_timing(True)
 e.set_background_cache(bool(int(os.environ.get("QP_CACHE", "0"))))
+e._lib.sthk_set_far_tier(e._h, int(os.environ.get("QP_FAR", "1")))
 modes = [int(m) for m in os.environ.get("QP_MODES", "0,1").split(",")]
 denses = [bool(int(d)) for d in os.environ.get("QP_DENSE", "0,1").split(",")]
 for name, p in [("post", [0.66, 1.6, 14, 0.344, 1440, 0.0695]), ("init", [1, 1.6, 14, 0.1, 1, 1])]:
@@ -36,5 +37,5 @@ for name, p in [("post", [0.66, 1.6, 14, 0.344, 1440, 0.0695]), ("init", [1, 1.6
                 print(f"{name} mode={mode} dense={int(dense)} grad={int(grad)} ll={r[0]:.12f} "
                       f"wall_ms={1e3*np.median(ts):.3f} pair_ms={st['pair_kernel_ms']:.3f} "
                       f"eval_ms={st['eval_ms']:.3f} sc={st['source_chunk']} bg={st['pairs_bg']:.3e} "
-                      f"tr={st['pairs_tr']:.3e} xbg={st['exec_bg']:.3e} xsym={st['exec_sym']:.3e}"
+                      f"tr={st['pairs_tr']:.3e} xbg={st['exec_bg']:.3e} xsym={st['exec_sym']:.3e} xfar={st['exec_far']:.3e}"
                       + (f" g0={g[0]:.12e} g5={g[5]:.12e}" if grad else ""), flush=True)
