@@ -410,6 +410,13 @@ def main():
             "flops_per_launch": flops_launch,
             "flop_model": "executed: 6*geometries + 38*bg_exps + 38*trigger_pairs + 6*symmetric "
                           "column pairs (SURVEY.md §8 d3 per-pair model, exp counted as 29)",
+            "note": "SURVEY d3 counts every evaluated pair as FP64 work with a 29-flop exp; the "
+                    "kernel's exp is 7 FP64 ops and far_tier_share of its pairs (every exponent "
+                    "provably < -40, terms < 4.3e-18) run on the FP32/MUFU pipes, so frac can "
+                    "exceed 1; the pipe-level evidence is the ncu FP64-pipe / issue utilisation "
+                    "in profiles/",
+            "far_tier_pairs": st["exec_far"],
+            "far_tier_share": st["exec_far"] / st["exec_geom"] if st["exec_geom"] else 0.0,
             "achieved_ordered_pair_equivalent": achieved_ord,
             "frac_ordered_pair_equivalent": achieved_ord / peak_best if peak_best else None,
             "flops_ordered_pair_equivalent": flops_ordered,

@@ -596,52 +596,101 @@ __device__ __forceinline__ float ex2f(float x) {
   return r;
 }
 
+// Packed FP32x2 arithmetic (sm_100 FADD2 / FMUL2 / FFMA2): rows (0,1) and
+// (2,3) share each instruction, halving the far tier's issue slots.
+struct f2 {
+  uint64_t v;
+};
+
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo2(f2 a) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+  return lo;
+}
+__device__ __forceinline__ float hi2(f2 a) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+  return hi;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return d;
+}
+__device__ __forceinline__ f2 ex2x2(f2 a) { return pk2(ex2f(lo2(a)), ex2f(hi2(a))); }
+
+// rows are held as two packed pairs: P = 0 -> rows (0, 1), P = 1 -> rows (2, 3)
 template <bool GRAD, bool BG, bool TR>
 __device__ __forceinline__ void far_pairs(int g, int perm, const float* __restrict__ sx,
                                           const float* __restrict__ sy,
                                           const float* __restrict__ st, int col0,
-                                          const float (&xi)[kSymR], const float (&yi)[kSymR],
-                                          const float (&ti)[kSymR], float c1, float c2,
-                                          float (&rf)[kSymR][GRAD ? kNSumGrad : kNSumVal],
+                                          const f2 (&xi)[2], const f2 (&yi)[2],
+                                          const f2 (&ti)[2], f2 c1, f2 c2,
+                                          f2 (&rf)[2][GRAD ? kNSumGrad : kNSumVal],
                                           float (&cp)[kSymG][GRAD ? 3 : 1]) {
   constexpr int T0 = GRAD ? 3 : 1;
 #pragma unroll
   for (int q = 0; q < kSymG; ++q) {
     const int j = col0 + kSymG * g + (q ^ perm);
-    const float xj = sx[j], yj = sy[j], tj = st[j];
-    float dt[kSymR], r2[kSymR], dt2[kSymR], e[kSymR];
+    const float xs = sx[j], ys = sy[j], ts = st[j];
+    const f2 xj = pk2(xs, xs), yj = pk2(ys, ys), tj = pk2(ts, ts);
+    f2 dt[2], r2[2], dt2[2], e[2];
 #pragma unroll
-    for (int r = 0; r < kSymR; ++r) {
-      const float dx = xi[r] - xj;
-      const float dy = yi[r] - yj;
-      dt[r] = ti[r] - tj;
-      r2[r] = fmaf(dx, dx, dy * dy);
+    for (int P = 0; P < 2; ++P) {
+      const f2 dx = sub2(xi[P], xj);
+      const f2 dy = sub2(yi[P], yj);
+      dt[P] = sub2(ti[P], tj);
+      r2[P] = fma2(dx, dx, mul2(dy, dy));
     }
     if constexpr (BG) {
 #pragma unroll
-      for (int r = 0; r < kSymR; ++r) {
-        dt2[r] = dt[r] * dt[r];
-        e[r] = ex2f(-(r2[r] + dt2[r]));
-        rf[r][0] += e[r];
+      for (int P = 0; P < 2; ++P) {
+        dt2[P] = mul2(dt[P], dt[P]);
+        const f2 sum = add2(r2[P], dt2[P]);
+        e[P] = pk2(ex2f(-lo2(sum)), ex2f(-hi2(sum)));  // (negation folds into MUFU)
+        rf[P][0] = add2(rf[P][0], e[P]);
         if constexpr (GRAD) {
-          rf[r][1] = fmaf(e[r], r2[r], rf[r][1]);
-          rf[r][2] = fmaf(e[r], dt2[r], rf[r][2]);
+          rf[P][1] = fma2(e[P], r2[P], rf[P][1]);
+          rf[P][2] = fma2(e[P], dt2[P], rf[P][2]);
         }
       }
-      cp[q][0] = (e[0] + e[1]) + (e[2] + e[3]);
+      const f2 es = add2(e[0], e[1]);  // (e0 + e2, e1 + e3)
+      cp[q][0] = lo2(es) + hi2(es);
       if constexpr (GRAD) {
-        cp[q][1] = fmaf(e[3], r2[3], fmaf(e[2], r2[2], fmaf(e[1], r2[1], e[0] * r2[0])));
-        cp[q][2] = fmaf(e[3], dt2[3], fmaf(e[2], dt2[2], fmaf(e[1], dt2[1], e[0] * dt2[0])));
+        const f2 wr = fma2(e[1], r2[1], mul2(e[0], r2[0]));
+        const f2 wt = fma2(e[1], dt2[1], mul2(e[0], dt2[0]));
+        cp[q][1] = lo2(wr) + hi2(wr);
+        cp[q][2] = lo2(wt) + hi2(wt);
       }
     }
     if constexpr (TR) {  // unmasked: every source strictly earlier than every row
 #pragma unroll
-      for (int r = 0; r < kSymR; ++r) {
-        const float et = ex2f(fmaf(c1, dt[r], c2 * r2[r]));
-        rf[r][T0] += et;
+      for (int P = 0; P < 2; ++P) {
+        const f2 et = ex2x2(fma2(c1, dt[P], mul2(c2, r2[P])));
+        rf[P][T0] = add2(rf[P][T0], et);
         if constexpr (GRAD) {
-          rf[r][4] = fmaf(et, dt[r], rf[r][4]);
-          rf[r][5] = fmaf(et, r2[r], rf[r][5]);
+          rf[P][4] = fma2(et, dt[P], rf[P][4]);
+          rf[P][5] = fma2(et, r2[P], rf[P][5]);
         }
       }
     }
@@ -665,17 +714,22 @@ __device__ __forceinline__ void far_block(const float* __restrict__ sx, const fl
   const int lane = threadIdx.x & 31;
   const int perm = (((lane >> 4) & 1) << 1) | ((lane >> 3) & 1);
   static_assert(kSymG == 4, "far tier assumes 4-column groups");
-  float rf[kSymR][NS];
+  f2 rf[2][NS];
 #pragma unroll
-  for (int r = 0; r < kSymR; ++r) {
+  for (int P = 0; P < 2; ++P) {
 #pragma unroll
-    for (int q = 0; q < NS; ++q) rf[r][q] = 0.0f;
+    for (int q = 0; q < NS; ++q) rf[P][q] = pk2(0.0f, 0.0f);
   }
+  // packed rows: lane rows (0, 1) and (2, 3)
+  const f2 px[2] = {pk2(xi[0], xi[1]), pk2(xi[2], xi[3])};
+  const f2 py[2] = {pk2(yi[0], yi[1]), pk2(yi[2], yi[3])};
+  const f2 pt[2] = {pk2(ti[0], ti[1]), pk2(ti[2], ti[3])};
+  const f2 c1 = pk2(k.fc1, k.fc1), c2 = pk2(k.fc2, k.fc2);
   const double cscale[3] = {1.0, k.fkr, k.fkt2};
 #pragma unroll 1
   for (int g = 0; g < 32 / kSymG; ++g) {
     float cp[kSymG][NSC];
-    far_pairs<GRAD, BG, TR>(g, perm, sx, sy, st, col0, xi, yi, ti, k.fc1, k.fc2, rf, cp);
+    far_pairs<GRAD, BG, TR>(g, perm, sx, sy, st, col0, px, py, pt, c1, c2, rf, cp);
     if constexpr (BG) {
       float v2[2][NSC], v1[NSC];
 #pragma unroll
@@ -700,20 +754,28 @@ __device__ __forceinline__ void far_block(const float* __restrict__ sx, const fl
       }
     }
   }
+  float rr[kSymR][NS];  // unpack: rows 0..3
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    rr[0][q] = lo2(rf[0][q]);
+    rr[1][q] = hi2(rf[0][q]);
+    rr[2][q] = lo2(rf[1][q]);
+    rr[3][q] = hi2(rf[1][q]);
+  }
 #pragma unroll
   for (int r = 0; r < kSymR; ++r) {
     if constexpr (BG) {
-      racc[r][0] += static_cast<double>(rf[r][0]);
+      racc[r][0] += static_cast<double>(rr[r][0]);
       if constexpr (GRAD) {
-        racc[r][1] = fma(static_cast<double>(rf[r][1]), k.fkr, racc[r][1]);
-        racc[r][2] = fma(static_cast<double>(rf[r][2]), k.fkt2, racc[r][2]);
+        racc[r][1] = fma(static_cast<double>(rr[r][1]), k.fkr, racc[r][1]);
+        racc[r][2] = fma(static_cast<double>(rr[r][2]), k.fkt2, racc[r][2]);
       }
     }
     if constexpr (TR) {
-      racc[r][T0] += static_cast<double>(rf[r][T0]);
+      racc[r][T0] += static_cast<double>(rr[r][T0]);
       if constexpr (GRAD) {
-        racc[r][4] = fma(static_cast<double>(rf[r][4]), k.fkt1, racc[r][4]);
-        racc[r][5] = fma(static_cast<double>(rf[r][5]), k.fkr, racc[r][5]);
+        racc[r][4] = fma(static_cast<double>(rr[r][4]), k.fkt1, racc[r][4]);
+        racc[r][5] = fma(static_cast<double>(rr[r][5]), k.fkr, racc[r][5]);
       }
     }
   }
@@ -937,14 +999,17 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
         }
       }
       if (!diag && bg) {  // (never in a trigger-only sweep)
-        // column sums of source tile J: one fixed-point flush per column
-        __syncthreads();
-        const int64_t col = s0 + tid;
+        // column sums of source tile J: one fixed-point flush per column.
+        // Warp w owns columns 32w..32w+31 (it wrote their s_col entries), so
+        // it flushes them itself after a warp-level sync: no CTA barrier.
+        __syncwarp();
+        const int jc = col0 + lane;
+        const int64_t col = s0 + jc;
 #pragma unroll
         for (int c = 0; c < NSC; ++c) {
           fx_add(a.fx + static_cast<size_t>(2 * c) * a.npad + col,
                  a.fx + static_cast<size_t>(2 * c + 1) * a.npad + col,
-                 s_col[tid * NSC + c] * a.fxq[c]);
+                 s_col[jc * NSC + c] * a.fxq[c]);
         }
       }
       if (tid == 0) {
