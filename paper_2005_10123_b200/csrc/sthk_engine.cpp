@@ -73,6 +73,13 @@ struct Slot {
   int dev = 0;
   int sms = 148;
   int occ[2][2] = {{1, 1}, {1, 1}};  // [mode][grad]
+  int occ_far[2] = {1, 1};           // far kernel [grad]
+  int2 *ranges_far = nullptr, *crange_far = nullptr, *items_far = nullptr;
+  size_t ranges_far_cap = 0, crange_far_cap = 0, items_far_cap = 0;
+  double* tpart_far = nullptr;       // far kernel trigger partials [nchunks][3][npad]
+  size_t tpart_far_cap = 0;
+  double2* tile_trange = nullptr;    // per tile: t first, t last
+  size_t trange_cap = 0;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   double *x = nullptr, *y = nullptr, *t = nullptr;
@@ -92,7 +99,8 @@ struct Slot {
   int2* items = nullptr;
   size_t items_cap = 0;
   int* scalars = nullptr;  // [0] n_items, [1] work counter, [2] pair CTAs done, [3] finalize
-                           // blocks done, [4..5] first invalid event index (uint64)
+                           // blocks done, [4..5] first invalid event index (uint64),
+                           // [6] far n_items, [7] far work counter, [8] far CTAs done
   unsigned long long* h_bad = nullptr;  // pinned
   unsigned long long* fx = nullptr;  // fixed-point background sums [6][npad]
   size_t fx_cap = 0;
@@ -121,6 +129,7 @@ struct Slot {
   bool plan_valid = false;
   double plan_dB = 0, plan_dT = 0;
   int plan_key[6] = {0, 0, 0, 0, 0, 0};  // tile0, tile1, sc, dense, sym, trig_only
+  double plan_tfar = 0;
   std::vector<std::pair<int, int>> runs;  // row ranges run on this slot
 };
 
@@ -183,8 +192,8 @@ void init_slot(Slot& s, int dev) {
   ck(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
   ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
   for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
-  ck(cudaMalloc(&s.scalars, 6 * sizeof(int)), "cudaMalloc");
-  ck(cudaMemset(s.scalars, 0, 6 * sizeof(int)), "memset");
+  ck(cudaMalloc(&s.scalars, 10 * sizeof(int)), "cudaMalloc");
+  ck(cudaMemset(s.scalars, 0, 10 * sizeof(int)), "memset");
   ck(cudaMallocHost(&s.h_bad, sizeof(unsigned long long)), "cudaMallocHost");
   ck(cudaMalloc(&s.out, kNOut * sizeof(double)), "cudaMalloc");
   ck(cudaMalloc(&s.pair_counts, sthk::kNCounts * sizeof(unsigned long long)), "cudaMalloc");
@@ -194,6 +203,8 @@ void init_slot(Slot& s, int dev) {
   for (int m = 0; m < 2; ++m) {
     s.occ[m][1] = sthk::pair_kernel_occupancy(true, m);
     s.occ[m][0] = sthk::pair_kernel_occupancy(false, m);
+    s.occ_far[1] = sthk::far_kernel_occupancy(true);
+    s.occ_far[0] = sthk::far_kernel_occupancy(false);
   }
   ck(cudaGetLastError(), "occupancy");
 }
@@ -205,6 +216,9 @@ void free_slot(Slot& s) {
   for (void* p : {static_cast<void*>(s.x), static_cast<void*>(s.y), static_cast<void*>(s.t),
                   static_cast<void*>(s.xs), static_cast<void*>(s.ys),
                   static_cast<void*>(s.xf), static_cast<void*>(s.yf), static_cast<void*>(s.tf),
+                  static_cast<void*>(s.ranges_far), static_cast<void*>(s.crange_far),
+                  static_cast<void*>(s.items_far), static_cast<void*>(s.tpart_far),
+                  static_cast<void*>(s.tile_trange),
                   static_cast<void*>(s.ranges), static_cast<void*>(s.counts),
                   static_cast<void*>(s.items), static_cast<void*>(s.scalars),
                   static_cast<void*>(s.fx), static_cast<void*>(s.block_partial),
@@ -265,6 +279,7 @@ struct EvalPlan {
   sthk::PairConsts k;
   double sx = 1.0;  // kSym coordinate scale sqrt(-cxL)
   double sxf = 1.0, stf = 1.0;  // far-tier FP32 coordinate scales
+  double tfar = 0.0;            // far split time gap (days)
   int sc = 0;
   int nchunks = 0;
   std::vector<int> cuts;  // shard row boundaries (size shards+1)
@@ -324,6 +339,9 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   pl.k.fkt1 = 1.0 / pl.stf;
   pl.k.fkt2 = 1.0 / (pl.stf * pl.stf);
   pl.k.fstf = pl.stf;
+  // far split: sources earlier than t_tile_first - tfar have every exponent
+  // below -kFarExponent (background: dt^2 / 2 tauT^2 >= A; trigger: omega dt >= A)
+  pl.tfar = std::max(p[2] * std::sqrt(2.0 * kFarExponent), kFarExponent / p[4]) * (1.0 + 1e-9);
   pl.k.nomL = static_cast<double>(-L * p[4]);
   const double inf = std::numeric_limits<double>::infinity();
   pl.k.dB = e.dense ? inf : dB;
@@ -446,6 +464,13 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     dev_grow(s.fx, s.fx_cap, static_cast<size_t>(kFxRows) * e.npad);
     dev_grow(s.tpart, s.tpart_cap, static_cast<size_t>(pl.nchunks) * 3 * e.npad);
     dev_grow(s.crange, s.crange_cap, static_cast<size_t>(ntiles_total));
+    if (far_on) {
+      dev_grow(s.ranges_far, s.ranges_far_cap, static_cast<size_t>(ntiles_total));
+      dev_grow(s.crange_far, s.crange_far_cap, static_cast<size_t>(ntiles_total));
+      dev_grow(s.items_far, s.items_far_cap,
+               static_cast<size_t>(std::max(ntiles, 1)) * pl.nchunks);
+      dev_grow(s.tpart_far, s.tpart_far_cap, static_cast<size_t>(pl.nchunks) * 3 * e.npad);
+    }
     dev_grow(s.block_partial, s.bp_cap, static_cast<size_t>(nb_total) * kNOut);
     if (want_pe) dev_grow(s.per_event, s.pe_cap, static_cast<size_t>(e.npad));
     if (want_ex) dev_grow(s.ex, s.ex_cap, static_cast<size_t>(3) * e.npad);
@@ -493,14 +518,24 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     pa.items = s.items;
     pa.n_items = s.scalars;
     pa.work_counter = s.scalars + 1;
+    pa.tfar = far_on ? pl.tfar : 0.0;
+    if (far_on) {
+      pa.ranges_far = s.ranges_far;
+      pa.crange_far = s.crange_far;
+      pa.items_far = s.items_far;
+      pa.n_items_far = s.scalars + 6;
+      pa.work_counter_far = s.scalars + 7;
+    }
     const int key[6] = {tile0, tile1, pl.sc, pa.dense, pa.sym, pa.trig_only};
     const bool plan_hit = e.bg_cache && !vshards && s.plan_valid && s.plan_dB == pa.dB &&
-                          s.plan_dT == pa.dT && std::equal(key, key + 6, s.plan_key);
-    if (!plan_hit) {  // (the work counter is re-armed by the last pair CTA)
+                          s.plan_dT == pa.dT && s.plan_tfar == pa.tfar &&
+                          std::equal(key, key + 6, s.plan_key);
+    if (!plan_hit) {  // (the work counters are re-armed by the last pair CTAs)
       ck(sthk::launch_plan(pa, st), "plan");
       s.plan_valid = e.bg_cache && !vshards;
       s.plan_dB = pa.dB;
       s.plan_dT = pa.dT;
+      s.plan_tfar = pa.tfar;
       std::copy(key, key + 6, s.plan_key);
     }
 
@@ -515,6 +550,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     qa.tf = s.tf;
     qa.far_on = far_on ? 1 : 0;
     qa.tile_box = s.tile_box;
+    qa.tile_trange = s.tile_trange;
     qa.n = e.n;
     qa.npad = e.npad;
     qa.k = pl.k;
@@ -535,6 +571,16 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     const int grid = s.sms * s.occ[e.mode][grad ? 1 : 0];
     if (e.timing && first_run) ck(cudaEventRecord(s.ev[1], st), "event");
     ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
+    if (far_on) {  // the far work list in FP32 (same stream, after the near sweep)
+      sthk::PairArgs fa_ = qa;
+      fa_.ranges = s.ranges_far;
+      fa_.items = s.items_far;
+      fa_.n_items = s.scalars + 6;
+      fa_.work_counter = s.scalars + 7;
+      fa_.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 8);
+      fa_.tpart = s.tpart_far;
+      ck(sthk::launch_far(fa_, grad, s.sms * s.occ_far[grad ? 1 : 0], st), "far kernel");
+    }
     if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
   }
 
@@ -575,6 +621,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     fa.tpart = s.tpart;
     fa.tr_r2_scale = sym ? 1.0 / (pl.sx * pl.sx) : 1.0;
     fa.crange = s.crange;
+    fa.tpart_far = far_on ? s.tpart_far : nullptr;
+    fa.crange_far = s.crange_far;
     for (int k = 0; k < sthk::kNSumGrad; ++k) fa.fxq[k] = fxq[k];
     fa.per_event = want_pe ? s.per_event : nullptr;
     fa.ex_out = want_ex ? s.ex : nullptr;
@@ -856,9 +904,11 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       ck(cudaMemcpyAsync(s.y, y, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
       ck(cudaMemcpyAsync(s.t, t, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
       dev_grow(s.tile_box, s.box_cap, static_cast<size_t>(npad / kTS));
+      dev_grow(s.tile_trange, s.trange_cap, static_cast<size_t>(npad / kTS));
       auto* bad = reinterpret_cast<unsigned long long*>(s.scalars + 4);
       ck(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s.stream), "memset");
-      ck(sthk::launch_tile_boxes(s.x, s.y, s.t, n, npad, s.tile_box, bad, s.stream),
+      ck(sthk::launch_tile_boxes(s.x, s.y, s.t, n, npad, s.tile_box, s.tile_trange, bad,
+                                 s.stream),
          "tile boxes + checks");
       ck(cudaMemcpyAsync(s.h_bad, bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                          s.stream),

@@ -86,7 +86,7 @@ __device__ __forceinline__ int64_t bound_t(const double* t, int64_t n, double v,
 // ---------------------------------------------------------------------------
 // Live source range [lo, hi) and chunk range [c0, c1] of one row tile.
 __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, int tile, int2& rg,
-                                          int2& cr) {
+                                          int2& cr, int2& rgf, int2& crf) {
   const int64_t first = static_cast<int64_t>(tile) * kTM;
   const int64_t last = min(first + kTM, a.n) - 1;
   int lo, hi;
@@ -107,8 +107,17 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
   }
   // symmetric mode: later tiles reach this one through their column sums
   if (a.sym || a.trig_only) hi = static_cast<int>(last + 1);
-  rg = make_int2(lo, hi);
-  cr = make_int2(a.dense ? 0 : lo / a.sc, (hi - 1) / a.sc);
+  // far split: whole 128-stages of sources earlier than t[first] - tfar
+  // (every term below e^-A) go to the far list; the rest stay near
+  int fb = lo;
+  if (a.tfar > 0.0 && last + 1 - first == kTM) {  // (full row tiles only)
+    const int b = static_cast<int>(bound_t<true>(a.t, a.n, a.t[first] - a.tfar, pv));
+    fb = max(lo, b - b % kTS);
+  }
+  rg = make_int2(fb, hi);
+  cr = make_int2(fb / a.sc, (hi - 1) / a.sc);
+  rgf = make_int2(lo, fb);
+  crf = fb > lo ? make_int2(lo / a.sc, (fb - 1) / a.sc) : make_int2(0, -1);
 }
 
 // Number of 128-source stages of work item (tile, chunk) -- the same bounds
@@ -128,33 +137,23 @@ constexpr int kPlanBins = 1024;  // item-size classes (stages, clamped)
 // ones (less idle time in the tail); resets the pair kernel's work counter.
 // The order only affects scheduling: every partial has a fixed destination
 // and integer (fixed-point) accumulation, so results do not depend on it.
-__global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
-  __shared__ int s_hist[kPlanBins];
-  __shared__ int s_warp[32];
-  __shared__ double s_piv[kPivots];
+// Work list of one kind (near or far) ordered by decreasing item size: a
+// histogram of the items' stage counts, an exclusive scan over the bins in
+// decreasing size, then placement (1024 threads, one CTA).
+__device__ void plan_list(const PlanArgs& a, const int2* ranges, const int2* crange, int2* items,
+                          int* n_items, int* work_counter, int* s_hist, int* s_warp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ntiles = a.tile1 - a.tile0;
   for (int b = tid; b < kPlanBins; b += 1024) s_hist[b] = 0;
-  Pivots pv;
-  pv.stride = (a.n + kPivots - 1) / kPivots;
-  pv.np = static_cast<int>((a.n + pv.stride - 1) / pv.stride);
-  pv.piv = s_piv;
-  for (int k = tid; k < pv.np; k += 1024) s_piv[k] = a.t[k * pv.stride];
   __syncthreads();
-  // pass 1: ranges and the item-size histogram
   for (int i = tid; i < ntiles; i += 1024) {
-    int2 rg, cr;
-    tile_plan(a, pv, a.tile0 + i, rg, cr);
-    a.ranges[a.tile0 + i] = rg;
-    a.crange[a.tile0 + i] = cr;
+    const int2 rg = ranges[a.tile0 + i], cr = crange[a.tile0 + i];
     for (int c = cr.x; c <= cr.y; ++c) {
       atomicAdd(&s_hist[min(item_stages(a, rg, c), kPlanBins - 1)], 1);
     }
   }
   __syncthreads();
-  // exclusive scan over the bins in decreasing size: bin b starts after all
-  // larger bins (thread t owns bin kPlanBins - 1 - t)
-  const int bin = kPlanBins - 1 - tid;
+  const int bin = kPlanBins - 1 - tid;  // thread t owns bin kPlanBins - 1 - t
   const int c = s_hist[bin];
   int v = c;
 #pragma unroll
@@ -176,20 +175,56 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   __syncthreads();
   const int incl = v + (warp > 0 ? s_warp[warp - 1] : 0);
   if (tid == 1023) {
-    *a.n_items = incl;
-    *a.work_counter = 0;
+    *n_items = incl;
+    *work_counter = 0;
   }
   __syncthreads();
   s_hist[bin] = incl - c;  // start offset of the bin
   __syncthreads();
-  // pass 2: place every item
   for (int i = tid; i < ntiles; i += 1024) {
     const int tile = a.tile0 + i;
-    const int2 rg = a.ranges[tile], cr = a.crange[tile];
+    const int2 rg = ranges[tile], cr = crange[tile];
     for (int ch = cr.x; ch <= cr.y; ++ch) {
       const int pos = atomicAdd(&s_hist[min(item_stages(a, rg, ch), kPlanBins - 1)], 1);
-      a.items[pos] = make_int2(tile, ch);
+      items[pos] = make_int2(tile, ch);
     }
+  }
+  __syncthreads();
+}
+
+// Single CTA: per-tile near / far ranges, then each work list ordered by
+// decreasing item size, so the persistent pair kernels hand out the long
+// items first and end on short ones (less idle time in the tail); resets the
+// kernels' work counters. The order only affects scheduling: every partial
+// has a fixed destination and integer (fixed-point) accumulation, so results
+// do not depend on it.
+__global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
+  __shared__ int s_hist[kPlanBins];
+  __shared__ int s_warp[32];
+  __shared__ double s_piv[kPivots];
+  const int tid = threadIdx.x;
+  const int ntiles = a.tile1 - a.tile0;
+  Pivots pv;
+  pv.stride = (a.n + kPivots - 1) / kPivots;
+  pv.np = static_cast<int>((a.n + pv.stride - 1) / pv.stride);
+  pv.piv = s_piv;
+  for (int k = tid; k < pv.np; k += 1024) s_piv[k] = a.t[k * pv.stride];
+  __syncthreads();
+  for (int i = tid; i < ntiles; i += 1024) {
+    int2 rg, cr, rgf, crf;
+    tile_plan(a, pv, a.tile0 + i, rg, cr, rgf, crf);
+    a.ranges[a.tile0 + i] = rg;
+    a.crange[a.tile0 + i] = cr;
+    if (a.ranges_far) {
+      a.ranges_far[a.tile0 + i] = rgf;
+      a.crange_far[a.tile0 + i] = crf;
+    }
+  }
+  __syncthreads();
+  plan_list(a, a.ranges, a.crange, a.items, a.n_items, a.work_counter, s_hist, s_warp);
+  if (a.ranges_far) {
+    plan_list(a, a.ranges_far, a.crange_far, a.items_far, a.n_items_far, a.work_counter_far,
+              s_hist, s_warp);
   }
 }
 
@@ -697,35 +732,24 @@ __device__ __forceinline__ void far_pairs(int g, int perm, const float* __restri
   }
 }
 
-// One far stage for one warp: 32 columns x 4 rows in FP32, column partials
-// reduce-scattered with FP32 shuffles (lane-permuted order as in sym_reduce),
-// column totals stored to s_col in the FP64 path's units, row partials merged
-// into the FP64 row sums at the end.
+// One far stage for one warp: 32 columns x this lane's 4 rows in FP32x2.
+// Row sums stay in FP32 registers for the whole item (every far term is
+// below 2^-57 of a row's self term, so FP32 accumulation error is
+// irrelevant); column partials are reduce-scattered with FP32 shuffles
+// (lane-permuted order, see sym_reduce) and stored to s_col in the FP64
+// path's units for the fixed-point flush.
 template <bool GRAD, bool BG, bool TR>
-__device__ __forceinline__ void far_block(const float* __restrict__ sx, const float* __restrict__ sy,
+__device__ __forceinline__ void far_stage(const float* __restrict__ sx, const float* __restrict__ sy,
                                           const float* __restrict__ st, int col0,
-                                          const float (&xi)[kSymR], const float (&yi)[kSymR],
-                                          const float (&ti)[kSymR], const PairConsts& k,
-                                          double (&racc)[kSymR][GRAD ? kNSumGrad : kNSumVal],
+                                          const f2 (&px)[2], const f2 (&py)[2],
+                                          const f2 (&pt)[2], f2 c1, f2 c2,
+                                          const double (&cscale)[3],
+                                          f2 (&rf)[2][GRAD ? kNSumGrad : kNSumVal],
                                           double* __restrict__ s_col) {
-  constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   constexpr int NSC = GRAD ? 3 : 1;
-  constexpr int T0 = GRAD ? 3 : 1;
   const int lane = threadIdx.x & 31;
   const int perm = (((lane >> 4) & 1) << 1) | ((lane >> 3) & 1);
   static_assert(kSymG == 4, "far tier assumes 4-column groups");
-  f2 rf[2][NS];
-#pragma unroll
-  for (int P = 0; P < 2; ++P) {
-#pragma unroll
-    for (int q = 0; q < NS; ++q) rf[P][q] = pk2(0.0f, 0.0f);
-  }
-  // packed rows: lane rows (0, 1) and (2, 3)
-  const f2 px[2] = {pk2(xi[0], xi[1]), pk2(xi[2], xi[3])};
-  const f2 py[2] = {pk2(yi[0], yi[1]), pk2(yi[2], yi[3])};
-  const f2 pt[2] = {pk2(ti[0], ti[1]), pk2(ti[2], ti[3])};
-  const f2 c1 = pk2(k.fc1, k.fc1), c2 = pk2(k.fc2, k.fc2);
-  const double cscale[3] = {1.0, k.fkr, k.fkt2};
 #pragma unroll 1
   for (int g = 0; g < 32 / kSymG; ++g) {
     float cp[kSymG][NSC];
@@ -751,31 +775,6 @@ __device__ __forceinline__ void far_block(const float* __restrict__ sx, const fl
         for (int c = 0; c < NSC; ++c) {
           s_col[(col0 + kSymG * g + perm) * NSC + c] = static_cast<double>(v1[c]) * cscale[c];
         }
-      }
-    }
-  }
-  float rr[kSymR][NS];  // unpack: rows 0..3
-#pragma unroll
-  for (int q = 0; q < NS; ++q) {
-    rr[0][q] = lo2(rf[0][q]);
-    rr[1][q] = hi2(rf[0][q]);
-    rr[2][q] = lo2(rf[1][q]);
-    rr[3][q] = hi2(rf[1][q]);
-  }
-#pragma unroll
-  for (int r = 0; r < kSymR; ++r) {
-    if constexpr (BG) {
-      racc[r][0] += static_cast<double>(rr[r][0]);
-      if constexpr (GRAD) {
-        racc[r][1] = fma(static_cast<double>(rr[r][1]), k.fkr, racc[r][1]);
-        racc[r][2] = fma(static_cast<double>(rr[r][2]), k.fkt2, racc[r][2]);
-      }
-    }
-    if constexpr (TR) {
-      racc[r][T0] += static_cast<double>(rr[r][T0]);
-      if constexpr (GRAD) {
-        racc[r][4] = fma(static_cast<double>(rr[r][4]), k.fkt1, racc[r][4]);
-        racc[r][5] = fma(static_cast<double>(rr[r][5]), k.fkr, racc[r][5]);
       }
     }
   }
@@ -810,7 +809,6 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   constexpr int NSC = GRAD ? 3 : 1;
   __shared__ __align__(128) double s_src[2][3][kTS];
-  __shared__ __align__(128) float s_srcf[2][3][kTS];  // far tier: FP32 copies of the stage
   extern __shared__ __align__(128) uint2 s_tab[];  // kExpTableSize entries (dynamic)
   __shared__ double s_col[kTS * NSC];
   __shared__ double s_red[4][NS][kTM];
@@ -839,7 +837,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
   uint32_t phase = 0;
   // ordered pairs covered (bg, trigger, any) and work executed (background
   // exps, pair geometries, symmetric pairs with a column accumulation)
-  unsigned long long cBg = 0, cTr = 0, cAny = 0, xBg = 0, xGeo = 0, xSym = 0, xFar = 0;
+  unsigned long long cBg = 0, cTr = 0, cAny = 0, xBg = 0, xGeo = 0, xSym = 0;
 
   for (int iter = 0;; ++iter) {
     if (tid == 0) s_item[iter & 1] = atomicAdd(a.work_counter, 1);
@@ -856,7 +854,6 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
     const double tmin = a.t[first], tmax = a.t[last];
     const double4 bt = a.tile_box[tile];
     double xi[kSymR], yi[kSymR], ti[kSymR];
-    float xfi[kSymR], yfi[kSymR], tfi[kSymR];
     bool rv[kSymR];
 #pragma unroll
     for (int r = 0; r < kSymR; ++r) {
@@ -865,11 +862,6 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       yi[r] = a.ys[row];
       ti[r] = a.t[row];
       rv[r] = row < n;
-      if (a.far_on) {
-        xfi[r] = a.xf[row];
-        yfi[r] = a.yf[row];
-        tfi[r] = a.tf[row];
-      }
     }
     // Background row sums live in registers for the whole item; the trigger
     // row sums (rarely active) are parked in this thread's s_red slots
@@ -891,15 +883,9 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
     const int nst = (s_end - s_begin + kTS - 1) / kTS;
 
     constexpr uint32_t kStageBytes = kTS * sizeof(double);
-    constexpr uint32_t kStageBytesF = kTS * sizeof(float);
     if (tid == 0 && nst > 0) {
-      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes + kBoxBytes + (a.far_on ? 3 * kStageBytesF : 0));
+      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes + kBoxBytes);
       tma_load_1d(&s_box[0], a.tile_box + s_begin / kTS, kBoxBytes, &s_bar[0]);
-      if (a.far_on) {
-        tma_load_1d(s_srcf[0][0], a.xf + s_begin, kStageBytesF, &s_bar[0]);
-        tma_load_1d(s_srcf[0][1], a.yf + s_begin, kStageBytesF, &s_bar[0]);
-        tma_load_1d(s_srcf[0][2], a.tf + s_begin, kStageBytesF, &s_bar[0]);
-      }
       tma_load_1d(s_src[0][0], a.xs + s_begin, kStageBytes, &s_bar[0]);
       tma_load_1d(s_src[0][1], a.ys + s_begin, kStageBytes, &s_bar[0]);
       tma_load_1d(s_src[0][2], a.t + s_begin, kStageBytes, &s_bar[0]);
@@ -911,13 +897,8 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       if (tid == 0 && s + 1 < nst) {
         const int nb = buf ^ 1;
         const int64_t s0n = s_begin + static_cast<int64_t>(s + 1) * kTS;
-        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes + kBoxBytes + (a.far_on ? 3 * kStageBytesF : 0));
+        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes + kBoxBytes);
         tma_load_1d(&s_box[nb], a.tile_box + s0n / kTS, kBoxBytes, &s_bar[nb]);
-        if (a.far_on) {
-          tma_load_1d(s_srcf[nb][0], a.xf + s0n, kStageBytesF, &s_bar[nb]);
-          tma_load_1d(s_srcf[nb][1], a.yf + s0n, kStageBytesF, &s_bar[nb]);
-          tma_load_1d(s_srcf[nb][2], a.tf + s0n, kStageBytesF, &s_bar[nb]);
-        }
         tma_load_1d(s_src[nb][0], a.xs + s0n, kStageBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][1], a.ys + s0n, kStageBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][2], a.t + s0n, kStageBytes, &s_bar[nb]);
@@ -942,17 +923,6 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       const double dtm = fmax(tmax - smin, smax - tmin);
       const bool safe = (!bg || a.k.cxL * r2m + a.k.ctL * (dtm * dtm) > kSafeExpL) &&
                         (!tr || a.k.nomL * dtm + a.k.chL * r2m > kSafeExpL);
-      // far tier: exponent UPPER bounds over the box pair (minimum distance
-      // and time gap) below farL for every live term
-      bool far = false;
-      if (a.far_on && !diag && rows_real == kTM && cnt == kTS && tr != 2 && (bg || tr)) {
-        const double gx = fmax(0.0, fmax(bs.x - bt.y, bt.x - bs.y));
-        const double gy = fmax(0.0, fmax(bs.z - bt.w, bt.z - bs.w));
-        const double r2g = gx * gx + gy * gy;
-        const double dtg = fmax(0.0, fmax(smin - tmax, tmin - smax));
-        far = (!bg || a.k.cxL * r2g + a.k.ctL * (dtg * dtg) < a.k.farL) &&
-              (!tr || a.k.nomL * dtg + a.k.chL * r2g < a.k.farL);
-      }
 
       const double* sx = s_src[buf][0];
       const double* sy = s_src[buf][1];
@@ -965,20 +935,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
           for (int q = NB; q < NS; ++q) racc[r][q] = s_red[warp][q][lane + 32 * r];
         }
       }
-      if (far) {
-        const float* fx = s_srcf[buf][0];
-        const float* fy = s_srcf[buf][1];
-        const float* ft = s_srcf[buf][2];
-        // row times re-based onto the source tile's origin: one FP32 offset
-        // per stage (the tile-to-tile time gap, rounded once)
-        const float dtile = static_cast<float>((tmin - smin) * a.k.fstf);
-        float tfr[kSymR];
-#pragma unroll
-        for (int r = 0; r < kSymR; ++r) tfr[r] = tfi[r] + dtile;
-        if (bg && tr) far_block<GRAD, true, true>(fx, fy, ft, col0, xfi, yfi, tfr, a.k, racc, s_col);
-        else if (bg) far_block<GRAD, true, false>(fx, fy, ft, col0, xfi, yfi, tfr, a.k, racc, s_col);
-        else far_block<GRAD, false, true>(fx, fy, ft, col0, xfi, yfi, tfr, a.k, racc, s_col);
-      } else if (diag) {
+      if (diag) {
         sym_dispatch<GRAD, false, true, true>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
                                               a.k, s_tab, racc, s_col);
       } else if (rows_real < kTM) {
@@ -1014,7 +971,6 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
       }
       if (tid == 0) {
         const unsigned long long pr = static_cast<unsigned long long>(cnt) * rows_real;
-        if (far) xFar += pr;
         if (diag) {
           if (bg) cBg += pr;
           if (tr) cTr += pr;
@@ -1061,6 +1017,194 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
     atomicAdd(&a.pair_counts[3], xBg);
     atomicAdd(&a.pair_counts[4], xGeo);
     atomicAdd(&a.pair_counts[5], xSym);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Far kernel (kSym far tier): the far work list -- source stages whose every
+// pair with the row tile is at least tfar earlier, so every background and
+// trigger exponent is below -A (A = 40) -- in FP32 on the FP32 / MUFU pipes,
+// with far fewer registers than the FP64 kernel (more resident warps).
+// Same structure as sym_kernel: persistent CTAs of 128 rows, bulk-copied
+// 128-source stages, symmetric background (rows and columns), unmasked
+// trigger (every far source is strictly earlier). Background sums go to the
+// same fixed-point accumulators; trigger partials to their own per-(chunk,
+// row) buffer (tpart_far), summed by finalize after the near ones.
+// ---------------------------------------------------------------------------
+#ifndef STHK_FAR_MINB
+#define STHK_FAR_MINB 4
+#endif
+
+template <bool GRAD>
+__global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs a) {
+  constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
+  constexpr int NSC = GRAD ? 3 : 1;
+  constexpr int NB = GRAD ? 3 : 1;
+  constexpr int NT = GRAD ? 3 : 1;
+  __shared__ __align__(128) float s_srcf[2][3][kTS];
+  __shared__ __align__(16) double2 s_tr[2];
+  __shared__ double s_col[kTS * NSC];
+  __shared__ float s_red[4][NS][kTM];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ int s_item[2];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int n_items = *a.n_items;
+  uint32_t phase = 0;
+  unsigned long long cBg = 0, cTr = 0, cAny = 0, xBg = 0, xGeo = 0, xSym = 0, xFar = 0;
+  const double cscale[3] = {1.0, a.k.fkr, a.k.fkt2};
+  const double tscale[3] = {1.0, a.k.fkt1, a.k.fkr};  // S_T, S_Tt, S_Tr
+  const f2 c1 = pk2(a.k.fc1, a.k.fc1), c2 = pk2(a.k.fc2, a.k.fc2);
+  constexpr uint32_t kStageBytesF = kTS * sizeof(float);
+  constexpr uint32_t kTrBytes = sizeof(double2);
+
+  for (int iter = 0;; ++iter) {
+    if (tid == 0) s_item[iter & 1] = atomicAdd(a.work_counter, 1);
+    __syncthreads();
+    const int item = s_item[iter & 1];
+    if (item >= n_items) break;
+
+    const int2 it = a.items[item];
+    const int tile = it.x, chunk = it.y;
+    const int2 rg = a.ranges[tile];
+    const int64_t first = static_cast<int64_t>(tile) * kTM;  // (full tiles only)
+    const double tmin = a.t[first], tmax = a.t[first + kTM - 1];
+    float xr[kSymR], yr[kSymR], tr_[kSymR];
+#pragma unroll
+    for (int r = 0; r < kSymR; ++r) {
+      const int64_t row = first + lane + 32 * r;
+      xr[r] = a.xf[row];
+      yr[r] = a.yf[row];
+      tr_[r] = a.tf[row];
+    }
+    const f2 px[2] = {pk2(xr[0], xr[1]), pk2(xr[2], xr[3])};
+    const f2 py[2] = {pk2(yr[0], yr[1]), pk2(yr[2], yr[3])};
+    const f2 ptr[2] = {pk2(tr_[0], tr_[1]), pk2(tr_[2], tr_[3])};
+    f2 rf[2][NS];
+#pragma unroll
+    for (int P = 0; P < 2; ++P) {
+#pragma unroll
+      for (int q = 0; q < NS; ++q) rf[P][q] = pk2(0.0f, 0.0f);
+    }
+
+    int s_begin = max(rg.x, chunk * a.sc);
+    s_begin -= s_begin % kTS;
+    const int s_end = min(rg.y, (chunk + 1) * a.sc);
+    const int nst = (s_end - s_begin + kTS - 1) / kTS;
+    if (tid == 0 && nst > 0) {
+      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytesF + kTrBytes);
+      tma_load_1d(&s_tr[0], a.tile_trange + s_begin / kTS, kTrBytes, &s_bar[0]);
+      tma_load_1d(s_srcf[0][0], a.xf + s_begin, kStageBytesF, &s_bar[0]);
+      tma_load_1d(s_srcf[0][1], a.yf + s_begin, kStageBytesF, &s_bar[0]);
+      tma_load_1d(s_srcf[0][2], a.tf + s_begin, kStageBytesF, &s_bar[0]);
+    }
+    for (int s = 0; s < nst; ++s) {
+      const int buf = s & 1;
+      __syncthreads();  // every warp is done with stage s-1's buffer
+      if (tid == 0 && s + 1 < nst) {
+        const int nb = buf ^ 1;
+        const int64_t s0n = s_begin + static_cast<int64_t>(s + 1) * kTS;
+        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytesF + kTrBytes);
+        tma_load_1d(&s_tr[nb], a.tile_trange + s0n / kTS, kTrBytes, &s_bar[nb]);
+        tma_load_1d(s_srcf[nb][0], a.xf + s0n, kStageBytesF, &s_bar[nb]);
+        tma_load_1d(s_srcf[nb][1], a.yf + s0n, kStageBytesF, &s_bar[nb]);
+        tma_load_1d(s_srcf[nb][2], a.tf + s0n, kStageBytesF, &s_bar[nb]);
+      }
+      const int64_t s0 = s_begin + static_cast<int64_t>(s) * kTS;
+      mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+      const double smin = s_tr[buf].x, smax = s_tr[buf].y;
+      const bool bg = !a.bg_off && !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
+      const bool trg = !(smin >= tmax || smax < tmin - a.k.dT);  // (all sources earlier)
+      // row times re-based onto the source tile's origin (tf is tile-relative)
+      const float dtile = static_cast<float>((tmin - smin) * a.k.fstf);
+      const f2 dd = pk2(dtile, dtile);
+      const f2 pt[2] = {add2(ptr[0], dd), add2(ptr[1], dd)};
+      const float* sx = s_srcf[buf][0];
+      const float* sy = s_srcf[buf][1];
+      const float* st = s_srcf[buf][2];
+      const int col0 = warp * 32;
+      if (bg && trg) far_stage<GRAD, true, true>(sx, sy, st, col0, px, py, pt, c1, c2, cscale, rf, s_col);
+      else if (bg) far_stage<GRAD, true, false>(sx, sy, st, col0, px, py, pt, c1, c2, cscale, rf, s_col);
+      else if (trg) far_stage<GRAD, false, true>(sx, sy, st, col0, px, py, pt, c1, c2, cscale, rf, s_col);
+      if (bg) {  // this warp's 32 columns: fixed-point flush (no CTA barrier)
+        __syncwarp();
+        const int jc = col0 + lane;
+        const int64_t col = s0 + jc;
+#pragma unroll
+        for (int c = 0; c < NSC; ++c) {
+          fx_add(a.fx + static_cast<size_t>(2 * c) * a.npad + col,
+                 a.fx + static_cast<size_t>(2 * c + 1) * a.npad + col,
+                 s_col[jc * NSC + c] * a.fxq[c]);
+        }
+      }
+      if (tid == 0) {
+        const unsigned long long pr = static_cast<unsigned long long>(kTS) * kTM;
+        if (bg) cBg += 2 * pr;
+        if (trg) cTr += pr;
+        cAny += bg ? 2 * pr : (trg ? pr : 0);
+        if (bg) xBg += pr;
+        if (bg) xSym += pr;
+        if (bg || trg) {
+          xGeo += pr;
+          xFar += pr;
+        }
+      }
+    }
+
+    // rows: combine the 4 warps' FP32 partials in a fixed order, then store
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      s_red[warp][q][lane] = lo2(rf[0][q]);
+      s_red[warp][q][lane + 32] = hi2(rf[0][q]);
+      s_red[warp][q][lane + 64] = lo2(rf[1][q]);
+      s_red[warp][q][lane + 96] = hi2(rf[1][q]);
+    }
+    __syncthreads();
+    // (lane l's packed pairs hold rows l, l+32 | l+64, l+96 of the tile)
+    const int64_t row = first + tid;
+    float v[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      v[q] = ((s_red[0][q][tid] + s_red[1][q][tid]) + s_red[2][q][tid]) + s_red[3][q][tid];
+    }
+    if (!a.bg_off) {
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        fx_add(a.fx + static_cast<size_t>(2 * q) * a.npad + row,
+               a.fx + static_cast<size_t>(2 * q + 1) * a.npad + row,
+               static_cast<double>(v[q]) * cscale[q] * a.fxq[q]);
+      }
+    }
+    double* out = a.tpart + static_cast<size_t>(chunk) * NT * a.npad + row;
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      out[static_cast<size_t>(q) * a.npad] = static_cast<double>(v[NB + q]) * tscale[q];
+    }
+  }
+
+  if (tid == 0) {  // the last CTA out re-arms the work counter for the next launch
+    __threadfence();
+    if (atomicAdd(a.done_counter, 1u) == gridDim.x - 1) {
+      *a.work_counter = 0;
+      *a.done_counter = 0u;
+    }
+  }
+  if (tid == 0 && a.pair_counts) {
+    atomicAdd(&a.pair_counts[0], cBg);
+    atomicAdd(&a.pair_counts[1], cTr);
+    atomicAdd(&a.pair_counts[2], cAny);
+    atomicAdd(&a.pair_counts[3], xBg);
+    atomicAdd(&a.pair_counts[4], xGeo);
+    atomicAdd(&a.pair_counts[5], xSym);
     atomicAdd(&a.pair_counts[6], xFar);
   }
 }
@@ -1069,7 +1213,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
 // independent; computed once per load). Feeds the no-underflow proofs.
 __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
                                 double* __restrict__ t, int64_t n, int64_t npad, double4* box,
-                                unsigned long long* bad) {
+                                double2* trange, unsigned long long* bad) {
   // zero the pad tail [n, npad) of the coordinate arrays (never read as sources)
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid < npad - n) {
@@ -1111,7 +1255,10 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
     y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, off));
     y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, off));
   }
-  if (lane == 0) box[tile] = make_double4(x0, x1, y0, y1);
+  if (lane == 0) {
+    box[tile] = make_double4(x0, x1, y0, y1);
+    trange[tile] = make_double2(t[first], t[last - 1]);
+  }
 }
 
 // Spatial coordinates pre-scaled by sx = sqrt(-cxL) for the symmetric
@@ -1203,6 +1350,14 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
       const double* p = a.tpart + static_cast<size_t>(c) * (NS - NB) * a.npad + r;
 #pragma unroll
       for (int k = NB; k < NS; ++k) s[k] += p[static_cast<size_t>(k - NB) * a.npad];
+    }
+    if (a.tpart_far) {  // then the far kernel's partials, in chunk order
+      const int2 cf = a.crange_far[r / kTM];
+      for (int c = cf.x; c <= cf.y; ++c) {
+        const double* p = a.tpart_far + static_cast<size_t>(c) * (NS - NB) * a.npad + r;
+#pragma unroll
+        for (int k = NB; k < NS; ++k) s[k] += p[static_cast<size_t>(k - NB) * a.npad];
+      }
     }
     if constexpr (GRAD) s[5] *= a.tr_r2_scale;  // kSym: sum of e * (-cxL) r^2
     const double sB = s[0];
@@ -1297,10 +1452,11 @@ __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict
 }  // namespace
 
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
-                              double4* box, unsigned long long* bad, cudaStream_t stream) {
+                              double4* box, double2* trange, unsigned long long* bad,
+                              cudaStream_t stream) {
   const int64_t ntiles = (n + kTS - 1) / kTS;
-  tile_box_kernel<<<static_cast<unsigned>((ntiles + 7) / 8), 256, 0, stream>>>(x, y, t, n, npad,
-                                                                                box, bad);
+  tile_box_kernel<<<static_cast<unsigned>((ntiles + 7) / 8), 256, 0, stream>>>(
+      x, y, t, n, npad, box, trange, bad);
   return cudaGetLastError();
 }
 
@@ -1365,6 +1521,19 @@ cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* o
                              cudaStream_t stream) {
   final_sum_kernel<<<1, 256, 0, stream>>>(block_partial, nblocks, out);
   return cudaGetLastError();
+}
+
+cudaError_t launch_far(const PairArgs& a, bool grad, int grid, cudaStream_t stream) {
+  if (grad) far_kernel<true><<<grid, kTM, 0, stream>>>(a);
+  else far_kernel<false><<<grid, kTM, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+int far_kernel_occupancy(bool grad) {
+  int occ = 0;
+  if (grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, far_kernel<true>, kTM, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, far_kernel<false>, kTM, 0);
+  return occ > 0 ? occ : 1;
 }
 
 int pair_kernel_occupancy(bool grad, int mode) {

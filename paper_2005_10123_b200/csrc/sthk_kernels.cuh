@@ -71,6 +71,14 @@ struct PlanArgs {
   int2* items;          // (row tile, chunk) work list
   int* n_items;         // device scalar
   int* work_counter;    // device scalar, reset here
+  // far tier (kSym): sources earlier than t_tile_first - tfar (whole
+  // 128-stages) go to a second list for the FP32 far kernel; tfar <= 0: off
+  double tfar;
+  int2* ranges_far;     // [ntiles] far source range [lo, fb)
+  int2* crange_far;     // [ntiles] far chunk range (empty: y < x)
+  int2* items_far;
+  int* n_items_far;
+  int* work_counter_far;
 };
 
 // Background sums (k = 0..2: S_B, S_Br, S_Bt) are fixed point,
@@ -88,6 +96,7 @@ struct PairArgs {
   const float* tf;
   int far_on;               // far tier enabled for this evaluation
   const double4* tile_box;  // per 128-event tile: xmin, xmax, ymin, ymax
+  const double2* tile_trange;  // per 128-event tile: t first, t last
   int64_t n;
   int64_t npad;
   PairConsts k;
@@ -120,6 +129,8 @@ struct FinArgs {
   const double* tpart;
   double tr_r2_scale;   // 1 (kRows) or 1/sx^2 (kSym: trigger r^2 sums on scaled coordinates)
   const int2* crange;
+  const double* tpart_far;  // far kernel's trigger partials (same layout), chunks crange_far
+  const int2* crange_far;
   double* per_event;    // nullable
   double* ex_out;       // nullable: excitation mu, xi, pi as [3][npad]
   double* block_partial;  // [ceil(n / kFB)][kNOut]
@@ -135,7 +146,8 @@ struct FinArgs {
 // runs the EventSet checks (finite, t >= 0, sorted): *bad = min(*bad, first
 // failing index) -- the caller initialises *bad to all ones.
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
-                              double4* box, unsigned long long* bad, cudaStream_t stream);
+                              double4* box, double2* trange, unsigned long long* bad,
+                              cudaStream_t stream);
 // kSym coordinates: xs, ys = (x, y) * sx; if xf: the far tier's FP32 copies
 // xf, yf = (x - x[0], y - y[0]) * sxf, tf = (t - t[tile start]) * stf.
 cudaError_t launch_scale_xy(const double* x, const double* y, const double* t, int64_t npad,
@@ -144,6 +156,10 @@ cudaError_t launch_scale_xy(const double* x, const double* y, const double* t, i
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_exp_probe(const double* x, int64_t n, double* out, cudaStream_t stream);
 cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaStream_t stream);
+// FP32 far kernel over the far work list (PairArgs' ranges / items / counters
+// / tpart point at the far list's buffers).
+cudaError_t launch_far(const PairArgs& a, bool grad, int grid, cudaStream_t stream);
+int far_kernel_occupancy(bool grad);
 cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream);
 cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,
                              cudaStream_t stream);
