@@ -156,6 +156,11 @@ int sthk_set_background_cache(sthk_engine* e, int enable);
  * is provably below -40 (terms < 4.3e-18 of the self term) run in FP32 on the
  * MUFU/FP32 pipes; 0 = every pair in FP64 (testing / accuracy comparisons). */
 int sthk_set_far_tier(sthk_engine* e, int enable);
+/* Far-tier schedule (tuning): concurrent = run the FP32 far kernel on a second
+ * stream beside the FP64 near kernel, which then uses near_ctas CTAs per SM;
+ * far_ctas far CTAs per SM are launched (extra ones start as near CTAs
+ * retire). Sequential (concurrent = 0) uses full occupancy for both. */
+int sthk_set_far_schedule(sthk_engine* e, int concurrent, int near_ctas, int far_ctas);
 
 #define STHK_KERNEL_ROWS 0
 #define STHK_KERNEL_SYM 1

@@ -81,6 +81,8 @@ struct Slot {
   double2* tile_trange = nullptr;    // per tile: t first, t last
   size_t trange_cap = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;    // far kernel, concurrent with the near sweep
+  cudaEvent_t fork = nullptr, join = nullptr;
   ncclComm_t comm = nullptr;
   double *x = nullptr, *y = nullptr, *t = nullptr;
   size_t x_cap = 0, y_cap = 0, t_cap = 0;
@@ -148,6 +150,12 @@ struct sthk_engine {
   bool timing = false, dense = false;
   int mode = sthk::kSym;   // pair-kernel variant (sthk_set_kernel)
   bool far_tier = true;    // FP32 far tier of the symmetric kernel (sthk_set_far_tier)
+  // The far kernel runs concurrently with the near (FP64) sweep on a second
+  // stream: the near kernel is limited to near_ctas CTAs per SM so that
+  // far_ctas_resident far CTAs fit beside it (FP64 and FP32/MUFU pipes busy
+  // at once); extra far CTAs queue until near CTAs retire.
+  bool far_concurrent = true;
+  int near_ctas = 2, far_ctas = 6;
   double ext_x = 0, ext_y = 0;  // max |x - x[0]|, |y - y[0]| of the loaded set
   double tile_tspan = 0;        // max time span of a 128-event tile
   // Background-sum cache: S_B (and S_Br, S_Bt) depend only on the events,
@@ -191,6 +199,9 @@ void init_slot(Slot& s, int dev) {
   set_dev(s);
   ck(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
   ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&s.stream2, cudaStreamNonBlocking), "stream");
+  ck(cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming), "event");
   for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
   ck(cudaMalloc(&s.scalars, 10 * sizeof(int)), "cudaMalloc");
   ck(cudaMemset(s.scalars, 0, 10 * sizeof(int)), "memset");
@@ -236,6 +247,10 @@ void free_slot(Slot& s) {
   for (auto& e : s.ev) {
     if (e) cudaEventDestroy(e);
   }
+  if (s.stream2) cudaStreamSynchronize(s.stream2);
+  if (s.fork) cudaEventDestroy(s.fork);
+  if (s.join) cudaEventDestroy(s.join);
+  if (s.stream2) cudaStreamDestroy(s.stream2);
   if (s.stream) cudaStreamDestroy(s.stream);
 }
 
@@ -339,9 +354,20 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   pl.k.fkt1 = 1.0 / pl.stf;
   pl.k.fkt2 = 1.0 / (pl.stf * pl.stf);
   pl.k.fstf = pl.stf;
-  // far split: sources earlier than t_tile_first - tfar have every exponent
-  // below -kFarExponent (background: dt^2 / 2 tauT^2 >= A; trigger: omega dt >= A)
-  pl.tfar = std::max(p[2] * std::sqrt(2.0 * kFarExponent), kFarExponent / p[4]) * (1.0 + 1e-9);
+  // far split: sources earlier than t_tile_first - tfar have every
+  // background exponent below -A (dt^2 / 2 tauT^2 >= A) and every trigger
+  // term below e^-A relative to the row's background self term: the trigger
+  // enters lambda with weight trNorm against mu0 bgNorm for the background,
+  // so its cut is omega dt >= A + ln(trNorm / (mu0 bgNorm)) when that ratio
+  // exceeds 1 (far-tier error bound).
+  {
+    const double kPi_ = 3.14159265358979323846;
+    const double cB = p[0] * std::pow(2.0 * kPi_, -1.5) / (p[1] * p[1] * p[2]);
+    const double cT = p[3] * p[4] / (2.0 * kPi_ * p[5] * p[5]);
+    const double boost = cT > cB ? std::log(cT / cB) : 0.0;
+    pl.tfar = std::max(p[2] * std::sqrt(2.0 * kFarExponent), (kFarExponent + boost) / p[4]) *
+              (1.0 + 1e-9);
+  }
   pl.k.nomL = static_cast<double>(-L * p[4]);
   const double inf = std::numeric_limits<double>::infinity();
   pl.k.dB = e.dense ? inf : dB;
@@ -568,10 +594,11 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     qa.pair_counts = e.timing ? s.pair_counts : nullptr;
     // a trigger-only sweep runs the same kernel with the background switched
     // off, so its trigger partials are summed exactly as in a full sweep
-    const int grid = s.sms * s.occ[e.mode][grad ? 1 : 0];
+    const int occ = s.occ[e.mode][grad ? 1 : 0];
+    const bool conc = far_on && e.far_concurrent;
+    const int grid = s.sms * (conc ? std::min(e.near_ctas, occ) : occ);
     if (e.timing && first_run) ck(cudaEventRecord(s.ev[1], st), "event");
-    ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
-    if (far_on) {  // the far work list in FP32 (same stream, after the near sweep)
+    if (far_on) {  // the far work list in FP32
       sthk::PairArgs fa_ = qa;
       fa_.ranges = s.ranges_far;
       fa_.items = s.items_far;
@@ -579,7 +606,19 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       fa_.work_counter = s.scalars + 7;
       fa_.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 8);
       fa_.tpart = s.tpart_far;
-      ck(sthk::launch_far(fa_, grad, s.sms * s.occ_far[grad ? 1 : 0], st), "far kernel");
+      if (conc) {  // forked onto the second stream, joined before finalize
+        ck(cudaEventRecord(s.fork, st), "event");
+        ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
+        ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
+        ck(cudaEventRecord(s.join, s.stream2), "event");
+        ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
+        ck(cudaStreamWaitEvent(st, s.join, 0), "wait");
+      } else {
+        ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
+        ck(sthk::launch_far(fa_, grad, s.sms * s.occ_far[grad ? 1 : 0], st), "far kernel");
+      }
+    } else {
+      ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
     }
     if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
   }
@@ -1095,6 +1134,15 @@ int sthk_set_background_cache(sthk_engine* e, int enable) {
       e->tr_cache_valid = false;
       for (Slot& s : e->slots) s.plan_valid = false;
     }
+  });
+}
+
+int sthk_set_far_schedule(sthk_engine* e, int concurrent, int near_ctas, int far_ctas) {
+  return guarded(e, [&] {
+    if (near_ctas < 1 || far_ctas < 1) throw InvalidArg("sthk_set_far_schedule: CTA counts must be >= 1");
+    e->far_concurrent = concurrent != 0;
+    e->near_ctas = near_ctas;
+    e->far_ctas = far_ctas;
   });
 }
 

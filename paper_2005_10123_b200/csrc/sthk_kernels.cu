@@ -1032,7 +1032,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
 // row) buffer (tpart_far), summed by finalize after the near ones.
 // ---------------------------------------------------------------------------
 #ifndef STHK_FAR_MINB
-#define STHK_FAR_MINB 4
+#define STHK_FAR_MINB 6
 #endif
 
 template <bool GRAD>

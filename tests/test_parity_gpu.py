@@ -421,3 +421,28 @@ def test_far_tier_guard_off_for_extreme_coordinates(engine):
         engine.set_timing(False)
         o = og.oracle_loglik_grad(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), p.as_array())
         assert abs(r[0] - o["loglik"]) <= 1e-10 * abs(o["loglik"])
+
+
+def test_far_schedule_bitwise_invariant(engine):
+    """The near (FP64) and far (FP32) kernels write disjoint trigger partials and
+    add background sums as integers: concurrent or sequential schedules, any CTA
+    counts, give bitwise-identical results."""
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=20000)
+    engine.load(ev)
+    engine.set_background_cache(False)
+    try:
+        res = []
+        for sched in ((True, 2, 6), (False, 2, 6), (True, 1, 3), (True, 3, 1)):
+            engine.set_far_schedule(*sched)
+            for theta in ([0.66, 1.6, 14, 0.344, 1440, 0.0695], [1, 1.6, 14, 0.1, 1, 1]):
+                engine.set_params(theta)
+                r = engine.loglik_grad()
+                res.append((sched, theta[4], r[0], tuple(r[2])))
+        base = {om: (ll, g) for s, om, ll, g in res if s == (True, 2, 6)}
+        for s, om, ll, g in res:
+            assert (ll, g) == base[om], s
+    finally:
+        engine.set_far_schedule(True, 2, 6)
+        engine.set_background_cache(True)

@@ -16,6 +16,9 @@ e.load(ev)
 e.set_timing(True)
 e.set_background_cache(bool(int(os.environ.get("QP_CACHE", "0"))))
 e._lib.sthk_set_far_tier(e._h, int(os.environ.get("QP_FAR", "1")))
+if "QP_SCHED" in os.environ:  # concurrent,near_ctas,far_ctas
+    c, nc, fc = (int(v) for v in os.environ["QP_SCHED"].split(","))
+    e._lib.sthk_set_far_schedule(e._h, c, nc, fc)
 modes = [int(m) for m in os.environ.get("QP_MODES", "0,1").split(",")]
 denses = [bool(int(d)) for d in os.environ.get("QP_DENSE", "0,1").split(",")]
 for name, p in [("post", [0.66, 1.6, 14, 0.344, 1440, 0.0695]), ("init", [1, 1.6, 14, 0.1, 1, 1])]:
