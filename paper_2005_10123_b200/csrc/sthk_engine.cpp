@@ -448,8 +448,13 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
                          e.tr_cache_h == e.p[5] && e.tr_cache_grad == grad;  // (tpart layout)
   e.last_cache_hit = cached;
   e.last_tr_cache_hit = tr_cached;
+  // (a far list that is provably empty -- every live source within tfar of
+  // its tile, e.g. a trigger-only sweep at large omega -- is not planned or
+  // launched; results are the same either way)
+  const double live_window = cached ? pl.k.dT : std::max(pl.k.dB, pl.k.dT);
   const bool far_on = sym && e.far_tier && e.ext_x * pl.sxf <= kFarCoordMax &&
-                      e.ext_y * pl.sxf <= kFarCoordMax && e.tile_tspan * pl.stf <= kFarCoordMax;
+                      e.ext_y * pl.sxf <= kFarCoordMax && e.tile_tspan * pl.stf <= kFarCoordMax &&
+                      !(live_window <= pl.tfar);
   e.cache_valid = false;  // re-armed below once the sweep is enqueued
   e.tr_cache_valid = false;
   const int64_t ntiles_total = (e.n + kTM - 1) / kTM;
