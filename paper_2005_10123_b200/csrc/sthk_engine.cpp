@@ -155,6 +155,7 @@ struct sthk_engine {
   // far_ctas_resident far CTAs fit beside it (FP64 and FP32/MUFU pipes busy
   // at once); extra far CTAs queue until near CTAs retire.
   bool far_concurrent = true;
+  int far_order = 1;  // 1: far launched first, 2: near first
   int near_ctas = 2, far_ctas = 6;
   double ext_x = 0, ext_y = 0;  // max |x - x[0]|, |y - y[0]| of the loaded set
   double tile_tspan = 0;        // max time span of a 128-event tile
@@ -614,9 +615,14 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       if (conc) {  // forked onto the second stream, joined before finalize
         ck(cudaEventRecord(s.fork, st), "event");
         ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
-        ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
+        if (e.far_order == 2) {  // near first: its CTAs are resident before far CTAs fill in
+          ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
+          ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
+        } else {
+          ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
+          ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
+        }
         ck(cudaEventRecord(s.join, s.stream2), "event");
-        ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
         ck(cudaStreamWaitEvent(st, s.join, 0), "wait");
       } else {
         ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
@@ -1146,6 +1152,7 @@ int sthk_set_far_schedule(sthk_engine* e, int concurrent, int near_ctas, int far
   return guarded(e, [&] {
     if (near_ctas < 1 || far_ctas < 1) throw InvalidArg("sthk_set_far_schedule: CTA counts must be >= 1");
     e->far_concurrent = concurrent != 0;
+    e->far_order = concurrent == 2 ? 2 : 1;
     e->near_ctas = near_ctas;
     e->far_ctas = far_ctas;
   });
