@@ -81,6 +81,47 @@ __device__ __forceinline__ int64_t bound_t(const double* t, int64_t n, double v,
   return lo;
 }
 
+// Three independent bound_t searches in lockstep: each level issues the
+// three dependent global loads back to back, so their latencies overlap
+// (the plan's cost is these load chains).
+__device__ __forceinline__ void bounds3(const double* t, int64_t n, const Pivots& p,
+                                        const double (&v)[3], const bool (&strict)[3],
+                                        int64_t (&out)[3]) {
+  int64_t lo[3], hi[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    int klo = 0, khi = p.np;
+    while (klo < khi) {
+      const int mid = (klo + khi) >> 1;
+      const double pv = p.piv[mid];
+      if (strict[k] ? pv < v[k] : pv <= v[k]) klo = mid + 1; else khi = mid;
+    }
+    if (klo == 0) {
+      lo[k] = hi[k] = 0;
+    } else {
+      lo[k] = static_cast<int64_t>(klo - 1) * p.stride + 1;
+      hi[k] = min(static_cast<int64_t>(klo) * p.stride, n);
+    }
+  }
+  while (lo[0] < hi[0] || lo[1] < hi[1] || lo[2] < hi[2]) {
+    int64_t mid[3];
+    double tv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      mid[k] = (lo[k] + hi[k]) >> 1;
+      tv[k] = lo[k] < hi[k] ? t[mid[k]] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (lo[k] < hi[k]) {
+        if (strict[k] ? tv[k] < v[k] : tv[k] <= v[k]) lo[k] = mid[k] + 1; else hi[k] = mid[k];
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) out[k] = lo[k];
+}
+
 // ---------------------------------------------------------------------------
 // Plan
 // ---------------------------------------------------------------------------
@@ -89,21 +130,24 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
                                           int2& cr, int2& rgf, int2& crf) {
   const int64_t first = static_cast<int64_t>(tile) * kTM;
   const int64_t last = min(first + kTM, a.n) - 1;
+  const double tmin = a.t[first], tmax = a.t[last];
+  // searches: live-range start, live-range end (full sweeps), far split
+  double v[3] = {a.trig_only ? tmin - a.dT : tmin - fmax(a.dB, a.dT), tmax + a.dB,
+                 tmin - a.tfar};
+  const bool strict[3] = {true, false, true};
+  int64_t b[3];
+  bounds3(a.t, a.n, pv, v, strict, b);
   int lo, hi;
   if (a.dense) {
     lo = 0;
     hi = static_cast<int>(a.n);
   } else if (a.trig_only) {
-    lo = min(static_cast<int>(bound_t<true>(a.t, a.n, a.t[first] - a.dT, pv)),
-             static_cast<int>(first));
+    lo = min(static_cast<int>(b[0]), static_cast<int>(first));
     hi = static_cast<int>(last + 1);
   } else {
-    const double tmin = a.t[first], tmax = a.t[last];
-    lo = static_cast<int>(bound_t<true>(a.t, a.n, tmin - fmax(a.dB, a.dT), pv));
-    hi = static_cast<int>(bound_t<false>(a.t, a.n, tmax + a.dB, pv));
     // the tile's own rows are always live (background self term)
-    lo = min(lo, static_cast<int>(first));
-    hi = max(hi, static_cast<int>(last + 1));
+    lo = min(static_cast<int>(b[0]), static_cast<int>(first));
+    hi = max(static_cast<int>(b[1]), static_cast<int>(last + 1));
   }
   // symmetric mode: later tiles reach this one through their column sums
   if (a.sym || a.trig_only) hi = static_cast<int>(last + 1);
@@ -111,8 +155,8 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
   // (every term below e^-A) go to the far list; the rest stay near
   int fb = lo;
   if (a.tfar > 0.0 && last + 1 - first == kTM) {  // (full row tiles only)
-    const int b = static_cast<int>(bound_t<true>(a.t, a.n, a.t[first] - a.tfar, pv));
-    fb = max(lo, b - b % kTS);
+    const int bb = static_cast<int>(b[2]);
+    fb = max(lo, bb - bb % kTS);
   }
   rg = make_int2(fb, hi);
   cr = make_int2(fb / a.sc, (hi - 1) / a.sc);
