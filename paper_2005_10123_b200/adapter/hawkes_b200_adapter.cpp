@@ -68,6 +68,9 @@ struct AdapterEngine {
     if (sthk_create(devs.data(), static_cast<int>(devs.size()), &h) != STHK_OK) {
       throw std::runtime_error(std::string("sthk_create: ") + sthk_last_error(nullptr));
     }
+    // STHK_SWEEP_CACHE=0: every call a full evaluation (timing harnesses)
+    const char* sc = std::getenv("STHK_SWEEP_CACHE");
+    if (sc && *sc == '0') sthk_set_background_cache(h, 0);
   }
   ~AdapterEngine() {
     if (h) sthk_destroy(h);

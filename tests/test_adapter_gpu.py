@@ -55,3 +55,15 @@ def test_mh_chain_matches_reference_cpu_chain():
     assert gpu["accepted"] == cpu["accepted"] and gpu["proposed"] == cpu["proposed"]
     assert gpu["draws_fnv1a"] == cpu["draws_fnv1a"]
     assert abs(gpu["final_logpost"] - cpu["final_logpost"]) <= 1e-10 * abs(cpu["final_logpost"])
+
+
+def test_reference_timing_harness_on_b200():
+    """The reference's timeLikelihood (bench.cpp, verbatim; it fails hard on any
+    drift between repeats) over the adapter, full evaluations, C2 at N=20k."""
+    exe = _exe("timing_b200")
+    env = dict(os.environ, STHK_SWEEP_CACHE="0")
+    out = subprocess.run([exe, "--n", "20000", "--repeats", "5", "--warmups", "1"],
+                         capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    rec = json.loads(out.stdout.strip().splitlines()[-1])
+    assert rec["impl"] == "b200" and rec["n"] == 20000 and rec["median_s"] > 0
