@@ -131,7 +131,7 @@ struct Slot {
   bool plan_valid = false;
   double plan_dB = 0, plan_dT = 0;
   int plan_key[6] = {0, 0, 0, 0, 0, 0};  // tile0, tile1, sc, dense, sym, trig_only
-  double plan_tfar = 0;
+  double plan_tfar = 0, plan_dfar = 0;
   std::vector<std::pair<int, int>> runs;  // row ranges run on this slot
 };
 
@@ -369,10 +369,24 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
     pl.tfar = std::max(p[2] * std::sqrt(2.0 * kFarExponent), (kFarExponent + boost) / p[4]) *
               (1.0 + 1e-9);
   }
+
   pl.k.nomL = static_cast<double>(-L * p[4]);
   const double inf = std::numeric_limits<double>::infinity();
   pl.k.dB = e.dense ? inf : dB;
   pl.k.dT = e.dense ? inf : dT;
+  // far-tier exact cull: ex2.approx.ftz returns +0 below 2^-126, i.e. for
+  // natural exponents below -126 ln2 = -87.34; with a margin of 1 (FP32
+  // exponent error << 1) every pair beyond these windows is exactly 0 in the
+  // far kernel, so skipping it leaves every sum bitwise unchanged
+  {
+    const double zf = 126.0 * 0.693147180559945309417232121458176568 + 1.0;
+    pl.k.dBf = e.dense ? std::numeric_limits<double>::infinity()
+                       : p[2] * std::sqrt(2.0 * zf) * (1.0 + 1e-9);
+    pl.k.dTf = e.dense ? std::numeric_limits<double>::infinity() : zf / p[4] * (1.0 + 1e-9);
+    // (never beyond the FP64 culling windows)
+    pl.k.dBf = std::min(pl.k.dBf, pl.k.dB);
+    pl.k.dTf = std::min(pl.k.dTf, pl.k.dT);
+  }
 
   // Chunk size: a function of N only (never of the parameters, the device
   // count or the culling mode). Partial sums are grouped per (tile, chunk), so
@@ -551,6 +565,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     pa.n_items = s.scalars;
     pa.work_counter = s.scalars + 1;
     pa.tfar = far_on ? pl.tfar : 0.0;
+    // far list start: the far tier's cull window (trigger-only sweeps: trigger only)
+    pa.dFar = cached ? pl.k.dTf : std::max(pl.k.dBf, pl.k.dTf);
     if (far_on) {
       pa.ranges_far = s.ranges_far;
       pa.crange_far = s.crange_far;
@@ -560,7 +576,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     }
     const int key[6] = {tile0, tile1, pl.sc, pa.dense, pa.sym, pa.trig_only};
     const bool plan_hit = e.bg_cache && !vshards && s.plan_valid && s.plan_dB == pa.dB &&
-                          s.plan_dT == pa.dT && s.plan_tfar == pa.tfar &&
+                          s.plan_dT == pa.dT && s.plan_tfar == pa.tfar && s.plan_dfar == pa.dFar &&
                           std::equal(key, key + 6, s.plan_key);
     if (!plan_hit) {  // (the work counters are re-armed by the last pair CTAs)
       ck(sthk::launch_plan(pa, st), "plan");
@@ -568,6 +584,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       s.plan_dB = pa.dB;
       s.plan_dT = pa.dT;
       s.plan_tfar = pa.tfar;
+      s.plan_dfar = pa.dFar;
       std::copy(key, key + 6, s.plan_key);
     }
 

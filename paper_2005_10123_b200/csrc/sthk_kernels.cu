@@ -131,9 +131,10 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
   const int64_t first = static_cast<int64_t>(tile) * kTM;
   const int64_t last = min(first + kTM, a.n) - 1;
   const double tmin = a.t[first], tmax = a.t[last];
-  // searches: live-range start, live-range end (full sweeps), far split
-  double v[3] = {a.trig_only ? tmin - a.dT : tmin - fmax(a.dB, a.dT), tmax + a.dB,
-                 tmin - a.tfar};
+  // searches: live-range start, live-range end (full row-kernel sweeps) or,
+  // in symmetric mode, the far tier's exact-cull start, and the far split
+  double v[3] = {a.trig_only ? tmin - a.dT : tmin - fmax(a.dB, a.dT),
+                 a.sym ? tmin - a.dFar : tmax + a.dB, tmin - a.tfar};
   const bool strict[3] = {true, false, true};
   int64_t b[3];
   bounds3(a.t, a.n, pv, v, strict, b);
@@ -147,21 +148,24 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
   } else {
     // the tile's own rows are always live (background self term)
     lo = min(static_cast<int>(b[0]), static_cast<int>(first));
-    hi = max(static_cast<int>(b[1]), static_cast<int>(last + 1));
+    hi = a.sym ? static_cast<int>(last + 1)
+               : max(static_cast<int>(b[1]), static_cast<int>(last + 1));
   }
   // symmetric mode: later tiles reach this one through their column sums
   if (a.sym || a.trig_only) hi = static_cast<int>(last + 1);
   // far split: whole 128-stages of sources earlier than t[first] - tfar
   // (every term below e^-A) go to the far list; the rest stay near
-  int fb = lo;
+  int fb = lo, flo = lo;
   if (a.tfar > 0.0 && last + 1 - first == kTM) {  // (full row tiles only)
     const int bb = static_cast<int>(b[2]);
     fb = max(lo, bb - bb % kTS);
+    // far sources before t[first] - dFar are exactly 0 in FP32: culled
+    if (!a.dense) flo = min(max(lo, static_cast<int>(b[1])), fb);
   }
   rg = make_int2(fb, hi);
   cr = make_int2(fb / a.sc, (hi - 1) / a.sc);
-  rgf = make_int2(lo, fb);
-  crf = fb > lo ? make_int2(lo / a.sc, (fb - 1) / a.sc) : make_int2(0, -1);
+  rgf = make_int2(flo, fb);
+  crf = fb > flo ? make_int2(flo / a.sc, (fb - 1) / a.sc) : make_int2(0, -1);
 }
 
 // Number of 128-source stages of work item (tile, chunk) -- the same bounds
@@ -1166,8 +1170,9 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
       mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
       phase ^= 1u << buf;
       const double smin = s_tr[buf].x, smax = s_tr[buf].y;
-      const bool bg = !a.bg_off && !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
-      const bool trg = !(smin >= tmax || smax < tmin - a.k.dT);  // (all sources earlier)
+      // live in FP32 (the far tier's exact cull; all sources strictly earlier)
+      const bool bg = !a.bg_off && !(smin > tmax + a.k.dBf || smax < tmin - a.k.dBf);
+      const bool trg = !(smin >= tmax || smax < tmin - a.k.dTf);
       // row times re-based onto the source tile's origin (tf is tile-relative)
       const float dtile = static_cast<float>((tmin - smin) * a.k.fstf);
       const f2 dd = pk2(dtile, dtile);

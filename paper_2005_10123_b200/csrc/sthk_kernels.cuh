@@ -54,6 +54,8 @@ struct PairConsts {
   double fkt1;  // dtf -> dt (days)
   double fkt2;  // dtf^2 -> dt^2
   double fstf;  // time scale of tf (tf = (t - t_tile0) * fstf)
+  double dBf;   // far tier: background nonzero in FP32 iff |dt| <= dBf (exact cull)
+  double dTf;   // far tier: trigger nonzero in FP32 iff dt <= dTf
 };
 
 struct PlanArgs {
@@ -74,6 +76,9 @@ struct PlanArgs {
   // far tier (kSym): sources earlier than t_tile_first - tfar (whole
   // 128-stages) go to a second list for the FP32 far kernel; tfar <= 0: off
   double tfar;
+  // far-tier exact cull: the FP32 ex2 flushes to +0 below 2^-126, so far
+  // sources earlier than t_tile_first - dFar contribute exactly 0 (+inf: dense)
+  double dFar;
   int2* ranges_far;     // [ntiles] far source range [lo, fb)
   int2* crange_far;     // [ntiles] far chunk range (empty: y < x)
   int2* items_far;
