@@ -156,7 +156,7 @@ struct sthk_engine {
   // at once); extra far CTAs queue until near CTAs retire.
   bool far_concurrent = true;
   int far_order = 1;  // 1: far launched first, 2: near first
-  int near_ctas = 2, far_ctas = 6;
+  int near_ctas = 3, far_ctas = 6;
   double ext_x = 0, ext_y = 0;  // max |x - x[0]|, |y - y[0]| of the loaded set
   double tile_tspan = 0;        // max time span of a 128-event tile
   // Background-sum cache: S_B (and S_Br, S_Bt) depend only on the events,

@@ -180,7 +180,7 @@ class Engine:
         """FP32 far tier of the symmetric kernel (default on; include/sthk.h)."""
         self._check(self._lib.sthk_set_far_tier(self._h, int(on)), "sthk_set_far_tier")
 
-    def set_far_schedule(self, concurrent: bool, near_ctas: int = 2, far_ctas: int = 6) -> None:
+    def set_far_schedule(self, concurrent: bool, near_ctas: int = 3, far_ctas: int = 6) -> None:
         self._check(self._lib.sthk_set_far_schedule(self._h, int(concurrent), near_ctas, far_ctas),
                     "sthk_set_far_schedule")
 
