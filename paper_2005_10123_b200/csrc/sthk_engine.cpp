@@ -348,7 +348,6 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   const double kLn2 = 0.693147180559945309417232121458176568;
   pl.sxf = 1.0 / (p[1] * std::sqrt(2.0 * kLn2));
   pl.stf = 1.0 / (p[2] * std::sqrt(2.0 * kLn2));
-  pl.k.farL = -kFarExponent * static_cast<double>(L);
   pl.k.fc1 = static_cast<float>(-p[4] / (pl.stf * kLn2));
   pl.k.fc2 = static_cast<float>(-(p[1] * p[1]) / (p[5] * p[5]));
   pl.k.fkr = pl.sx * pl.sx * 2.0 * p[1] * p[1] * kLn2;
@@ -597,7 +596,6 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     qa.xf = s.xf;
     qa.yf = s.yf;
     qa.tf = s.tf;
-    qa.far_on = far_on ? 1 : 0;
     qa.tile_box = s.tile_box;
     qa.tile_trange = s.tile_trange;
     qa.n = e.n;

@@ -45,9 +45,7 @@ struct PairConsts {
   double nomL;  // -L omega
   double dB;    // background live iff |dt| <= dB   (inf when dense)
   double dT;    // trigger live iff 0 < dt <= dT    (inf when dense)
-  // far tier (kSym, FP32): a stage is far when every exponent on its box
-  // bounds is below farL (L units); FP32 coordinates xf, yf, tf (log2 units)
-  double farL;  // -A * kExpL, A = 40; +inf... disables (0 when off)
+  // far tier (kSym, FP32 far_kernel): coordinates xf, yf, tf in log2 units
   float fc1;    // trigger exponent, log2 units: fc1 * dtf + fc2 * r2f
   float fc2;
   double fkr;   // r2f -> r2 (kSym units, -cxL r^2)
@@ -99,7 +97,6 @@ struct PairArgs {
   const float* xf;          // kSym far tier: FP32 (x - x0) sxf, (y - y0) sxf, (t - t_tile0) stf
   const float* yf;
   const float* tf;
-  int far_on;               // far tier enabled for this evaluation
   const double4* tile_box;  // per 128-event tile: xmin, xmax, ymin, ymax
   const double2* tile_trange;  // per 128-event tile: t first, t last
   int64_t n;
