@@ -446,3 +446,32 @@ def test_far_schedule_bitwise_invariant(engine):
     finally:
         engine.set_far_schedule(True, 3, 6)
         engine.set_background_cache(True)
+
+
+def _clustered_events(rng, n, t_end, tau_hot=0.5):
+    """Bursty synthetic set: a Poisson background plus tight space-time bursts."""
+    k = max(1, n // 20)
+    cx, cy, ct = rng.uniform(0, 10, k), rng.uniform(0, 10, k), rng.uniform(0, t_end, k)
+    pick = rng.integers(0, k, n // 2)
+    x = np.concatenate([rng.uniform(0, 10, n - n // 2), cx[pick] + 0.05 * rng.standard_normal(n // 2)])
+    y = np.concatenate([rng.uniform(0, 10, n - n // 2), cy[pick] + 0.05 * rng.standard_normal(n // 2)])
+    t = np.concatenate([rng.uniform(0, t_end, n - n // 2),
+                        np.clip(ct[pick] + tau_hot * rng.exponential(1.0, n // 2), 0, t_end)])
+    return pk.EventSet.sortedByTime(x, y, t)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_regimes_vs_oracle(engine, seed):
+    """Fuzz across parameter regimes (small / large tauT, omega from 0.05 to 5000,
+    theta up to 0.95, tiny h) and bursty data: the full engine (far tier, caches,
+    both kernels' stage modes) against the long-double oracle at the north-star
+    tolerances."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(1500, 6000))
+    ev = _clustered_events(rng, n, float(rng.choice([50.0, 500.0, 3000.0])))
+    p = pk.Params(float(rng.uniform(0.05, 3.0)), float(rng.uniform(0.2, 3.0)),
+                  float(np.exp(rng.uniform(np.log(0.5), np.log(60.0)))),
+                  float(rng.uniform(0.0, 0.95)),
+                  float(np.exp(rng.uniform(np.log(0.05), np.log(5000.0)))),
+                  float(np.exp(rng.uniform(np.log(0.01), np.log(2.0)))))
+    _check(engine, ev, p)
