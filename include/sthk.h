@@ -156,6 +156,11 @@ int sthk_set_background_cache(sthk_engine* e, int enable);
  * is provably below -40 (terms < 4.3e-18 of the self term) run in FP32 on the
  * MUFU/FP32 pipes; 0 = every pair in FP64 (testing / accuracy comparisons). */
 int sthk_set_far_tier(sthk_engine* e, int enable);
+/* Trigger-free near kernel (default on): in full symmetric sweeps whose
+ * trigger window dT is narrower than the near band, near stages of sources
+ * earlier than t_tile_first - dT run in a variant without trigger code paths
+ * (fewer registers, more resident warps). 0 = one near kernel for all. */
+int sthk_set_bgonly_kernel(sthk_engine* e, int enable);
 /* Far-tier schedule (tuning): concurrent = run the FP32 far kernel on a second
  * stream beside the FP64 near kernel, which then uses near_ctas CTAs per SM;
  * far_ctas far CTAs per SM are launched (extra ones start as near CTAs

@@ -69,6 +69,7 @@ SIGNATURES = [
     ("sthk_set_virtual_shards", c_int, [c_void_p, c_int]),
     ("sthk_set_kernel", c_int, [c_void_p, c_int]),
     ("sthk_set_far_tier", c_int, [c_void_p, c_int]),
+    ("sthk_set_bgonly_kernel", c_int, [c_void_p, c_int]),
     ("sthk_set_far_schedule", c_int, [c_void_p, c_int, c_int, c_int]),
     ("sthk_set_background_cache", c_int, [c_void_p, c_int]),
     ("sthk_measure_fp64_peak", c_int, [c_int, c_int, _DPTR, _DPTR]),

@@ -74,6 +74,9 @@ struct Slot {
   int sms = 148;
   int occ[2][2] = {{1, 1}, {1, 1}};  // [mode][grad]
   int occ_far[2] = {1, 1};           // far kernel [grad]
+  int occ_bg[2] = {1, 1};            // trigger-free near kernel [grad]
+  int2 *ranges_bg = nullptr, *crange_bg = nullptr, *items_bg = nullptr;
+  size_t ranges_bg_cap = 0, crange_bg_cap = 0, items_bg_cap = 0;
   int2 *ranges_far = nullptr, *crange_far = nullptr, *items_far = nullptr;
   size_t ranges_far_cap = 0, crange_far_cap = 0, items_far_cap = 0;
   double* tpart_far = nullptr;       // far kernel trigger partials [nchunks][3][npad]
@@ -102,7 +105,8 @@ struct Slot {
   size_t items_cap = 0;
   int* scalars = nullptr;  // [0] n_items, [1] work counter, [2] pair CTAs done, [3] finalize
                            // blocks done, [4..5] first invalid event index (uint64),
-                           // [6] far n_items, [7] far work counter, [8] far CTAs done
+                           // [6] far n_items, [7] far work counter, [8] far CTAs done,
+                           // [9] bg-only n_items, [10] its work counter, [11] its CTAs done
   unsigned long long* h_bad = nullptr;  // pinned
   unsigned long long* fx = nullptr;  // fixed-point background sums [6][npad]
   size_t fx_cap = 0;
@@ -130,7 +134,7 @@ struct Slot {
   // is a function of (times, culling windows, mode, rows, chunking) only
   bool plan_valid = false;
   double plan_dB = 0, plan_dT = 0;
-  int plan_key[6] = {0, 0, 0, 0, 0, 0};  // tile0, tile1, sc, dense, sym, trig_only
+  int plan_key[7] = {0, 0, 0, 0, 0, 0, 0};  // tile0, tile1, sc, dense, sym, trig_only, bg split
   double plan_tfar = 0, plan_dfar = 0;
   std::vector<std::pair<int, int>> runs;  // row ranges run on this slot
 };
@@ -150,6 +154,7 @@ struct sthk_engine {
   bool timing = false, dense = false;
   int mode = sthk::kSym;   // pair-kernel variant (sthk_set_kernel)
   bool far_tier = true;    // FP32 far tier of the symmetric kernel (sthk_set_far_tier)
+  bool bg_split = true;    // trigger-free near kernel for stages beyond the trigger window
   // The far kernel runs concurrently with the near (FP64) sweep on a second
   // stream: the near kernel is limited to near_ctas CTAs per SM so that
   // far_ctas_resident far CTAs fit beside it (FP64 and FP32/MUFU pipes busy
@@ -159,6 +164,10 @@ struct sthk_engine {
   int near_ctas = 3, far_ctas = 6;
   double ext_x = 0, ext_y = 0;  // max |x - x[0]|, |y - y[0]| of the loaded set
   double tile_tspan = 0;        // max time span of a 128-event tile
+  // adj_gap[k-1]: min over tiles of t[first] - t[first - 128k - 1], the time
+  // from a tile's first event back to the last source before its k preceding
+  // stages (the trigger-free split keeps those k stages with the tile)
+  std::vector<double> adj_gap;
   // Background-sum cache: S_B (and S_Br, S_Bt) depend only on the events,
   // tauX, tauT -- fixed for a whole MH chain (sampler.cpp:48-49) -- so while
   // they are unchanged an evaluation sweeps only the trigger band. The
@@ -174,7 +183,9 @@ struct sthk_engine {
   double cache_tx = 0, cache_tt = 0;
   int cache_mode = -1;
   bool cache_dense = false;
-  bool cache_far = true;
+  bool cache_far_full = false;
+  double cache_tfar = 0.0;
+  int cache_bg_adj = 0;
   int virtual_shards = 1;  // testing: partition rows over k shards on one device
   std::string err;
   bool pending = false, last_grad = false, last_pe = false, last_ex = false;
@@ -192,6 +203,7 @@ constexpr int kChunksTarget = 48;  // source chunks across N (work-item granular
 // i.e. < 1% of a term below 4.3e-18.
 constexpr double kFarExponent = 40.0;
 constexpr double kFarCoordMax = 4096.0;
+constexpr int kMaxAdj = 16;  // trigger-free split: at most 16 stages kept with the tile
 
 void set_dev(const Slot& s) { ck(cudaSetDevice(s.dev), "cudaSetDevice"); }
 
@@ -204,8 +216,8 @@ void init_slot(Slot& s, int dev) {
   ck(cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming), "event");
   for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
-  ck(cudaMalloc(&s.scalars, 10 * sizeof(int)), "cudaMalloc");
-  ck(cudaMemset(s.scalars, 0, 10 * sizeof(int)), "memset");
+  ck(cudaMalloc(&s.scalars, 12 * sizeof(int)), "cudaMalloc");
+  ck(cudaMemset(s.scalars, 0, 12 * sizeof(int)), "memset");
   ck(cudaMallocHost(&s.h_bad, sizeof(unsigned long long)), "cudaMallocHost");
   ck(cudaMalloc(&s.out, kNOut * sizeof(double)), "cudaMalloc");
   ck(cudaMalloc(&s.pair_counts, sthk::kNCounts * sizeof(unsigned long long)), "cudaMalloc");
@@ -217,6 +229,8 @@ void init_slot(Slot& s, int dev) {
     s.occ[m][0] = sthk::pair_kernel_occupancy(false, m);
     s.occ_far[1] = sthk::far_kernel_occupancy(true);
     s.occ_far[0] = sthk::far_kernel_occupancy(false);
+    s.occ_bg[1] = sthk::bgonly_kernel_occupancy(true);
+    s.occ_bg[0] = sthk::bgonly_kernel_occupancy(false);
   }
   ck(cudaGetLastError(), "occupancy");
 }
@@ -231,6 +245,8 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.ranges_far), static_cast<void*>(s.crange_far),
                   static_cast<void*>(s.items_far), static_cast<void*>(s.tpart_far),
                   static_cast<void*>(s.tile_trange),
+                  static_cast<void*>(s.ranges_bg), static_cast<void*>(s.crange_bg),
+                  static_cast<void*>(s.items_bg),
                   static_cast<void*>(s.ranges), static_cast<void*>(s.counts),
                   static_cast<void*>(s.items), static_cast<void*>(s.scalars),
                   static_cast<void*>(s.fx), static_cast<void*>(s.block_partial),
@@ -455,20 +471,40 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
   }
   const EvalPlan pl = make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym}, shards);
   e.last_sc = pl.sc;
+  // Split structure of a full sweep (it fixes how the background sums are
+  // grouped, so a cached background is reused only under the same structure):
+  //  * far tier on/off and its split tfar;
+  //  * the trigger-free near split bg_adj, chosen from the physical trigger
+  //    window 709/omega -- not the dense mode's infinite one -- so dense and
+  //    culled sweeps split alike; it moves only when omega crosses a
+  //    threshold (then the background is recomputed).
+  const bool far_guard = sym && e.far_tier && e.ext_x * pl.sxf <= kFarCoordMax &&
+                         e.ext_y * pl.sxf <= kFarCoordMax && e.tile_tspan * pl.stf <= kFarCoordMax;
+  const bool far_full = far_guard && !(std::max(pl.k.dB, pl.k.dT) <= pl.tfar);
+  int bg_adj = 0;
+  if (sym && e.bg_split && !e.adj_gap.empty()) {
+    const double dT_phys = sthk::kCullExponent / e.p[4] * (1.0 + 1e-9);
+    for (int k = 1; k <= kMaxAdj; ++k) {
+      if (e.adj_gap[k - 1] > dT_phys) {
+        bg_adj = k;
+        break;
+      }
+    }
+  }
   const bool cached = e.bg_cache && e.cache_valid && e.cache_gen == e.load_gen &&
-                      e.cache_tx == e.p[1] && e.cache_tt == e.p[2] && e.cache_mode == e.mode && e.cache_far == e.far_tier &&
-                      e.cache_dense == e.dense && (e.cache_grad || !grad);
+                      e.cache_tx == e.p[1] && e.cache_tt == e.p[2] && e.cache_mode == e.mode &&
+                      e.cache_far_full == far_full && e.cache_tfar == (far_full ? pl.tfar : 0.0) &&
+                      e.cache_bg_adj == bg_adj && e.cache_dense == e.dense &&
+                      (e.cache_grad || !grad);
   const bool tr_cached = cached && e.tr_cache_valid && e.tr_cache_omega == e.p[4] &&
                          e.tr_cache_h == e.p[5] && e.tr_cache_grad == grad;  // (tpart layout)
   e.last_cache_hit = cached;
   e.last_tr_cache_hit = tr_cached;
+  const bool bg_split = !cached && bg_adj > 0;
   // (a far list that is provably empty -- every live source within tfar of
   // its tile, e.g. a trigger-only sweep at large omega -- is not planned or
   // launched; results are the same either way)
-  const double live_window = cached ? pl.k.dT : std::max(pl.k.dB, pl.k.dT);
-  const bool far_on = sym && e.far_tier && e.ext_x * pl.sxf <= kFarCoordMax &&
-                      e.ext_y * pl.sxf <= kFarCoordMax && e.tile_tspan * pl.stf <= kFarCoordMax &&
-                      !(live_window <= pl.tfar);
+  const bool far_on = far_full && !(cached && pl.k.dT <= pl.tfar);
   e.cache_valid = false;  // re-armed below once the sweep is enqueued
   e.tr_cache_valid = false;
   const int64_t ntiles_total = (e.n + kTM - 1) / kTM;
@@ -509,6 +545,11 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     dev_grow(s.fx, s.fx_cap, static_cast<size_t>(kFxRows) * e.npad);
     dev_grow(s.tpart, s.tpart_cap, static_cast<size_t>(pl.nchunks) * 3 * e.npad);
     dev_grow(s.crange, s.crange_cap, static_cast<size_t>(ntiles_total));
+    if (bg_split) {
+      dev_grow(s.ranges_bg, s.ranges_bg_cap, static_cast<size_t>(ntiles_total));
+      dev_grow(s.crange_bg, s.crange_bg_cap, static_cast<size_t>(ntiles_total));
+      dev_grow(s.items_bg, s.items_bg_cap, static_cast<size_t>(std::max(ntiles, 1)) * pl.nchunks);
+    }
     if (far_on) {
       dev_grow(s.ranges_far, s.ranges_far_cap, static_cast<size_t>(ntiles_total));
       dev_grow(s.crange_far, s.crange_far_cap, static_cast<size_t>(ntiles_total));
@@ -566,6 +607,14 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     pa.tfar = far_on ? pl.tfar : 0.0;
     // far list start: the far tier's cull window (trigger-only sweeps: trigger only)
     pa.dFar = cached ? pl.k.dTf : std::max(pl.k.dBf, pl.k.dTf);
+    if (bg_split) {
+      pa.bg_adj = bg_adj;
+      pa.ranges_bg = s.ranges_bg;
+      pa.crange_bg = s.crange_bg;
+      pa.items_bg = s.items_bg;
+      pa.n_items_bg = s.scalars + 9;
+      pa.work_counter_bg = s.scalars + 10;
+    }
     if (far_on) {
       pa.ranges_far = s.ranges_far;
       pa.crange_far = s.crange_far;
@@ -573,10 +622,10 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       pa.n_items_far = s.scalars + 6;
       pa.work_counter_far = s.scalars + 7;
     }
-    const int key[6] = {tile0, tile1, pl.sc, pa.dense, pa.sym, pa.trig_only};
+    const int key[7] = {tile0, tile1, pl.sc, pa.dense, pa.sym, pa.trig_only, bg_split ? bg_adj : 0};
     const bool plan_hit = e.bg_cache && !vshards && s.plan_valid && s.plan_dB == pa.dB &&
                           s.plan_dT == pa.dT && s.plan_tfar == pa.tfar && s.plan_dfar == pa.dFar &&
-                          std::equal(key, key + 6, s.plan_key);
+                          std::equal(key, key + 7, s.plan_key);
     if (!plan_hit) {  // (the work counters are re-armed by the last pair CTAs)
       ck(sthk::launch_plan(pa, st), "plan");
       s.plan_valid = e.bg_cache && !vshards;
@@ -584,7 +633,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       s.plan_dT = pa.dT;
       s.plan_tfar = pa.tfar;
       s.plan_dfar = pa.dFar;
-      std::copy(key, key + 6, s.plan_key);
+      std::copy(key, key + 7, s.plan_key);
     }
 
     sthk::PairArgs qa{};
@@ -615,6 +664,16 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     qa.pair_counts = e.timing ? s.pair_counts : nullptr;
     // a trigger-only sweep runs the same kernel with the background switched
     // off, so its trigger partials are summed exactly as in a full sweep
+    auto launch_bg = [&] {  // the trigger-free kernel over the background-only list
+      if (!bg_split) return;
+      sthk::PairArgs ba = qa;
+      ba.ranges = s.ranges_bg;
+      ba.items = s.items_bg;
+      ba.n_items = s.scalars + 9;
+      ba.work_counter = s.scalars + 10;
+      ba.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 11);
+      ck(sthk::launch_bgonly(ba, grad, s.sms * s.occ_bg[grad ? 1 : 0], st), "bg-only kernel");
+    };
     const int occ = s.occ[e.mode][grad ? 1 : 0];
     const bool conc = far_on && e.far_concurrent;
     const int grid = s.sms * (conc ? std::min(e.near_ctas, occ) : occ);
@@ -630,6 +689,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       if (conc) {  // forked onto the second stream, joined before finalize
         ck(cudaEventRecord(s.fork, st), "event");
         ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
+        launch_bg();
         if (e.far_order == 2) {  // near first: its CTAs are resident before far CTAs fill in
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
           ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
@@ -640,10 +700,12 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
         ck(cudaEventRecord(s.join, s.stream2), "event");
         ck(cudaStreamWaitEvent(st, s.join, 0), "wait");
       } else {
+        launch_bg();
         ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
         ck(sthk::launch_far(fa_, grad, s.sms * s.occ_far[grad ? 1 : 0], st), "far kernel");
       }
     } else {
+      launch_bg();
       ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
     }
     if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
@@ -761,7 +823,9 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     e.cache_tt = e.p[2];
     e.cache_mode = e.mode;
     e.cache_dense = e.dense;
-    e.cache_far = e.far_tier;
+    e.cache_far_full = far_full;
+    e.cache_tfar = far_full ? pl.tfar : 0.0;
+    e.cache_bg_adj = bg_adj;
   }
   e.cache_valid = true;
   if (!tr_cached) {
@@ -1013,6 +1077,15 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
         span = std::max(span, t[std::min(k * kTS + kTS, n) - 1] - t[k * kTS]);
       }
       e->tile_tspan = span;
+      e->adj_gap.assign(kMaxAdj, std::numeric_limits<double>::infinity());
+      for (int k = 1; k <= kMaxAdj; ++k) {
+        double g = std::numeric_limits<double>::infinity();
+        for (int64_t tile = k + 1; tile < nt; ++tile) {
+          const int64_t fi = tile * kTS;
+          g = std::min(g, t[fi] - t[fi - static_cast<int64_t>(k) * kTS - 1]);
+        }
+        e->adj_gap[k - 1] = g;
+      }
     }
     e->n = n;
     e->npad = npad;
@@ -1170,6 +1243,13 @@ int sthk_set_far_schedule(sthk_engine* e, int concurrent, int near_ctas, int far
     e->far_order = concurrent == 2 ? 2 : 1;
     e->near_ctas = near_ctas;
     e->far_ctas = far_ctas;
+  });
+}
+
+int sthk_set_bgonly_kernel(sthk_engine* e, int enable) {
+  return guarded(e, [&] {
+    e->bg_split = enable != 0;
+    for (Slot& s : e->slots) s.plan_valid = false;
   });
 }
 

@@ -81,15 +81,16 @@ __device__ __forceinline__ int64_t bound_t(const double* t, int64_t n, double v,
   return lo;
 }
 
-// Three independent bound_t searches in lockstep: each level issues the
-// three dependent global loads back to back, so their latencies overlap
-// (the plan's cost is these load chains).
-__device__ __forceinline__ void bounds3(const double* t, int64_t n, const Pivots& p,
-                                        const double (&v)[3], const bool (&strict)[3],
-                                        int64_t (&out)[3]) {
-  int64_t lo[3], hi[3];
+// K independent bound_t searches in lockstep: each level issues the K
+// dependent global loads back to back, so their latencies overlap (the
+// plan's cost is these load chains).
+template <int K>
+__device__ __forceinline__ void bounds_lockstep(const double* t, int64_t n, const Pivots& p,
+                                                const double (&v)[K], const bool (&strict)[K],
+                                                int64_t (&out)[K]) {
+  int64_t lo[K], hi[K];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < K; ++k) {
     int klo = 0, khi = p.np;
     while (klo < khi) {
       const int mid = (klo + khi) >> 1;
@@ -103,23 +104,27 @@ __device__ __forceinline__ void bounds3(const double* t, int64_t n, const Pivots
       hi[k] = min(static_cast<int64_t>(klo) * p.stride, n);
     }
   }
-  while (lo[0] < hi[0] || lo[1] < hi[1] || lo[2] < hi[2]) {
-    int64_t mid[3];
-    double tv[3];
+  for (;;) {
+    bool any = false;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < K; ++k) any |= lo[k] < hi[k];
+    if (!any) break;
+    int64_t mid[K];
+    double tv[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
       mid[k] = (lo[k] + hi[k]) >> 1;
       tv[k] = lo[k] < hi[k] ? t[mid[k]] : 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < K; ++k) {
       if (lo[k] < hi[k]) {
         if (strict[k] ? tv[k] < v[k] : tv[k] <= v[k]) lo[k] = mid[k] + 1; else hi[k] = mid[k];
       }
     }
   }
 #pragma unroll
-  for (int k = 0; k < 3; ++k) out[k] = lo[k];
+  for (int k = 0; k < K; ++k) out[k] = lo[k];
 }
 
 // ---------------------------------------------------------------------------
@@ -127,17 +132,17 @@ __device__ __forceinline__ void bounds3(const double* t, int64_t n, const Pivots
 // ---------------------------------------------------------------------------
 // Live source range [lo, hi) and chunk range [c0, c1] of one row tile.
 __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, int tile, int2& rg,
-                                          int2& cr, int2& rgf, int2& crf) {
+                                          int2& cr, int2& rgf, int2& crf, int2& rgb, int2& crb) {
   const int64_t first = static_cast<int64_t>(tile) * kTM;
   const int64_t last = min(first + kTM, a.n) - 1;
   const double tmin = a.t[first], tmax = a.t[last];
   // searches: live-range start, live-range end (full row-kernel sweeps) or,
-  // in symmetric mode, the far tier's exact-cull start, and the far split
+  // in symmetric mode, the far tier's exact-cull start; the far split
   double v[3] = {a.trig_only ? tmin - a.dT : tmin - fmax(a.dB, a.dT),
                  a.sym ? tmin - a.dFar : tmax + a.dB, tmin - a.tfar};
   const bool strict[3] = {true, false, true};
   int64_t b[3];
-  bounds3(a.t, a.n, pv, v, strict, b);
+  bounds_lockstep<3>(a.t, a.n, pv, v, strict, b);
   int lo, hi;
   if (a.dense) {
     lo = 0;
@@ -162,10 +167,21 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
     // far sources before t[first] - dFar are exactly 0 in FP32: culled
     if (!a.dense) flo = min(max(lo, static_cast<int>(b[1])), fb);
   }
-  rg = make_int2(fb, hi);
-  cr = make_int2(fb / a.sc, (hi - 1) / a.sc);
+  // background-only split of the near range: the near stages before the
+  // last bg_adj stages ahead of the tile go to the trigger-free kernel. The
+  // host picks bg_adj so that those sources are beyond every tile's trigger
+  // window; the split is structural (it does not move with omega), so the
+  // background sums' grouping -- hence their cached values -- stays the same.
+  int fbt = fb;
+  if (a.ranges_bg && !a.trig_only) {
+    fbt = min(max(fb, static_cast<int>(first) - a.bg_adj * kTS), static_cast<int>(first));
+  }
+  rg = make_int2(fbt, hi);
+  cr = make_int2(fbt / a.sc, (hi - 1) / a.sc);
   rgf = make_int2(flo, fb);
   crf = fb > flo ? make_int2(flo / a.sc, (fb - 1) / a.sc) : make_int2(0, -1);
+  rgb = make_int2(fb, fbt);
+  crb = fbt > fb ? make_int2(fb / a.sc, (fbt - 1) / a.sc) : make_int2(0, -1);
 }
 
 // Number of 128-source stages of work item (tile, chunk) -- the same bounds
@@ -259,13 +275,17 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   for (int k = tid; k < pv.np; k += 1024) s_piv[k] = a.t[k * pv.stride];
   __syncthreads();
   for (int i = tid; i < ntiles; i += 1024) {
-    int2 rg, cr, rgf, crf;
-    tile_plan(a, pv, a.tile0 + i, rg, cr, rgf, crf);
+    int2 rg, cr, rgf, crf, rgb, crb;
+    tile_plan(a, pv, a.tile0 + i, rg, cr, rgf, crf, rgb, crb);
     a.ranges[a.tile0 + i] = rg;
     a.crange[a.tile0 + i] = cr;
     if (a.ranges_far) {
       a.ranges_far[a.tile0 + i] = rgf;
       a.crange_far[a.tile0 + i] = crf;
+    }
+    if (a.ranges_bg) {
+      a.ranges_bg[a.tile0 + i] = rgb;
+      a.crange_bg[a.tile0 + i] = crb;
     }
   }
   __syncthreads();
@@ -273,6 +293,10 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   if (a.ranges_far) {
     plan_list(a, a.ranges_far, a.crange_far, a.items_far, a.n_items_far, a.work_counter_far,
               s_hist, s_warp);
+  }
+  if (a.ranges_bg) {
+    plan_list(a, a.ranges_bg, a.crange_bg, a.items_bg, a.n_items_bg, a.work_counter_bg, s_hist,
+              s_warp);
   }
 }
 
@@ -828,7 +852,7 @@ __device__ __forceinline__ void far_stage(const float* __restrict__ sx, const fl
   }
 }
 
-template <bool GRAD, bool SYM, bool CHECK, bool VALID>
+template <bool GRAD, bool SYM, bool CHECK, bool VALID, bool BGONLY = false>
 __device__ __forceinline__ void sym_dispatch(bool bg, int tr, const double* sx, const double* sy,
                                              const double* st, int col0, int cnt,
                                              const double (&xi)[kSymR], const double (&yi)[kSymR],
@@ -838,9 +862,10 @@ __device__ __forceinline__ void sym_dispatch(bool bg, int tr, const double* sx, 
                                              double* s_col) {
 #define STHK_SYM_CALL(B, T) \
   sym_block<GRAD, SYM, B, T, CHECK, VALID>(sx, sy, st, col0, cnt, xi, yi, ti, rv, k, tab, racc, s_col)
-#ifdef STHK_SYM_NO_TRIGGER_EXPERIMENT
-  tr = 0;  // timing experiment only: drops the trigger term
-#endif
+  if constexpr (BGONLY) {  // (the plan guarantees no live trigger term)
+    if (bg) STHK_SYM_CALL(true, 0);
+    return;
+  }
   if (bg) {
     if (tr == 0) STHK_SYM_CALL(true, 0);
     else if (tr == 1) STHK_SYM_CALL(true, 1);
@@ -852,8 +877,17 @@ __device__ __forceinline__ void sym_dispatch(bool bg, int tr, const double* sx, 
 #undef STHK_SYM_CALL
 }
 
-template <bool GRAD>
-__global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs a) {
+#ifndef STHK_SYMBG_MINB
+#define STHK_SYMBG_MINB 4  // trigger-free variant: fewer registers, 4 CTAs per SM
+#endif
+
+// BGONLY: the trigger-free variant for the background-only list (stages of
+// sources earlier than t_tile_first - dT, never the diagonal stage): no
+// trigger code paths, so it fits 128 registers and 4 CTAs per SM; it stores
+// only background (fixed-point) row sums.
+template <bool GRAD, bool BGONLY = false>
+__global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
+    sym_kernel(const PairArgs a) {
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   constexpr int NSC = GRAD ? 3 : 1;
   __shared__ __align__(128) double s_src[2][3][kTS];
@@ -962,7 +996,7 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
 
       const bool bg = !a.bg_off && !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
       int tr;
-      if (smin >= tmax || smax < tmin - a.k.dT) tr = 0;
+      if (BGONLY || smin >= tmax || smax < tmin - a.k.dT) tr = 0;
       else if (smax < tmin) tr = 1;
       else tr = 2;
       const double dxm = fmax(bt.y - bs.x, bs.y - bt.x);
@@ -984,16 +1018,16 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
         }
       }
       if (diag) {
-        sym_dispatch<GRAD, false, true, true>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
+        sym_dispatch<GRAD, false, true, true, BGONLY>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
                                               a.k, s_tab, racc, s_col);
       } else if (rows_real < kTM) {
-        sym_dispatch<GRAD, true, true, true>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv, a.k,
+        sym_dispatch<GRAD, true, true, true, BGONLY>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv, a.k,
                                              s_tab, racc, s_col);
       } else if (safe) {
-        sym_dispatch<GRAD, true, false, false>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
+        sym_dispatch<GRAD, true, false, false, BGONLY>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
                                                a.k, s_tab, racc, s_col);
       } else {
-        sym_dispatch<GRAD, true, true, false>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
+        sym_dispatch<GRAD, true, true, false, BGONLY>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
                                               a.k, s_tab, racc, s_col);
       }
       if (tr) {
@@ -1048,7 +1082,17 @@ __global__ void __launch_bounds__(kTM, STHK_SYM_MINB) sym_kernel(const PairArgs 
     for (int q = 0; q < NS; ++q) {
       v[q] = ((s_red[0][q][tid] + s_red[1][q][tid]) + s_red[2][q][tid]) + s_red[3][q][tid];
     }
-    store_row_sums<GRAD>(a, chunk, first + tid, v);
+    if constexpr (BGONLY) {  // background rows only (no trigger partials)
+      if (first + tid < n && !a.bg_off) {
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+          fx_add(a.fx + static_cast<size_t>(2 * q) * a.npad + first + tid,
+                 a.fx + static_cast<size_t>(2 * q + 1) * a.npad + first + tid, v[q] * a.fxq[q]);
+        }
+      }
+    } else {
+      store_row_sums<GRAD>(a, chunk, first + tid, v);
+    }
   }
 
   if (tid == 0) {  // the last CTA out re-arms the work counter for the next launch
@@ -1541,6 +1585,8 @@ cudaError_t prepare_pair_kernels() {
   };
   set(reinterpret_cast<const void*>(&sym_kernel<true>));
   set(reinterpret_cast<const void*>(&sym_kernel<false>));
+  set(reinterpret_cast<const void*>(&sym_kernel<true, true>));
+  set(reinterpret_cast<const void*>(&sym_kernel<false, true>));
   set(reinterpret_cast<const void*>(&pair_kernel<true>));
   set(reinterpret_cast<const void*>(&pair_kernel<false>));
   return err;
@@ -1570,6 +1616,20 @@ cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* o
                              cudaStream_t stream) {
   final_sum_kernel<<<1, 256, 0, stream>>>(block_partial, nblocks, out);
   return cudaGetLastError();
+}
+
+cudaError_t launch_bgonly(const PairArgs& a, bool grad, int grid, cudaStream_t stream) {
+  if (grad) sym_kernel<true, true><<<grid, kTM, kTabBytes, stream>>>(a);
+  else sym_kernel<false, true><<<grid, kTM, kTabBytes, stream>>>(a);
+  return cudaGetLastError();
+}
+
+int bgonly_kernel_occupancy(bool grad) {
+  int occ = 0;
+  if (prepare_pair_kernels() != cudaSuccess) return 1;
+  if (grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel<true, true>, kTM, kTabBytes);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel<false, true>, kTM, kTabBytes);
+  return occ > 0 ? occ : 1;
 }
 
 cudaError_t launch_far(const PairArgs& a, bool grad, int grid, cudaStream_t stream) {

@@ -82,6 +82,15 @@ struct PlanArgs {
   int2* items_far;
   int* n_items_far;
   int* work_counter_far;
+  // background-only split of the near range (kSym full sweeps): near stages
+  // before first - bg_adj * 128 (no live trigger, host-checked) go to a third
+  // list for the trigger-free FP64 kernel; nullptr: off
+  int bg_adj;           // near stages kept with the tile for the general kernel (>= 1)
+  int2* ranges_bg;
+  int2* crange_bg;
+  int2* items_bg;
+  int* n_items_bg;
+  int* work_counter_bg;
 };
 
 // Background sums (k = 0..2: S_B, S_Br, S_Bt) are fixed point,
@@ -158,6 +167,10 @@ cudaError_t launch_scale_xy(const double* x, const double* y, const double* t, i
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_exp_probe(const double* x, int64_t n, double* out, cudaStream_t stream);
 cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaStream_t stream);
+// Trigger-free symmetric FP64 kernel over the background-only list (PairArgs'
+// ranges / items / counters point at that list's buffers).
+cudaError_t launch_bgonly(const PairArgs& a, bool grad, int grid, cudaStream_t stream);
+int bgonly_kernel_occupancy(bool grad);
 // FP32 far kernel over the far work list (PairArgs' ranges / items / counters
 // / tpart point at the far list's buffers).
 cudaError_t launch_far(const PairArgs& a, bool grad, int grid, cudaStream_t stream);

@@ -176,6 +176,10 @@ class Engine:
                                           _dptr(pe) if pe is not None else None), "sthk_result")
         return ll.value, bool(ok.value), g, pe
 
+    def set_bgonly_kernel(self, on: bool) -> None:
+        """Trigger-free near kernel for stages beyond the trigger window (default on)."""
+        self._check(self._lib.sthk_set_bgonly_kernel(self._h, int(on)), "sthk_set_bgonly_kernel")
+
     def set_far_tier(self, on: bool) -> None:
         """FP32 far tier of the symmetric kernel (default on; include/sthk.h)."""
         self._check(self._lib.sthk_set_far_tier(self._h, int(on)), "sthk_set_far_tier")
