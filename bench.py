@@ -396,11 +396,13 @@ def main():
                 "h2d_bytes_per_step": 3 * 8 * n,
                 "d2h_bytes_per_step": 8 * 8 + 3 * 8,
                 "path": "Engine.load_events(pinned x,y,t) + set_params + loglik_grad (C ABI)"},
-        "gpu_launches": (5 if st["exec_far"] else 4) * K,  # scale, plan, sym, [far], finalize
+        # scale, plan, [sym bg-only], sym, [far], finalize
+        "gpu_launches": (4 + (1 if st["exec_far"] else 0) + 1) * K,
         "roofline": {
             "bound": "fp64",
-            "kernel": ("sym_kernel<GRAD=true> (FP64 near) || far_kernel<GRAD=true> (FP32 far tier), "
-                       "concurrent" if st["exec_far"] else "sym_kernel<GRAD=true>")
+            "kernel": ("sym_kernel<GRAD=true> (FP64 near, trigger-free + general) || "
+                       "far_kernel<GRAD=true> (FP32 far tier), concurrent"
+                       if st["exec_far"] else "sym_kernel<GRAD=true>")
                       if st["kernel_mode"] == 1 else "pair_kernel<GRAD=true>",
             "achieved": achieved,
             "peak": peak_best,
