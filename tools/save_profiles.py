@@ -29,7 +29,7 @@ if os.path.exists(lc):
         agg[name][0] += 1
         agg[name][1] += float(r[vi].replace(",", ""))
     ours = {k: v for k, v in agg.items() if any(s in k for s in
-            ("pair_kernel", "sym_kernel", "finalize", "plan_", "final_sum", "tile_box"))}
+            ("pair_kernel", "sym_kernel", "far_kernel", "finalize", "plan_", "final_sum", "tile_box"))}
     tot = sum(v[1] for v in ours.values())
     with open(f"{p}/{tag}_launch_list_summary.txt", "w") as f:
         f.write(f"ncu --metrics gpu__time_duration.sum --clock-control none -- "
@@ -52,17 +52,21 @@ if os.path.exists(rep):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    d = dict(zip(hdr, zip(vals, units)))
+    hdr, units = rows[0], rows[1]
+    traffic, names = 0.0, []
+    for vals in rows[2:]:  # every captured pair kernel of one evaluation
+        d = dict(zip(hdr, zip(vals, units)))
 
-    def b(key):
-        v, u = d[key]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
-        return float(v.replace(",", "")) * scale
-    traffic = b("dram__bytes_read.sum") + b("dram__bytes_write.sum")
-    json.dump({"tag": tag, "kernel": "pair_kernel<GRAD=true>",
+        def b(key):
+            v, u = d[key]
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
+            return float(v.replace(",", "")) * scale
+        traffic += b("dram__bytes_read.sum") + b("dram__bytes_write.sum")
+        names.append(d.get("Kernel Name", ("?", ""))[0].split("(")[0])
+    json.dump({"tag": tag, "kernels": names,
                "dram_bytes_per_launch": traffic,
                "source": f"ncu --set full capture gpurun_out/prof_pair_{tag}.ncu-rep "
-                         "(tools/profile_one.py: C2 at Theta_post)"},
+                         "(tools/profile_one.py: C2 at Theta_post; sum over the pair kernels of "
+                         "one evaluation)"},
               open(f"{p}/pair_kernel_traffic.json", "w"), indent=1)
 print(open(f"{p}/{tag}_launch_list_summary.txt").read() if os.path.exists(lc) else "")
