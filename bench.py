@@ -264,7 +264,7 @@ def main():
         for _ in range(warmup):
             eng.loglik_grad()
         barrier()
-        pair_ms, evals_ms, dev_ms = [], [], []
+        pair_ms, evals_ms, dev_ms, lls = [], [], [], []
         st = None
         for _ in range(steps):
             with torch.cuda.stream(stream):
@@ -279,6 +279,7 @@ def main():
             res = eng.result()
             e1.synchronize()
             dev_ms.append(e0.elapsed_time(e1))
+            lls.append(res[0])
             st = eng.stats()
             pair_ms.append(st["pair_kernel_ms"])
             evals_ms.append(st["eval_ms"])
@@ -287,6 +288,7 @@ def main():
         return dict(total_ms=tot_ms, pair_ms=statistics.mean(pair_ms),
                     pair_ms_max=max_over_ranks(statistics.mean(pair_ms)),
                     eval_ms=statistics.mean(evals_ms), stats=st, loglik=res[0], valid=res[1],
+                    bitwise_repeats=len(set(lls)) == 1,
                     grad=list(res[2]))
 
     # FP64 roofline denominator, measured on this device
@@ -394,6 +396,7 @@ def main():
                            "geometries_executed": st["exec_geom"],
                            "symmetric_column_pairs": st["exec_sym"]},
         "loglik": main_run["loglik"],
+        "bitwise_identical_repeats": main_run["bitwise_repeats"],
         "grad": main_run["grad"],
         "e2e": {"value": K / e2e_s, "unit": "evals/s",
                 "h2d_bytes_per_step": 3 * 8 * n,
