@@ -689,14 +689,12 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       if (conc) {  // forked onto the second stream, joined before finalize
         ck(cudaEventRecord(s.fork, st), "event");
         ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
-        launch_bg();
-        if (e.far_order == 3) {  // the small general near kernel follows far on stream 2
-          ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
-          ck(sthk::launch_pairs(qa, grad, e.mode, grid, s.stream2), "pair kernel");
-        } else if (e.far_order == 2) {  // near first: its CTAs are resident before far CTAs fill in
+        if (e.far_order == 2) {  // near first: its CTAs are resident before far CTAs fill in
+          launch_bg();
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
           ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
         } else {
+          launch_bg();
           ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
         }
@@ -1243,7 +1241,7 @@ int sthk_set_far_schedule(sthk_engine* e, int concurrent, int near_ctas, int far
   return guarded(e, [&] {
     if (near_ctas < 1 || far_ctas < 1) throw InvalidArg("sthk_set_far_schedule: CTA counts must be >= 1");
     e->far_concurrent = concurrent != 0;
-    e->far_order = concurrent >= 2 ? concurrent : 1;
+    e->far_order = concurrent == 2 ? 2 : 1;
     e->near_ctas = near_ctas;
     e->far_ctas = far_ctas;
   });
