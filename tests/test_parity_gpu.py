@@ -480,13 +480,14 @@ def test_random_regimes_vs_oracle(engine, seed):
 
 
 def test_bgonly_kernel_consistent(engine):
-    """Near stages beyond the trigger window run in the trigger-free kernel. With
+    """Near stages beyond the trigger window run in the trigger-free kernel (from
+    64k events). With
     it on, results are bitwise identical with the caches on or off; against the
     single near kernel they differ only by the grouping of the per-item FP64 row
     partials (<= 1e-14 relative)."""
     ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
                                       pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
-                                      keep=20000)
+                                      keep=70000)
     engine.load(ev)
     seq = [[0.66, 1.6, 14, 0.344, 1440, 0.0695], [0.7, 1.6, 14, 0.344, 1440, 0.0695],
            [0.7, 1.6, 14, 0.344, 30.0, 0.0695], [1, 1.6, 14, 0.1, 1, 1]]
