@@ -82,6 +82,9 @@ struct Slot {
   double* tpart_far = nullptr;       // far kernel trigger partials [nchunks][3][npad]
   size_t tpart_far_cap = 0;
   double2* tile_trange = nullptr;    // per tile: t first, t last
+  double* comp = nullptr;            // compensator terms [4][npad] (prep_kernel)
+  size_t comp_cap = 0;
+  cudaEvent_t prepped = nullptr;     // prep done (stream 2) -> pair kernels (stream 1)
   size_t trange_cap = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;    // far kernel, concurrent with the near sweep
@@ -178,6 +181,10 @@ struct sthk_engine {
   // partials of the last sweep stay valid while omega and h are unchanged,
   // so an evaluation that moves only mu0 / theta is a finalize pass.
   bool tr_cache_valid = false, tr_cache_grad = false, last_tr_cache_hit = false;
+  // compensator terms depend only on (events, tauT, omega)
+  bool comp_valid = false;
+  uint64_t comp_gen = 0;
+  double comp_tt = 0, comp_om = 0;
   double tr_cache_omega = 0, tr_cache_h = 0;
   uint64_t load_gen = 0, cache_gen = 0;
   double cache_tx = 0, cache_tt = 0;
@@ -216,6 +223,7 @@ void init_slot(Slot& s, int dev) {
   ck(cudaStreamCreateWithFlags(&s.stream2, cudaStreamNonBlocking), "stream");
   ck(cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&s.prepped, cudaEventDisableTiming), "event");
   for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
   ck(cudaMalloc(&s.scalars, 12 * sizeof(int)), "cudaMalloc");
   ck(cudaMemset(s.scalars, 0, 12 * sizeof(int)), "memset");
@@ -245,7 +253,7 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.xf), static_cast<void*>(s.yf), static_cast<void*>(s.tf),
                   static_cast<void*>(s.ranges_far), static_cast<void*>(s.crange_far),
                   static_cast<void*>(s.items_far), static_cast<void*>(s.tpart_far),
-                  static_cast<void*>(s.tile_trange),
+                  static_cast<void*>(s.tile_trange), static_cast<void*>(s.comp),
                   static_cast<void*>(s.ranges_bg), static_cast<void*>(s.crange_bg),
                   static_cast<void*>(s.items_bg),
                   static_cast<void*>(s.ranges), static_cast<void*>(s.counts),
@@ -268,6 +276,7 @@ void free_slot(Slot& s) {
   if (s.stream2) cudaStreamSynchronize(s.stream2);
   if (s.fork) cudaEventDestroy(s.fork);
   if (s.join) cudaEventDestroy(s.join);
+  if (s.prepped) cudaEventDestroy(s.prepped);
   if (s.stream2) cudaStreamDestroy(s.stream2);
   if (s.stream) cudaStreamDestroy(s.stream);
 }
@@ -532,8 +541,12 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
   }
   for (Slot& s : e.slots) s.runs.clear();
 
+  const bool need_comp = !(e.comp_valid && e.comp_gen == e.load_gen && e.comp_tt == p[2] &&
+                           e.comp_om == p[4]);
+  if (need_comp) e.comp_valid = false;  // re-armed once the prep pass is enqueued
   // phase 1: zero the accumulators, plan and run the pair kernel per run
   for (const Run& run : runs) {
+    bool prep_pending = false;
     Slot& s = e.slots[run.slot];
     const bool first_run = s.runs.empty();
     s.runs.emplace_back(run.row0, run.row1);
@@ -561,6 +574,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       dev_grow(s.tpart_far, s.tpart_far_cap, static_cast<size_t>(pl.nchunks) * 3 * e.npad);
     }
     dev_grow(s.block_partial, s.bp_cap, static_cast<size_t>(nb_total) * kNOut);
+    dev_grow(s.comp, s.comp_cap, static_cast<size_t>(4) * e.npad);
     if (want_pe) dev_grow(s.per_event, s.pe_cap, static_cast<size_t>(e.npad));
     if (want_ex) dev_grow(s.ex, s.ex_cap, static_cast<size_t>(3) * e.npad);
 
@@ -571,17 +585,49 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
         ck(cudaMemsetAsync(s.pair_counts, 0, sthk::kNCounts * sizeof(unsigned long long), st),
            "memset");
       }
-      if (!cached) {
-        ck(cudaMemsetAsync(s.fx, 0, sizeof(unsigned long long) * kFxRows * e.npad, st),
-           "memset");
+      // one prep pass on stream 2, beside the plan (stream 1): scaled / FP32
+      // coordinates (a cached sweep has the same tauX, tauT: copies still
+      // valid), zeroed background accumulators, compensator terms
+      sthk::PrepArgs pr{};
+      pr.x = s.x;
+      pr.y = s.y;
+      pr.t = s.t;
+      pr.n = e.n;
+      pr.npad = e.npad;
+      if (sym && !cached) {
+        pr.sx = pl.sx;
+        pr.xs = s.xs;
+        pr.ys = s.ys;
+        if (far_on) {
+          pr.sxf = pl.sxf;
+          pr.stf = pl.stf;
+          pr.xf = s.xf;
+          pr.yf = s.yf;
+          pr.tf = s.tf;
+        }
       }
-      if (sym && !cached) {  // (a cached sweep has the same tauX, tauT: copies still valid)
-        ck(sthk::launch_scale_xy(s.x, s.y, s.t, e.npad, pl.sx, s.xs, s.ys, pl.sxf, pl.stf,
-                                 far_on ? s.xf : nullptr, s.yf, s.tf, st),
-           "scale xy");
+      if (!cached) pr.fx = s.fx;
+      if (need_comp) {
+        pr.comp = s.comp;
+        pr.window_end = e.window_end;
+        pr.tauT = p[2];
+        pr.omega = p[4];
+      }
+      if (pr.xs || pr.fx || pr.comp) {
+        ck(cudaEventRecord(s.fork, st), "event");
+        ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
+        ck(sthk::launch_prep(pr, s.stream2), "prep");
+        ck(cudaEventRecord(s.prepped, s.stream2), "event");
+        prep_pending = true;
       }
       if (shards > 1) {
         ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
+      }
+    }
+    if (ntiles == 0 || tr_cached) {
+      if (prep_pending) {
+        ck(cudaStreamWaitEvent(st, s.prepped, 0), "wait");
+        prep_pending = false;
       }
     }
     if (ntiles == 0) continue;
@@ -639,6 +685,10 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       std::copy(key, key + 7, s.plan_key);
     }
 
+    if (prep_pending) {  // pair kernels need the prepared coordinates / zeroed sums
+      ck(cudaStreamWaitEvent(st, s.prepped, 0), "wait");
+      prep_pending = false;
+    }
     sthk::PairArgs qa{};
     qa.x = s.x;
     qa.y = s.y;
@@ -752,6 +802,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     fa.tpart = s.tpart;
     fa.tr_r2_scale = sym ? 1.0 / (pl.sx * pl.sx) : 1.0;
     fa.crange = s.crange;
+    fa.comp = s.comp;
     fa.tpart_far = far_on ? s.tpart_far : nullptr;
     fa.crange_far = s.crange_far;
     for (int k = 0; k < sthk::kNSumGrad; ++k) fa.fxq[k] = fxq[k];
@@ -838,6 +889,10 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     e.tr_cache_h = e.p[5];
   }
   e.tr_cache_valid = e.bg_cache;
+  e.comp_valid = true;
+  e.comp_gen = e.load_gen;
+  e.comp_tt = p[2];
+  e.comp_om = p[4];
 }
 
 void collect(sthk_engine& e, double* loglik, int* valid, double* grad6, double* per_event) {
@@ -1098,6 +1153,7 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
     e->load_gen += 1;
     e->cache_valid = false;
     e->tr_cache_valid = false;
+    e->comp_valid = false;
     for (Slot& s : e->slots) s.plan_valid = false;
   });
 }

@@ -1354,26 +1354,49 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
   }
 }
 
-// Spatial coordinates pre-scaled by sx = sqrt(-cxL) for the symmetric
-// kernel, so that its squared distance is already the background exponent's
-// spatial part (one multiply less per pair). Time is not scaled: the strict
-// t_j < t_i rule and the trigger's small dt need the raw times.
-__global__ void scale_xy_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                                const double* __restrict__ t, int64_t npad, double sx,
-                                double* __restrict__ xs, double* __restrict__ ys, double sxf,
-                                double stf, float* __restrict__ xf, float* __restrict__ yf,
-                                float* __restrict__ tf) {
+// Per-evaluation preparation, one pass over the (padded) events, each part
+// optional:
+//  * kSym coordinates: xs, ys = (x, y) * sx, so the symmetric kernels' squared
+//    distance is already the background exponent's spatial part; the far
+//    tier's FP32 copies xf, yf (relative to event 0) and tf (relative to the
+//    first event of the event's own 128-tile), in log2-exponent units;
+//  * zero the fixed-point background accumulators (6 words per event);
+//  * the compensator terms (kernels.hpp:54-65 and their derivatives), which
+//    depend only on (t, T, tauT, omega): comp[0] = Phi((T-t)/tauT) -
+//    Phi(-t/tauT), comp[1] = (phi(z1) D + phi(z0) t) / tauT^2 (d Lambda / d tauT
+//    = -mu0 comp[1]), comp[2] = expm1(-omega D), comp[3] = D exp(-omega D),
+//    D = T - t; finalize combines them with mu0 and theta.
+__global__ void prep_kernel(const PrepArgs a) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= npad) return;
-  const double xv = x[i], yv = y[i];  // (the pad tail of x, y, t is zero)
-  xs[i] = xv * sx;
-  ys[i] = yv * sx;
-  if (xf) {
-    // space relative to event 0; time relative to the first event of the
-    // event's own 128-tile (the kernel adds the tile-to-tile offset per stage)
-    xf[i] = static_cast<float>((xv - x[0]) * sxf);
-    yf[i] = static_cast<float>((yv - y[0]) * sxf);
-    tf[i] = static_cast<float>((t[i] - t[i - i % kTS]) * stf);
+  if (i >= a.npad) return;
+  if (a.xs) {
+    const double xv = a.x[i], yv = a.y[i];  // (the pad tail of x, y, t is zero)
+    a.xs[i] = xv * a.sx;
+    a.ys[i] = yv * a.sx;
+    if (a.xf) {
+      a.xf[i] = static_cast<float>((xv - a.x[0]) * a.sxf);
+      a.yf[i] = static_cast<float>((yv - a.y[0]) * a.sxf);
+      a.tf[i] = static_cast<float>((a.t[i] - a.t[i - i % kTS]) * a.stf);
+    }
+  }
+  if (a.fx) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) a.fx[static_cast<size_t>(k) * a.npad + i] = 0ULL;
+  }
+  if (a.comp && i < a.n) {
+    const double ti = a.t[i];
+    const double D = a.window_end - ti;
+    // normalCdf = 0.5 erfc(-z/sqrt2), kernels.hpp:21
+    const double Phi1 = 0.5 * erfc(-(D / a.tauT) * kInvSqrt2);
+    const double Phi0 = 0.5 * erfc(-(-ti / a.tauT) * kInvSqrt2);
+    const double z1 = D / a.tauT, z0 = ti / a.tauT;
+    const double phi1 = kInvSqrt2Pi * exp(-0.5 * z1 * z1);
+    const double phi0 = kInvSqrt2Pi * exp(-0.5 * z0 * z0);
+    a.comp[i] = Phi1 - Phi0;
+    a.comp[a.npad + i] = (phi1 * D + phi0 * ti) / (a.tauT * a.tauT);
+    a.comp[2 * a.npad + i] = expm1(-a.omega * D);
+    // exp(-omega D) directly: 1 + expm1 cancels when omega D is large
+    a.comp[3 * a.npad + i] = D * exp(-a.omega * D);
   }
 }
 
@@ -1459,13 +1482,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
     const double Tr = a.trNorm * sT;
     const double lam = a.mu0 * B + Tr;  // likelihood.cpp:35
 
-    const double ti = a.t[r];
-    const double D = a.window_end - ti;
-    // compensatorTerm, kernels.hpp:54-65; normalCdf = 0.5 erfc(-z/sqrt2)
-    const double Phi1 = 0.5 * erfc(-(D / a.tauT) * kInvSqrt2);
-    const double Phi0 = 0.5 * erfc(-(-ti / a.tauT) * kInvSqrt2);
-    const double em1 = expm1(-a.omega * D);
-    const double Lam = a.mu0 * (Phi1 - Phi0) + (-a.theta * em1);
+    // compensatorTerm, kernels.hpp:54-65, from the prepared terms (prep_kernel)
+    const double dPhi = a.comp[r];
+    const double em1 = a.comp[2 * a.npad + r];
+    const double Lam = a.mu0 * dPhi + (-a.theta * em1);
 
     if (a.ex_out) {  // excitation split, excitation.cpp:31-51
       a.ex_out[r] = a.mu0 * B;
@@ -1492,17 +1512,13 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
       const double dl3 = a.cT * sT;
       const double dl4 = a.trNorm * (sT / a.omega - s[4]);
       const double dl5 = a.trNorm * (-2.0 * sT / a.h + s[5] / h3);
-      // d Lambda / d p
-      const double z1 = D / a.tauT, z0 = ti / a.tauT;
-      const double phi1 = kInvSqrt2Pi * exp(-0.5 * z1 * z1);
-      const double phi0 = kInvSqrt2Pi * exp(-0.5 * z0 * z0);
-      const double dL2 = -a.mu0 * (phi1 * D + phi0 * ti) / (a.tauT * a.tauT);
-      acc[1] += B * inv - (Phi1 - Phi0);
+      // d Lambda / d p (prepared: dPhi, em1, (phi1 D + phi0 t) / tauT^2, D e^(-omega D))
+      const double dL2 = -a.mu0 * a.comp[a.npad + r];
+      acc[1] += B * inv - dPhi;
       acc[2] += dl1 * inv;
       acc[3] += dl2 * inv - dL2;
       acc[4] += dl3 * inv + em1;
-      // exp(-omega D) directly: 1 + expm1 cancels when omega D is large
-      acc[5] += dl4 * inv - a.theta * D * exp(-a.omega * D);
+      acc[5] += dl4 * inv - a.theta * a.comp[3 * a.npad + r];
       acc[6] += dl5 * inv;
     }
   } while (false);
@@ -1553,11 +1569,8 @@ cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_
   return cudaGetLastError();
 }
 
-cudaError_t launch_scale_xy(const double* x, const double* y, const double* t, int64_t npad,
-                            double sx, double* xs, double* ys, double sxf, double stf,
-                            float* xf, float* yf, float* tf, cudaStream_t stream) {
-  scale_xy_kernel<<<static_cast<unsigned>((npad + 255) / 256), 256, 0, stream>>>(
-      x, y, t, npad, sx, xs, ys, sxf, stf, xf, yf, tf);
+cudaError_t launch_prep(const PrepArgs& a, cudaStream_t stream) {
+  prep_kernel<<<static_cast<unsigned>((a.npad + 255) / 256), 256, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -140,6 +140,7 @@ struct FinArgs {
   const double* tpart;
   double tr_r2_scale;   // 1 (kRows) or 1/sx^2 (kSym: trigger r^2 sums on scaled coordinates)
   const int2* crange;
+  const double* comp;   // prepared compensator terms [4][npad] (prep_kernel)
   const double* tpart_far;  // far kernel's trigger partials (same layout), chunks crange_far
   const int2* crange_far;
   double* per_event;    // nullable
@@ -159,11 +160,27 @@ struct FinArgs {
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
                               double4* box, double2* trange, unsigned long long* bad,
                               cudaStream_t stream);
-// kSym coordinates: xs, ys = (x, y) * sx; if xf: the far tier's FP32 copies
-// xf, yf = (x - x[0], y - y[0]) * sxf, tf = (t - t[tile start]) * stf.
-cudaError_t launch_scale_xy(const double* x, const double* y, const double* t, int64_t npad,
-                            double sx, double* xs, double* ys, double sxf, double stf,
-                            float* xf, float* yf, float* tf, cudaStream_t stream);
+// Per-evaluation preparation (prep_kernel); every output optional (nullptr):
+// kSym coordinates xs, ys = (x, y) * sx and the far tier's FP32 copies
+// xf, yf = (x - x[0], y - y[0]) * sxf, tf = (t - t[tile start]) * stf; zeroed
+// fixed-point accumulators fx[6][npad]; compensator terms comp[4][npad].
+struct PrepArgs {
+  const double* x;
+  const double* y;
+  const double* t;
+  int64_t n, npad;
+  double sx;
+  double* xs;
+  double* ys;
+  double sxf, stf;
+  float* xf;
+  float* yf;
+  float* tf;
+  unsigned long long* fx;
+  double* comp;
+  double window_end, tauT, omega;
+};
+cudaError_t launch_prep(const PrepArgs& a, cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_exp_probe(const double* x, int64_t n, double* out, cudaStream_t stream);
 cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaStream_t stream);
