@@ -225,8 +225,8 @@ void init_slot(Slot& s, int dev) {
   ck(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.prepped, cudaEventDisableTiming), "event");
   for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
-  ck(cudaMalloc(&s.scalars, 12 * sizeof(int)), "cudaMalloc");
-  ck(cudaMemset(s.scalars, 0, 12 * sizeof(int)), "memset");
+  ck(cudaMalloc(&s.scalars, 16 * sizeof(int)), "cudaMalloc");
+  ck(cudaMemset(s.scalars, 0, 16 * sizeof(int)), "memset");
   ck(cudaMallocHost(&s.h_bad, sizeof(unsigned long long)), "cudaMallocHost");
   ck(cudaMalloc(&s.out, kNOut * sizeof(double)), "cudaMalloc");
   ck(cudaMalloc(&s.pair_counts, sthk::kNCounts * sizeof(unsigned long long)), "cudaMalloc");
@@ -546,7 +546,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
   if (need_comp) e.comp_valid = false;  // re-armed once the prep pass is enqueued
   // phase 1: zero the accumulators, plan and run the pair kernel per run
   for (const Run& run : runs) {
-    bool prep_pending = false;
+    bool prep_pending = false, prep_unlaunched = false;
+    sthk::PrepArgs pr{};
     Slot& s = e.slots[run.slot];
     const bool first_run = s.runs.empty();
     s.runs.emplace_back(run.row0, run.row1);
@@ -588,7 +589,6 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       // one prep pass on stream 2, beside the plan (stream 1): scaled / FP32
       // coordinates (a cached sweep has the same tauX, tauT: copies still
       // valid), zeroed background accumulators, compensator terms
-      sthk::PrepArgs pr{};
       pr.x = s.x;
       pr.y = s.y;
       pr.t = s.t;
@@ -613,18 +613,27 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
         pr.tauT = p[2];
         pr.omega = p[4];
       }
-      if (pr.xs || pr.fx || pr.comp) {
+      if (pr.xs || pr.fx || pr.comp) {  // (launched right after the plan, see below)
         ck(cudaEventRecord(s.fork, st), "event");
-        ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
-        ck(sthk::launch_prep(pr, s.stream2), "prep");
-        ck(cudaEventRecord(s.prepped, s.stream2), "event");
-        prep_pending = true;
+        prep_unlaunched = true;
       }
       if (shards > 1) {
         ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
       }
     }
+    // The plan kernel goes first: its few CTAs take whole SMs (1024 threads,
+    // the full register file) before the prep pass spreads over the rest, so
+    // the plan's latency-bound searches do not queue behind prep traffic.
+    auto launch_prep_now = [&] {
+      if (!prep_unlaunched) return;
+      ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
+      ck(sthk::launch_prep(pr, s.stream2), "prep");
+      ck(cudaEventRecord(s.prepped, s.stream2), "event");
+      prep_unlaunched = false;
+      prep_pending = true;
+    };
     if (ntiles == 0 || tr_cached) {
+      launch_prep_now();
       if (prep_pending) {
         ck(cudaStreamWaitEvent(st, s.prepped, 0), "wait");
         prep_pending = false;
@@ -684,6 +693,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       s.plan_dfar = pa.dFar;
       std::copy(key, key + 7, s.plan_key);
     }
+    launch_prep_now();
 
     if (prep_pending) {  // pair kernels need the prepared coordinates / zeroed sums
       ck(cudaStreamWaitEvent(st, s.prepped, 0), "wait");

@@ -5,7 +5,7 @@ set -e
 NAME=$1; DEFS=$2
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 C=$ROOT/paper_2005_10123_b200/csrc
-OUT=$ROOT/tools/variants; mkdir -p $OUT/obj_$NAME
+OUT=${VOUT:-$ROOT/tools/variants}; mkdir -p $OUT/obj_$NAME
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $DEFS -c $C/sthk_kernels.cu -o $OUT/obj_$NAME/k.o -Xptxas -v 2> $OUT/obj_$NAME/ptxas.log
 grep -A2 "sym_kernelILb1" $OUT/obj_$NAME/ptxas.log | grep -E "registers|spill" | tr '\n' ' '; echo
