@@ -517,6 +517,10 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
   // its tile, e.g. a trigger-only sweep at large omega -- is not planned or
   // launched; results are the same either way)
   const bool far_on = far_full && !(cached && pl.k.dT <= pl.tfar);
+  // every far source lies more than tfar before its tile's rows: with the far
+  // tier's trigger cull window dTf <= tfar no far trigger term is live, and
+  // its (all-zero) trigger partials are neither stored nor summed
+  const bool far_tr = far_on && !(pl.k.dTf <= pl.tfar);
   e.cache_valid = false;  // re-armed below once the sweep is enqueued
   e.tr_cache_valid = false;
   const int64_t ntiles_total = (e.n + kTM - 1) / kTM;
@@ -748,7 +752,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       fa_.n_items = s.scalars + 6;
       fa_.work_counter = s.scalars + 7;
       fa_.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 8);
-      fa_.tpart = s.tpart_far;
+      fa_.tpart = far_tr ? s.tpart_far : nullptr;
       if (conc) {  // forked onto the second stream, joined before finalize
         ck(cudaEventRecord(s.fork, st), "event");
         ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
@@ -813,7 +817,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     fa.tr_r2_scale = sym ? 1.0 / (pl.sx * pl.sx) : 1.0;
     fa.crange = s.crange;
     fa.comp = s.comp;
-    fa.tpart_far = far_on ? s.tpart_far : nullptr;
+    fa.tpart_far = far_tr ? s.tpart_far : nullptr;
     fa.crange_far = s.crange_far;
     for (int k = 0; k < sthk::kNSumGrad; ++k) fa.fxq[k] = fxq[k];
     fa.per_event = want_pe ? s.per_event : nullptr;

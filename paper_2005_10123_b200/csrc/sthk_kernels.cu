@@ -1277,10 +1277,12 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
                static_cast<double>(v[q]) * cscale[q] * a.fxq[q]);
       }
     }
-    double* out = a.tpart + static_cast<size_t>(chunk) * NT * a.npad + row;
+    if (a.tpart) {  // (nullptr: the host proved every far trigger term culled)
+      double* out = a.tpart + static_cast<size_t>(chunk) * NT * a.npad + row;
 #pragma unroll
-    for (int q = 0; q < NT; ++q) {
-      out[static_cast<size_t>(q) * a.npad] = static_cast<double>(v[NB + q]) * tscale[q];
+      for (int q = 0; q < NT; ++q) {
+        out[static_cast<size_t>(q) * a.npad] = static_cast<double>(v[NB + q]) * tscale[q];
+      }
     }
   }
 
