@@ -119,7 +119,6 @@ struct Slot {
   size_t crange_cap = 0;
   double* block_partial = nullptr;
   size_t bp_cap = 0;
-  double* out = nullptr;  // kNOut
   double* per_event = nullptr;
   size_t pe_cap = 0;
   double* ex = nullptr;  // excitation mu, xi, pi [3][npad]
@@ -127,7 +126,9 @@ struct Slot {
   double* h_ex = nullptr;  // pinned
   size_t h_ex_cap = 0;
   unsigned long long* pair_counts = nullptr;
-  double* h_out = nullptr;                 // pinned kNOut
+  double* h_out = nullptr;                 // pinned, device-mapped kNOut (kernels write it)
+  double* d_hout = nullptr;                // device alias of h_out
+  unsigned long long* d_hcounts = nullptr;  // device alias of h_counts
   unsigned long long* h_counts = nullptr;  // pinned kNCounts
   double* h_per_event = nullptr;           // pinned
   size_t h_pe_cap = 0;
@@ -228,11 +229,18 @@ void init_slot(Slot& s, int dev) {
   ck(cudaMalloc(&s.scalars, 16 * sizeof(int)), "cudaMalloc");
   ck(cudaMemset(s.scalars, 0, 16 * sizeof(int)), "memset");
   ck(cudaMallocHost(&s.h_bad, sizeof(unsigned long long)), "cudaMallocHost");
-  ck(cudaMalloc(&s.out, kNOut * sizeof(double)), "cudaMalloc");
   ck(cudaMalloc(&s.pair_counts, sthk::kNCounts * sizeof(unsigned long long)), "cudaMalloc");
-  ck(cudaMallocHost(&s.h_out, kNOut * sizeof(double)), "cudaMallocHost");
-  ck(cudaMallocHost(&s.h_counts, sthk::kNCounts * sizeof(unsigned long long)),
-     "cudaMallocHost");
+  ck(cudaMemset(s.pair_counts, 0, sthk::kNCounts * sizeof(unsigned long long)), "memset");
+  // results and counters are written by the last kernel straight into
+  // device-mapped pinned memory: no D2H copy on the evaluation's stream
+  constexpr unsigned kMapped = cudaHostAllocMapped | cudaHostAllocPortable;
+  ck(cudaHostAlloc(&s.h_out, kNOut * sizeof(double), kMapped), "cudaHostAlloc");
+  ck(cudaHostAlloc(&s.h_counts, sthk::kNCounts * sizeof(unsigned long long), kMapped),
+     "cudaHostAlloc");
+  ck(cudaHostGetDevicePointer(&s.d_hout, s.h_out, 0), "cudaHostGetDevicePointer");
+  ck(cudaHostGetDevicePointer(&s.d_hcounts, s.h_counts, 0), "cudaHostGetDevicePointer");
+  std::fill(s.h_out, s.h_out + kNOut, 0.0);
+  std::fill(s.h_counts, s.h_counts + sthk::kNCounts, 0ULL);
   for (int m = 0; m < 2; ++m) {
     s.occ[m][1] = sthk::pair_kernel_occupancy(true, m);
     s.occ[m][0] = sthk::pair_kernel_occupancy(false, m);
@@ -261,7 +269,7 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.fx), static_cast<void*>(s.block_partial),
                   static_cast<void*>(s.tpart), static_cast<void*>(s.crange),
                   static_cast<void*>(s.ex),
-                  static_cast<void*>(s.out), static_cast<void*>(s.per_event),
+                  static_cast<void*>(s.per_event),
                   static_cast<void*>(s.pair_counts), static_cast<void*>(s.tile_box)}) {
     if (p) cudaFree(p);
   }
@@ -586,10 +594,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     cudaStream_t st = s.stream;
     if (first_run) {
       if (e.timing) ck(cudaEventRecord(s.ev[0], st), "event");
-      if (e.timing) {  // pair counters feed the stats / roofline only
-        ck(cudaMemsetAsync(s.pair_counts, 0, sthk::kNCounts * sizeof(unsigned long long), st),
-           "memset");
-      }
+      // (pair counters, timing only, are zero here: the final kernel of the
+      // previous timed evaluation re-zeroed them after copying them out)
       // one prep pass on stream 2, beside the plan (stream 1): scaled / FP32
       // coordinates (a cached sweep has the same tauX, tauT: copies still
       // valid), zeroed background accumulators, compensator terms
@@ -824,7 +830,9 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     fa.ex_out = want_ex ? s.ex : nullptr;
     fa.block_partial = s.block_partial;
     // one shard on this slot and no collective: the final sum rides along
-    fa.fused_out = (shards == 1) ? s.out : nullptr;
+    fa.fused_out = (shards == 1) ? s.d_hout : nullptr;
+    fa.counts = (shards == 1 && e.timing) ? s.pair_counts : nullptr;
+    fa.counts_out = s.d_hcounts;
     fa.nblocks_total = nb_total;
     fa.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 3);
     ck(sthk::launch_finalize(fa, grad, s.stream), "finalize");
@@ -846,17 +854,11 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     set_dev(s);
     cudaStream_t st = s.stream;
     if (shards > 1) {
-      ck(sthk::launch_final_sum(s.block_partial, nb_total, s.out, st), "final sum");
+      ck(sthk::launch_final_sum(s.block_partial, nb_total, s.d_hout,
+                                e.timing ? s.pair_counts : nullptr, s.d_hcounts, st),
+         "final sum");
     }
-    ck(cudaMemcpyAsync(s.h_out, s.out, kNOut * sizeof(double), cudaMemcpyDeviceToHost, st),
-       "D2H");
-    if (e.timing) {
-      ck(cudaMemcpyAsync(s.h_counts, s.pair_counts, sthk::kNCounts * sizeof(unsigned long long),
-                         cudaMemcpyDeviceToHost, st),
-         "D2H");
-    } else {
-      std::fill(s.h_counts, s.h_counts + sthk::kNCounts, 0ULL);
-    }
+    if (!e.timing) std::fill(s.h_counts, s.h_counts + sthk::kNCounts, 0ULL);
     if (want_pe && s.row1 > s.row0) {  // runs on one slot are contiguous
       if (s.h_pe_cap < static_cast<size_t>(e.npad)) {
         if (s.h_per_event) ck(cudaFreeHost(s.h_per_event), "cudaFreeHost");

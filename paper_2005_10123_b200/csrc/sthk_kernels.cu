@@ -1549,15 +1549,25 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
     if (s_last) {
       __threadfence();
       final_sum_block(a.block_partial, a.nblocks_total, a.fused_out, s_red);
+      if (a.counts && tid < kNCounts) {
+        a.counts_out[tid] = a.counts[tid];
+        a.counts[tid] = 0ULL;
+      }
       if (tid == 0) *a.done_counter = 0u;
     }
   }
 }
 
 __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict__ bp,
-                                                        int nblocks, double* out) {
+                                                        int nblocks, double* out,
+                                                        unsigned long long* counts,
+                                                        unsigned long long* counts_out) {
   __shared__ double s_red[kNOut][256];
   final_sum_block(bp, nblocks, out, s_red);
+  if (counts && threadIdx.x < kNCounts) {
+    counts_out[threadIdx.x] = counts[threadIdx.x];
+    counts[threadIdx.x] = 0ULL;
+  }
 }
 
 }  // namespace
@@ -1628,8 +1638,9 @@ cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream) {
 }
 
 cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,
+                             unsigned long long* counts, unsigned long long* counts_out,
                              cudaStream_t stream) {
-  final_sum_kernel<<<1, 256, 0, stream>>>(block_partial, nblocks, out);
+  final_sum_kernel<<<1, 256, 0, stream>>>(block_partial, nblocks, out, counts, counts_out);
   return cudaGetLastError();
 }
 

@@ -147,10 +147,15 @@ struct FinArgs {
   double* ex_out;       // nullable: excitation mu, xi, pi as [3][npad]
   double* block_partial;  // [ceil(n / kFB)][kNOut]
   // single shard: fuse the final sum (the last block sums all nblocks_total
-  // block partials into fused_out); nullptr when a collective sits between
+  // block partials into fused_out -- host-mapped pinned memory, so no D2H
+  // copy follows); nullptr when a collective sits between
   double* fused_out;
   int nblocks_total;
   unsigned int* done_counter;
+  // with fused_out: the pair counters are copied to counts_out (host-mapped)
+  // and re-zeroed for the next evaluation; nullptr: untouched
+  unsigned long long* counts;
+  unsigned long long* counts_out;
 };
 
 // Launch wrappers (sthk_kernels.cu). All enqueue on `stream`.
@@ -193,7 +198,10 @@ int bgonly_kernel_occupancy(bool grad);
 cudaError_t launch_far(const PairArgs& a, bool grad, int grid, cudaStream_t stream);
 int far_kernel_occupancy(bool grad);
 cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream);
+// (out and counts_out may be host-mapped; counts, if non-null, are copied to
+// counts_out and re-zeroed)
 cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,
+                             unsigned long long* counts, unsigned long long* counts_out,
                              cudaStream_t stream);
 // Resident CTAs per SM of a pair kernel (for the persistent grid size).
 int pair_kernel_occupancy(bool grad, int mode);
