@@ -109,7 +109,8 @@ struct Slot {
   int* scalars = nullptr;  // [0] n_items, [1] work counter, [2] pair CTAs done, [3] finalize
                            // blocks done, [4..5] first invalid event index (uint64),
                            // [6] far n_items, [7] far work counter, [8] far CTAs done,
-                           // [9] bg-only n_items, [10] its work counter, [11] its CTAs done
+                           // [9] bg-only n_items, [10] its work counter, [11] its CTAs done,
+                           // [12] load-check blocks done
   unsigned long long* h_bad = nullptr;  // pinned
   unsigned long long* fx = nullptr;  // fixed-point background sums [6][npad]
   size_t fx_cap = 0;
@@ -228,7 +229,11 @@ void init_slot(Slot& s, int dev) {
   for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
   ck(cudaMalloc(&s.scalars, 16 * sizeof(int)), "cudaMalloc");
   ck(cudaMemset(s.scalars, 0, 16 * sizeof(int)), "memset");
-  ck(cudaMallocHost(&s.h_bad, sizeof(unsigned long long)), "cudaMallocHost");
+  ck(cudaHostAlloc(&s.h_bad, sizeof(unsigned long long),
+                   cudaHostAllocMapped | cudaHostAllocPortable),
+     "cudaHostAlloc");
+  // the load checks' device minimum starts (and is re-armed) at all ones
+  ck(cudaMemset(s.scalars + 4, 0xff, sizeof(unsigned long long)), "memset");
   ck(cudaMalloc(&s.pair_counts, sthk::kNCounts * sizeof(unsigned long long)), "cudaMalloc");
   ck(cudaMemset(s.pair_counts, 0, sthk::kNCounts * sizeof(unsigned long long)), "memset");
   // results and counters are written by the last kernel straight into
@@ -1110,24 +1115,26 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       dev_grow(s.tile_box, s.box_cap, static_cast<size_t>(npad / kTS));
       dev_grow(s.tile_trange, s.trange_cap, static_cast<size_t>(npad / kTS));
       auto* bad = reinterpret_cast<unsigned long long*>(s.scalars + 4);
-      ck(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s.stream), "memset");
-      ck(sthk::launch_tile_boxes(s.x, s.y, s.t, n, npad, s.tile_box, s.tile_trange, bad,
-                                 s.stream),
-         "tile boxes + checks");
-      ck(cudaMemcpyAsync(s.h_bad, bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                         s.stream),
-         "D2H");
-      if (&s == &e->slots[0]) {  // coordinate extents for the far-tier guard
+      auto* done = reinterpret_cast<unsigned int*>(s.scalars + 12);
+      double4* d_hbox = nullptr;
+      if (&s == &e->slots[0]) {  // coordinate extents for the far-tier guard (host-mapped)
         const size_t nt = static_cast<size_t>(npad / kTS);
         if (s.h_box_cap < nt) {
           if (s.h_box) ck(cudaFreeHost(s.h_box), "cudaFreeHost");
-          ck(cudaMallocHost(&s.h_box, sizeof(double4) * nt), "cudaMallocHost");
+          s.h_box = nullptr;
+          s.h_box_cap = 0;
+          ck(cudaHostAlloc(&s.h_box, sizeof(double4) * nt,
+                           cudaHostAllocMapped | cudaHostAllocPortable),
+             "cudaHostAlloc");
           s.h_box_cap = nt;
         }
-        ck(cudaMemcpyAsync(s.h_box, s.tile_box, sizeof(double4) * nt, cudaMemcpyDeviceToHost,
-                           s.stream),
-           "D2H");
+        ck(cudaHostGetDevicePointer(&d_hbox, s.h_box, 0), "cudaHostGetDevicePointer");
       }
+      unsigned long long* d_hbad = nullptr;
+      ck(cudaHostGetDevicePointer(&d_hbad, s.h_bad, 0), "cudaHostGetDevicePointer");
+      ck(sthk::launch_tile_boxes(s.x, s.y, s.t, n, npad, s.tile_box, s.tile_trange, bad, done,
+                                 d_hbad, d_hbox, s.stream),
+         "tile boxes + checks");
     }
     for (Slot& s : e->slots) {
       set_dev(s);

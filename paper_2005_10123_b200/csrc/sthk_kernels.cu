@@ -1308,7 +1308,8 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
 // independent; computed once per load). Feeds the no-underflow proofs.
 __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
                                 double* __restrict__ t, int64_t n, int64_t npad, double4* box,
-                                double2* trange, unsigned long long* bad) {
+                                double2* trange, unsigned long long* bad, unsigned int* done,
+                                unsigned long long* h_bad, double4* h_box) {
   // zero the pad tail [n, npad) of the coordinate arrays (never read as sources)
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid < npad - n) {
@@ -1318,41 +1319,55 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
   }
   // one warp per tile: 4 coalesced loads per lane, then a shuffle min/max
   const int lane = threadIdx.x & 31;
-  const int64_t tile = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t tile = gid >> 5;
   const int64_t first = tile * kTS;
-  if (first >= n) return;
-  const int64_t last = min(first + kTS, n);
-  double x0 = x[first], x1 = x0, y0 = y[first], y1 = y0;
-  int64_t first_bad = INT64_MAX;
-  for (int64_t i = first + lane; i < last; i += 32) {
-    const double xv = x[i], yv = y[i], tv = t[i];
-    x0 = fmin(x0, xv);
-    x1 = fmax(x1, xv);
-    y0 = fmin(y0, yv);
-    y1 = fmax(y1, yv);
-    // EventSet checks (types.hpp:85-109): finite, t >= 0, nondecreasing
-    const double prev = i > 0 ? t[i - 1] : 0.0;
-    const bool ok = isfinite(xv) && isfinite(yv) && isfinite(tv) && tv >= prev;
-    if (!ok && i < first_bad) first_bad = i;
-  }
+  if (first < n) {
+    const int64_t last = min(first + kTS, n);
+    double x0 = x[first], x1 = x0, y0 = y[first], y1 = y0;
+    int64_t first_bad = INT64_MAX;
+    for (int64_t i = first + lane; i < last; i += 32) {
+      const double xv = x[i], yv = y[i], tv = t[i];
+      x0 = fmin(x0, xv);
+      x1 = fmax(x1, xv);
+      y0 = fmin(y0, yv);
+      y1 = fmax(y1, yv);
+      // EventSet checks (types.hpp:85-109): finite, t >= 0, nondecreasing
+      const double prev = i > 0 ? t[i - 1] : 0.0;
+      const bool ok = isfinite(xv) && isfinite(yv) && isfinite(tv) && tv >= prev;
+      if (!ok && i < first_bad) first_bad = i;
+    }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    first_bad = min(first_bad, static_cast<int64_t>(__shfl_xor_sync(0xffffffffu,
-                                                                    static_cast<long long>(first_bad), off)));
-  }
-  if (lane == 0 && first_bad != INT64_MAX) {
-    atomicMin(bad, static_cast<unsigned long long>(first_bad));
-  }
+    for (int off = 16; off > 0; off >>= 1) {
+      first_bad = min(first_bad, static_cast<int64_t>(__shfl_xor_sync(
+                                     0xffffffffu, static_cast<long long>(first_bad), off)));
+    }
+    if (lane == 0 && first_bad != INT64_MAX) {
+      atomicMin(bad, static_cast<unsigned long long>(first_bad));
+    }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, off));
-    x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, off));
-    y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, off));
-    y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, off));
+    for (int off = 16; off > 0; off >>= 1) {
+      x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+      x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+      y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, off));
+      y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, off));
+    }
+    if (lane == 0) {
+      const double4 b = make_double4(x0, x1, y0, y1);
+      box[tile] = b;
+      if (h_box) h_box[tile] = b;  // (host-mapped: the extents need no D2H copy)
+      trange[tile] = make_double2(t[first], t[last - 1]);
+    }
   }
-  if (lane == 0) {
-    box[tile] = make_double4(x0, x1, y0, y1);
-    trange[tile] = make_double2(t[first], t[last - 1]);
+  // the last block out hands the first bad index to the host (mapped) and
+  // re-arms the device minimum for the next load
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      __threadfence();
+      *h_bad = atomicExch(bad, ~0ULL);
+      *done = 0u;
+    }
   }
 }
 
@@ -1574,10 +1589,11 @@ __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict
 
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
                               double4* box, double2* trange, unsigned long long* bad,
+                              unsigned int* done, unsigned long long* h_bad, double4* h_box,
                               cudaStream_t stream) {
   const int64_t ntiles = (n + kTS - 1) / kTS;
   tile_box_kernel<<<static_cast<unsigned>((ntiles + 7) / 8), 256, 0, stream>>>(
-      x, y, t, n, npad, box, trange, bad);
+      x, y, t, n, npad, box, trange, bad, done, h_bad, h_box);
   return cudaGetLastError();
 }
 

@@ -159,11 +159,14 @@ struct FinArgs {
 };
 
 // Launch wrappers (sthk_kernels.cu). All enqueue on `stream`.
-// Per-tile bounding boxes; also zeroes the pad tail [n, npad) of x, y, t and
-// runs the EventSet checks (finite, t >= 0, sorted): *bad = min(*bad, first
-// failing index) -- the caller initialises *bad to all ones.
+// Per-tile bounding boxes (also into h_box, host-mapped, if non-null); also
+// zeroes the pad tail [n, npad) of x, y, t and runs the EventSet checks
+// (finite, t >= 0, sorted): the first failing index (all ones: none) lands in
+// *h_bad (host-mapped). *bad (device, all ones between loads) and *done (0)
+// are re-armed by the kernel's last block.
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
                               double4* box, double2* trange, unsigned long long* bad,
+                              unsigned int* done, unsigned long long* h_bad, double4* h_box,
                               cudaStream_t stream);
 // Per-evaluation preparation (prep_kernel); every output optional (nullptr):
 // kSym coordinates xs, ys = (x, y) * sx and the far tier's FP32 copies
