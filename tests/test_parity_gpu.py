@@ -122,6 +122,40 @@ def test_partition_bitwise_invariant(engine, k):
         assert a[0] == b[0] and np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
 
 
+def test_pair_counters_and_results_through_mapped_memory(engine):
+    """Results and (timing) pair counters reach the host through device-mapped
+    memory written by the last kernel (fused final sum for one shard, the
+    final-sum kernel for several), which also re-zeroes the counters: repeated
+    timed evaluations report the same counts, equal across shard counts, and
+    the result matches an untimed evaluation bitwise."""
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=12000)
+    engine.load(ev)
+    engine.set_params(pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695))
+    engine.set_background_cache(False)
+    keys = ("pairs_bg", "pairs_tr", "pairs_any", "exec_bg", "exec_geom", "exec_sym", "exec_far")
+    try:
+        base = engine.loglik_grad()
+        counts = []
+        for k in (1, 1, 3, 3, 1):
+            engine.set_virtual_shards(k)
+            engine.set_timing(True)
+            r = engine.loglik_grad()
+            st = engine.stats()
+            engine.set_timing(False)
+            counts.append(tuple(st[q] for q in keys))
+            assert r[0] == base[0] and np.array_equal(r[2], base[2])
+        assert counts[0][0] > 0 and len(set(counts)) == 1, counts
+        engine.set_virtual_shards(1)
+        engine.loglik_grad()  # untimed: counters untouched, reported as 0
+        assert all(engine.stats()[q] == 0 for q in keys)
+    finally:
+        engine.set_virtual_shards(1)
+        engine.set_timing(False)
+        engine.set_background_cache(True)
+
+
 def test_per_event_sums_to_total(engine):
     # test_likelihood.cpp:134-146
     ev = pk.generateBenchmarkCloud(120, pk.SimWindow(0, 4, 0, 4, 60), 5)
