@@ -1,30 +1,33 @@
 // sm_100a kernels of the B200 spatiotemporal-Hawkes likelihood engine.
 //
-// One evaluation = plan -> pairs -> finalize -> [NCCL all-reduce] -> final sum.
+// One evaluation = (plan || prep) -> pair kernels -> finalize [-> NCCL
+// all-reduce -> final sum]; the host side is sthk_engine.cpp, the reference
+// algorithm pairReduceBlock (backend.hpp:95-137) with HawkesPairTerm
+// (kernels.hpp:76-106) and logLikelihood (likelihood.cpp:10-55).
 //
-//  plan_ranges / plan_items   per 128-row target tile, the live source range
-//                             [lo, hi) from a binary search on the sorted
-//                             times (exact underflow culling),
-//                             cut into (tile, chunk) work items.
-//  pair_kernel<GRAD>          the O(N^2) hot loop (reference: pairReduceBlock,
-//                             backend.hpp:95-137, with HawkesPairTerm,
-//                             kernels.hpp:76-106). Persistent CTAs pull work
-//                             items from an atomic counter; each CTA owns 128
-//                             targets in registers (one per thread) and
-//                             streams 128-source stages through shared memory
-//                             with double-buffered cp.async.bulk (TMA) copies.
-//                             Per stage a CTA-uniform mode is chosen from the
-//                             stage/tile time ranges: background on/off and
-//                             trigger none / unmasked / masked (the strict
-//                             t_src < t_tgt rule, kernels.hpp:44,99-100).
-//                             With GRAD the 4 extra gradient sums are fused
-//                             into the same pass.
-//  finalize_kernel<GRAD>      per row: sum chunk partials in chunk order,
-//                             lambda, compensator (kernels.hpp:54-65), log,
-//                             gradient terms, degenerate flag
-//                             (likelihood.cpp:34-43); then a fixed-order
-//                             block tree-reduction into per-1024-row partials.
-//  final_sum_kernel           fixed-order sum of the block partials.
+//  tile_box_kernel        (once per load) per 128-event tile bounding box and
+//                         time range, pad zeroing, the EventSet checks.
+//  plan_kernel            per 128-row target tile the live source ranges from
+//                         sorted-time searches (exact underflow culling), split
+//                         into the general near list, the trigger-free near
+//                         list and the FP32 far list, each ordered largest
+//                         item first.
+//  prep_kernel            scaled FP64 / FP32 coordinates, zeroed fixed-point
+//                         accumulators, compensator terms (kernels.hpp:54-65).
+//  sym_kernel<GRAD, BGONLY>  the FP64 near sweep: symmetric background (row
+//                         and column sums, fixed-point integer atomics),
+//                         trigger rows (the strict t_src < t_tgt rule,
+//                         kernels.hpp:99-100), gradient sums fused (SURVEY.md
+//                         §8 a16); BGONLY: the trigger-free variant.
+//  far_kernel<GRAD>       the FP32 far tier (every exponent < -40), concurrent
+//                         with the near sweep on a second stream.
+//  pair_kernel<GRAD>      the row-only (non-symmetric) sweep, kernel mode 0.
+//  finalize_kernel<GRAD>  per row: chunk partials in chunk order, lambda, log,
+//                         gradient terms, degenerate flag (likelihood.cpp:
+//                         34-43); block partials, and for one shard the fused
+//                         fixed-order final sum into host-mapped memory.
+//  final_sum_kernel       fixed-order sum of the block partials (several
+//                         shards, after the NCCL all-reduce).
 //
 // Determinism: every floating-point sum has a fixed order that depends only
 // on (events, params) -- not on scheduling, culling decisions or the number
