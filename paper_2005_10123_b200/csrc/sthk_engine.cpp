@@ -213,7 +213,7 @@ constexpr int kChunksTarget = 48;  // source chunks across N (work-item granular
 constexpr double kFarExponent = 40.0;
 constexpr double kFarCoordMax = 4096.0;
 constexpr int kMaxAdj = 16;  // trigger-free split: at most 16 stages kept with the tile
-constexpr int64_t kBgSplitMinEvents = 64 * 1024;  // trigger-free split only from 64k events
+constexpr int64_t kBgSplitMinEvents = 36 * 1024;  // trigger-free split only from 36k events
 
 void set_dev(const Slot& s) { ck(cudaSetDevice(s.dev), "cudaSetDevice"); }
 
@@ -505,7 +505,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
                          e.ext_y * pl.sxf <= kFarCoordMax && e.tile_tspan * pl.stf <= kFarCoordMax;
   const bool far_full = far_guard && !(std::max(pl.k.dB, pl.k.dT) <= pl.tfar);
   // (a third kernel only pays off with enough row tiles to amortise its
-  // launch and per-CTA setup: measured break-even between N = 50k and 85k)
+  // launch and per-CTA setup: measured break-even between N = 30k and 40k)
   int bg_adj = 0;
   if (sym && e.bg_split && !e.adj_gap.empty() && e.n >= kBgSplitMinEvents) {
     const double dT_phys = sthk::kCullExponent / e.p[4] * (1.0 + 1e-9);

@@ -515,7 +515,7 @@ def test_random_regimes_vs_oracle(engine, seed):
 
 def test_bgonly_kernel_consistent(engine):
     """Near stages beyond the trigger window run in the trigger-free kernel (from
-    64k events). With
+    36k events). With
     it on, results are bitwise identical with the caches on or off; against the
     single near kernel they differ only by the grouping of the per-item FP64 row
     partials (<= 1e-14 relative)."""
