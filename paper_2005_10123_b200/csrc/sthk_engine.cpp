@@ -96,8 +96,7 @@ struct Slot {
   size_t xs_cap = 0, ys_cap = 0;
   float *xf = nullptr, *yf = nullptr, *tf = nullptr;  // kSym far tier: FP32 coordinates
   size_t xf_cap = 0, yf_cap = 0, tf_cap = 0;
-  double4* h_box = nullptr;  // pinned: tile boxes (coordinate extents at load)
-  size_t h_box_cap = 0;
+  double* h_stats = nullptr;  // pinned, device-mapped: load statistics (sthk::kLoadStats)
   double4* tile_box = nullptr;
   size_t box_cap = 0;
   int2* ranges = nullptr;
@@ -212,7 +211,7 @@ constexpr int kChunksTarget = 48;  // source chunks across N (work-item granular
 // i.e. < 1% of a term below 4.3e-18.
 constexpr double kFarExponent = 40.0;
 constexpr double kFarCoordMax = 4096.0;
-constexpr int kMaxAdj = 16;  // trigger-free split: at most 16 stages kept with the tile
+constexpr int kMaxAdj = sthk::kLoadAdj;  // trigger-free split: at most 16 stages kept with the tile
 constexpr int64_t kBgSplitMinEvents = 36 * 1024;  // trigger-free split only from 36k events
 
 void set_dev(const Slot& s) { ck(cudaSetDevice(s.dev), "cudaSetDevice"); }
@@ -230,6 +229,9 @@ void init_slot(Slot& s, int dev) {
   ck(cudaMalloc(&s.scalars, 16 * sizeof(int)), "cudaMalloc");
   ck(cudaMemset(s.scalars, 0, 16 * sizeof(int)), "memset");
   ck(cudaHostAlloc(&s.h_bad, sizeof(unsigned long long),
+                   cudaHostAllocMapped | cudaHostAllocPortable),
+     "cudaHostAlloc");
+  ck(cudaHostAlloc(&s.h_stats, sizeof(double) * sthk::kLoadStats,
                    cudaHostAllocMapped | cudaHostAllocPortable),
      "cudaHostAlloc");
   // the load checks' device minimum starts (and is re-armed) at all ones
@@ -279,7 +281,7 @@ void free_slot(Slot& s) {
     if (p) cudaFree(p);
   }
   for (void* p : {static_cast<void*>(s.h_out), static_cast<void*>(s.h_counts),
-                  static_cast<void*>(s.h_bad), static_cast<void*>(s.h_box),
+                  static_cast<void*>(s.h_bad), static_cast<void*>(s.h_stats),
                   static_cast<void*>(s.h_per_event), static_cast<void*>(s.h_ex)}) {
     if (p) cudaFreeHost(p);
   }
@@ -1116,24 +1118,12 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       dev_grow(s.tile_trange, s.trange_cap, static_cast<size_t>(npad / kTS));
       auto* bad = reinterpret_cast<unsigned long long*>(s.scalars + 4);
       auto* done = reinterpret_cast<unsigned int*>(s.scalars + 12);
-      double4* d_hbox = nullptr;
-      if (&s == &e->slots[0]) {  // coordinate extents for the far-tier guard (host-mapped)
-        const size_t nt = static_cast<size_t>(npad / kTS);
-        if (s.h_box_cap < nt) {
-          if (s.h_box) ck(cudaFreeHost(s.h_box), "cudaFreeHost");
-          s.h_box = nullptr;
-          s.h_box_cap = 0;
-          ck(cudaHostAlloc(&s.h_box, sizeof(double4) * nt,
-                           cudaHostAllocMapped | cudaHostAllocPortable),
-             "cudaHostAlloc");
-          s.h_box_cap = nt;
-        }
-        ck(cudaHostGetDevicePointer(&d_hbox, s.h_box, 0), "cudaHostGetDevicePointer");
-      }
       unsigned long long* d_hbad = nullptr;
       ck(cudaHostGetDevicePointer(&d_hbad, s.h_bad, 0), "cudaHostGetDevicePointer");
+      double* d_hstats = nullptr;
+      ck(cudaHostGetDevicePointer(&d_hstats, s.h_stats, 0), "cudaHostGetDevicePointer");
       ck(sthk::launch_tile_boxes(s.x, s.y, s.t, n, npad, s.tile_box, s.tile_trange, bad, done,
-                                 d_hbad, d_hbox, s.stream),
+                                 d_hbad, d_hstats, s.stream),
          "tile boxes + checks");
     }
     for (Slot& s : e->slots) {
@@ -1143,31 +1133,13 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
     const unsigned long long first_bad = *e->slots[0].h_bad;
     if (first_bad != ~0ULL) throw_event_error(x, y, t, static_cast<int64_t>(first_bad));
     validate_window_end(t, n, window_end);
-    {
-      const Slot& s0 = e->slots[0];
-      const int64_t nt = (n + kTS - 1) / kTS;
-      double ex = 0, ey = 0;
-      for (int64_t k = 0; k < nt; ++k) {
-        const double4 b = s0.h_box[k];
-        ex = std::max({ex, std::fabs(b.x - x[0]), std::fabs(b.y - x[0])});
-        ey = std::max({ey, std::fabs(b.z - y[0]), std::fabs(b.w - y[0])});
-      }
-      e->ext_x = ex;
-      e->ext_y = ey;
-      double span = 0;
-      for (int64_t k = 0; k < nt; ++k) {
-        span = std::max(span, t[std::min(k * kTS + kTS, n) - 1] - t[k * kTS]);
-      }
-      e->tile_tspan = span;
-      e->adj_gap.assign(kMaxAdj, std::numeric_limits<double>::infinity());
-      for (int k = 1; k <= kMaxAdj; ++k) {
-        double g = std::numeric_limits<double>::infinity();
-        for (int64_t tile = k + 1; tile < nt; ++tile) {
-          const int64_t fi = tile * kTS;
-          g = std::min(g, t[fi] - t[fi - static_cast<int64_t>(k) * kTS - 1]);
-        }
-        e->adj_gap[k - 1] = g;
-      }
+    {  // load statistics from the check kernel (coordinate extents for the far-tier
+       // guard, tile time span, stage gaps for the trigger-free split)
+      const double* st = e->slots[0].h_stats;
+      e->ext_x = st[0];
+      e->ext_y = st[1];
+      e->tile_tspan = st[2];
+      e->adj_gap.assign(st + 3, st + 3 + kMaxAdj);
     }
     e->n = n;
     e->npad = npad;

@@ -1312,7 +1312,7 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
 __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
                                 double* __restrict__ t, int64_t n, int64_t npad, double4* box,
                                 double2* trange, unsigned long long* bad, unsigned int* done,
-                                unsigned long long* h_bad, double4* h_box) {
+                                unsigned long long* h_bad, double* h_stats) {
   // zero the pad tail [n, npad) of the coordinate arrays (never read as sources)
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid < npad - n) {
@@ -1357,20 +1357,64 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
     if (lane == 0) {
       const double4 b = make_double4(x0, x1, y0, y1);
       box[tile] = b;
-      if (h_box) h_box[tile] = b;  // (host-mapped: the extents need no D2H copy)
       trange[tile] = make_double2(t[first], t[last - 1]);
     }
   }
-  // the last block out hands the first bad index to the host (mapped) and
-  // re-arms the device minimum for the next load
+  // the last block out hands the first bad index and the load statistics to
+  // the host (mapped) and re-arms the device minimum for the next load
+  __shared__ bool s_last;
+  __shared__ double s_w[8][kLoadStats];
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(done, 1u) == gridDim.x - 1) {
-      __threadfence();
-      *h_bad = atomicExch(bad, ~0ULL);
-      *done = 0u;
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int64_t nt = (n + kTS - 1) / kTS;
+  const double x00 = __ldcg(x), y00 = __ldcg(y);
+  double v[kLoadStats];  // maxima [0..2], minima [3..]
+#pragma unroll
+  for (int q = 0; q < kLoadStats; ++q) v[q] = q < 3 ? 0.0 : __longlong_as_double(0x7ff0000000000000LL);
+  for (int64_t k = threadIdx.x; k < nt; k += blockDim.x) {
+    const double2 bxy = __ldcg(reinterpret_cast<const double2*>(&box[k]));
+    const double2 bzw = __ldcg(reinterpret_cast<const double2*>(&box[k]) + 1);
+    const double4 b = make_double4(bxy.x, bxy.y, bzw.x, bzw.y);
+    const double2 tr = __ldcg(&trange[k]);
+    v[0] = fmax(v[0], fmax(fabs(b.x - x00), fabs(b.y - x00)));
+    v[1] = fmax(v[1], fmax(fabs(b.z - y00), fabs(b.w - y00)));
+    v[2] = fmax(v[2], tr.y - tr.x);
+#pragma unroll
+    for (int a = 1; a <= kLoadAdj; ++a) {
+      if (k >= a + 1) v[2 + a] = fmin(v[2 + a], tr.x - __ldcg(&trange[k - a - 1]).y);
     }
+  }
+#pragma unroll
+  for (int q = 0; q < kLoadStats; ++q) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, v[q], off);
+      v[q] = q < 3 ? fmax(v[q], o) : fmin(v[q], o);
+    }
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int q = 0; q < kLoadStats; ++q) s_w[w][q] = v[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < kLoadStats) {
+    const int q = threadIdx.x;
+    double r = s_w[0][q];
+    for (int ww = 1; ww < static_cast<int>(blockDim.x >> 5); ++ww) {
+      r = q < 3 ? fmax(r, s_w[ww][q]) : fmin(r, s_w[ww][q]);
+    }
+    h_stats[q] = r;
+  }
+  if (threadIdx.x == 0) {
+    *h_bad = atomicExch(bad, ~0ULL);
+    *done = 0u;
   }
 }
 
@@ -1592,11 +1636,11 @@ __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict
 
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
                               double4* box, double2* trange, unsigned long long* bad,
-                              unsigned int* done, unsigned long long* h_bad, double4* h_box,
+                              unsigned int* done, unsigned long long* h_bad, double* h_stats,
                               cudaStream_t stream) {
   const int64_t ntiles = (n + kTS - 1) / kTS;
   tile_box_kernel<<<static_cast<unsigned>((ntiles + 7) / 8), 256, 0, stream>>>(
-      x, y, t, n, npad, box, trange, bad, done, h_bad, h_box);
+      x, y, t, n, npad, box, trange, bad, done, h_bad, h_stats);
   return cudaGetLastError();
 }
 

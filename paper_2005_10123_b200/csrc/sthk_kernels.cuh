@@ -159,14 +159,21 @@ struct FinArgs {
 };
 
 // Launch wrappers (sthk_kernels.cu). All enqueue on `stream`.
-// Per-tile bounding boxes (also into h_box, host-mapped, if non-null); also
-// zeroes the pad tail [n, npad) of x, y, t and runs the EventSet checks
-// (finite, t >= 0, sorted): the first failing index (all ones: none) lands in
-// *h_bad (host-mapped). *bad (device, all ones between loads) and *done (0)
-// are re-armed by the kernel's last block.
+// Load-time statistics of an event set (tile_box_kernel, host-mapped):
+// [0] max |x - x[0]|, [1] max |y - y[0]|, [2] max time span of a 128-event
+// tile, [3 + k - 1] (k = 1..kLoadAdj) min over tiles of t[first] -
+// t[first - 128 k - 1] (the gap k stages ahead of a tile's first event).
+constexpr int kLoadAdj = 16;
+constexpr int kLoadStats = 3 + kLoadAdj;
+
+// Per-tile bounding boxes and time ranges; also zeroes the pad tail [n, npad)
+// of x, y, t and runs the EventSet checks (finite, t >= 0, sorted). The
+// kernel's last block writes the first failing index (all ones: none) to
+// *h_bad and the load statistics to h_stats (both host-mapped), and re-arms
+// *bad (device, all ones between loads) and *done (0).
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
                               double4* box, double2* trange, unsigned long long* bad,
-                              unsigned int* done, unsigned long long* h_bad, double4* h_box,
+                              unsigned int* done, unsigned long long* h_bad, double* h_stats,
                               cudaStream_t stream);
 // Per-evaluation preparation (prep_kernel); every output optional (nullptr):
 // kSym coordinates xs, ys = (x, y) * sx and the far tier's FP32 copies
