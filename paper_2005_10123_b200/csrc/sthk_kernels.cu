@@ -184,15 +184,15 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
   rgf = make_int2(flo, fb);
   crf = fb > flo ? make_int2(flo / a.sc, (fb - 1) / a.sc) : make_int2(0, -1);
   rgb = make_int2(fb, fbt);
-  crb = fbt > fb ? make_int2(fb / a.sc, (fbt - 1) / a.sc) : make_int2(0, -1);
+  crb = fbt > fb ? make_int2(fb / a.sc_bg, (fbt - 1) / a.sc_bg) : make_int2(0, -1);
 }
 
 // Number of 128-source stages of work item (tile, chunk) -- the same bounds
 // the pair kernels compute.
-__device__ __forceinline__ int item_stages(const PlanArgs& a, int2 rg, int chunk) {
-  int s_begin = max(rg.x, chunk * a.sc);
+__device__ __forceinline__ int item_stages(int sc, int2 rg, int chunk) {
+  int s_begin = max(rg.x, chunk * sc);
   s_begin -= s_begin % kTS;
-  const int s_end = min(rg.y, (chunk + 1) * a.sc);
+  const int s_end = min(rg.y, (chunk + 1) * sc);
   return max((s_end - s_begin + kTS - 1) / kTS, 0);
 }
 
@@ -207,8 +207,8 @@ constexpr int kPlanBins = 1024;  // item-size classes (stages, clamped)
 // Work list of one kind (near or far) ordered by decreasing item size: a
 // histogram of the items' stage counts, an exclusive scan over the bins in
 // decreasing size, then placement (1024 threads, one CTA).
-__device__ void plan_list(const PlanArgs& a, const int2* ranges, const int2* crange, int2* items,
-                          int* n_items, int* work_counter, int* s_hist, int* s_warp) {
+__device__ void plan_list(const PlanArgs& a, int sc, const int2* ranges, const int2* crange,
+                          int2* items, int* n_items, int* work_counter, int* s_hist, int* s_warp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ntiles = a.tile1 - a.tile0;
   for (int b = tid; b < kPlanBins; b += 1024) s_hist[b] = 0;
@@ -216,7 +216,7 @@ __device__ void plan_list(const PlanArgs& a, const int2* ranges, const int2* cra
   for (int i = tid; i < ntiles; i += 1024) {
     const int2 rg = ranges[a.tile0 + i], cr = crange[a.tile0 + i];
     for (int c = cr.x; c <= cr.y; ++c) {
-      atomicAdd(&s_hist[min(item_stages(a, rg, c), kPlanBins - 1)], 1);
+      atomicAdd(&s_hist[min(item_stages(sc, rg, c), kPlanBins - 1)], 1);
     }
   }
   __syncthreads();
@@ -252,7 +252,7 @@ __device__ void plan_list(const PlanArgs& a, const int2* ranges, const int2* cra
     const int tile = a.tile0 + i;
     const int2 rg = ranges[tile], cr = crange[tile];
     for (int ch = cr.x; ch <= cr.y; ++ch) {
-      const int pos = atomicAdd(&s_hist[min(item_stages(a, rg, ch), kPlanBins - 1)], 1);
+      const int pos = atomicAdd(&s_hist[min(item_stages(sc, rg, ch), kPlanBins - 1)], 1);
       items[pos] = make_int2(tile, ch);
     }
   }
@@ -292,14 +292,14 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
     }
   }
   __syncthreads();
-  plan_list(a, a.ranges, a.crange, a.items, a.n_items, a.work_counter, s_hist, s_warp);
+  plan_list(a, a.sc, a.ranges, a.crange, a.items, a.n_items, a.work_counter, s_hist, s_warp);
   if (a.ranges_far) {
-    plan_list(a, a.ranges_far, a.crange_far, a.items_far, a.n_items_far, a.work_counter_far,
-              s_hist, s_warp);
+    plan_list(a, a.sc, a.ranges_far, a.crange_far, a.items_far, a.n_items_far,
+              a.work_counter_far, s_hist, s_warp);
   }
   if (a.ranges_bg) {
-    plan_list(a, a.ranges_bg, a.crange_bg, a.items_bg, a.n_items_bg, a.work_counter_bg, s_hist,
-              s_warp);
+    plan_list(a, a.sc_bg, a.ranges_bg, a.crange_bg, a.items_bg, a.n_items_bg,
+              a.work_counter_bg, s_hist, s_warp);
   }
 }
 

@@ -86,6 +86,7 @@ struct PlanArgs {
   // before first - bg_adj * 128 (no live trigger, host-checked) go to a third
   // list for the trigger-free FP64 kernel; nullptr: off
   int bg_adj;           // near stages kept with the tile for the general kernel (>= 1)
+  int sc_bg;            // sources per chunk of the background-only list (multiple of kTS)
   int2* ranges_bg;
   int2* crange_bg;
   int2* items_bg;
