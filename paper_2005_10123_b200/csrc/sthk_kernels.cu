@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
 // Row partials of the 4 warps are combined in a fixed order at item end.
 constexpr int kSymR = 4;  // rows per thread
 #ifndef STHK_SYM_G
-#define STHK_SYM_G 4      // columns per shuffle reduce-scatter group (2 or 4)
+#define STHK_SYM_G 4      // columns per shuffle reduce-scatter group (the far tier assumes 4)
 #endif
 #ifndef STHK_SYM_MINB
 #define STHK_SYM_MINB 3   // resident sym CTAs per SM the register budget targets
