@@ -83,6 +83,7 @@ struct Slot {
   size_t tpart_far_cap = 0;
   double2* tile_trange = nullptr;    // per tile: t first, t last
   double* comp = nullptr;            // compensator terms [4][npad] (prep_kernel)
+  double* piv = nullptr;             // plan search pivots [kPlanPivots] (written at load)
   size_t comp_cap = 0;
   cudaEvent_t prepped = nullptr;     // prep done (stream 2) -> pair kernels (stream 1)
   size_t trange_cap = 0;
@@ -269,6 +270,7 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.ranges_far), static_cast<void*>(s.crange_far),
                   static_cast<void*>(s.items_far), static_cast<void*>(s.tpart_far),
                   static_cast<void*>(s.tile_trange), static_cast<void*>(s.comp),
+                  static_cast<void*>(s.piv),
                   static_cast<void*>(s.ranges_bg), static_cast<void*>(s.crange_bg),
                   static_cast<void*>(s.items_bg),
                   static_cast<void*>(s.ranges), static_cast<void*>(s.counts),
@@ -676,6 +678,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     }
     sthk::PlanArgs pa{};
     pa.t = s.t;
+    pa.piv = s.piv;
+    pa.tile_trange = s.tile_trange;
     pa.n = e.n;
     pa.tile0 = tile0;
     pa.tile1 = tile1;
@@ -1136,8 +1140,9 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       ck(cudaHostGetDevicePointer(&d_hbad, s.h_bad, 0), "cudaHostGetDevicePointer");
       double* d_hstats = nullptr;
       ck(cudaHostGetDevicePointer(&d_hstats, s.h_stats, 0), "cudaHostGetDevicePointer");
-      ck(sthk::launch_tile_boxes(s.x, s.y, s.t, n, npad, s.tile_box, s.tile_trange, bad, done,
-                                 d_hbad, d_hstats, s.stream),
+      if (!s.piv) ck(cudaMalloc(&s.piv, sizeof(double) * sthk::kPlanPivots), "cudaMalloc");
+      ck(sthk::launch_tile_boxes(s.x, s.y, s.t, n, npad, s.tile_box, s.tile_trange, s.piv, bad,
+                                 done, d_hbad, d_hstats, s.stream),
          "tile boxes + checks");
     }
     for (Slot& s : e->slots) {

@@ -49,11 +49,13 @@ constexpr double kInvSqrt2 = 0.7071067811865475244;     // kernels.hpp:14
 constexpr double kInvSqrt2Pi = 0.3989422804014326779;   // kernels.hpp:13
 
 // Sorted-time searches in two levels: kPivots evenly spaced pivots
-// piv[k] = t[k * stride] in shared memory narrow the range to one stride,
-// then a binary search over global memory finishes it (log2(stride) dependent
-// loads instead of log2(n)). STRICT: first i with t[i] >= v (lower bound),
-// else first i with t[i] > v (upper bound).
-constexpr int kPivots = 1024;
+// piv[k] = t[k * stride] (computed at load, +inf padded) in shared memory
+// narrow the range to one stride, then a binary search over global memory
+// finishes it (log2(stride) loads, 4 at C2). The plan is one CTA, so its
+// global loads are bounded by one SM's outstanding-miss capacity: fewer loads
+// per search, not fewer dependent steps, is what shortens it.
+constexpr int kPivots = kPlanPivots;
+__device__ __forceinline__ int64_t pivot_stride(int64_t n) { return (n + kPivots - 1) / kPivots; }
 
 struct Pivots {
   const double* piv;  // shared memory, np entries
@@ -61,69 +63,51 @@ struct Pivots {
   int64_t stride;
 };
 
-template <bool STRICT>
-__device__ __forceinline__ bool before(double tv, double v) {
-  return STRICT ? (tv < v) : (tv <= v);
-}
-
-template <bool STRICT>
-__device__ __forceinline__ int64_t bound_t(const double* t, int64_t n, double v, const Pivots& p) {
-  // last pivot k with piv[k] "before" v (pivots are sorted)
-  int klo = 0, khi = p.np;  // answer k = (first pivot not before v) - 1
-  while (klo < khi) {
-    const int mid = (klo + khi) >> 1;
-    if (before<STRICT>(p.piv[mid], v)) klo = mid + 1; else khi = mid;
-  }
-  if (klo == 0) return 0;  // t[0] is not before v
-  int64_t lo = static_cast<int64_t>(klo - 1) * p.stride + 1;
-  int64_t hi = min(static_cast<int64_t>(klo) * p.stride, n);
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (before<STRICT>(t[mid], v)) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-// K independent bound_t searches in lockstep: each level issues the K
-// dependent global loads back to back, so their latencies overlap (the
-// plan's cost is these load chains).
+// K independent searches in lockstep. Result: the first index in [0, n) whose
+// time is not "before" v (t < v when strict, t <= v otherwise).
 template <int K>
 __device__ __forceinline__ void bounds_lockstep(const double* t, int64_t n, const Pivots& p,
                                                 const double (&v)[K], const bool (&strict)[K],
                                                 int64_t (&out)[K]) {
-  int64_t lo[K], hi[K];
+  auto before = [&](int k, double tv) { return strict[k] ? tv < v[k] : tv <= v[k]; };
+  // pivot level: branch-free power-of-two steps over the +inf-padded pivots,
+  // the K shared-memory chains interleaved; kp = number of pivots before v
+  int kp[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    int klo = 0, khi = p.np;
-    while (klo < khi) {
-      const int mid = (klo + khi) >> 1;
-      const double pv = p.piv[mid];
-      if (strict[k] ? pv < v[k] : pv <= v[k]) klo = mid + 1; else khi = mid;
-    }
-    if (klo == 0) {
-      lo[k] = hi[k] = 0;
-    } else {
-      lo[k] = static_cast<int64_t>(klo - 1) * p.stride + 1;
-      hi[k] = min(static_cast<int64_t>(klo) * p.stride, n);
-    }
+  for (int k = 0; k < K; ++k) kp[k] = 0;
+#pragma unroll
+  for (int step = kPivots / 2; step > 0; step >>= 1) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) kp[k] = before(k, p.piv[kp[k] + step - 1]) ? kp[k] + step : kp[k];
   }
-  for (;;) {
-    bool any = false;
 #pragma unroll
-    for (int k = 0; k < K; ++k) any |= lo[k] < hi[k];
-    if (!any) break;
-    int64_t mid[K];
+  for (int k = 0; k < K; ++k) kp[k] = before(k, p.piv[kPivots - 1]) ? kPivots : kp[k];
+  int lo[K], hi[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {  // (kp == 0: t[0] is not before v)
+    lo[k] = kp[k] == 0 ? 0 : (kp[k] - 1) * static_cast<int>(p.stride) + 1;
+    hi[k] = kp[k] == 0 ? 0 : static_cast<int>(min(static_cast<int64_t>(kp[k]) * p.stride, n));
+  }
+  // global level: a uniform number of binary rounds (segments are at most
+  // stride - 1 long), one load per search per round (clamped in range; an
+  // empty segment ignores it)
+  const int nmax = static_cast<int>(n) - 1;
+  int rounds = 0;
+  for (int64_t len = p.stride - 1; len > 0; len >>= 1) ++rounds;
+  for (int it = 0; it < rounds; ++it) {
+    int m[K];
     double tv[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      mid[k] = (lo[k] + hi[k]) >> 1;
-      tv[k] = lo[k] < hi[k] ? t[mid[k]] : 0.0;
+      m[k] = (lo[k] + hi[k]) >> 1;
+      tv[k] = t[min(m[k], nmax)];
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      if (lo[k] < hi[k]) {
-        if (strict[k] ? tv[k] < v[k] : tv[k] <= v[k]) lo[k] = mid[k] + 1; else hi[k] = mid[k];
-      }
+      const bool live = lo[k] < hi[k];
+      const bool b = before(k, tv[k]);
+      lo[k] = live && b ? m[k] + 1 : lo[k];
+      hi[k] = live && !b ? m[k] : hi[k];
     }
   }
 #pragma unroll
@@ -138,7 +122,8 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
                                           int2& cr, int2& rgf, int2& crf, int2& rgb, int2& crb) {
   const int64_t first = static_cast<int64_t>(tile) * kTM;
   const int64_t last = min(first + kTM, a.n) - 1;
-  const double tmin = a.t[first], tmax = a.t[last];
+  const double2 tr = a.tile_trange[tile];  // (t[first], t[last]), one load
+  const double tmin = tr.x, tmax = tr.y;
   // searches: live-range start, live-range end (full row-kernel sweeps) or,
   // in symmetric mode, the far tier's exact-cull start; the far split
   double v[3] = {a.trig_only ? tmin - a.dT : tmin - fmax(a.dB, a.dT),
@@ -207,14 +192,17 @@ constexpr int kPlanBins = 1024;  // item-size classes (stages, clamped)
 // Work list of one kind (near or far) ordered by decreasing item size: a
 // histogram of the items' stage counts, an exclusive scan over the bins in
 // decreasing size, then placement (1024 threads, one CTA).
+// (my_rg / my_cr: this thread's first tile, kept in registers since phase 1)
 __device__ void plan_list(const PlanArgs& a, int sc, const int2* ranges, const int2* crange,
-                          int2* items, int* n_items, int* work_counter, int* s_hist, int* s_warp) {
+                          int2 my_rg, int2 my_cr, int2* items, int* n_items, int* work_counter,
+                          int* s_hist, int* s_warp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ntiles = a.tile1 - a.tile0;
   for (int b = tid; b < kPlanBins; b += 1024) s_hist[b] = 0;
   __syncthreads();
   for (int i = tid; i < ntiles; i += 1024) {
-    const int2 rg = ranges[a.tile0 + i], cr = crange[a.tile0 + i];
+    const int2 rg = i == tid ? my_rg : ranges[a.tile0 + i];
+    const int2 cr = i == tid ? my_cr : crange[a.tile0 + i];
     for (int c = cr.x; c <= cr.y; ++c) {
       atomicAdd(&s_hist[min(item_stages(sc, rg, c), kPlanBins - 1)], 1);
     }
@@ -250,7 +238,8 @@ __device__ void plan_list(const PlanArgs& a, int sc, const int2* ranges, const i
   __syncthreads();
   for (int i = tid; i < ntiles; i += 1024) {
     const int tile = a.tile0 + i;
-    const int2 rg = ranges[tile], cr = crange[tile];
+    const int2 rg = i == tid ? my_rg : ranges[tile];
+    const int2 cr = i == tid ? my_cr : crange[tile];
     for (int ch = cr.x; ch <= cr.y; ++ch) {
       const int pos = atomicAdd(&s_hist[min(item_stages(sc, rg, ch), kPlanBins - 1)], 1);
       items[pos] = make_int2(tile, ch);
@@ -268,15 +257,24 @@ __device__ void plan_list(const PlanArgs& a, int sc, const int2* ranges, const i
 __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   __shared__ int s_hist[kPlanBins];
   __shared__ int s_warp[32];
-  __shared__ double s_piv[kPivots];
+  __shared__ __align__(8) uint64_t s_bar;
+  extern __shared__ __align__(128) double s_piv[];  // kPivots (dynamic: 64 KB)
   const int tid = threadIdx.x;
   const int ntiles = a.tile1 - a.tile0;
   Pivots pv;
-  pv.stride = (a.n + kPivots - 1) / kPivots;
+  pv.stride = pivot_stride(a.n);
   pv.np = static_cast<int>((a.n + pv.stride - 1) / pv.stride);
   pv.piv = s_piv;
-  for (int k = tid; k < pv.np; k += 1024) s_piv[k] = a.t[k * pv.stride];
+  if (tid == 0) {  // the pivots (precomputed at load): one bulk copy
+    mbar_init(&s_bar, 1);
+    mbar_fence_init();
+    mbar_arrive_expect_tx(&s_bar, kPivots * sizeof(double));
+    tma_load_1d(s_piv, a.piv, kPivots * sizeof(double), &s_bar);
+  }
   __syncthreads();
+  mbar_wait(&s_bar, 0);
+  int2 my[6] = {make_int2(0, 0), make_int2(0, -1), make_int2(0, 0), make_int2(0, -1),
+                make_int2(0, 0), make_int2(0, -1)};  // first tile: near, far, bg (range, chunks)
   for (int i = tid; i < ntiles; i += 1024) {
     int2 rg, cr, rgf, crf, rgb, crb;
     tile_plan(a, pv, a.tile0 + i, rg, cr, rgf, crf, rgb, crb);
@@ -290,15 +288,24 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
       a.ranges_bg[a.tile0 + i] = rgb;
       a.crange_bg[a.tile0 + i] = crb;
     }
+    if (i == tid) {
+      my[0] = rg;
+      my[1] = cr;
+      my[2] = rgf;
+      my[3] = crf;
+      my[4] = rgb;
+      my[5] = crb;
+    }
   }
   __syncthreads();
-  plan_list(a, a.sc, a.ranges, a.crange, a.items, a.n_items, a.work_counter, s_hist, s_warp);
+  plan_list(a, a.sc, a.ranges, a.crange, my[0], my[1], a.items, a.n_items, a.work_counter,
+            s_hist, s_warp);
   if (a.ranges_far) {
-    plan_list(a, a.sc, a.ranges_far, a.crange_far, a.items_far, a.n_items_far,
+    plan_list(a, a.sc, a.ranges_far, a.crange_far, my[2], my[3], a.items_far, a.n_items_far,
               a.work_counter_far, s_hist, s_warp);
   }
   if (a.ranges_bg) {
-    plan_list(a, a.sc_bg, a.ranges_bg, a.crange_bg, a.items_bg, a.n_items_bg,
+    plan_list(a, a.sc_bg, a.ranges_bg, a.crange_bg, my[4], my[5], a.items_bg, a.n_items_bg,
               a.work_counter_bg, s_hist, s_warp);
   }
 }
@@ -1311,7 +1318,8 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
 // independent; computed once per load). Feeds the no-underflow proofs.
 __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
                                 double* __restrict__ t, int64_t n, int64_t npad, double4* box,
-                                double2* trange, unsigned long long* bad, unsigned int* done,
+                                double2* trange, double* __restrict__ piv,
+                                unsigned long long* bad, unsigned int* done,
                                 unsigned long long* h_bad, double* h_stats) {
   // zero the pad tail [n, npad) of the coordinate arrays (never read as sources)
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1319,6 +1327,13 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
     x[n + gid] = 0.0;
     y[n + gid] = 0.0;
     t[n + gid] = 0.0;
+  }
+  // the plan's search pivots t[k * stride], +inf padded to kPivots
+  {
+    const int64_t stride = pivot_stride(n), np = (n + stride - 1) / stride;
+    for (int64_t k = gid; k < kPivots; k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      piv[k] = k < np ? t[k * stride] : __longlong_as_double(0x7ff0000000000000LL);
+    }
   }
   // one warp per tile: 4 coalesced loads per lane, then a shuffle min/max
   const int lane = threadIdx.x & 31;
@@ -1635,12 +1650,12 @@ __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict
 }  // namespace
 
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
-                              double4* box, double2* trange, unsigned long long* bad,
-                              unsigned int* done, unsigned long long* h_bad, double* h_stats,
-                              cudaStream_t stream) {
+                              double4* box, double2* trange, double* piv,
+                              unsigned long long* bad, unsigned int* done,
+                              unsigned long long* h_bad, double* h_stats, cudaStream_t stream) {
   const int64_t ntiles = (n + kTS - 1) / kTS;
   tile_box_kernel<<<static_cast<unsigned>((ntiles + 7) / 8), 256, 0, stream>>>(
-      x, y, t, n, npad, box, trange, bad, done, h_bad, h_stats);
+      x, y, t, n, npad, box, trange, piv, bad, done, h_bad, h_stats);
   return cudaGetLastError();
 }
 
@@ -1658,12 +1673,13 @@ cudaError_t launch_exp_probe(const double* x, int64_t n, double* out, cudaStream
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
   const int ntiles = a.tile1 - a.tile0;
   if (ntiles <= 0) return cudaSuccess;
-  plan_kernel<<<1, 1024, 0, stream>>>(a);
+  plan_kernel<<<1, 1024, kPivots * sizeof(double), stream>>>(a);
   return cudaGetLastError();
 }
 
-// The exp table lives in dynamic shared memory (static + dynamic > 48 KB
-// needs the opt-in attribute); set once per device before the first launch.
+// The exp table (pair kernels) and the search pivots (plan) live in dynamic
+// shared memory (static + dynamic > 48 KB needs the opt-in attribute); set
+// once per device before the first launch.
 cudaError_t prepare_pair_kernels() {
   cudaError_t err = cudaSuccess;
   auto set = [&](const void* f) {
@@ -1677,6 +1693,10 @@ cudaError_t prepare_pair_kernels() {
   set(reinterpret_cast<const void*>(&sym_kernel<false, true>));
   set(reinterpret_cast<const void*>(&pair_kernel<true>));
   set(reinterpret_cast<const void*>(&pair_kernel<false>));
+  const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&plan_kernel),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kPivots * sizeof(double)));
+  if (e != cudaSuccess) err = e;
   return err;
 }
 

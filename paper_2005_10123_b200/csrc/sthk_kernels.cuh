@@ -56,8 +56,12 @@ struct PairConsts {
   double dTf;   // far tier: trigger nonzero in FP32 iff dt <= dTf
 };
 
+constexpr int kPlanPivots = 8192;  // sorted-time search pivots (a power of two; 64 KB)
+
 struct PlanArgs {
   const double* t;
+  const double* piv;            // [kPlanPivots] t[k * ceil(n / kPlanPivots)], +inf padded (load)
+  const double2* tile_trange;   // per 128-event tile: t first, t last (load)
   int64_t n;
   int tile0, tile1;     // this shard's row tiles [tile0, tile1)
   double dB, dT;
@@ -167,15 +171,16 @@ struct FinArgs {
 constexpr int kLoadAdj = 16;
 constexpr int kLoadStats = 3 + kLoadAdj;
 
-// Per-tile bounding boxes and time ranges; also zeroes the pad tail [n, npad)
+// Per-tile bounding boxes and time ranges, and the plan's search pivots
+// (PlanArgs::piv); also zeroes the pad tail [n, npad)
 // of x, y, t and runs the EventSet checks (finite, t >= 0, sorted). The
 // kernel's last block writes the first failing index (all ones: none) to
 // *h_bad and the load statistics to h_stats (both host-mapped), and re-arms
 // *bad (device, all ones between loads) and *done (0).
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
-                              double4* box, double2* trange, unsigned long long* bad,
-                              unsigned int* done, unsigned long long* h_bad, double* h_stats,
-                              cudaStream_t stream);
+                              double4* box, double2* trange, double* piv,
+                              unsigned long long* bad, unsigned int* done,
+                              unsigned long long* h_bad, double* h_stats, cudaStream_t stream);
 // Per-evaluation preparation (prep_kernel); every output optional (nullptr):
 // kSym coordinates xs, ys = (x, y) * sx and the far tier's FP32 copies
 // xf, yf = (x - x[0], y - y[0]) * sxf, tf = (t - t[tile start]) * stf; zeroed
