@@ -3,6 +3,7 @@ reference engine (oracle/_ref). Tolerances from BASELINE.json north_star:
 <= 1e-10 relative on loglik, <= 1e-8 per gradient component (scale-aware
 norm sum_i |d l_i / d p_k| near stationary points)."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -545,3 +546,100 @@ def test_bgonly_kernel_consistent(engine):
     for (a, ga), (b, gb) in zip(out[(True, False)], out[(False, False)]):
         assert abs(a - b) <= 1e-14 * abs(b)
         assert np.allclose(ga, gb, rtol=1e-11, atol=0)
+
+
+def _c2(keep=85000):
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=keep)
+    return ev
+
+
+@pytest.mark.parametrize("theta", [(0.66, 1.6, 14, 0.344, 1440, 0.0695), (1, 1.6, 14, 0.1, 1, 1)])
+def test_full_size_c2_matches_reference_engine(engine, theta):
+    """The bench workload itself (C2, N = 85,000) against the verbatim reference
+    engine on all host cores: loglik to 1e-10 and every per-event term to 1e-12
+    (absolute, or relative above 1)."""
+    if not og.ref_available():
+        pytest.skip("oracle/_ref not built")
+    ev = _c2()
+    lanes = 8 if og.has_avx512() else 4
+    ref, ok, ref_pe = og.ref_loglik(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), np.array(theta),
+                                    os.cpu_count() or 1, lanes, per_event=True)
+    engine.load(ev)
+    engine.set_params(list(theta))
+    ll, valid, pe = engine.loglik(per_event=True)
+    assert ok and valid
+    assert abs(ll - ref) <= LL_TOL * abs(ref), (ll, ref)
+    assert np.all(np.abs(pe - ref_pe) <= 1e-12 * np.maximum(1.0, np.abs(ref_pe)))
+
+
+def test_full_size_properties(engine):
+    """Size-independent properties at the bench size (C2, N = 85,000, loglik +
+    gradient): repeat-bitwise, culled == dense bitwise, 4 virtual shards bitwise,
+    per-event terms summing to the total, far tier vs all-FP64 to 1e-13."""
+    ev = _c2()
+    engine.load(ev)
+    engine.set_params([0.66, 1.6, 14, 0.344, 1440, 0.0695])
+    engine.set_background_cache(False)
+    try:
+        a = engine.loglik_grad(per_event=True)
+        b = engine.loglik_grad(per_event=True)
+        assert a[0] == b[0] and np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
+        engine.set_dense(True)
+        d = engine.loglik_grad()
+        engine.set_dense(False)
+        assert d[0] == a[0] and np.array_equal(d[2], a[2])
+        engine.set_virtual_shards(4)
+        s = engine.loglik_grad()
+        engine.set_virtual_shards(1)
+        assert s[0] == a[0] and np.array_equal(s[2], a[2])
+        assert abs(math.fsum(a[3]) - a[0]) <= 1e-12 * abs(a[0])
+        engine.set_far_tier(False)
+        f = engine.loglik_grad()
+        engine.set_far_tier(True)
+        assert abs(f[0] - a[0]) <= 1e-13 * abs(a[0])
+        assert np.all(np.abs(f[2] - a[2]) <= 1e-11 * np.abs(a[2]) + 1e-9)
+    finally:
+        engine.set_dense(False)
+        engine.set_virtual_shards(1)
+        engine.set_far_tier(True)
+        engine.set_background_cache(True)
+
+
+def test_c3_250k_matches_reference_engine(engine):
+    """The largest C3 sweep point (generateBenchmarkCloud, N = 250,000) against
+    the verbatim reference engine on all host cores, loglik to 1e-10."""
+    if not og.ref_available():
+        pytest.skip("oracle/_ref not built")
+    n = 250000
+    ev = pk.generateBenchmarkCloud(n, pk.SimWindow(0, 15, 0, 15, 4750), n)
+    theta = np.array([0.66, 1.6, 14, 0.344, 1440, 0.0695])
+    ref, ok, _ = og.ref_loglik(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), theta,
+                               os.cpu_count() or 1, 8 if og.has_avx512() else 4)
+    engine.load(ev)
+    engine.set_params(list(theta))
+    ll, valid, _ = engine.loglik()
+    assert ok and valid and abs(ll - ref) <= LL_TOL * abs(ref), (ll, ref)
+
+
+def test_c4_1m_properties(engine):
+    """C4 size (N = 1,000,000, one GPU): bitwise repeatable, bitwise equal over
+    2 virtual shards (the multi-GPU split), per-event terms summing to the total."""
+    n = 1000000
+    ev = pk.generateBenchmarkCloud(n, pk.SimWindow(0, 15, 0, 15, 4750), n)
+    engine.load(ev)
+    engine.set_params([0.66, 1.6, 14, 0.344, 1440, 0.0695])
+    engine.set_background_cache(False)
+    try:
+        a = engine.loglik_grad(per_event=True)
+        b = engine.loglik_grad()
+        engine.set_virtual_shards(2)
+        s = engine.loglik_grad()
+        engine.set_virtual_shards(1)
+        assert a[1] and a[0] == b[0] == s[0]
+        assert np.array_equal(a[2], b[2]) and np.array_equal(a[2], s[2])
+        assert abs(math.fsum(a[3]) - a[0]) <= 1e-12 * abs(a[0])
+    finally:
+        engine.set_virtual_shards(1)
+        engine.set_background_cache(True)
