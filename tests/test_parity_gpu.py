@@ -643,3 +643,22 @@ def test_c4_1m_properties(engine):
     finally:
         engine.set_virtual_shards(1)
         engine.set_background_cache(True)
+
+
+@pytest.mark.parametrize("theta", [(0.66, 1.6, 14, 0.344, 1440, 0.0695), (1, 1.6, 14, 0.1, 1, 1)])
+def test_c2_shaped_gradient_vs_oracle(engine, theta):
+    """Gradient parity on C2-shaped data (first 30,000 events of the bench set:
+    the far tier, the trigger-free split and culling all active) against the
+    long-double oracle: loglik to 1e-10, each component to 1e-8 of its
+    scale (sum of |per-event contributions|) and, away from a stationary point,
+    to 1e-8 relative."""
+    ev = _c2(keep=30000)
+    o = og.oracle_loglik_grad(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), np.array(theta))
+    engine.load(ev)
+    engine.set_params(list(theta))
+    ll, valid, g, _ = engine.loglik_grad()
+    assert valid and o["valid"]
+    assert abs(ll - o["loglik"]) <= LL_TOL * abs(o["loglik"])
+    assert np.all(np.abs(g - o["grad"]) <= 1e-8 * o["grad_abs"]), (g, o["grad"])
+    big = np.abs(o["grad"]) > 1e-3 * o["grad_abs"]
+    assert np.all(np.abs(g - o["grad"])[big] <= 1e-8 * np.abs(o["grad"])[big])
