@@ -386,7 +386,8 @@ def main():
         "dtype": "f64",
         "precision_note": "results FP64 (loglik within 1e-13 of an all-FP64 evaluation); pairs whose "
                           "every term is provably < 4.3e-18 of the row's self term run on the FP32 "
-                          "far tier (DESIGN.md §3)",
+                          "far tier, and far terms whose total is provably below half an ulp of the "
+                          "row's background sum (< 2^-54 S_B) are not evaluated (DESIGN.md §3)",
         "data": "synthetic (reference simulator restated bit-exactly)",
         "config": config_dict(world),
         "pair_interactions_per_s": evals_s * float(n) * float(n),

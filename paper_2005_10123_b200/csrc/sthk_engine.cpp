@@ -339,6 +339,7 @@ struct EvalPlan {
   double sx = 1.0;  // kSym coordinate scale sqrt(-cxL)
   double sxf = 1.0, stf = 1.0;  // far-tier FP32 coordinate scales
   double tfar = 0.0;            // far split time gap (days)
+  double boost = 0.0;           // ln(trNorm / (mu0 bgNorm)) when > 0
   int sc = 0;
   int nchunks = 0;
   int sc_bg = 0;       // chunk size of the background-only list (finer: a function of N only)
@@ -412,21 +413,27 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
     const double boost = cT > cB ? std::log(cT / cB) : 0.0;
     pl.tfar = std::max(p[2] * std::sqrt(2.0 * kFarExponent), (kFarExponent + boost) / p[4]) *
               (1.0 + 1e-9);
+    pl.boost = boost;
   }
 
   pl.k.nomL = static_cast<double>(-L * p[4]);
   const double inf = std::numeric_limits<double>::infinity();
   pl.k.dB = e.dense ? inf : dB;
   pl.k.dT = e.dense ? inf : dT;
-  // far-tier exact cull: ex2.approx.ftz returns +0 below 2^-126, i.e. for
-  // natural exponents below -126 ln2 = -87.34; with a margin of 1 (FP32
-  // exponent error << 1) every pair beyond these windows is exactly 0 in the
-  // far kernel, so skipping it leaves every sum bitwise unchanged
+  // far-tier cull. Every background term has a self term e^0 = 1 in its row's
+  // S_B, and lambda >= mu0 bgNorm S_B, so far terms below e^-C relative to
+  // that (background exponent < -C; trigger: omega dt > C + ln(trNorm /
+  // (mu0 bgNorm))) sum, over at most N sources, to less than N e^-C of S_B.
+  // With C = ln N + 54 ln 2 that is below 2^-54 S_B: under half an ulp of
+  // S_B, invisible in the FP64 sums, so those pairs are not evaluated. (The
+  // FP32 exponent itself underflows to +0 below 126 ln 2 + 1, which caps C.)
+  // The same windows apply with culling off (dense), so dense == culled.
   {
     const double zf = 126.0 * 0.693147180559945309417232121458176568 + 1.0;
-    pl.k.dBf = e.dense ? std::numeric_limits<double>::infinity()
-                       : p[2] * std::sqrt(2.0 * zf) * (1.0 + 1e-9);
-    pl.k.dTf = e.dense ? std::numeric_limits<double>::infinity() : zf / p[4] * (1.0 + 1e-9);
+    const double zc = std::min(zf, std::log(static_cast<double>(std::max<int64_t>(e.n, 2))) +
+                                       54.0 * 0.693147180559945309417232121458176568);
+    pl.k.dBf = p[2] * std::sqrt(2.0 * zc) * (1.0 + 1e-9);
+    pl.k.dTf = std::min(zf, zc + pl.boost) / p[4] * (1.0 + 1e-9);
     // (never beyond the FP64 culling windows)
     pl.k.dBf = std::min(pl.k.dBf, pl.k.dB);
     pl.k.dTf = std::min(pl.k.dTf, pl.k.dT);

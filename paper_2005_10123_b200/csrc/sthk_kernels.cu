@@ -152,7 +152,7 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
   if (a.tfar > 0.0 && last + 1 - first == kTM) {  // (full row tiles only)
     const int bb = static_cast<int>(b[2]);
     fb = max(lo, bb - bb % kTS);
-    // far sources before t[first] - dFar are exactly 0 in FP32: culled
+    // far sources before t[first] - dFar are culled (invisible in the FP64 sums)
     if (!a.dense) flo = min(max(lo, static_cast<int>(b[1])), fb);
   }
   // background-only split of the near range: the near stages before the

@@ -52,8 +52,8 @@ struct PairConsts {
   double fkt1;  // dtf -> dt (days)
   double fkt2;  // dtf^2 -> dt^2
   double fstf;  // time scale of tf (tf = (t - t_tile0) * fstf)
-  double dBf;   // far tier: background nonzero in FP32 iff |dt| <= dBf (exact cull)
-  double dTf;   // far tier: trigger nonzero in FP32 iff dt <= dTf
+  double dBf;   // far tier: background evaluated iff |dt| <= dBf (beyond: < 2^-54 S_B in total)
+  double dTf;   // far tier: trigger evaluated iff dt <= dTf (same bound)
 };
 
 constexpr int kPlanPivots = 8192;  // sorted-time search pivots (a power of two; 64 KB)
@@ -78,8 +78,9 @@ struct PlanArgs {
   // far tier (kSym): sources earlier than t_tile_first - tfar (whole
   // 128-stages) go to a second list for the FP32 far kernel; tfar <= 0: off
   double tfar;
-  // far-tier exact cull: the FP32 ex2 flushes to +0 below 2^-126, so far
-  // sources earlier than t_tile_first - dFar contribute exactly 0 (+inf: dense)
+  // far-tier cull: far sources earlier than t_tile_first - dFar are not
+  // evaluated (their terms sum to under half an ulp of every row's S_B, see
+  // make_plan in sthk_engine.cpp and DESIGN.md §3)
   double dFar;
   int2* ranges_far;     // [ntiles] far source range [lo, fb)
   int2* crange_far;     // [ntiles] far chunk range (empty: y < x)

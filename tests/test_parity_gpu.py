@@ -449,7 +449,9 @@ def test_far_tier_guard_off_for_extreme_coordinates(engine):
     for xs, tspan, want_far in ((5.0, 1800.0, True), (3e4, 1800.0, False)):
         t = np.sort(rng.uniform(0, tspan, n))
         ev = pk.EventSet(rng.uniform(0, xs, n), rng.uniform(0, 5, n), t)
-        p = pk.Params(0.6, 0.9, 3.0, 0.3, 2.0, 0.3)
+        # (tauT = 60 days: the far band [tfar, dBf] = [8.9, 9.7] tauT holds a few
+        # whole 128-event stages at this event density)
+        p = pk.Params(0.6, 0.9, 60.0, 0.3, 2.0, 0.3)
         engine.load(ev)
         engine.set_params(p)
         engine.set_timing(True)
