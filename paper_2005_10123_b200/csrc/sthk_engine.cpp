@@ -210,7 +210,9 @@ constexpr int kChunksTarget = 48;  // source chunks across N (work-item granular
 // event, in kernel units) stay within kFarCoordMax: a coordinate rounding of
 // <= 2.4e-4 units perturbs an exponent near the threshold by < 0.01 (log2),
 // i.e. < 1% of a term below 4.3e-18.
-constexpr double kFarExponent = 40.0;
+constexpr double kFarExponent = 40.0;     // far threshold A: at most (error-bound driven below)
+constexpr double kFarExponentMin = 30.0;  // ... and at least
+constexpr double kFarRowBound = 1e-13;    // bound on the far tier's error, relative to each S_B
 constexpr double kFarCoordMax = 4096.0;
 constexpr int kMaxAdj = sthk::kLoadAdj;  // trigger-free split: at most 16 stages kept with the tile
 constexpr int64_t kBgSplitMinEvents = 36 * 1024;  // trigger-free split only from 36k events
@@ -340,6 +342,7 @@ struct EvalPlan {
   double sxf = 1.0, stf = 1.0;  // far-tier FP32 coordinate scales
   double tfar = 0.0;            // far split time gap (days)
   double boost = 0.0;           // ln(trNorm / (mu0 bgNorm)) when > 0
+  double far_a = 0.0;           // far threshold A actually used
   int sc = 0;
   int nchunks = 0;
   int sc_bg = 0;       // chunk size of the background-only list (finer: a function of N only)
@@ -367,6 +370,8 @@ struct PlanInput {
   const double* p;
   bool dense;
   bool sym;
+  // load statistics (far-tier error bound): max |x - x0|, |y - y0|, tile time span
+  double ext_x = 0, ext_y = 0, tile_tspan = 0;
 };
 
 int chunk_size(int64_t n, int64_t npad) {
@@ -375,6 +380,15 @@ int chunk_size(int64_t n, int64_t npad) {
   sc = std::max<int64_t>(sc, 4 * kTS);
   sc = std::min<int64_t>(sc, npad);
   return static_cast<int>(sc);
+}
+
+// Far-tier cull exponent C = ln N + 54 ln 2, capped by the FP32 flush point
+// 126 ln 2 + 1: far terms below e^-C sum to < 2^-54 of every row's S_B
+// (DESIGN.md §3).
+double far_cull_exponent(int64_t n) {
+  const double ln2 = 0.693147180559945309417232121458176568;
+  return std::min(126.0 * ln2 + 1.0,
+                  std::log(static_cast<double>(std::max<int64_t>(n, 2))) + 54.0 * ln2);
 }
 
 EvalPlan make_plan(const PlanInput& e, int shards) {
@@ -411,9 +425,27 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
     const double cB = p[0] * std::pow(2.0 * kPi_, -1.5) / (p[1] * p[1] * p[2]);
     const double cT = p[3] * p[4] / (2.0 * kPi_ * p[5] * p[5]);
     const double boost = cT > cB ? std::log(cT / cB) : 0.0;
-    pl.tfar = std::max(p[2] * std::sqrt(2.0 * kFarExponent), (kFarExponent + boost) / p[4]) *
-              (1.0 + 1e-9);
     pl.boost = boost;
+    // Far threshold A: the FP32 far terms (< e^-A of S_B each, at most N of
+    // them per row) carry a relative error eps, bounded from the actual FP32
+    // coordinate magnitudes (load statistics), ex2.approx (<= 2 ulp) and the
+    // FP32 accumulation of at most one chunk of terms; A is the smallest value
+    // in [kFarExponentMin, kFarExponent] keeping N e^-A eps <= kFarRowBound of
+    // every row's S_B (1e-13: the loglik moves by < 3e-13 relative at C2).
+    const double zc = far_cull_exponent(e.n);
+    const double u = std::ldexp(1.0, -24);
+    const double dmax = std::sqrt(zc / kLn2);  // max |coordinate difference| of a far pair
+    const double sxf = 1.0 / (p[1] * std::sqrt(2.0 * kLn2));
+    const double stf = 1.0 / (p[2] * std::sqrt(2.0 * kLn2));
+    const double dfar = std::max(p[2] * std::sqrt(2.0 * zc), (zc + boost) / p[4]);
+    const double cc = std::max({e.ext_x * sxf, e.ext_y * sxf, (e.tile_tspan + dfar) * stf});
+    const double dd = (2.0 * cc + dmax) * u + dmax * u;
+    const double dE = 3.0 * (2.0 * dmax * dd + dmax * dmax * u) + 3.0 * dmax * dmax * u;
+    const double eps = kLn2 * dE + 4.0 * u + static_cast<double>(chunk_size(e.n, e.npad)) * u;
+    const double a_need = std::log(static_cast<double>(std::max<int64_t>(e.n, 2)) * eps / kFarRowBound);
+    pl.far_a = std::min(kFarExponent, std::max(kFarExponentMin, a_need));
+    pl.tfar = std::max(p[2] * std::sqrt(2.0 * pl.far_a), (pl.far_a + boost) / p[4]) *
+              (1.0 + 1e-9);
   }
 
   pl.k.nomL = static_cast<double>(-L * p[4]);
@@ -429,9 +461,8 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   // FP32 exponent itself underflows to +0 below 126 ln 2 + 1, which caps C.)
   // The same windows apply with culling off (dense), so dense == culled.
   {
-    const double zf = 126.0 * 0.693147180559945309417232121458176568 + 1.0;
-    const double zc = std::min(zf, std::log(static_cast<double>(std::max<int64_t>(e.n, 2))) +
-                                       54.0 * 0.693147180559945309417232121458176568);
+    const double zf = 126.0 * kLn2 + 1.0;
+    const double zc = far_cull_exponent(e.n);
     pl.k.dBf = p[2] * std::sqrt(2.0 * zc) * (1.0 + 1e-9);
     pl.k.dTf = std::min(zf, zc + pl.boost) / p[4] * (1.0 + 1e-9);
     // (never beyond the FP64 culling windows)
@@ -514,7 +545,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     ck(cudaStreamSynchronize(s0.stream), "D2H");
     e.ht_valid = true;
   }
-  const EvalPlan pl = make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym}, shards);
+  const EvalPlan pl = make_plan(
+      PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym, e.ext_x, e.ext_y, e.tile_tspan}, shards);
   e.last_sc = pl.sc;
   // Split structure of a full sweep (it fixes how the background sums are
   // grouped, so a cached background is reused only under the same structure):
