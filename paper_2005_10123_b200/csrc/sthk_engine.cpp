@@ -736,7 +736,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     pa.work_counter = s.scalars + 1;
     pa.tfar = far_on ? pl.tfar : 0.0;
     // far list start: the far tier's cull window (trigger-only sweeps: trigger only)
-    pa.dFar = cached ? pl.k.dTf : std::max(pl.k.dBf, pl.k.dTf);
+    // (only with a far list: its window then keys the plan cache)
+    pa.dFar = !far_on ? 0.0 : cached ? pl.k.dTf : std::max(pl.k.dBf, pl.k.dTf);
     if (bg_split) {
       pa.bg_adj = bg_adj;
       pa.sc_bg = pl.sc_bg;
