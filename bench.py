@@ -387,8 +387,8 @@ def main():
         "precision_note": "results FP64 (identical digits to an all-FP64 evaluation at C2); pairs whose "
                           "every term is provably < e^-A of the row's self term run on the FP32 far "
                           "tier, A chosen so the tier moves each row's background sum by <= 1e-13 "
-                          "relative, and far terms whose total is provably below half an ulp of that "
-                          "sum (< 2^-54 S_B) are not evaluated (DESIGN.md §3)",
+                          "relative, and far or trigger terms whose total is provably below half an "
+                          "ulp of lambda (< 2^-54) are not evaluated (DESIGN.md §3)",
         "data": "synthetic (reference simulator restated bit-exactly)",
         "config": config_dict(world),
         "pair_interactions_per_s": evals_s * float(n) * float(n),

@@ -187,7 +187,7 @@ struct sthk_engine {
   bool comp_valid = false;
   uint64_t comp_gen = 0;
   double comp_tt = 0, comp_om = 0;
-  double tr_cache_omega = 0, tr_cache_h = 0;
+  double tr_cache_omega = 0, tr_cache_h = 0, tr_cache_dT = 0;
   uint64_t load_gen = 0, cache_gen = 0;
   double cache_tx = 0, cache_tt = 0;
   int cache_mode = -1;
@@ -350,11 +350,29 @@ struct EvalPlan {
   std::vector<int> cuts;  // shard row boundaries (size shards+1)
 };
 
-// Culling windows: background term is exactly 0 when |dt| > dB, trigger term
-// when dt > dT (fexp flushes below -708.40; we cut at -709).
-void culling_windows(const double* p, double& dB, double& dT) {
+// ln(trNorm / (mu0 bgNorm)) when positive, else 0: the trigger's weight in
+// lambda against the background self term's (kernels.hpp:78-84).
+double trigger_boost(const double* p) {
+  const double kPi_ = 3.14159265358979323846;
+  const double cB = p[0] * std::pow(2.0 * kPi_, -1.5) / (p[1] * p[1] * p[2]);
+  const double cT = p[3] * p[4] / (2.0 * kPi_ * p[5] * p[5]);
+  return cT > cB ? std::log(cT / cB) : 0.0;
+}
+
+double far_cull_exponent(int64_t n);
+
+// Culling windows: the background term is exactly 0 when |dt| > dB (fexp
+// flushes below -708.40; we cut at -709). The trigger term is cut at
+// dt > dT, the nearer of its exact underflow (omega dt > 709) and the
+// half-ulp window omega dt > C + ceil(boost) (C = ln N + 54 ln 2): lambda >=
+// mu0 bgNorm S_B >= mu0 bgNorm, so the skipped trigger terms sum, over at
+// most N sources, to < 2^-54 lambda -- invisible in FP64. The
+// boost is rounded up to an integer so the window (and with it the trigger
+// sums, cached per window) moves only in whole steps as theta and mu0 move.
+void culling_windows(const double* p, int64_t n, double& dB, double& dT) {
   dB = p[2] * std::sqrt(2.0 * sthk::kCullExponent) * (1.0 + 1e-9);
-  dT = sthk::kCullExponent / p[4] * (1.0 + 1e-9);
+  const double zt = std::min(sthk::kCullExponent, far_cull_exponent(n) + std::ceil(trigger_boost(p)));
+  dT = zt / p[4] * (1.0 + 1e-9);
 }
 
 int64_t lb(const std::vector<double>& t, int64_t n, double v) {
@@ -395,7 +413,7 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   EvalPlan pl;
   const double* p = e.p;
   double dB, dT;
-  culling_windows(p, dB, dT);
+  culling_windows(p, e.n, dB, dT);
   // exponent constants in L units (x 2048/ln2), see exp_l (sthk_device.cuh)
   const long double L = 2048.0L / 0.693147180559945309417232121458176568L;
   pl.k.cxL = static_cast<double>(-0.5L * L / (static_cast<long double>(p[1]) * p[1]));
@@ -421,10 +439,7 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   // so its cut is omega dt >= A + ln(trNorm / (mu0 bgNorm)) when that ratio
   // exceeds 1 (far-tier error bound).
   {
-    const double kPi_ = 3.14159265358979323846;
-    const double cB = p[0] * std::pow(2.0 * kPi_, -1.5) / (p[1] * p[1] * p[2]);
-    const double cT = p[3] * p[4] / (2.0 * kPi_ * p[5] * p[5]);
-    const double boost = cT > cB ? std::log(cT / cB) : 0.0;
+    const double boost = trigger_boost(p);
     pl.boost = boost;
     // Far threshold A: the FP32 far terms (< e^-A of S_B each, at most N of
     // them per row) carry a relative error eps, bounded from the actual FP32
@@ -451,7 +466,7 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   pl.k.nomL = static_cast<double>(-L * p[4]);
   const double inf = std::numeric_limits<double>::infinity();
   pl.k.dB = e.dense ? inf : dB;
-  pl.k.dT = e.dense ? inf : dT;
+  pl.k.dT = dT;  // (dense too: the half-ulp trigger window applies in both modes, so dense == culled)
   // far-tier cull. Every background term has a self term e^0 = 1 in its row's
   // S_B, and lambda >= mu0 bgNorm S_B, so far terms below e^-C relative to
   // that (background exponent < -C; trigger: omega dt > C + ln(trNorm /
@@ -576,7 +591,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
                       e.cache_bg_adj == bg_adj && e.cache_dense == e.dense &&
                       (e.cache_grad || !grad);
   const bool tr_cached = cached && e.tr_cache_valid && e.tr_cache_omega == e.p[4] &&
-                         e.tr_cache_h == e.p[5] && e.tr_cache_grad == grad;  // (tpart layout)
+                         e.tr_cache_h == e.p[5] && e.tr_cache_dT == pl.k.dT &&
+                         e.tr_cache_grad == grad;  // (tpart layout)
   e.last_cache_hit = cached;
   e.last_tr_cache_hit = tr_cached;
   const bool bg_split = !cached && bg_adj > 0;
@@ -972,6 +988,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     e.tr_cache_grad = grad;
     e.tr_cache_omega = e.p[4];
     e.tr_cache_h = e.p[5];
+    e.tr_cache_dT = pl.k.dT;
   }
   e.tr_cache_valid = e.bg_cache;
   e.comp_valid = true;
