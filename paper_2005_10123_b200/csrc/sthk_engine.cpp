@@ -203,7 +203,7 @@ struct sthk_engine {
 
 namespace {
 
-constexpr int kChunksTarget = 48;  // source chunks across N (work-item granularity)
+constexpr int kChunksTarget = 64;  // source chunks across N (work-item granularity; measured 32/48/64/96)
 // Far tier: a stage runs in FP32 when every exponent on its bounding boxes is
 // below -kFarExponent (terms < 4.3e-18), and only if the FP32 coordinates
 // (space relative to event 0, time relative to each 128-event tile's first
