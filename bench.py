@@ -8,27 +8,32 @@ DC-gunshot-shaped events from the reference's cluster simulator
 (simulateClusterProcess, Rng(2005), rate 0.053217 on 15x15 km x 4750 d,
 first 85,000 in time order), evaluated at Theta_post=(0.66, 1.6, 14, 0.344,
 1440, 0.0695). One step = one loglik+gradient evaluation (all N^2 pairs
-accounted for; provably-zero tiles skipped exactly). Theta_init from the MH
-sampler is reported as a secondary line.
+accounted for; provably-zero tiles skipped exactly).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Multi-GPU (torchrun, one process per GPU): target rows are partitioned
-across ranks (cost-balanced, 1024-row blocks) and the block partials are
-combined with one NCCL all-reduce inside the engine: strong scaling of a
-single evaluation, timed as the max over ranks.
+--gpus N > 1 without torchrun in the environment re-launches itself under
+torch.distributed.run (one process per GPU; fails loudly when the box has
+fewer GPUs). Target rows are partitioned across the ranks (cost-balanced,
+1024-row blocks); each rank ships the column sums it added to other ranks'
+rows to their owner (ncclSend / ncclRecv) and one NCCL all-reduce combines
+the block partials: strong scaling of one evaluation, timed as the max over
+ranks. Secondary lines: Theta_init, the all-FP64 path (far tier off), C4
+(N=1,000,000, the same ranks) and, on one GPU, C5 (the reference MH driver,
+10,000 iterations at N=85k, over the B200 adapter).
 
 --impl reference times the reference's own multithreaded SIMD CPU engine
 (hawkes::logLikelihood compiled verbatim from /root/reference into
-oracle/_ref) on all host cores, log-likelihood only (the reference has no
-gradient), on rank 0.
+oracle/_ref, inputs from the reference's own simulator in the same library)
+on all host cores, log-likelihood only (the reference has no gradient), on
+rank 0; other ranks exit without work.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,6 +45,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 N_EVENTS = 85_000
+N_C4 = 1_000_000
 THETA_POST = [0.66, 1.6, 14.0, 0.344, 1440.0, 0.0695]
 THETA_INIT = [1.0, 1.6, 14.0, 0.1, 1.0, 1.0]
 SIM_TRUTH = [1.0, 1.6, 14.0, 0.344, 1440.0, 0.0695]
@@ -49,9 +55,9 @@ SIM_SEED = 2005
 METRIC = "loglik+gradient evals/sec and pair-interactions/sec at N=85k"
 # counted flops per evaluated pair (exp = 29 flops)
 FLOPS_ANY, FLOPS_BG_GRAD, FLOPS_TR_GRAD = 6, 38, 38
-FLOPS_SYM_COLUMN = 6  # symmetric kernel: 3 column accumulations (FMA) per background pair
 NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 64 DFMA/clk x 2 x 1.965 GHz
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+REF_MAX_STEPS = 150  # reference arm: full evaluations (~1.1 s each on 16 cores)
 
 
 def env_int(name, default):
@@ -61,11 +67,44 @@ def env_int(name, default):
         return default
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: one process per GPU under torch.distributed.run."""
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this box has {have}",
+                  file=sys.stderr)
+            sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def make_workload():
     import paper_2005_10123_b200 as pk
     ev, _ = pk.simulateClusterProcess(pk.Params(*SIM_TRUTH), pk.SimWindow(*SIM_WINDOW), SIM_RATE,
                                       SIM_SEED, keep=N_EVENTS)
-    return ev
+    return ev.xs(), ev.ys(), ev.ts(), ev.windowEnd()
+
+
+def make_workload_reference():
+    """The same C2 events from the reference's own simulator (oracle/_ref):
+    the reference arm maps no library of this repo."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_glue as og
+    x, y, t, _ = og.ref_sim_cluster(SIM_TRUTH, SIM_WINDOW, SIM_RATE, SIM_SEED)
+    x, y, t = x[:N_EVENTS].copy(), y[:N_EVENTS].copy(), t[:N_EVENTS].copy()
+    return x, y, t, float(t[-1])
 
 
 def config_dict(world):
@@ -74,7 +113,8 @@ def config_dict(world):
                     "loglik + 6-parameter gradient, FP64",
         "n_events": N_EVENTS,
         "theta": THETA_POST,
-        "parallelism": f"row-partition x{world} + NCCL all-reduce" if world > 1 else "1 GPU",
+        "parallelism": (f"row partition over {world} ranks (owner-directed fx exchange + "
+                        "NCCL all-reduce of block partials)") if world > 1 else "1 GPU",
         "l2": "flushed between timed steps (256 MiB write); inputs (2 MB) are L2-resident within a step",
     }
 
@@ -128,31 +168,25 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None}
 
 
+def _ref_setup():
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_glue as og
+    return og, os.cpu_count() or 1, (8 if og.has_avx512() else 4)
+
+
 def run_reference(args, rank, world):
     """--impl reference: the verbatim reference CPU engine on rank 0."""
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import oracle_glue as og
-    ev = make_workload()
-    cores = os.cpu_count() or 1
-    lanes = 8 if og.has_avx512() else 4
-    base = {"impl": "reference", "metric": METRIC, "unit": "evals/s", "n_gpus": world,
-            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(world), "vs_baseline": None}
+    og, cores, lanes = _ref_setup()
     if not og.ref_available():
         print(json.dumps({"impl": "reference",
                           "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
         return
-    x, y, t, T = ev.xs(), ev.ys(), ev.ts(), ev.windowEnd()
-    # bounded sample: full N=85k evaluations, step count capped at ~150 s
-    t0 = time.perf_counter()
-    og.ref_loglik(x, y, t, T, THETA_POST, threads=cores, lanes=lanes)
-    one = time.perf_counter() - t0
-    steps = max(3, min(args.steps, int(150.0 / max(one, 1e-3))))
-    warm = max(0, min(args.warmup, 1) - 1)  # the probe above is the first warm-up
-    for _ in range(warm):
+    x, y, t, T = make_workload_reference()
+    for _ in range(args.warmup):
         og.ref_loglik(x, y, t, T, THETA_POST, threads=cores, lanes=lanes)
+    steps = min(args.steps, REF_MAX_STEPS)
     times, vals = [], []
     for _ in range(steps):
         t0 = time.perf_counter()
@@ -164,30 +198,27 @@ def run_reference(args, rank, world):
     v = steps / total
     sample = (f"{steps} full N=85,000 log-likelihood evaluations (reference threads{cores}+simd{lanes}, "
               f"no gradient: the reference has none)")
-    out = dict(base)
-    out.update({
-        "value": v, "steps": steps, "warmup": warm + 1, "ms_per_step": 1e3 * total / steps,
-        "pair_interactions_per_s": v * N_EVENTS ** 2,
-        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "reference",
-                         "sample": sample, "hardware": og.ref_hardware()},
-        "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "loglik": vals[0], "steps_requested": args.steps,
-        "gpu_launches": 0,
-    })
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": world,
+           "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / steps,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (the reference's own simulateClusterProcess, oracle/_ref)",
+           "config": config_dict(world),
+           "pair_interactions_per_s": v * N_EVENTS ** 2,
+           "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "reference",
+                            "sample": sample, "hardware": og.ref_hardware()},
+           "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "loglik": vals[0], "steps_requested": args.steps, "gpu_launches": 0}
     print(json.dumps(out))
 
 
 def cpu_baseline_probe():
-    """Reference CPU engine on this host's cores, a bounded sample (rank 0, N=1)."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import oracle_glue as og
+    """Reference CPU engine on this host's cores, a bounded sample (rank 0,
+    N=1), run before this process touches CUDA."""
+    og, cores, lanes = _ref_setup()
     if not og.ref_available():
-        return {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
+        return {"value": None, "unit": "evals/s", "cores": cores, "kind": "reference",
                 "sample": "unavailable: oracle/_ref not built"}
-    ev = make_workload()
-    cores = os.cpu_count() or 1
-    lanes = 8 if og.has_avx512() else 4
-    x, y, t, T = ev.xs(), ev.ys(), ev.ts(), ev.windowEnd()
+    x, y, t, T = make_workload_reference()
     og.ref_loglik(x, y, t, T, THETA_POST, threads=cores, lanes=lanes)  # warm-up
     times = []
     t_start = time.perf_counter()
@@ -198,8 +229,15 @@ def cpu_baseline_probe():
     med = statistics.median(times)
     return {"value": 1.0 / med, "unit": "evals/s", "cores": cores, "kind": "reference",
             "sample": f"{len(times)} full N=85,000 loglik evals (threads{cores}+simd{lanes}, "
-                      "median; loglik only, the reference has no gradient)",
+                      "median, before CUDA initialisation; loglik only, the reference has no gradient)",
             "hardware": og.ref_hardware(), "s_per_eval": med}
+
+
+def strict_flops(st):
+    """SURVEY.md §8 d3 over the pairs actually executed: 6 (geometry) + 38
+    per background exp, 38 per trigger pair (one symmetric background exp
+    serves two ordered pairs and is charged once)."""
+    return FLOPS_ANY * st["exec_geom"] + FLOPS_BG_GRAD * st["exec_bg"] + FLOPS_TR_GRAD * st["pairs_tr"]
 
 
 def main():
@@ -209,16 +247,27 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="headline + e2e only (profiling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch(args)
+        return
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
 
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+
+    cpu_base = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        cpu_base = cpu_baseline_probe()  # (before CUDA: no driver threads competing)
 
     import torch
     import torch.distributed as dist
@@ -233,15 +282,15 @@ def main():
     else:
         eng = pk.Engine((local_rank,))
 
-    ev = make_workload()
-    n = ev.size()
+    x, y, t, T = make_workload()
+    n = t.size
     # pinned host copies for the end-to-end arm
-    hx = torch.from_numpy(np.array(ev.xs())).pin_memory()
-    hy = torch.from_numpy(np.array(ev.ys())).pin_memory()
-    ht = torch.from_numpy(np.array(ev.ts())).pin_memory()
-    eng.load_events(hx.numpy(), hy.numpy(), ht.numpy(), ev.windowEnd())
+    hx = torch.from_numpy(np.array(x)).pin_memory()
+    hy = torch.from_numpy(np.array(y)).pin_memory()
+    ht = torch.from_numpy(np.array(t)).pin_memory()
+    eng.load_events(hx.numpy(), hy.numpy(), ht.numpy(), T)
     eng.set_timing(True)
-    # every timed step is a full evaluation: no background-sum reuse
+    # every timed step is a full evaluation: no sweep caches
     eng.set_background_cache(False)
     stream = torch.cuda.ExternalStream(eng.stream(0))
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
@@ -252,19 +301,21 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(v):
+    def reduce_over_ranks(v, op="max"):
         if world == 1:
             return v
-        tt = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tt = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
         return float(tt.item())
 
     def timed_device(theta, steps, warmup):
+        """Device time per evaluation on the engine's stream (CUDA events),
+        L2 flushed before every step; max over ranks."""
         eng.set_params(theta)
         for _ in range(warmup):
             eng.loglik_grad()
         barrier()
-        pair_ms, evals_ms, dev_ms, lls = [], [], [], []
+        pair_ms, dev_ms, lls, launches = [], [], [], 0
         st = None
         for _ in range(steps):
             with torch.cuda.stream(stream):
@@ -282,14 +333,11 @@ def main():
             lls.append(res[0])
             st = eng.stats()
             pair_ms.append(st["pair_kernel_ms"])
-            evals_ms.append(st["eval_ms"])
+            launches += st["kernel_launches"]
         barrier()
-        tot_ms = max_over_ranks(sum(dev_ms))
-        return dict(total_ms=tot_ms, pair_ms=statistics.mean(pair_ms),
-                    pair_ms_max=max_over_ranks(statistics.mean(pair_ms)),
-                    eval_ms=statistics.mean(evals_ms), stats=st, loglik=res[0], valid=res[1],
-                    bitwise_repeats=len(set(lls)) == 1,
-                    grad=list(res[2]))
+        return dict(total_ms=reduce_over_ranks(sum(dev_ms)), pair_ms=statistics.mean(pair_ms),
+                    stats=st, loglik=res[0], valid=res[1], bitwise_repeats=len(set(lls)) == 1,
+                    grad=list(res[2]), launches=int(reduce_over_ranks(launches, "sum")))
 
     # FP64 roofline denominator, measured on this device
     peak_best, peak_mean = eng_peak(pk, local_rank)
@@ -297,29 +345,49 @@ def main():
     sampler = ClockSampler(local_rank) if rank == 0 else None
     main_run = timed_device(THETA_POST, args.steps, args.warmup)
     clocks = sampler.stop() if sampler else None
-    sec_run = timed_device(THETA_INIT, max(10, args.steps // 5), 3)
 
-    # end to end through the public API: pinned host inputs -> H2D -> eval -> D2H
+    # end to end through the public API: pinned host inputs -> H2D -> eval -> results
     def e2e(theta, steps):
         for _ in range(2):
-            eng.load_events(hx.numpy(), hy.numpy(), ht.numpy(), ev.windowEnd())
+            eng.load_events(hx.numpy(), hy.numpy(), ht.numpy(), T)
             eng.set_params(theta)
             eng.loglik_grad()
         barrier()
         t0 = time.perf_counter()
         for _ in range(steps):
-            eng.load_events(hx.numpy(), hy.numpy(), ht.numpy(), ev.windowEnd())
+            eng.load_events(hx.numpy(), hy.numpy(), ht.numpy(), T)
             eng.set_params(theta)
             eng.loglik_grad()
         el = time.perf_counter() - t0
         barrier()
-        return max_over_ranks(el)
+        return reduce_over_ranks(el)
 
     e2e_s = e2e(THETA_POST, args.steps)
 
-    # MH-chain-style steps (informational, not the headline): tauX/tauT fixed,
-    # one of (mu0, theta, omega, h) moves per step, background sums reused.
-    def mh_style(steps):
+    secondary = {}
+    if not args.no_secondary:
+        k2 = max(10, args.steps // 5)
+        sec_run = timed_device(THETA_INIT, k2, 3)
+        st2 = sec_run["stats"]
+        secondary["theta_init"] = {
+            "theta": THETA_INIT, "evals_per_s": 1e3 * k2 / sec_run["total_ms"],
+            "pair_kernel_ms": sec_run["pair_ms"],
+            "roofline_achieved_tflops": strict_flops(st2) / (sec_run["pair_ms"] * 1e-3) / 1e12,
+            "pairs": {"ordered_bg": st2["pairs_bg"], "trigger": st2["pairs_tr"],
+                      "bg_exps_executed": st2["exec_bg"]},
+            "loglik": sec_run["loglik"]}
+        # the precision policy's cost: every pair in FP64 (far tier off)
+        eng.set_far_tier(False)
+        fp64 = timed_device(THETA_POST, k2, 3)
+        eng.set_far_tier(True)
+        secondary["all_fp64"] = {
+            "what": "C2 at Theta_post with the FP32 far tier off (every evaluated pair in FP64)",
+            "evals_per_s": 1e3 * k2 / fp64["total_ms"], "pair_kernel_ms": fp64["pair_ms"],
+            "loglik": fp64["loglik"], "grad": fp64["grad"],
+            "loglik_rel_diff_vs_far_tier": abs(fp64["loglik"] - main_run["loglik"]) / abs(fp64["loglik"])}
+
+        # MH-chain-style steps (wall clock): tauX/tauT fixed, one of (mu0,
+        # theta, omega, h) moves per step, sweep caches on
         eng.set_background_cache(True)
         rng = np.random.default_rng(1)
         theta = list(THETA_POST)
@@ -328,18 +396,50 @@ def main():
         barrier()
         t0 = time.perf_counter()
         hits = 0
-        for _ in range(steps):
+        for _ in range(args.steps):
             k = [0, 3, 4, 5][int(rng.integers(4))]
             cand = list(theta)
             cand[k] = theta[k] * float(np.exp(0.01 * rng.standard_normal()))
             eng.set_params(cand)
             eng.loglik()
             hits += eng.stats()["cache_hit"]
-        el = time.perf_counter() - t0
+        mh_s = reduce_over_ranks(time.perf_counter() - t0)
         eng.set_background_cache(False)
-        return max_over_ranks(el), hits
+        secondary["mh_style_loglik"] = {
+            "evals_per_s": args.steps / mh_s, "unit": "evals/s", "cache_hits": hits,
+            "what": "wall-clock loglik calls, one of mu0/theta/omega/h perturbed per step (tauX, "
+                    "tauT fixed as in the reference sampler): cached background, trigger band swept"}
 
-    mh_s, mh_hits = mh_style(args.steps)
+        # C4: N = 1,000,000 (generateBenchmarkCloud, Rng(1e6)) on the same ranks
+        c4 = pk.generateBenchmarkCloud(N_C4, pk.SimWindow(*SIM_WINDOW), N_C4)
+        eng.load_events(c4.xs(), c4.ys(), c4.ts(), c4.windowEnd())
+        k4 = 5
+        c4run = timed_device(THETA_POST, k4, 2)
+        secondary["c4_1m"] = {
+            "what": f"C4: N=1,000,000 cloud, loglik+grad at Theta_post, {world} rank(s)",
+            "evals_per_s": 1e3 * k4 / c4run["total_ms"], "ms_per_eval": c4run["total_ms"] / k4,
+            "pair_interactions_per_s": 1e3 * k4 / c4run["total_ms"] * float(N_C4) ** 2,
+            "loglik": c4run["loglik"], "fx_exchange_bytes_rank0": eng.exchange_bytes(),
+            "roofline_achieved_tflops_rank0": strict_flops(c4run["stats"]) / (c4run["pair_ms"] * 1e-3) / 1e12}
+        del c4
+
+        # C5: the reference's own MH driver (runChain, verbatim) over the B200
+        # adapter, 10,000 iterations at N=85k (one GPU)
+        chain = os.path.join(ROOT, "oracle", "_ref", "mh_chain_b200")
+        if world == 1 and os.path.exists(chain):
+            try:
+                r = subprocess.run([chain, "--n", "85000", "--data", "c2", "--iters", "10000",
+                                    "--burnin", "1000", "--seed", "1"], capture_output=True,
+                                   text=True, timeout=300,
+                                   env=dict(os.environ, STHK_DEVICES=str(local_rank)))
+                cj = json.loads(r.stdout.strip().splitlines()[-1])
+                secondary["c5_mh_chain"] = {
+                    "what": "C5: reference runChain (sampler.cpp, verbatim) over the B200 adapter, "
+                            "10,000 iterations, N=85,000, wall clock",
+                    "seconds": cj["seconds"], "s_per_iter": cj["s_per_iter"],
+                    "draws_fnv1a": cj["draws_fnv1a"], "accepted": cj["accepted"]}
+            except Exception as ex:  # (reported, never fatal)
+                secondary["c5_mh_chain"] = {"error": repr(ex)[:200]}
 
     if rank != 0:
         eng.close()
@@ -351,13 +451,7 @@ def main():
     ms_step = total_ms / K
     evals_s = 1e3 / ms_step
     st = main_run["stats"]
-    # counts are this rank's pairs. Executed work (the roofline numerator):
-    # SURVEY §8 d3 flops per pair actually evaluated -- in the symmetric
-    # kernel one background exp serves two ordered pairs and adds 3 column
-    # FMAs. Ordered-pair equivalent: the same model charged per ordered pair
-    # (what a non-symmetric kernel would have to execute).
-    flops_launch = (FLOPS_ANY * st["exec_geom"] + FLOPS_BG_GRAD * st["exec_bg"]
-                    + FLOPS_TR_GRAD * st["pairs_tr"] + FLOPS_SYM_COLUMN * st["exec_sym"])
+    flops_launch = strict_flops(st)
     flops_ordered = (FLOPS_ANY * st["pairs_any"] + FLOPS_BG_GRAD * st["pairs_bg"]
                      + FLOPS_TR_GRAD * st["pairs_tr"])
     achieved = flops_launch / (main_run["pair_ms"] * 1e-3) / 1e12
@@ -369,9 +463,6 @@ def main():
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    st2 = sec_run["stats"]
-    flops2 = (FLOPS_ANY * st2["exec_geom"] + FLOPS_BG_GRAD * st2["exec_bg"]
-              + FLOPS_TR_GRAD * st2["pairs_tr"] + FLOPS_SYM_COLUMN * st2["exec_sym"])
     out = {
         "metric": METRIC,
         "value": evals_s,
@@ -384,11 +475,11 @@ def main():
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "precision_note": "results FP64 (identical digits to an all-FP64 evaluation at C2); pairs whose "
-                          "every term is provably < e^-A of the row's self term run on the FP32 far "
-                          "tier, A chosen so the tier moves each row's background sum by <= 1e-13 "
-                          "relative, and far or trigger terms whose total is provably below half an "
-                          "ulp of lambda (< 2^-54) are not evaluated (DESIGN.md §3)",
+        "precision_note": "results FP64 (secondary.all_fp64 gives the every-pair-FP64 line); pairs "
+                          "whose every term is provably < e^-A of the row's self term run on the "
+                          "FP32 far tier, A chosen so the tier moves each row's background sum by "
+                          "<= 1e-13 relative, and terms whose total is provably below half an ulp "
+                          "of lambda (< 2^-54) are not evaluated (DESIGN.md §3)",
         "data": "synthetic (reference simulator restated bit-exactly)",
         "config": config_dict(world),
         "pair_interactions_per_s": evals_s * float(n) * float(n),
@@ -396,22 +487,22 @@ def main():
                            "ordered_any": st["pairs_any"], "dense": st["pairs_dense"],
                            "bg_exps_executed": st["exec_bg"],
                            "geometries_executed": st["exec_geom"],
-                           "symmetric_column_pairs": st["exec_sym"]},
+                           "far_tier_pairs": st["exec_far"],
+                           "rank": "rank 0" if world > 1 else "all"},
         "loglik": main_run["loglik"],
         "bitwise_identical_repeats": main_run["bitwise_repeats"],
         "grad": main_run["grad"],
         "e2e": {"value": K / e2e_s, "unit": "evals/s",
-                "h2d_bytes_per_step": 3 * 8 * n,
-                "d2h_bytes_per_step": 8 * 8 + 3 * 8,
-                "path": "Engine.load_events(pinned x,y,t) + set_params + loglik_grad (C ABI)"},
-        # scale, plan, [sym bg-only], sym, [far], finalize
-        "gpu_launches": (4 + (1 if st["exec_far"] else 0) + 1) * K,
+                "h2d_bytes_per_step": 3 * 8 * n * world,
+                "d2h_bytes_per_step": 8 * 8 * world,
+                "path": "Engine.load_events(pinned x,y,t) + set_params + loglik_grad (C ABI), "
+                        "every rank"},
+        "gpu_launches": main_run["launches"],
         "roofline": {
             "bound": "fp64",
             "kernel": ("sym_kernel<GRAD=true> (FP64 near, trigger-free + general) || "
                        "far_kernel<GRAD=true> (FP32 far tier), concurrent"
-                       if st["exec_far"] else "sym_kernel<GRAD=true>")
-                      if st["kernel_mode"] == 1 else "pair_kernel<GRAD=true>",
+                       if st["exec_far"] else "sym_kernel<GRAD=true>"),
             "achieved": achieved,
             "peak": peak_best,
             "unit": "TFLOP/s",
@@ -420,47 +511,29 @@ def main():
                            "MEASURED_PEAKS.json has no FP64 entry",
             "frac_of_nominal_37.2": achieved / NOMINAL_FP64_TFLOPS,
             "flops_per_launch": flops_launch,
-            "flop_model": "executed: 6*geometries + 38*bg_exps + 38*trigger_pairs + 6*symmetric "
-                          "column pairs (SURVEY.md §8 d3 per-pair model, exp counted as 29)",
-            "note": "SURVEY d3 counts every evaluated pair as FP64 work with a 29-flop exp; the "
-                    "kernel's exp is 7 FP64 ops and far_tier_share of its pairs (every exponent "
-                    "provably < -40, terms < 4.3e-18) run on the FP32/MUFU pipes, so frac can "
-                    "exceed 1; the pipe-level evidence is the ncu FP64-pipe / issue utilisation "
-                    "in profiles/",
-            "far_tier_pairs": st["exec_far"],
+            "flop_model": "SURVEY.md §8 d3 over executed pairs: 6*geometries + 38*background exps "
+                          "+ 38*trigger pairs (exp counted as 29 flops; a symmetric background exp "
+                          "serves two ordered pairs and is charged once)",
+            "note": "the kernel's exp is 7 FP64 ops, not 29, and far_tier_share of its pairs run "
+                    "on the FP32/MUFU pipes; the pipe-level evidence is the ncu FP64-pipe "
+                    "utilisation in profiles/",
             "far_tier_share": st["exec_far"] / st["exec_geom"] if st["exec_geom"] else 0.0,
             "achieved_ordered_pair_equivalent": achieved_ord,
-            "frac_ordered_pair_equivalent": achieved_ord / peak_best if peak_best else None,
             "flops_ordered_pair_equivalent": flops_ordered,
             "pair_kernel_ms": main_run["pair_ms"],
             "pair_kernel_share_of_step": main_run["pair_ms"] / ms_step,
             "traffic": traffic,
+            "rank": "rank 0" if world > 1 else "all",
         },
-        "secondary": {
-            "theta_init": {
-                "theta": THETA_INIT,
-                "evals_per_s": 1e3 * max(10, K // 5) / sec_run["total_ms"],
-                "pair_kernel_ms": sec_run["pair_ms"],
-                "roofline_achieved_tflops": flops2 / (sec_run["pair_ms"] * 1e-3) / 1e12,
-                "pairs": {"ordered_bg": st2["pairs_bg"], "trigger": st2["pairs_tr"], "bg_exps_executed": st2["exec_bg"]},
-                "loglik": sec_run["loglik"],
-            },
-        },
-        "mh_style_loglik": {
-            "evals_per_s": K / mh_s, "unit": "evals/s", "cache_hits": mh_hits, "steps": K,
-            "what": "wall-clock loglik (value) calls with one of mu0/theta/omega/h perturbed per "
-                    "step (tauX, tauT fixed as in the reference sampler): background sums reused, "
-                    "trigger band swept; bitwise identical to full evaluations",
-        },
+        "secondary": secondary,
         "clocks": clocks,
         "fp64_peak_tflops": {"best": peak_best, "mean": peak_mean},
     }
-    if world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline_probe()
-        out["cpu_baseline"] = cb
-        if cb.get("value"):
-            out["speedup_vs_cpu_baseline"] = {"value": evals_s / cb["value"],
-                                              "e2e": (K / e2e_s) / cb["value"]}
+    if cpu_base is not None:
+        out["cpu_baseline"] = cpu_base
+        if cpu_base.get("value"):
+            out["speedup_vs_cpu_baseline"] = {"value": evals_s / cpu_base["value"],
+                                              "e2e": (K / e2e_s) / cpu_base["value"]}
     print(json.dumps(out))
     eng.close()
     if world > 1:

@@ -52,8 +52,14 @@ extern "C" {
 typedef struct sthk_engine sthk_engine;
 
 /* Engine over n_devices GPUs driven from this process (n_devices >= 1).
- * Target rows are partitioned across the devices; one NCCL all-reduce
- * combines the per-block partial sums. */
+ * Target rows are partitioned across the devices (one shard per entry of
+ * device_ids, cost-balanced 1024-row blocks). Distinct device ids combine
+ * the shards with NCCL (ncclCommInitAll): each shard ships the column sums it
+ * added to other shards' rows to their owner (ncclSend / ncclRecv), and one
+ * all-reduce combines the per-block partials. A device id may repeat: the
+ * shards that share a device are separate rank engines (own accumulators,
+ * plans and partials) combined by device copies along exactly the same
+ * owner-directed routes -- the multi-GPU data flow emulated on one GPU. */
 int sthk_create(const int* device_ids, int n_devices, sthk_engine** out);
 
 /* One-process-per-GPU engine: this process owns `device` and is `rank` of
@@ -63,12 +69,33 @@ int sthk_nccl_unique_id(void* nccl_id);
 int sthk_create_rank(int device, int rank, int world, const void* nccl_id,
                      sthk_engine** out);
 
+/* Rank engine whose two collectives run through caller-supplied host
+ * callbacks instead of NCCL (e.g. torch.distributed gloo in tests, several
+ * ranks sharing one GPU). Buffers passed to the callbacks are host memory
+ * owned by the engine, valid for the duration of the call; a callback
+ * returns 0 on success (anything else fails the evaluation, STHK_ENCCL). */
+#define STHK_DTYPE_U64 0
+#define STHK_DTYPE_F64 1
+typedef struct sthk_host_comm {
+  void* ctx;
+  /* in-place element-wise sum over all ranks of `count` elements */
+  int (*allreduce_sum)(void* ctx, void* buf, int64_t count, int dtype);
+  /* post every send and receive (byte buffers, peers are ranks), return
+   * once all have completed */
+  int (*exchange)(void* ctx, int n_send, const int* send_peer, const void* const* send_buf,
+                  const int64_t* send_bytes, int n_recv, const int* recv_peer,
+                  void* const* recv_buf, const int64_t* recv_bytes);
+} sthk_host_comm;
+int sthk_create_rank_hosted(int device, int rank, int world, const sthk_host_comm* comm,
+                            sthk_engine** out);
+
 int sthk_destroy(sthk_engine* e);
 
 /* Copies n events (time-sorted SoA, km / days) to every device.
  * Validation and messages follow the EventSet constructor (types.hpp:85-109):
  * n >= 1, finite entries, t >= 0, t nondecreasing, window_end finite and
- * >= t[n-1]. Replaces any previously loaded set. */
+ * >= t[n-1]. At most 2^23 events (the fixed-point background sums hold
+ * totals below 2^23 per row). Replaces any previously loaded set. */
 int sthk_load_events(sthk_engine* e, const double* x, const double* y,
                      const double* t, int64_t n, double window_end);
 
@@ -77,8 +104,8 @@ int sthk_set_params(sthk_engine* e, const double* params6);
 
 /* Synchronous evaluations with the current params.
  * per_event (nullable, length n): log(lambda_i) - Lambda_i, 0 for degenerate
- * rows (likelihood.cpp:25,41). grad6 receives d loglik / d params in Params
- * order. */
+ * rows (likelihood.cpp:25,41); a rank engine fills its own rows only.
+ * grad6 receives d loglik / d params in Params order. */
 int sthk_loglik(sthk_engine* e, double* loglik, int* valid, double* per_event);
 int sthk_loglik_grad(sthk_engine* e, double* loglik, int* valid, double* grad6,
                      double* per_event);
@@ -127,7 +154,8 @@ typedef struct sthk_stats {
   int32_t trigger_cache_hit; /* 1 if it also reused the trigger sums (only mu0 /
                                 theta changed: no pair sweep at all) */
   int64_t exec_far;          /* pairs evaluated in the FP32 far tier (every exponent
-                                provably < -40) */
+                                provably < -A, A in [30, 40]) */
+  int64_t kernel_launches;   /* kernels the last evaluation launched (all devices) */
 } sthk_stats;
 
 int sthk_set_timing(sthk_engine* e, int enable);
@@ -171,11 +199,10 @@ int sthk_set_far_schedule(sthk_engine* e, int concurrent, int near_ctas, int far
 #define STHK_KERNEL_SYM 1
 int sthk_set_kernel(sthk_engine* e, int mode);
 
-/* Testing knob for the multi-device partition on one device: split the rows
- * into k cost-balanced shards run one after another on the single device and
- * combined exactly as the NCCL path combines them (k = 1: off). Results must
- * be bitwise identical for every k. Single-device handles only. */
-int sthk_set_virtual_shards(sthk_engine* e, int k);
+/* Bytes of fixed-point background sums this handle's shards sent to other
+ * shards' owners in the last evaluation (owner-directed exchange; 0 with one
+ * shard, for a cached background or in row mode). */
+int sthk_get_exchange_bytes(sthk_engine* e, int64_t* bytes);
 
 /* Host-only planning (no device): the cost-balanced row partition the engine
  * uses for `shards` devices/ranks -- cuts[0..shards], multiples of 1024 rows,

@@ -38,6 +38,7 @@ from .engine import (
 )
 from .simulate import SimWindow, generateBenchmarkCloud, simulateClusterProcess
 from . import io
+from . import partition
 from .io import (
     EventFileSpec,
     readEvents,

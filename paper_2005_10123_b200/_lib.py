@@ -43,7 +43,21 @@ class StatsStruct(ctypes.Structure):
         ("cache_hit", ctypes.c_int32),
         ("trigger_cache_hit", ctypes.c_int32),
         ("exec_far", c_int64),
+        ("kernel_launches", c_int64),
     ]
+
+
+STHK_DTYPE_U64 = 0
+STHK_DTYPE_F64 = 1
+ALLREDUCE_FN = ctypes.CFUNCTYPE(c_int, c_void_p, c_void_p, c_int64, c_int)
+EXCHANGE_FN = ctypes.CFUNCTYPE(c_int, c_void_p, c_int, POINTER(c_int), POINTER(c_void_p),
+                               POINTER(c_int64), c_int, POINTER(c_int), POINTER(c_void_p),
+                               POINTER(c_int64))
+
+
+class HostCommStruct(ctypes.Structure):
+    """sthk_host_comm (include/sthk.h)."""
+    _fields_ = [("ctx", c_void_p), ("allreduce_sum", ALLREDUCE_FN), ("exchange", EXCHANGE_FN)]
 
 
 # (name, restype, argtypes) for every entry point declared in include/*.h
@@ -53,6 +67,8 @@ SIGNATURES = [
     ("sthk_create", c_int, [POINTER(c_int), c_int, POINTER(c_void_p)]),
     ("sthk_nccl_unique_id", c_int, [c_void_p]),
     ("sthk_create_rank", c_int, [c_int, c_int, c_int, c_void_p, POINTER(c_void_p)]),
+    ("sthk_create_rank_hosted", c_int,
+     [c_int, c_int, c_int, POINTER(HostCommStruct), POINTER(c_void_p)]),
     ("sthk_destroy", c_int, [c_void_p]),
     ("sthk_load_events", c_int, [c_void_p, _DPTR, _DPTR, _DPTR, c_int64, c_double]),
     ("sthk_set_params", c_int, [c_void_p, _DPTR]),
@@ -66,7 +82,7 @@ SIGNATURES = [
     ("sthk_get_stats", c_int, [c_void_p, POINTER(StatsStruct)]),
     ("sthk_get_stream", c_int, [c_void_p, c_int, POINTER(c_void_p)]),
     ("sthk_set_dense", c_int, [c_void_p, c_int]),
-    ("sthk_set_virtual_shards", c_int, [c_void_p, c_int]),
+    ("sthk_get_exchange_bytes", c_int, [c_void_p, POINTER(c_int64)]),
     ("sthk_set_kernel", c_int, [c_void_p, c_int]),
     ("sthk_set_far_tier", c_int, [c_void_p, c_int]),
     ("sthk_set_bgonly_kernel", c_int, [c_void_p, c_int]),

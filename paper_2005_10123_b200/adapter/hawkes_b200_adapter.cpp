@@ -14,22 +14,27 @@
 // (excitation semantics: proj/src/excitation.cpp:13-130).
 //
 // State: one process-wide engine on the devices in $STHK_DEVICES (default
-// "0"), created on first use. The device copy of the events is cached and
-// reused when the call's EventSet has the cached set's data pointers, size
-// and windowEnd and agrees with the cached host copy on its first and last
-// events plus a fixed spread of 509 sampled indices per coordinate (an O(1)
-// check: a full 3 x N memcmp would cost ~100 us per call at N = 85k, more
-// than an MH iteration's device work). A set at other addresses is compared
-// in full (memcmp) before it can reuse the device copy. EventSet is
-// immutable, so the sampled check can only miss a *different* set rebuilt at
-// the very same three heap addresses with the same size and windowEnd that
-// also agrees at every sampled index; STHK_ADAPTER_FULL_CHECK=1 restores the
-// full comparison on every call.
+// "0"), created on first use. The device copy of the events is reused only
+// for a set whose size, windowEnd and full contents equal the cached host
+// copy -- the reference API is stateless, so an EventSet
+// destroyed and rebuilt at the same heap addresses with different data must
+// never see the old set's results. The full comparison (3 x N doubles,
+// parallel over the host cores) of a set at the cached addresses runs while
+// the device evaluates on the cached copy; on a mismatch the result is
+// discarded, the set reloaded and the evaluation repeated. A set at other
+// addresses is compared before anything is enqueued.
+// STHK_ADAPTER_FAST_CHECK=1 (opt-in) trusts the cached addresses after a
+// sampled check (first, last and 509 spread indices): faster MH iterations,
+// but it can miss a rebuilt set that differs only at unsampled indices.
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <mutex>
 #include <sstream>
 #include <stdexcept>
@@ -46,6 +51,85 @@ namespace hawkes {
 
 namespace {
 
+// Exact content comparison of an EventSet against the adapter's host copy,
+// split over a small persistent team of host threads (the 3 x N doubles are
+// compared in 64 KB blocks). Workers spin briefly between calls -- MH
+// iterations arrive every few tens of microseconds -- then sleep.
+class CompareTeam {
+ public:
+  CompareTeam() {
+    const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+    const int workers = static_cast<int>(std::min(7u, hc > 2 ? hc / 2 - 1 : 0u));
+    for (int w = 0; w < workers; ++w) th_.emplace_back([this, w] { loop(w + 1); });
+  }
+  ~CompareTeam() {
+    {
+      std::lock_guard<std::mutex> l(m_);
+      stop_ = true;
+      gen_.fetch_add(1);
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  bool equal(const double* const* a, const double* const* b, int64_t n) {
+    a_ = a;
+    b_ = b;
+    n_ = n;
+    nb_ = (n + kBlock - 1) / kBlock;
+    diff_.store(0);
+    const int team = static_cast<int>(th_.size()) + 1;
+    if (3 * nb_ < 2 * team || th_.empty()) {
+      work(0, 1);
+      return diff_.load() == 0;
+    }
+    pending_.store(static_cast<int>(th_.size()));
+    {
+      std::lock_guard<std::mutex> l(m_);
+      gen_.fetch_add(1);
+    }
+    cv_.notify_all();
+    work(0, team);
+    while (pending_.load(std::memory_order_acquire) != 0) std::this_thread::yield();
+    return diff_.load() == 0;
+  }
+
+ private:
+  static constexpr int64_t kBlock = 8192;
+  void work(int w, int team) {
+    int d = 0;
+    for (int64_t k = w; k < 3 * nb_; k += team) {
+      const int64_t arr = k / nb_, b0 = (k % nb_) * kBlock;
+      const int64_t len = std::min(kBlock, n_ - b0);
+      d |= std::memcmp(a_[arr] + b0, b_[arr] + b0, sizeof(double) * static_cast<size_t>(len)) != 0;
+    }
+    if (d) diff_.store(1);
+  }
+  void loop(int w) {
+    uint64_t seen = 0;
+    for (;;) {
+      int spins = 0;
+      while (gen_.load(std::memory_order_acquire) == seen && spins < 200000) ++spins;
+      if (gen_.load(std::memory_order_acquire) == seen) {
+        std::unique_lock<std::mutex> l(m_);
+        cv_.wait(l, [&] { return gen_.load() != seen; });
+      }
+      seen = gen_.load();
+      if (stop_) return;
+      work(w, static_cast<int>(th_.size()) + 1);
+      pending_.fetch_sub(1, std::memory_order_release);
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_;
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> pending_{0}, diff_{0};
+  bool stop_ = false;
+  const double* const* a_ = nullptr;
+  const double* const* b_ = nullptr;
+  int64_t n_ = 0, nb_ = 0;
+};
+
 struct AdapterEngine {
   std::mutex mu;
   sthk_engine* h = nullptr;
@@ -55,7 +139,8 @@ struct AdapterEngine {
   Index n = -1;
   double windowEnd = 0;
   std::vector<double> cx, cy, ct;  // host copy of the cached set
-  bool full_check = false;
+  bool fast_check = false;
+  std::unique_ptr<CompareTeam> team = std::make_unique<CompareTeam>();
 
   AdapterEngine() {
     std::vector<int> devs;
@@ -63,8 +148,8 @@ struct AdapterEngine {
     std::stringstream ss(env && *env ? env : "0");
     std::string tok;
     while (std::getline(ss, tok, ',')) devs.push_back(std::stoi(tok));
-    const char* fc = std::getenv("STHK_ADAPTER_FULL_CHECK");
-    full_check = fc && *fc == '1';
+    const char* fc = std::getenv("STHK_ADAPTER_FAST_CHECK");
+    fast_check = fc && *fc == '1';
     if (sthk_create(devs.data(), static_cast<int>(devs.size()), &h) != STHK_OK) {
       throw std::runtime_error(std::string("sthk_create: ") + sthk_last_error(nullptr));
     }
@@ -83,23 +168,43 @@ struct AdapterEngine {
     throw std::runtime_error("B200 engine: " + msg);
   }
 
-  void ensureLoaded(const EventSet& ev) {
+  // Makes the device hold `ev`. Returns true when the cached copy is reused
+  // on the strength of the set's addresses alone: the caller must confirm
+  // with contentEqual() before trusting the result.
+  bool ensureLoaded(const EventSet& ev) {
     const Index m = ev.size();
     const double* x = ev.xs().data();
     const double* y = ev.ys().data();
     const double* t = ev.ts().data();
-    const size_t bytes = sizeof(double) * static_cast<size_t>(m);
     if (m == n && ev.windowEnd() == windowEnd) {
       const bool same_ptrs = x == px && y == py && t == pt;
-      if (same_ptrs && !full_check && sampled_equal(x, y, t, m)) return;
-      if (std::memcmp(x, cx.data(), bytes) == 0 && std::memcmp(y, cy.data(), bytes) == 0 &&
-          std::memcmp(t, ct.data(), bytes) == 0) {
+      if (same_ptrs && fast_check && sampled_equal(x, y, t, m)) return false;
+      if (same_ptrs) return true;
+      if (contentEqual(ev)) {
         px = x;  // same data at new addresses: keep the device copy
         py = y;
         pt = t;
-        return;
+        return false;
       }
     }
+    reload(ev);
+    return false;
+  }
+
+  // Exact: every coordinate of every event, over the host cores.
+  bool contentEqual(const EventSet& ev) const {
+    const Index m = ev.size();
+    if (m != n) return false;
+    const double* src[3] = {ev.xs().data(), ev.ys().data(), ev.ts().data()};
+    const double* mine[3] = {cx.data(), cy.data(), ct.data()};
+    return team->equal(src, mine, static_cast<int64_t>(m));
+  }
+
+  void reload(const EventSet& ev) {
+    const Index m = ev.size();
+    const double* x = ev.xs().data();
+    const double* y = ev.ys().data();
+    const double* t = ev.ts().data();
     n = -1;  // a failed load leaves the engine without events
     check(sthk_load_events(h, x, y, t, m, ev.windowEnd()));
     px = x;
@@ -126,6 +231,25 @@ struct AdapterEngine {
     const double v[6] = {p.mu0, p.tauX, p.tauT, p.theta, p.omega, p.h};
     check(sthk_set_params(h, v));
   }
+
+  // One evaluation of `ev` at the current params: enqueued on the cached
+  // copy while the host confirms the contents; redone after a reload on a
+  // mismatch. per_event (nullable, length n) as sthk_result.
+  void evaluate(const EventSet& ev, bool grad, double* ll, int* ok, double* g, double* pe) {
+    const bool verify = ensureLoaded(ev);
+    check(sthk_enqueue(h, grad ? 1 : 0, pe != nullptr ? 1 : 0));
+    if (verify && !contentEqual(ev)) {
+      check(sthk_result(h, nullptr, nullptr, nullptr, nullptr));  // (discarded)
+      reload(ev);
+      check(sthk_enqueue(h, grad ? 1 : 0, pe != nullptr ? 1 : 0));
+    }
+    check(sthk_result(h, ll, ok, g, pe));
+  }
+
+  // Contents confirmed before anything is enqueued (batch / excitation paths).
+  void ensureLoadedExact(const EventSet& ev) {
+    if (ensureLoaded(ev) && !contentEqual(ev)) reload(ev);
+  }
 };
 
 AdapterEngine& engine() {
@@ -141,13 +265,12 @@ LikelihoodResult logLikelihood(const EventSet& events, const Params& params,
   backend.validate();
   AdapterEngine& e = engine();
   std::lock_guard<std::mutex> lock(e.mu);
-  e.ensureLoaded(events);
   e.setParams(params);
   LikelihoodResult r;
   if (keepPerEvent) r.perEvent.setZero(events.size());
   double ll = 0;
   int ok = 0;
-  e.check(sthk_loglik(e.h, &ll, &ok, keepPerEvent ? r.perEvent.data() : nullptr));
+  e.evaluate(events, false, &ll, &ok, nullptr, keepPerEvent ? r.perEvent.data() : nullptr);
   r.valid = ok != 0;
   r.logLik = r.valid ? ll : -std::numeric_limits<double>::infinity();
   return r;
@@ -159,14 +282,13 @@ LikelihoodGradient logLikelihoodGradient(const EventSet& events, const Params& p
   backend.validate();
   AdapterEngine& e = engine();
   std::lock_guard<std::mutex> lock(e.mu);
-  e.ensureLoaded(events);
   e.setParams(params);
   LikelihoodGradient out;
   if (keepPerEvent) out.result.perEvent.setZero(events.size());
   double ll = 0;
   int ok = 0;
-  e.check(sthk_loglik_grad(e.h, &ll, &ok, out.grad.data(),
-                           keepPerEvent ? out.result.perEvent.data() : nullptr));
+  e.evaluate(events, true, &ll, &ok, out.grad.data(),
+             keepPerEvent ? out.result.perEvent.data() : nullptr);
   out.result.valid = ok != 0;
   out.result.logLik = out.result.valid ? ll : -std::numeric_limits<double>::infinity();
   return out;
@@ -195,7 +317,7 @@ std::vector<LikelihoodResult> logLikelihoodBatch(const EventSet& events,
     backend.validate();
     AdapterEngine& e = engine();
     std::lock_guard<std::mutex> lock(e.mu);
-    e.ensureLoaded(events);
+    e.ensureLoadedExact(events);
     const size_t P = paramsList.size();
     std::vector<double> pv(6 * P), ll(P);
     std::vector<int> ok(P);
@@ -231,7 +353,7 @@ ExcitationVector excitationProbabilities(const EventSet& events, const Params& p
   backend.validate();
   AdapterEngine& e = engine();
   std::lock_guard<std::mutex> lock(e.mu);
-  e.ensureLoaded(events);
+  e.ensureLoadedExact(events);
   e.setParams(params);
   const Index n = events.size();
   ExcitationVector out;

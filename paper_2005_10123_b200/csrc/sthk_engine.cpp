@@ -1,7 +1,9 @@
 // Host engine behind the sthk.h C ABI: device-resident event sets, per-eval
 // planning (exact culling windows, chunk size, cost-balanced row partition),
-// kernel sequencing on one CUDA stream per device, and the single NCCL
-// all-reduce that combines per-block partials across devices / ranks.
+// kernel sequencing on one CUDA stream per device, and the two multi-rank
+// collectives: the owner-directed exchange of the symmetric sweep's column
+// sums and the all-reduce of the per-block partials, over NCCL, device copies
+// (ranks sharing a GPU) or caller-supplied host callbacks.
 //
 // Reference behaviour mirrored here (file:line under /root/reference/proj):
 //   Params::validate         include/sthawkes/types.hpp:59-72 (same message)
@@ -47,6 +49,9 @@ struct NcclErr : std::runtime_error {
 struct NotLoaded : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct CommErr : std::runtime_error {  // host-callback collective failed
+  using std::runtime_error::runtime_error;
+};
 
 void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
@@ -90,7 +95,11 @@ struct Slot {
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;    // far kernel, concurrent with the near sweep
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t pairs_done = nullptr, fin_done = nullptr;  // cross-slot ordering (local transport)
   ncclComm_t comm = nullptr;
+  int shard = 0;                     // this slot's shard (= rank)
+  unsigned long long* fx_stage = nullptr;  // received fx segments ([6][len] each)
+  size_t fx_stage_cap = 0;
   double *x = nullptr, *y = nullptr, *t = nullptr;
   size_t x_cap = 0, y_cap = 0, t_cap = 0;
   double *xs = nullptr, *ys = nullptr;  // kSym: x, y scaled by sqrt(-cxL) (per evaluation)
@@ -146,10 +155,22 @@ struct Slot {
 
 }  // namespace
 
+// How the shards of one evaluation are combined.
+enum class Xport {
+  kSingle,  // one shard
+  kNccl,    // NCCL: ncclSend / ncclRecv + ncclAllReduce (devices or torchrun ranks)
+  kLocal,   // shards of one process, possibly sharing a GPU: device copies
+  kHosted,  // rank engine with caller-supplied host callbacks (sthk_host_comm)
+};
+
 struct sthk_engine {
   std::vector<Slot> slots;
   bool rank_mode = false;
   int rank = 0, world = 1;
+  Xport xport = Xport::kSingle;
+  sthk_host_comm hcomm{};
+  int64_t exch_bytes = 0;  // fx bytes sent to other owners by the last evaluation
+  int64_t launches = 0;    // kernels launched by the last evaluation (all slots)
   std::vector<double> ht;  // host copy of times (multi-shard planning only; lazy)
   bool ht_valid = false;
   int64_t n = 0, npad = 0;
@@ -187,7 +208,8 @@ struct sthk_engine {
   bool comp_valid = false;
   uint64_t comp_gen = 0;
   double comp_tt = 0, comp_om = 0;
-  double tr_cache_omega = 0, tr_cache_h = 0, tr_cache_dT = 0;
+  double tr_cache_omega = 0, tr_cache_h = 0, tr_cache_dT = 0, tr_cache_dTf = 0;
+  bool tr_cache_far_tr = false;  // the cached sweep stored far-tier trigger partials
   uint64_t load_gen = 0, cache_gen = 0;
   double cache_tx = 0, cache_tt = 0;
   int cache_mode = -1;
@@ -195,7 +217,7 @@ struct sthk_engine {
   bool cache_far_full = false;
   double cache_tfar = 0.0;
   int cache_bg_adj = 0;
-  int virtual_shards = 1;  // testing: partition rows over k shards on one device
+  std::vector<int> cache_cuts;  // shard cuts the cached sums were combined under
   std::string err;
   bool pending = false, last_grad = false, last_pe = false, last_ex = false;
   int last_sc = 0, last_items_est = 0;
@@ -228,6 +250,8 @@ void init_slot(Slot& s, int dev) {
   ck(cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.prepped, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&s.pairs_done, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&s.fin_done, cudaEventDisableTiming), "event");
   for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
   ck(cudaMalloc(&s.scalars, 16 * sizeof(int)), "cudaMalloc");
   ck(cudaMemset(s.scalars, 0, 16 * sizeof(int)), "memset");
@@ -281,7 +305,8 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.tpart), static_cast<void*>(s.crange),
                   static_cast<void*>(s.ex),
                   static_cast<void*>(s.per_event),
-                  static_cast<void*>(s.pair_counts), static_cast<void*>(s.tile_box)}) {
+                  static_cast<void*>(s.pair_counts), static_cast<void*>(s.tile_box),
+                  static_cast<void*>(s.fx_stage)}) {
     if (p) cudaFree(p);
   }
   for (void* p : {static_cast<void*>(s.h_out), static_cast<void*>(s.h_counts),
@@ -296,6 +321,8 @@ void free_slot(Slot& s) {
   if (s.fork) cudaEventDestroy(s.fork);
   if (s.join) cudaEventDestroy(s.join);
   if (s.prepped) cudaEventDestroy(s.prepped);
+  if (s.pairs_done) cudaEventDestroy(s.pairs_done);
+  if (s.fin_done) cudaEventDestroy(s.fin_done);
   if (s.stream2) cudaStreamDestroy(s.stream2);
   if (s.stream) cudaStreamDestroy(s.stream);
 }
@@ -319,7 +346,9 @@ void validate_params(const double* p) {
 void validate_event_args(const double* x, const double* y, const double* t, int64_t n) {
   if (n < 1) throw InvalidArg("EventSet: need at least one event");
   if (!x || !y || !t) throw InvalidArg("EventSet: coordinate/time length mismatch");
-  if (n > (int64_t{1} << 30)) throw InvalidArg("sthk: at most 2^30 events supported");
+  // The fixed-point background sums (sthk_device.cuh fx_add) hold per-row
+  // totals below 2^23; a row's S_B can reach N (every term <= 1).
+  if (n > (int64_t{1} << 23)) throw InvalidArg("sthk: at most 2^23 events supported");
 }
 
 [[noreturn]] void throw_event_error(const double* x, const double* y, const double* t, int64_t i) {
@@ -350,28 +379,82 @@ struct EvalPlan {
   std::vector<int> cuts;  // shard row boundaries (size shards+1)
 };
 
-// ln(trNorm / (mu0 bgNorm)) when positive, else 0: the trigger's weight in
-// lambda against the background self term's (kernels.hpp:78-84).
+constexpr double kFarPairCost = 0.4;     // FP32 far pair vs FP64 near pair (208 vs 485 instr / 16 pairs)
+constexpr double kNearExponentNominal = 35.0;  // partition cost only: typical far threshold A
+
+// ln(trNorm / (mu0 bgNorm)) when positive, else 0 -- the trigger's weight in
+// lambda against the background self term's (kernels.hpp:78-84) -- rounded
+// up to an integer. Every window built on it is conservative in the boost,
+// and the rounding makes the windows (and the sweep caches keyed on them)
+// move only in whole steps as theta and mu0 move.
 double trigger_boost(const double* p) {
   const double kPi_ = 3.14159265358979323846;
   const double cB = p[0] * std::pow(2.0 * kPi_, -1.5) / (p[1] * p[1] * p[2]);
   const double cT = p[3] * p[4] / (2.0 * kPi_ * p[5] * p[5]);
-  return cT > cB ? std::log(cT / cB) : 0.0;
+  return cT > cB ? std::ceil(std::log(cT / cB)) : 0.0;
 }
 
 double far_cull_exponent(int64_t n);
+int64_t lb(const std::vector<double>& t, int64_t n, double v);
+int64_t ub(const std::vector<double>& t, int64_t n, double v);
+
+// Cost-balanced partition of the rows into `shards` contiguous ranges cut at
+// 1024-row block boundaries (the reference's contiguous target blocks,
+// backend.hpp:139-166). The cost model uses only the background windows --
+// functions of (events, tauT, N), which the reference MH sampler keeps fixed
+// (sampler.cpp:48-49) -- so the cuts do not move with mu0, theta, omega, h
+// and the cached background sums of a shard's rows stay valid across a chain.
+// A row block costs its live source width times its rows; in symmetric
+// sweeps the width ends at the block (sources J <= I), and far-tier pairs
+// (FP32) are charged kFarPairCost of an FP64 near pair.
+std::vector<int> plan_cuts(const std::vector<double>& ht, int64_t n, const double* p, bool dense,
+                           bool sym, bool far, int shards) {
+  std::vector<int> cuts(shards + 1, 0);
+  cuts[shards] = static_cast<int>(n);
+  if (shards <= 1) return cuts;
+  const int64_t nb = (n + kRB - 1) / kRB;
+  const double dB = p[2] * std::sqrt(2.0 * sthk::kCullExponent);
+  const double dnear = p[2] * std::sqrt(2.0 * kNearExponentNominal);
+  const double dfar = p[2] * std::sqrt(2.0 * far_cull_exponent(n));
+  std::vector<double> cost(nb);
+  double tot = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t first = b * kRB, last = std::min(first + kRB, n) - 1;
+    double w;
+    if (dense) {
+      w = static_cast<double>(sym ? last + 1 : n);
+    } else if (sym && far) {
+      const int64_t near_lo = lb(ht, n, ht[first] - dnear), far_lo = lb(ht, n, ht[first] - dfar);
+      w = static_cast<double>(last + 1 - near_lo) + kFarPairCost * static_cast<double>(near_lo - far_lo);
+    } else {
+      const int64_t lo = lb(ht, n, ht[first] - dB);
+      const int64_t hi = sym ? last + 1 : ub(ht, n, ht[last] + dB);
+      w = static_cast<double>(hi - lo);
+    }
+    cost[b] = std::max(w, 1.0) * static_cast<double>(last - first + 1);
+    tot += cost[b];
+  }
+  double run = 0;
+  int64_t b = 0;
+  for (int s = 1; s < shards; ++s) {
+    const double target = tot * s / shards;
+    while (b < nb && run + 0.5 * cost[b] < target) run += cost[b++];
+    cuts[s] = static_cast<int>(std::min<int64_t>(b * kRB, n));
+  }
+  return cuts;
+}
 
 // Culling windows: the background term is exactly 0 when |dt| > dB (fexp
 // flushes below -708.40; we cut at -709). The trigger term is cut at
 // dt > dT, the nearer of its exact underflow (omega dt > 709) and the
-// half-ulp window omega dt > C + ceil(boost) (C = ln N + 54 ln 2): lambda >=
+// half-ulp window omega dt > C + boost (C = ln N + 54 ln 2): lambda >=
 // mu0 bgNorm S_B >= mu0 bgNorm, so the skipped trigger terms sum, over at
 // most N sources, to < 2^-54 lambda -- invisible in FP64. The
-// boost is rounded up to an integer so the window (and with it the trigger
-// sums, cached per window) moves only in whole steps as theta and mu0 move.
+// boost is a whole number (trigger_boost), so the window (and with it the
+// trigger sums, cached per window) moves only in whole steps.
 void culling_windows(const double* p, int64_t n, double& dB, double& dT) {
   dB = p[2] * std::sqrt(2.0 * sthk::kCullExponent) * (1.0 + 1e-9);
-  const double zt = std::min(sthk::kCullExponent, far_cull_exponent(n) + std::ceil(trigger_boost(p)));
+  const double zt = std::min(sthk::kCullExponent, far_cull_exponent(n) + trigger_boost(p));
   dT = zt / p[4] * (1.0 + 1e-9);
 }
 
@@ -388,6 +471,7 @@ struct PlanInput {
   const double* p;
   bool dense;
   bool sym;
+  bool far;  // far tier enabled (partition cost)
   // load statistics (far-tier error bound): max |x - x0|, |y - y0|, tile time span
   double ext_x = 0, ext_y = 0, tile_tspan = 0;
 };
@@ -483,6 +567,11 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
     // (never beyond the FP64 culling windows)
     pl.k.dBf = std::min(pl.k.dBf, pl.k.dB);
     pl.k.dTf = std::min(pl.k.dTf, pl.k.dT);
+    // A trigger term that matters can sit below the FP32 flush point once
+    // C + boost > 126 ln 2 + 1 (the far kernel's exponent omits the boost):
+    // then every live trigger source stays in the FP64 near list, and the far
+    // tier carries background terms only (its trigger window dTf <= tfar).
+    if (zc + pl.boost > zf) pl.tfar = std::max(pl.tfar, dT * (1.0 + 1e-9));
   }
 
   // Chunk size: a function of N only (never of the parameters, the device
@@ -502,31 +591,8 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   const int bg_div = n < 64 * 1024 ? 2 : 1;
   pl.sc_bg = std::max(kTS, (pl.sc / bg_div + kTS - 1) / kTS * kTS);
   pl.nchunks_bg = static_cast<int>((n + pl.sc_bg - 1) / pl.sc_bg);
+  pl.cuts = plan_cuts(e.ht, n, p, e.dense, e.sym, e.far, shards);
 
-  // Cost-balanced partition of 1024-row blocks across shards (background
-  // window is two-sided, trigger one-sided: cost ~ live source width).
-  const int64_t nb = (n + kRB - 1) / kRB;
-  pl.cuts.assign(shards + 1, 0);
-  pl.cuts[shards] = static_cast<int>(n);
-  if (shards > 1) {
-    std::vector<double> cost(nb);
-    double tot = 0;
-    for (int64_t b = 0; b < nb; ++b) {
-      const int64_t first = b * kRB, last = std::min(first + kRB, n) - 1;
-      const int64_t lo = e.dense ? 0 : lb(e.ht, n, e.ht[first] - std::max(dB, dT));
-      const int64_t hi = e.sym ? last + 1 : (e.dense ? n : ub(e.ht, n, e.ht[last] + dB));
-      const double w = static_cast<double>(std::max<int64_t>(hi - lo, 1));
-      cost[b] = w * static_cast<double>(last - first + 1);
-      tot += cost[b];
-    }
-    double run = 0;
-    int64_t b = 0;
-    for (int s = 1; s < shards; ++s) {
-      const double target = tot * s / shards;
-      while (b < nb && run + 0.5 * cost[b] < target) run += cost[b++];
-      pl.cuts[s] = static_cast<int>(std::min<int64_t>(b * kRB, n));
-    }
-  }
   return pl;
 }
 
@@ -544,12 +610,256 @@ void fixed_point_scales(const double* p, double* q) {
 
 constexpr int kFxRows = 2 * 3;  // fixed-point words per event (3 background sums)
 
+// One owner-directed transfer of fixed-point background sums: rows
+// [row, row + len) of shard `from`'s accumulators go to their owner `to`.
+struct FxXfer {
+  int from, to;
+  int64_t row, len;
+};
+
+// First source row a shard's symmetric sweep can touch (its column sums land
+// on rows >= this): the live-range start of plan_kernel's tile_plan for the
+// shard's first tile -- the far tier's culled start when the far list is on
+// -- and, for the globally last (partial) tile, its own exact-window start;
+// every start is monotone in the tile. One stage of slack below the
+// stage-aligned start keeps the host computation conservative (extra rows
+// carry zeros).
+int64_t sweep_floor(const sthk_engine& e, const EvalPlan& pl, bool far_on, int row0, int row1) {
+  if (e.dense) return 0;
+  auto start = [&](int64_t first) {
+    const int64_t last = std::min<int64_t>(first + kTM, e.n) - 1;
+    const double tmin = e.ht[first];
+    int64_t lo = std::min(lb(e.ht, e.n, tmin - std::max(pl.k.dB, pl.k.dT)), first);
+    if (far_on && last + 1 - first == kTM) {
+      const int64_t bb = lb(e.ht, e.n, tmin - pl.tfar);
+      const int64_t fb = std::max(lo, bb - bb % kTS);
+      const int64_t b1 = lb(e.ht, e.n, tmin - std::max(pl.k.dBf, pl.k.dTf));
+      lo = std::min(std::max(lo, b1), fb);
+    }
+    return lo;
+  };
+  int64_t lo = start(row0);
+  const int64_t last_tile = (static_cast<int64_t>(row1) - 1) / kTM * kTM;
+  if (e.n % kTM != 0 && row1 == e.n) lo = std::min(lo, start(last_tile));
+  return std::max<int64_t>(0, lo / kTS * kTS - kTS);
+}
+
+std::vector<FxXfer> fx_transfers(const sthk_engine& e, const EvalPlan& pl, bool far_on,
+                                 int shards) {
+  std::vector<FxXfer> v;
+  for (int r = 1; r < shards; ++r) {
+    if (pl.cuts[r] >= pl.cuts[r + 1]) continue;
+    const int64_t lo = sweep_floor(e, pl, far_on, pl.cuts[r], pl.cuts[r + 1]);
+    for (int o = 0; o < r; ++o) {
+      const int64_t a = std::max<int64_t>(lo, pl.cuts[o]);
+      const int64_t b = std::min<int64_t>(pl.cuts[o + 1], pl.cuts[r]);
+      if (b > a) v.push_back({r, o, a, b - a});
+    }
+  }
+  return v;
+}
+
+// Owner-directed exchange of the fixed-point background sums after the pair
+// kernels (symmetric full sweeps with several shards). Every transport moves
+// the same segments along the same routes and ends with fx_accumulate on
+// the owner, so a shard's own rows end up holding exactly the single-shard
+// sums (integer addition).
+void exchange_fx(sthk_engine& e, const std::vector<FxXfer>& xf) {
+  e.exch_bytes = 0;
+  const int nslots = static_cast<int>(e.slots.size());
+  auto slot_of = [&](int shard) -> int {  // local slot running `shard`, or -1
+    for (int i = 0; i < nslots; ++i) {
+      if (e.slots[i].shard == shard) return i;
+    }
+    return -1;
+  };
+  // receive-side staging layout: per owner, its incoming segments in order
+  std::vector<std::vector<sthk::FxSeg>> segs(nslots);
+  std::vector<int64_t> need(nslots, 0);
+  std::vector<std::vector<int>> seg_xfer(nslots);
+  for (size_t i = 0; i < xf.size(); ++i) {
+    const int sf = slot_of(xf[i].from);
+    if (sf >= 0) e.exch_bytes += 6 * 8 * xf[i].len;
+    const int st = slot_of(xf[i].to);
+    if (st < 0) continue;
+    segs[st].push_back({xf[i].row, xf[i].len, need[st]});
+    seg_xfer[st].push_back(static_cast<int>(i));
+    need[st] += 6 * xf[i].len;
+  }
+  for (int i = 0; i < nslots; ++i) {
+    if (need[i] == 0) continue;
+    Slot& s = e.slots[i];
+    set_dev(s);
+    dev_grow(s.fx_stage, s.fx_stage_cap, static_cast<size_t>(need[i]));
+  }
+  const size_t seg_bytes_per_row = sizeof(unsigned long long);
+  if (e.xport == Xport::kLocal) {
+    for (int i = 0; i < nslots; ++i) {
+      Slot& d = e.slots[i];
+      if (segs[i].empty()) continue;
+      set_dev(d);
+      for (size_t k = 0; k < segs[i].size(); ++k) {
+        const FxXfer& x = xf[seg_xfer[i][k]];
+        const Slot& src = e.slots[slot_of(x.from)];
+        ck(cudaStreamWaitEvent(d.stream, src.pairs_done, 0), "wait");
+        for (int w = 0; w < kFxRows; ++w) {
+          unsigned long long* dst = d.fx_stage + segs[i][k].off + w * x.len;
+          const unsigned long long* from = src.fx + static_cast<size_t>(w) * e.npad + x.row;
+          const size_t bytes = seg_bytes_per_row * static_cast<size_t>(x.len);
+          if (src.dev == d.dev) {
+            ck(cudaMemcpyAsync(dst, from, bytes, cudaMemcpyDeviceToDevice, d.stream), "fx copy");
+          } else {
+            ck(cudaMemcpyPeerAsync(dst, d.dev, from, src.dev, bytes, d.stream), "fx peer copy");
+          }
+        }
+      }
+    }
+  } else if (e.xport == Xport::kNccl) {
+    ckn(ncclGroupStart(), "ncclGroupStart");
+    for (int i = 0; i < nslots; ++i) {
+      Slot& s = e.slots[i];
+      for (const FxXfer& x : xf) {
+        if (x.from != s.shard) continue;
+        for (int w = 0; w < kFxRows; ++w) {
+          ckn(ncclSend(s.fx + static_cast<size_t>(w) * e.npad + x.row, static_cast<size_t>(x.len),
+                       ncclUint64, x.to, s.comm, s.stream),
+              "ncclSend(fx)");
+        }
+      }
+      for (size_t k = 0; k < segs[i].size(); ++k) {
+        const FxXfer& x = xf[seg_xfer[i][k]];
+        for (int w = 0; w < kFxRows; ++w) {
+          ckn(ncclRecv(s.fx_stage + segs[i][k].off + w * x.len, static_cast<size_t>(x.len),
+                       ncclUint64, x.from, s.comm, s.stream),
+              "ncclRecv(fx)");
+        }
+      }
+    }
+    ckn(ncclGroupEnd(), "ncclGroupEnd");
+  } else if (e.xport == Xport::kHosted) {
+    Slot& s = e.slots[0];
+    set_dev(s);
+    std::vector<std::vector<unsigned long long>> sbuf;
+    std::vector<int> speer, rpeer;
+    std::vector<const void*> sptr;
+    std::vector<void*> rptr;
+    std::vector<int64_t> sbytes, rbytes;
+    for (const FxXfer& x : xf) {
+      if (x.from != s.shard) continue;
+      sbuf.emplace_back(static_cast<size_t>(6 * x.len));
+      for (int w = 0; w < kFxRows; ++w) {
+        ck(cudaMemcpyAsync(sbuf.back().data() + w * x.len,
+                           s.fx + static_cast<size_t>(w) * e.npad + x.row,
+                           seg_bytes_per_row * static_cast<size_t>(x.len), cudaMemcpyDeviceToHost,
+                           s.stream),
+           "D2H fx");
+      }
+      speer.push_back(x.to);
+      sbytes.push_back(6 * 8 * x.len);
+    }
+    std::vector<unsigned long long> rbuf(static_cast<size_t>(need[0]));
+    for (size_t k = 0; k < segs[0].size(); ++k) {
+      const FxXfer& x = xf[seg_xfer[0][k]];
+      rpeer.push_back(x.from);
+      rptr.push_back(rbuf.data() + segs[0][k].off);
+      rbytes.push_back(6 * 8 * x.len);
+    }
+    for (auto& b : sbuf) sptr.push_back(b.data());
+    ck(cudaStreamSynchronize(s.stream), "D2H fx");
+    if (e.hcomm.exchange(e.hcomm.ctx, static_cast<int>(speer.size()), speer.data(), sptr.data(),
+                         sbytes.data(), static_cast<int>(rpeer.size()), rpeer.data(), rptr.data(),
+                         rbytes.data()) != 0) {
+      throw CommErr("sthk: host exchange callback failed");
+    }
+    if (need[0] > 0) {
+      ck(cudaMemcpyAsync(s.fx_stage, rbuf.data(), sizeof(unsigned long long) * rbuf.size(),
+                         cudaMemcpyHostToDevice, s.stream),
+         "H2D fx");
+    }
+    ck(cudaStreamSynchronize(s.stream), "H2D fx");  // (rbuf is pageable and local)
+  }
+  for (int i = 0; i < nslots; ++i) {
+    Slot& s = e.slots[i];
+    set_dev(s);
+    for (size_t k0 = 0; k0 < segs[i].size(); k0 += sthk::kMaxFxSegs) {
+      sthk::FxAccArgs aa{};
+      aa.fx = s.fx;
+      aa.npad = e.npad;
+      aa.stage = s.fx_stage;
+      aa.nseg = static_cast<int>(std::min<size_t>(sthk::kMaxFxSegs, segs[i].size() - k0));
+      for (int k = 0; k < aa.nseg; ++k) aa.seg[k] = segs[i][k0 + k];
+      ck(sthk::launch_fx_accumulate(aa, s.stream), "fx accumulate");
+      e.launches += 1;
+    }
+  }
+}
+
+// Combination of the per-block partials (each block has exactly one
+// non-zero contributor, so every transport is exact), then the fixed-order
+// final sum into the host-mapped result.
+void combine_blocks(sthk_engine& e, int nb_total) {
+  const size_t words = static_cast<size_t>(nb_total) * kNOut;
+  if (e.xport == Xport::kNccl) {
+    ckn(ncclGroupStart(), "ncclGroupStart");
+    for (Slot& s : e.slots) {
+      ckn(ncclAllReduce(s.block_partial, s.block_partial, words, ncclDouble, ncclSum, s.comm,
+                        s.stream),
+          "ncclAllReduce(blocks)");
+    }
+    ckn(ncclGroupEnd(), "ncclGroupEnd");
+  } else if (e.xport == Xport::kHosted) {
+    Slot& s = e.slots[0];
+    set_dev(s);
+    std::vector<double> hb(words);
+    ck(cudaMemcpyAsync(hb.data(), s.block_partial, sizeof(double) * words, cudaMemcpyDeviceToHost,
+                       s.stream),
+       "D2H blocks");
+    ck(cudaStreamSynchronize(s.stream), "D2H blocks");
+    if (e.hcomm.allreduce_sum(e.hcomm.ctx, hb.data(), static_cast<int64_t>(words),
+                              STHK_DTYPE_F64) != 0) {
+      throw CommErr("sthk: host all-reduce callback failed");
+    }
+    ck(cudaMemcpyAsync(s.block_partial, hb.data(), sizeof(double) * words, cudaMemcpyHostToDevice,
+                       s.stream),
+       "H2D blocks");
+    ck(cudaStreamSynchronize(s.stream), "H2D blocks");
+  } else if (e.xport == Xport::kLocal) {
+    // gather every shard's own blocks into slot 0 (the one that is read)
+    Slot& s0 = e.slots[0];
+    set_dev(s0);
+    for (size_t i = 1; i < e.slots.size(); ++i) {
+      const Slot& s = e.slots[i];
+      if (s.row1 <= s.row0) continue;
+      ck(cudaStreamWaitEvent(s0.stream, s.fin_done, 0), "wait");
+      const size_t b0 = static_cast<size_t>(s.row0 / sthk::kFB);
+      const size_t b1 = static_cast<size_t>((s.row1 + sthk::kFB - 1) / sthk::kFB);
+      const size_t bytes = sizeof(double) * kNOut * (b1 - b0);
+      if (s.dev == s0.dev) {
+        ck(cudaMemcpyAsync(s0.block_partial + b0 * kNOut, s.block_partial + b0 * kNOut, bytes,
+                           cudaMemcpyDeviceToDevice, s0.stream),
+           "block copy");
+      } else {
+        ck(cudaMemcpyPeerAsync(s0.block_partial + b0 * kNOut, s0.dev, s.block_partial + b0 * kNOut,
+                               s.dev, bytes, s0.stream),
+           "block peer copy");
+      }
+    }
+  }
+  for (size_t i = 0; i < e.slots.size(); ++i) {
+    Slot& s = e.slots[i];
+    set_dev(s);
+    const bool reads_out = e.xport != Xport::kLocal || i == 0;
+    ck(sthk::launch_final_sum(s.block_partial, nb_total, reads_out ? s.d_hout : nullptr,
+                              e.timing ? s.pair_counts : nullptr, s.d_hcounts, s.stream),
+       "final sum");
+    e.launches += 1;
+  }
+}
+
 void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false) {
   if (!e.loaded) throw NotLoaded("sthk: no events loaded");
   if (!e.has_params) throw NotLoaded("sthk: no parameters set");
-  const bool vshards = !e.rank_mode && e.slots.size() == 1 && e.virtual_shards > 1;
-  const int shards = vshards ? e.virtual_shards
-                             : (e.rank_mode ? e.world : static_cast<int>(e.slots.size()));
+  const int shards = e.rank_mode ? e.world : static_cast<int>(e.slots.size());
   const bool sym = e.mode == sthk::kSym;
   if (shards > 1 && !e.ht_valid) {  // the cost-balanced partition needs the times on the host
     Slot& s0 = e.slots[0];
@@ -560,16 +870,20 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     ck(cudaStreamSynchronize(s0.stream), "D2H");
     e.ht_valid = true;
   }
-  const EvalPlan pl = make_plan(
-      PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym, e.ext_x, e.ext_y, e.tile_tspan}, shards);
+  const EvalPlan pl = make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym, sym && e.far_tier,
+                                          e.ext_x, e.ext_y, e.tile_tspan},
+                                shards);
   e.last_sc = pl.sc;
+  e.exch_bytes = 0;
+  e.launches = 0;
   // Split structure of a full sweep (it fixes how the background sums are
   // grouped, so a cached background is reused only under the same structure):
   //  * far tier on/off and its split tfar;
   //  * the trigger-free near split bg_adj, chosen from the physical trigger
   //    window 709/omega -- not the dense mode's infinite one -- so dense and
   //    culled sweeps split alike; it moves only when omega crosses a
-  //    threshold (then the background is recomputed).
+  //    threshold (then the background is recomputed);
+  //  * the shard cuts (a shard's accumulators hold its own rows only).
   const bool far_guard = sym && e.far_tier && e.ext_x * pl.sxf <= kFarCoordMax &&
                          e.ext_y * pl.sxf <= kFarCoordMax && e.tile_tspan * pl.stf <= kFarCoordMax;
   const bool far_full = far_guard && !(std::max(pl.k.dB, pl.k.dT) <= pl.tfar);
@@ -589,12 +903,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
                       e.cache_tx == e.p[1] && e.cache_tt == e.p[2] && e.cache_mode == e.mode &&
                       e.cache_far_full == far_full && e.cache_tfar == (far_full ? pl.tfar : 0.0) &&
                       e.cache_bg_adj == bg_adj && e.cache_dense == e.dense &&
-                      (e.cache_grad || !grad);
-  const bool tr_cached = cached && e.tr_cache_valid && e.tr_cache_omega == e.p[4] &&
-                         e.tr_cache_h == e.p[5] && e.tr_cache_dT == pl.k.dT &&
-                         e.tr_cache_grad == grad;  // (tpart layout)
+                      e.cache_cuts == pl.cuts && (e.cache_grad || !grad);
   e.last_cache_hit = cached;
-  e.last_tr_cache_hit = tr_cached;
   const bool bg_split = !cached && bg_adj > 0;
   // (a far list that is provably empty -- every live source within tfar of
   // its tile, e.g. a trigger-only sweep at large omega -- is not planned or
@@ -604,6 +914,14 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
   // tier's trigger cull window dTf <= tfar no far trigger term is live, and
   // its (all-zero) trigger partials are neither stored nor summed
   const bool far_tr = far_on && !(pl.k.dTf <= pl.tfar);
+  // Trigger sums cached from the last sweep: same omega, h and trigger
+  // windows, and the same far-tier trigger split (which fixes whether far
+  // trigger partials exist and which chunks finalize sums).
+  const bool tr_cached = cached && e.tr_cache_valid && e.tr_cache_omega == e.p[4] &&
+                         e.tr_cache_h == e.p[5] && e.tr_cache_dT == pl.k.dT &&
+                         e.tr_cache_dTf == pl.k.dTf && e.tr_cache_far_tr == far_tr &&
+                         e.tr_cache_grad == grad;  // (tpart layout)
+  e.last_tr_cache_hit = tr_cached;
   e.cache_valid = false;  // re-armed below once the sweep is enqueued
   e.tr_cache_valid = false;
   const int64_t ntiles_total = (e.n + kTM - 1) / kTM;
@@ -613,36 +931,23 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
   double fxq[sthk::kNSumGrad];
   fixed_point_scales(p, fxq);
 
-  // (slot, shard) runs: one per device, or every virtual shard on slot 0
-  struct Run {
-    int slot, row0, row1;
-  };
-  std::vector<Run> runs;
-  if (vshards) {
-    for (int k = 0; k < shards; ++k) runs.push_back({0, pl.cuts[k], pl.cuts[k + 1]});
-  } else {
-    for (int si = 0; si < static_cast<int>(e.slots.size()); ++si) {
-      const int shard = e.rank_mode ? e.rank : si;
-      runs.push_back({si, pl.cuts[shard], pl.cuts[shard + 1]});
-    }
+  for (size_t si = 0; si < e.slots.size(); ++si) {
+    Slot& s = e.slots[si];
+    s.row0 = pl.cuts[s.shard];
+    s.row1 = pl.cuts[s.shard + 1];
   }
-  for (Slot& s : e.slots) s.runs.clear();
 
-  const bool need_comp = !(e.comp_valid && e.comp_gen == e.load_gen && e.comp_tt == p[2] &&
-                           e.comp_om == p[4]);
+  // compensator terms: cached (exact) while tauT and omega are unchanged
+  const bool need_comp = !(e.bg_cache && e.comp_valid && e.comp_gen == e.load_gen &&
+                           e.comp_tt == p[2] && e.comp_om == p[4]);
   if (need_comp) e.comp_valid = false;  // re-armed once the prep pass is enqueued
-  // phase 1: zero the accumulators, plan and run the pair kernel per run
-  for (const Run& run : runs) {
+  // phase 1: zero the accumulators, plan and run the pair kernels per shard
+  for (Slot& s : e.slots) {
     bool prep_pending = false, prep_unlaunched = false;
     sthk::PrepArgs pr{};
-    Slot& s = e.slots[run.slot];
-    const bool first_run = s.runs.empty();
-    s.runs.emplace_back(run.row0, run.row1);
-    if (first_run) s.row0 = run.row0;
-    s.row1 = run.row1;
     set_dev(s);
-    const int tile0 = run.row0 / kTM;
-    const int tile1 = static_cast<int>((run.row1 + kTM - 1) / kTM);
+    const int tile0 = s.row0 / kTM;
+    const int tile1 = static_cast<int>((s.row1 + kTM - 1) / kTM);
     const int ntiles = std::max(tile1 - tile0, 0);
     dev_grow(s.ranges, s.ranges_cap, static_cast<size_t>(ntiles_total));
     dev_grow(s.items, s.items_cap, static_cast<size_t>(std::max(ntiles, 1)) * pl.nchunks);
@@ -668,44 +973,42 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     if (want_ex) dev_grow(s.ex, s.ex_cap, static_cast<size_t>(3) * e.npad);
 
     cudaStream_t st = s.stream;
-    if (first_run) {
-      if (e.timing) ck(cudaEventRecord(s.ev[0], st), "event");
-      // (pair counters, timing only, are zero here: the final kernel of the
-      // previous timed evaluation re-zeroed them after copying them out)
-      // one prep pass on stream 2, beside the plan (stream 1): scaled / FP32
-      // coordinates (a cached sweep has the same tauX, tauT: copies still
-      // valid), zeroed background accumulators, compensator terms
-      pr.x = s.x;
-      pr.y = s.y;
-      pr.t = s.t;
-      pr.n = e.n;
-      pr.npad = e.npad;
-      if (sym && !cached) {
-        pr.sx = pl.sx;
-        pr.xs = s.xs;
-        pr.ys = s.ys;
-        if (far_on) {
-          pr.sxf = pl.sxf;
-          pr.stf = pl.stf;
-          pr.xf = s.xf;
-          pr.yf = s.yf;
-          pr.tf = s.tf;
-        }
+    if (e.timing) ck(cudaEventRecord(s.ev[0], st), "event");
+    // (pair counters, timing only, are zero here: the final kernel of the
+    // previous timed evaluation re-zeroed them after copying them out)
+    // one prep pass on stream 2, beside the plan (stream 1): scaled / FP32
+    // coordinates (a cached sweep has the same tauX, tauT: copies still
+    // valid), zeroed background accumulators, compensator terms
+    pr.x = s.x;
+    pr.y = s.y;
+    pr.t = s.t;
+    pr.n = e.n;
+    pr.npad = e.npad;
+    if (sym && !cached) {
+      pr.sx = pl.sx;
+      pr.xs = s.xs;
+      pr.ys = s.ys;
+      if (far_on) {
+        pr.sxf = pl.sxf;
+        pr.stf = pl.stf;
+        pr.xf = s.xf;
+        pr.yf = s.yf;
+        pr.tf = s.tf;
       }
-      if (!cached) pr.fx = s.fx;
-      if (need_comp) {
-        pr.comp = s.comp;
-        pr.window_end = e.window_end;
-        pr.tauT = p[2];
-        pr.omega = p[4];
-      }
-      if (pr.xs || pr.fx || pr.comp) {  // (launched right after the plan, see below)
-        ck(cudaEventRecord(s.fork, st), "event");
-        prep_unlaunched = true;
-      }
-      if (shards > 1) {
-        ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
-      }
+    }
+    if (!cached) pr.fx = s.fx;
+    if (need_comp) {
+      pr.comp = s.comp;
+      pr.window_end = e.window_end;
+      pr.tauT = p[2];
+      pr.omega = p[4];
+    }
+    if (pr.xs || pr.fx || pr.comp) {  // (launched right after the plan, see below)
+      ck(cudaEventRecord(s.fork, st), "event");
+      prep_unlaunched = true;
+    }
+    if (shards > 1) {
+      ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
     }
     // The plan kernel goes first: its few CTAs take whole SMs (1024 threads,
     // the full register file) before the prep pass spreads over the rest, so
@@ -714,22 +1017,23 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       if (!prep_unlaunched) return;
       ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
       ck(sthk::launch_prep(pr, s.stream2), "prep");
+      e.launches += 1;
       ck(cudaEventRecord(s.prepped, s.stream2), "event");
       prep_unlaunched = false;
       prep_pending = true;
     };
+    auto join_prep = [&] {
+      if (!prep_pending) return;
+      ck(cudaStreamWaitEvent(st, s.prepped, 0), "wait");
+      prep_pending = false;
+    };
     if (ntiles == 0 || tr_cached) {
       launch_prep_now();
-      if (prep_pending) {
-        ck(cudaStreamWaitEvent(st, s.prepped, 0), "wait");
-        prep_pending = false;
-      }
-    }
-    if (ntiles == 0) continue;
-    if (tr_cached) {  // every pair sum is cached: finalize only
-      if (e.timing && first_run) ck(cudaEventRecord(s.ev[1], st), "event");
+      join_prep();
+      ck(cudaEventRecord(s.ev[1], st), "event");
       if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
-      continue;
+      ck(cudaEventRecord(s.pairs_done, st), "event");
+      continue;  // (tr_cached: every pair sum is cached, finalize only)
     }
     sthk::PlanArgs pa{};
     pa.t = s.t;
@@ -771,12 +1075,13 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       pa.work_counter_far = s.scalars + 7;
     }
     const int key[7] = {tile0, tile1, pl.sc, pa.dense, pa.sym, pa.trig_only, bg_split ? bg_adj : 0};
-    const bool plan_hit = e.bg_cache && !vshards && s.plan_valid && s.plan_dB == pa.dB &&
+    const bool plan_hit = e.bg_cache && s.plan_valid && s.plan_dB == pa.dB &&
                           s.plan_dT == pa.dT && s.plan_tfar == pa.tfar && s.plan_dfar == pa.dFar &&
                           std::equal(key, key + 7, s.plan_key);
     if (!plan_hit) {  // (the work counters are re-armed by the last pair CTAs)
       ck(sthk::launch_plan(pa, st), "plan");
-      s.plan_valid = e.bg_cache && !vshards;
+      e.launches += 1;
+      s.plan_valid = e.bg_cache;
       s.plan_dB = pa.dB;
       s.plan_dT = pa.dT;
       s.plan_tfar = pa.tfar;
@@ -784,11 +1089,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       std::copy(key, key + 7, s.plan_key);
     }
     launch_prep_now();
+    join_prep();  // pair kernels need the prepared coordinates / zeroed sums
 
-    if (prep_pending) {  // pair kernels need the prepared coordinates / zeroed sums
-      ck(cudaStreamWaitEvent(st, s.prepped, 0), "wait");
-      prep_pending = false;
-    }
     sthk::PairArgs qa{};
     qa.x = s.x;
     qa.y = s.y;
@@ -827,6 +1129,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
       ba.work_counter = s.scalars + 10;
       ba.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 11);
       ck(sthk::launch_bgonly(ba, grad, s.sms * s.occ_bg[grad ? 1 : 0], st), "bg-only kernel");
+      e.launches += 1;
     };
     const int occ = s.occ[e.mode][grad ? 1 : 0];
     const bool conc = far_on && e.far_concurrent;
@@ -835,7 +1138,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     // timing event here, between the prep join and the far fork, measurably
     // lets the near kernel's CTAs reach the SMs ahead of the far kernel's
     // (C2, Θ_post: 0.472 -> 0.444 ms with timing off; no effect at Θ_init)
-    if (first_run) ck(cudaEventRecord(s.ev[1], st), "event");
+    ck(cudaEventRecord(s.ev[1], st), "event");
     if (far_on) {  // the far work list in FP32
       sthk::PairArgs fa_ = qa;
       fa_.ranges = s.ranges_far;
@@ -850,101 +1153,90 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
         if (e.far_order == 2) {  // near first: its CTAs are resident before far CTAs fill in
           launch_bg();
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
+          e.launches += 1;
           ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
+          e.launches += 1;
         } else {
           launch_bg();
           ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
+          e.launches += 1;
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
+          e.launches += 1;
         }
         ck(cudaEventRecord(s.join, s.stream2), "event");
         ck(cudaStreamWaitEvent(st, s.join, 0), "wait");
       } else {
         launch_bg();
         ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
+        e.launches += 1;
         ck(sthk::launch_far(fa_, grad, s.sms * s.occ_far[grad ? 1 : 0], st), "far kernel");
+        e.launches += 1;
       }
     } else {
       launch_bg();
       ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
+      e.launches += 1;
     }
     if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
+    ck(cudaEventRecord(s.pairs_done, st), "event");
   }
 
-  // phase 2: symmetric mode adds column sums to rows other devices own
-  if (sym && !cached && shards > 1 && !vshards) {
-    ckn(ncclGroupStart(), "ncclGroupStart");
-    for (Slot& s : e.slots) {
-      ckn(ncclAllReduce(s.fx, s.fx, static_cast<size_t>(kFxRows) * e.npad, ncclUint64, ncclSum,
-                        s.comm, s.stream),
-          "ncclAllReduce(fx)");
-    }
-    ckn(ncclGroupEnd(), "ncclGroupEnd");
-  }
+  // phase 2: symmetric sweeps add column sums to earlier rows, some owned by
+  // other shards: each shard ships those rows to their owner
+  if (sym && !cached && shards > 1) exchange_fx(e, fx_transfers(e, pl, far_on, shards));
 
-  // phase 3: per-row finalize into 1024-row block partials
-  for (const Run& run : runs) {
-    if (run.row1 <= run.row0) continue;
-    Slot& s = e.slots[run.slot];
+  // phase 3: per-row finalize into 256-row block partials
+  for (Slot& s : e.slots) {
     set_dev(s);
-    sthk::FinArgs fa{};
-    fa.t = s.t;
-    fa.n = e.n;
-    fa.npad = e.npad;
-    fa.row0 = run.row0;
-    fa.row1 = run.row1;
-    fa.window_end = e.window_end;
-    fa.mu0 = p[0];
-    fa.tauX = p[1];
-    fa.tauT = p[2];
-    fa.theta = p[3];
-    fa.omega = p[4];
-    fa.h = p[5];
-    // HawkesPairTerm constants, kernels.hpp:78-84
-    fa.bgNorm = std::pow(2.0 * kPi, -1.5) / (p[1] * p[1] * p[2]);
-    fa.trNorm = p[3] * p[4] / (2.0 * kPi * p[5] * p[5]);
-    fa.cT = p[4] / (2.0 * kPi * p[5] * p[5]);
-    fa.fx = s.fx;
-    fa.tpart = s.tpart;
-    fa.tr_r2_scale = sym ? 1.0 / (pl.sx * pl.sx) : 1.0;
-    fa.crange = s.crange;
-    fa.comp = s.comp;
-    fa.tpart_far = far_tr ? s.tpart_far : nullptr;
-    fa.crange_far = s.crange_far;
-    for (int k = 0; k < sthk::kNSumGrad; ++k) fa.fxq[k] = fxq[k];
-    fa.per_event = want_pe ? s.per_event : nullptr;
-    fa.ex_out = want_ex ? s.ex : nullptr;
-    fa.block_partial = s.block_partial;
-    // one shard on this slot and no collective: the final sum rides along
-    fa.fused_out = (shards == 1) ? s.d_hout : nullptr;
-    fa.counts = (shards == 1 && e.timing) ? s.pair_counts : nullptr;
-    fa.counts_out = s.d_hcounts;
-    fa.nblocks_total = nb_total;
-    fa.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 3);
-    ck(sthk::launch_finalize(fa, grad, s.stream), "finalize");
+    if (s.row1 > s.row0) {
+      sthk::FinArgs fa{};
+      fa.t = s.t;
+      fa.n = e.n;
+      fa.npad = e.npad;
+      fa.row0 = s.row0;
+      fa.row1 = s.row1;
+      fa.window_end = e.window_end;
+      fa.mu0 = p[0];
+      fa.tauX = p[1];
+      fa.tauT = p[2];
+      fa.theta = p[3];
+      fa.omega = p[4];
+      fa.h = p[5];
+      // HawkesPairTerm constants, kernels.hpp:78-84
+      fa.bgNorm = std::pow(2.0 * kPi, -1.5) / (p[1] * p[1] * p[2]);
+      fa.trNorm = p[3] * p[4] / (2.0 * kPi * p[5] * p[5]);
+      fa.cT = p[4] / (2.0 * kPi * p[5] * p[5]);
+      fa.fx = s.fx;
+      fa.tpart = s.tpart;
+      fa.tr_r2_scale = sym ? 1.0 / (pl.sx * pl.sx) : 1.0;
+      fa.crange = s.crange;
+      fa.comp = s.comp;
+      fa.tpart_far = far_tr ? s.tpart_far : nullptr;
+      fa.crange_far = s.crange_far;
+      for (int k = 0; k < sthk::kNSumGrad; ++k) fa.fxq[k] = fxq[k];
+      fa.per_event = want_pe ? s.per_event : nullptr;
+      fa.ex_out = want_ex ? s.ex : nullptr;
+      fa.block_partial = s.block_partial;
+      // one shard and no collective: the final sum rides along
+      fa.fused_out = (shards == 1) ? s.d_hout : nullptr;
+      fa.counts = (shards == 1 && e.timing) ? s.pair_counts : nullptr;
+      fa.counts_out = s.d_hcounts;
+      fa.nblocks_total = nb_total;
+      fa.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 3);
+      ck(sthk::launch_finalize(fa, grad, s.stream), "finalize");
+      e.launches += 1;
+    }
+    ck(cudaEventRecord(s.fin_done, s.stream), "event");
   }
 
-  // phase 4: exact combination of the block partials (each block has one
-  // non-zero contributor), then the fixed-order final sum on every device
-  if (shards > 1 && !vshards) {
-    ckn(ncclGroupStart(), "ncclGroupStart");
-    for (Slot& s : e.slots) {
-      ckn(ncclAllReduce(s.block_partial, s.block_partial, static_cast<size_t>(nb_total) * kNOut,
-                        ncclDouble, ncclSum, s.comm, s.stream),
-          "ncclAllReduce");
-    }
-    ckn(ncclGroupEnd(), "ncclGroupEnd");
-  }
+  // phase 4: exact combination of the block partials, fixed-order final sum
+  if (shards > 1) combine_blocks(e, nb_total);
 
   for (Slot& s : e.slots) {
     set_dev(s);
     cudaStream_t st = s.stream;
-    if (shards > 1) {
-      ck(sthk::launch_final_sum(s.block_partial, nb_total, s.d_hout,
-                                e.timing ? s.pair_counts : nullptr, s.d_hcounts, st),
-         "final sum");
-    }
     if (!e.timing) std::fill(s.h_counts, s.h_counts + sthk::kNCounts, 0ULL);
-    if (want_pe && s.row1 > s.row0) {  // runs on one slot are contiguous
+    if (want_pe && s.row1 > s.row0) {
       if (s.h_pe_cap < static_cast<size_t>(e.npad)) {
         if (s.h_per_event) ck(cudaFreeHost(s.h_per_event), "cudaFreeHost");
         ck(cudaMallocHost(&s.h_per_event, sizeof(double) * e.npad), "cudaMallocHost");
@@ -982,6 +1274,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     e.cache_far_full = far_full;
     e.cache_tfar = far_full ? pl.tfar : 0.0;
     e.cache_bg_adj = bg_adj;
+    e.cache_cuts = pl.cuts;
   }
   e.cache_valid = true;
   if (!tr_cached) {
@@ -989,9 +1282,11 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
     e.tr_cache_omega = e.p[4];
     e.tr_cache_h = e.p[5];
     e.tr_cache_dT = pl.k.dT;
+    e.tr_cache_dTf = pl.k.dTf;
+    e.tr_cache_far_tr = far_tr;
   }
   e.tr_cache_valid = e.bg_cache;
-  e.comp_valid = true;
+  e.comp_valid = e.bg_cache;
   e.comp_gen = e.load_gen;
   e.comp_tt = p[2];
   e.comp_om = p[4];
@@ -1040,6 +1335,8 @@ int guarded(sthk_engine* e, F&& f) {
   } catch (const NotLoaded& x) {
     return fail(e, STHK_ENOTLOADED, x.what());
   } catch (const NcclErr& x) {
+    return fail(e, STHK_ENCCL, x.what());
+  } catch (const CommErr& x) {
     return fail(e, STHK_ENCCL, x.what());
   } catch (const CudaErr& x) {
     return fail(e, STHK_ECUDA, x.what());
@@ -1095,8 +1392,17 @@ int sthk_create(const int* device_ids, int n_devices, sthk_engine** out) {
       }
     }
     e->slots.resize(n_devices);
-    for (int i = 0; i < n_devices; ++i) init_slot(e->slots[i], device_ids[i]);
-    if (n_devices > 1) {
+    for (int i = 0; i < n_devices; ++i) {
+      init_slot(e->slots[i], device_ids[i]);
+      e->slots[i].shard = i;
+    }
+    // a repeated device id: shards sharing a GPU, combined by device copies
+    // (NCCL needs one rank per device)
+    std::vector<int> ids(device_ids, device_ids + n_devices);
+    std::sort(ids.begin(), ids.end());
+    const bool dup = std::adjacent_find(ids.begin(), ids.end()) != ids.end();
+    e->xport = n_devices == 1 ? Xport::kSingle : dup ? Xport::kLocal : Xport::kNccl;
+    if (e->xport == Xport::kNccl) {
       std::vector<ncclComm_t> comms(n_devices);
       ckn(ncclCommInitAll(comms.data(), n_devices, device_ids), "ncclCommInitAll");
       for (int i = 0; i < n_devices; ++i) e->slots[i].comm = comms[i];
@@ -1138,9 +1444,11 @@ int sthk_create_rank(int device, int rank, int world, const void* nccl_id,
   e->rank_mode = true;
   e->rank = rank;
   e->world = world;
+  e->xport = world > 1 ? Xport::kNccl : Xport::kSingle;
   try {
     e->slots.resize(1);
     init_slot(e->slots[0], device);
+    e->slots[0].shard = rank;
     if (world > 1) {
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));
@@ -1150,6 +1458,33 @@ int sthk_create_rank(int device, int rank, int world, const void* nccl_id,
     g_create_err = x.what();
     for (auto& s : e->slots) free_slot(s);
     return STHK_ENCCL;
+  } catch (const std::exception& x) {
+    g_create_err = x.what();
+    for (auto& s : e->slots) free_slot(s);
+    return STHK_ECUDA;
+  }
+  *out = e.release();
+  return STHK_OK;
+}
+
+int sthk_create_rank_hosted(int device, int rank, int world, const sthk_host_comm* comm,
+                            sthk_engine** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world || !comm || !comm->allreduce_sum ||
+      !comm->exchange) {
+    g_create_err = "sthk_create_rank_hosted: invalid rank/world/callbacks";
+    return STHK_EINVAL;
+  }
+  *out = nullptr;
+  auto e = std::make_unique<sthk_engine>();
+  e->rank_mode = true;
+  e->rank = rank;
+  e->world = world;
+  e->xport = world > 1 ? Xport::kHosted : Xport::kSingle;
+  e->hcomm = *comm;
+  try {
+    e->slots.resize(1);
+    init_slot(e->slots[0], device);
+    e->slots[0].shard = rank;
   } catch (const std::exception& x) {
     g_create_err = x.what();
     for (auto& s : e->slots) free_slot(s);
@@ -1350,7 +1685,7 @@ int sthk_plan_partition(const double* t, int64_t n, const double* params6, int s
     validate_params(params6);
     const std::vector<double> ht(t, t + n);
     const int64_t npad = (n + kTM - 1) / kTM * kTM;
-    const EvalPlan pl = make_plan(PlanInput{ht, n, npad, params6, dense != 0, true}, shards);
+    const EvalPlan pl = make_plan(PlanInput{ht, n, npad, params6, dense != 0, true, true}, shards);
     for (int k = 0; k <= shards; ++k) cuts[k] = pl.cuts[k];
     if (source_chunk) *source_chunk = pl.sc;
     return STHK_OK;
@@ -1401,13 +1736,10 @@ int sthk_set_kernel(sthk_engine* e, int mode) {
   });
 }
 
-int sthk_set_virtual_shards(sthk_engine* e, int k) {
+int sthk_get_exchange_bytes(sthk_engine* e, int64_t* bytes) {
   return guarded(e, [&] {
-    if (k < 1 || k > 4096) throw InvalidArg("sthk_set_virtual_shards: k must be in [1, 4096]");
-    if (e->rank_mode || e->slots.size() != 1) {
-      throw InvalidArg("sthk_set_virtual_shards: single-device handles only");
-    }
-    e->virtual_shards = k;
+    if (!bytes) throw InvalidArg("sthk_get_exchange_bytes: null");
+    *bytes = e->exch_bytes;
   });
 }
 
@@ -1433,6 +1765,7 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
     out->kernel_mode = e->mode;
     out->cache_hit = e->last_cache_hit ? 1 : 0;
     out->trigger_cache_hit = e->last_tr_cache_hit ? 1 : 0;
+    out->kernel_launches = e->launches;
     for (Slot& s : e->slots) {
       out->pairs_bg += static_cast<int64_t>(s.h_counts[0]);
       out->pairs_tr += static_cast<int64_t>(s.h_counts[1]);

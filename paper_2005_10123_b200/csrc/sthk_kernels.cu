@@ -1640,14 +1640,37 @@ __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict
                                                         unsigned long long* counts,
                                                         unsigned long long* counts_out) {
   __shared__ double s_red[kNOut][256];
-  final_sum_block(bp, nblocks, out, s_red);
+  if (out) final_sum_block(bp, nblocks, out, s_red);
   if (counts && threadIdx.x < kNCounts) {
     counts_out[threadIdx.x] = counts[threadIdx.x];
     counts[threadIdx.x] = 0ULL;
   }
 }
 
+// Adds received fx segments (blockIdx.y = segment) into this rank's
+// accumulators; several senders may cover the same rows, hence the atomics.
+__global__ void __launch_bounds__(256) fx_accumulate_kernel(const FxAccArgs a) {
+  const FxSeg sg = a.seg[blockIdx.y];
+  const int64_t words = 6 * sg.len;
+  for (int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < words;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k = w / sg.len, i = w - k * sg.len;
+    const unsigned long long v = a.stage[sg.off + w];
+    if (v != 0ULL) atomicAdd(&a.fx[k * a.npad + sg.row + i], v);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_fx_accumulate(const FxAccArgs& a, cudaStream_t stream) {
+  if (a.nseg <= 0) return cudaSuccess;
+  int64_t maxlen = 0;
+  for (int s = 0; s < a.nseg; ++s) maxlen = a.seg[s].len > maxlen ? a.seg[s].len : maxlen;
+  const int64_t bx = (6 * maxlen + 255) / 256;
+  const dim3 grid(static_cast<unsigned>(bx < 592 ? (bx > 0 ? bx : 1) : 592), a.nseg);
+  fx_accumulate_kernel<<<grid, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
                               double4* box, double2* trange, double* piv,

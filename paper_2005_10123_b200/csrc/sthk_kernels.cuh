@@ -216,10 +216,29 @@ cudaError_t launch_far(const PairArgs& a, bool grad, int grid, cudaStream_t stre
 int far_kernel_occupancy(bool grad);
 cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream);
 // (out and counts_out may be host-mapped; counts, if non-null, are copied to
-// counts_out and re-zeroed)
+// counts_out and re-zeroed; out == nullptr: counters only)
 cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,
                              unsigned long long* counts, unsigned long long* counts_out,
                              cudaStream_t stream);
+
+// Owner-directed exchange of the fixed-point background sums (multi-rank
+// symmetric sweeps): a rank's column sums land on earlier rows,
+// some owned by other ranks; each sender ships rows [row, row + len) of its
+// six fx words to their owner, which adds them into its own accumulators.
+// Segment s of `stage` is laid out [6][len] at word offset off. Integer
+// addition: exact and order-free.
+struct FxSeg {
+  int64_t row, len, off;
+};
+constexpr int kMaxFxSegs = 32;  // segments per launch (the host loops beyond)
+struct FxAccArgs {
+  unsigned long long* fx;
+  int64_t npad;
+  const unsigned long long* stage;
+  int nseg;
+  FxSeg seg[kMaxFxSegs];
+};
+cudaError_t launch_fx_accumulate(const FxAccArgs& a, cudaStream_t stream);
 // Resident CTAs per SM of a pair kernel (for the persistent grid size).
 int pair_kernel_occupancy(bool grad, int mode);
 

@@ -31,22 +31,30 @@ def _dptr(a: np.ndarray):
 class Engine:
     """Stateful device engine: events stay resident in HBM across calls.
 
-    devices: local CUDA device ids driven from this process (rows are
-    partitioned across them, one NCCL all-reduce per evaluation).
+    devices: local CUDA device ids driven from this process, one row shard
+    each (NCCL between distinct devices; a repeated id runs several shards
+    on one GPU, combined by device copies -- the multi-GPU data flow
+    emulated on one device).
     rank/world/nccl_id: one-process-per-GPU mode (torchrun); pass the id
     from Engine.nccl_unique_id() on rank 0 to every rank.
+    rank/world/comm: rank mode whose collectives run through host callbacks
+    (hostcomm.TorchDistComm over gloo), e.g. several ranks on one GPU.
     """
 
     def __init__(self, devices: Sequence[int] = (0,), *, rank: Optional[int] = None,
-                 world: int = 1, nccl_id: Optional[bytes] = None):
+                 world: int = 1, nccl_id: Optional[bytes] = None, comm=None):
         self._lib = _lib.load_library()
         self._h = c_void_p()
         self._lock = threading.Lock()
         self._events_key = None
         self._n = 0
+        self._comm = comm  # (keeps the host callbacks alive)
         if rank is None:
             ids = (c_int * len(devices))(*devices)
             rc = self._lib.sthk_create(ids, len(devices), byref(self._h))
+        elif comm is not None:
+            rc = self._lib.sthk_create_rank_hosted(int(devices[0]), int(rank), int(world),
+                                                   byref(comm.struct), byref(self._h))
         else:
             buf = None
             if world > 1:
@@ -203,8 +211,11 @@ class Engine:
         """0 = rows (ordered pairs), 1 = symmetric background (default)."""
         self._check(self._lib.sthk_set_kernel(self._h, int(mode)), "sthk_set_kernel")
 
-    def set_virtual_shards(self, k: int) -> None:
-        self._check(self._lib.sthk_set_virtual_shards(self._h, int(k)), "sthk_set_virtual_shards")
+    def exchange_bytes(self) -> int:
+        """Background-sum bytes shipped to other shards' owners by the last evaluation."""
+        v = ctypes.c_int64()
+        self._check(self._lib.sthk_get_exchange_bytes(self._h, byref(v)), "sthk_get_exchange_bytes")
+        return v.value
 
     def stats(self) -> dict:
         s = _lib.StatsStruct()

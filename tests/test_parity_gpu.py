@@ -107,20 +107,22 @@ def test_matches_reference_engine(engine):
 
 @pytest.mark.parametrize("k", [2, 3, 8])
 def test_partition_bitwise_invariant(engine, k):
-    """Row partition across k shards (the multi-GPU split, run on one device
-    and combined as the NCCL path does) gives bitwise-identical results."""
+    """Row partition across k shards -- k separate rank engines on one device
+    (own accumulators, plans and partials) combined along the multi-GPU
+    routes -- gives bitwise-identical results."""
     ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
                                       pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
                                       keep=20000)
     engine.load(ev)
-    for p in (pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695), pk.Params(1, 1.6, 14, 0.1, 1, 1)):
-        engine.set_params(p)
-        engine.set_virtual_shards(1)
-        a = engine.loglik_grad(per_event=True)
-        engine.set_virtual_shards(k)
-        b = engine.loglik_grad(per_event=True)
-        engine.set_virtual_shards(1)
-        assert a[0] == b[0] and np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
+    with pk.Engine((0,) * k) as sh:
+        sh.load(ev)
+        for p in (pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695), pk.Params(1, 1.6, 14, 0.1, 1, 1)):
+            engine.set_params(p)
+            sh.set_params(p)
+            a = engine.loglik_grad(per_event=True)
+            b = sh.loglik_grad(per_event=True)
+            assert a[0] == b[0] and np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
+            assert sh.exchange_bytes() > 0
 
 
 def test_pair_counters_and_results_through_mapped_memory(engine):
@@ -136,23 +138,26 @@ def test_pair_counters_and_results_through_mapped_memory(engine):
     engine.set_params(pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695))
     engine.set_background_cache(False)
     keys = ("pairs_bg", "pairs_tr", "pairs_any", "exec_bg", "exec_geom", "exec_sym", "exec_far")
+    sh = pk.Engine((0, 0, 0))
+    sh.load(ev)
+    sh.set_params(pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695))
+    sh.set_background_cache(False)
     try:
         base = engine.loglik_grad()
         counts = []
-        for k in (1, 1, 3, 3, 1):
-            engine.set_virtual_shards(k)
-            engine.set_timing(True)
-            r = engine.loglik_grad()
-            st = engine.stats()
-            engine.set_timing(False)
+        for eng in (engine, engine, sh, sh, engine):
+            eng.set_timing(True)
+            r = eng.loglik_grad()
+            st = eng.stats()
+            eng.set_timing(False)
             counts.append(tuple(st[q] for q in keys))
             assert r[0] == base[0] and np.array_equal(r[2], base[2])
         assert counts[0][0] > 0 and len(set(counts)) == 1, counts
-        engine.set_virtual_shards(1)
-        engine.loglik_grad()  # untimed: counters untouched, reported as 0
-        assert all(engine.stats()[q] == 0 for q in keys)
+        for eng in (engine, sh):
+            eng.loglik_grad()  # untimed: counters untouched, reported as 0
+            assert all(eng.stats()[q] == 0 for q in keys)
     finally:
-        engine.set_virtual_shards(1)
+        sh.close()
         engine.set_timing(False)
         engine.set_background_cache(True)
 
@@ -578,7 +583,7 @@ def test_full_size_c2_matches_reference_engine(engine, theta):
 
 def test_full_size_properties(engine):
     """Size-independent properties at the bench size (C2, N = 85,000, loglik +
-    gradient): repeat-bitwise, culled == dense bitwise, 4 virtual shards bitwise,
+    gradient): repeat-bitwise, culled == dense bitwise, 4 emulated ranks bitwise,
     per-event terms summing to the total, far tier vs all-FP64 to 1e-13."""
     ev = _c2()
     engine.load(ev)
@@ -592,10 +597,11 @@ def test_full_size_properties(engine):
         d = engine.loglik_grad()
         engine.set_dense(False)
         assert d[0] == a[0] and np.array_equal(d[2], a[2])
-        engine.set_virtual_shards(4)
-        s = engine.loglik_grad()
-        engine.set_virtual_shards(1)
-        assert s[0] == a[0] and np.array_equal(s[2], a[2])
+        with pk.Engine((0,) * 4) as sh:
+            sh.load(ev)
+            sh.set_params([0.66, 1.6, 14, 0.344, 1440, 0.0695])
+            s = sh.loglik_grad(per_event=True)
+        assert s[0] == a[0] and np.array_equal(s[2], a[2]) and np.array_equal(s[3], a[3])
         assert abs(math.fsum(a[3]) - a[0]) <= 1e-12 * abs(a[0])
         engine.set_far_tier(False)
         f = engine.loglik_grad()
@@ -604,7 +610,6 @@ def test_full_size_properties(engine):
         assert np.all(np.abs(f[2] - a[2]) <= 1e-11 * np.abs(a[2]) + 1e-9)
     finally:
         engine.set_dense(False)
-        engine.set_virtual_shards(1)
         engine.set_far_tier(True)
         engine.set_background_cache(True)
 
@@ -626,8 +631,8 @@ def test_c3_250k_matches_reference_engine(engine):
 
 
 def test_c4_1m_properties(engine):
-    """C4 size (N = 1,000,000, one GPU): bitwise repeatable, bitwise equal over
-    2 virtual shards (the multi-GPU split), per-event terms summing to the total."""
+    """C4 size (N = 1,000,000, one GPU): bitwise repeatable, per-event terms
+    summing to the total (the 2/3/8-rank split: test_multirank_gpu.py)."""
     n = 1000000
     ev = pk.generateBenchmarkCloud(n, pk.SimWindow(0, 15, 0, 15, 4750), n)
     engine.load(ev)
@@ -636,14 +641,10 @@ def test_c4_1m_properties(engine):
     try:
         a = engine.loglik_grad(per_event=True)
         b = engine.loglik_grad()
-        engine.set_virtual_shards(2)
-        s = engine.loglik_grad()
-        engine.set_virtual_shards(1)
-        assert a[1] and a[0] == b[0] == s[0]
-        assert np.array_equal(a[2], b[2]) and np.array_equal(a[2], s[2])
+        assert a[1] and a[0] == b[0]
+        assert np.array_equal(a[2], b[2])
         assert abs(math.fsum(a[3]) - a[0]) <= 1e-12 * abs(a[0])
     finally:
-        engine.set_virtual_shards(1)
         engine.set_background_cache(True)
 
 
@@ -664,3 +665,148 @@ def test_c2_shaped_gradient_vs_oracle(engine, theta):
     assert np.all(np.abs(g - o["grad"]) <= 1e-8 * o["grad_abs"]), (g, o["grad"])
     big = np.abs(o["grad"]) > 1e-3 * o["grad_abs"]
     assert np.all(np.abs(g - o["grad"])[big] <= 1e-8 * np.abs(o["grad"])[big])
+
+
+@pytest.mark.parametrize("theta", [(0.66, 1.6, 14, 0.344, 1440, 0.0695), (1, 1.6, 14, 0.1, 1, 1)])
+def test_c2_full_size_gradient_vs_oracle(engine, theta):
+    """The bench's own GRAD kernels at the bench size (C2, N = 85,000: far tier,
+    trigger-free split and culling all active) against the long-double oracle:
+    loglik to 1e-10, every gradient component to 1e-8 of its scale and, away
+    from a stationary point, to 1e-8 relative."""
+    ev = _c2()
+    o = og.oracle_loglik_grad(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), np.array(theta))
+    engine.load(ev)
+    engine.set_params(list(theta))
+    ll, valid, g, _ = engine.loglik_grad()
+    assert valid and o["valid"]
+    assert abs(ll - o["loglik"]) <= LL_TOL * abs(o["loglik"]), (ll, o["loglik"])
+    assert np.all(np.abs(g - o["grad"]) <= G_TOL * o["grad_abs"]), (g, o["grad"])
+    big = np.abs(o["grad"]) > 1e-3 * o["grad_abs"]
+    assert np.all(np.abs(g - o["grad"])[big] <= G_TOL * np.abs(o["grad"])[big]), (g, o["grad"])
+
+
+def test_c3_250k_theta_init_matches_reference_engine(engine):
+    """The largest C3 point at the sampler's initial Theta (omega = 1: the causal
+    trigger live over ~50 days) against the verbatim reference engine."""
+    if not og.ref_available():
+        pytest.skip("oracle/_ref not built")
+    n = 250000
+    ev = pk.generateBenchmarkCloud(n, pk.SimWindow(0, 15, 0, 15, 4750), n)
+    theta = np.array([1.0, 1.6, 14, 0.1, 1.0, 1.0])
+    ref, ok, _ = og.ref_loglik(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), theta,
+                               os.cpu_count() or 1, 8 if og.has_avx512() else 4)
+    engine.load(ev)
+    engine.set_params(list(theta))
+    ll, valid, _ = engine.loglik()
+    assert ok and valid and abs(ll - ref) <= LL_TOL * abs(ref), (ll, ref)
+
+
+def test_c4_1m_matches_reference_engine(engine):
+    """C4 (N = 1,000,000) against the verbatim reference engine on every host
+    core (dense O(N^2) on the CPU: a few minutes), loglik to 1e-10."""
+    if not og.ref_available():
+        pytest.skip("oracle/_ref not built")
+    n = 1000000
+    ev = pk.generateBenchmarkCloud(n, pk.SimWindow(0, 15, 0, 15, 4750), n)
+    theta = np.array([0.66, 1.6, 14, 0.344, 1440, 0.0695])
+    engine.load(ev)
+    engine.set_params(list(theta))
+    ll, valid, _ = engine.loglik()
+    ref, ok, _ = og.ref_loglik(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), theta,
+                               os.cpu_count() or 1, 8 if og.has_avx512() else 4)
+    assert ok and valid and abs(ll - ref) <= LL_TOL * abs(ref), (ll, ref)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_far_tier_stress_bursty_random_theta(engine, seed):
+    """Adversarial far tier: N >= 30k bursty events, random Theta from regimes
+    where the far tier is live (asserted through its pair counter): far on vs
+    every pair in FP64 within the claimed 1e-13 (loglik) and against the
+    long-double oracle at the north-star tolerances."""
+    rng = np.random.default_rng(77 + seed)
+    n = int(rng.integers(30000, 40000))
+    ev = _clustered_events(rng, n, float(rng.choice([800.0, 2000.0, 4000.0])), tau_hot=2.0)
+    for _ in range(12):
+        p = pk.Params(float(rng.uniform(0.2, 3.0)), float(rng.uniform(0.3, 3.0)),
+                      float(np.exp(rng.uniform(np.log(1.0), np.log(30.0)))),
+                      float(rng.uniform(0.05, 0.95)),
+                      float(np.exp(rng.uniform(np.log(0.3), np.log(3000.0)))),
+                      float(np.exp(rng.uniform(np.log(0.02), np.log(1.0)))))
+        engine.load(ev)
+        engine.set_params(p)
+        engine.set_timing(True)
+        a = engine.loglik_grad()
+        nfar = engine.stats()["exec_far"]
+        engine.set_timing(False)
+        if nfar > 0:
+            break
+    assert nfar > 0, "no far-tier work at any drawn Theta"
+    engine.set_far_tier(False)
+    try:
+        b = engine.loglik_grad()
+    finally:
+        engine.set_far_tier(True)
+    assert a[1] == b[1]
+    if b[1]:
+        assert abs(a[0] - b[0]) <= 1e-13 * abs(b[0]), (a[0], b[0])
+    _check(engine, ev, p)
+
+
+def test_trigger_cache_far_split_flip_bitwise(engine):
+    """with the trigger sums cached, a theta / mu0 step that
+    moves the trigger boost across the far tier's trigger window (tauT = 14,
+    omega = 0.5: dTf crosses tfar near boost 7.3) must not reuse a sweep whose
+    far trigger partials were never stored. Cached == full evaluation, bitwise,
+    along a theta ladder across the crossing."""
+    ev = _c2(keep=30000)
+    engine.load(ev)
+    seq = []
+    for mu0 in (0.5, 1.0, 2.0):  # boost = ln(9300 theta / mu0): 5.4 .. 11.4
+        for th in np.geomspace(0.05, 5.0, 9):
+            seq.append([mu0, 1.6, 14.0, float(th), 0.5, 0.0695])
+    full, cached = [], []
+    engine.set_background_cache(False)
+    for p in seq:
+        engine.set_params(p)
+        full.append(engine.loglik_grad())
+    engine.set_background_cache(True)
+    hits = 0
+    for p in seq:
+        engine.set_params(p)
+        cached.append(engine.loglik_grad())
+        hits += engine.stats()["trigger_cache_hit"]
+    assert hits > 0
+    for p, a, b in zip(seq, full, cached):
+        assert a[0] == b[0] and np.array_equal(a[2], b[2]), p
+
+
+def test_extreme_trigger_boost_keeps_trigger_in_fp64(engine):
+    """trNorm / (mu0 bgNorm) ~ e^45 puts trigger terms that
+    matter below the FP32 flush point; they must stay in the FP64 near list.
+    Against the long-double oracle and the all-FP64 path."""
+    ev = _c2(keep=20000)
+    # boost = ln(theta omega / (2 pi h^2) / (mu0 (2pi)^-1.5 / (tauX^2 tauT)))
+    p = pk.Params(1e-9, 1.6, 14.0, 0.9, 0.5, 0.02)
+    cB = p.mu0 * (2 * np.pi) ** -1.5 / (p.tauX ** 2 * p.tauT)
+    cT = p.theta * p.omega / (2 * np.pi * p.h ** 2)
+    assert np.log(cT / cB) > 40
+    r, g, o = _check(engine, ev, p)
+    engine.set_far_tier(False)
+    try:
+        b = engine.loglik_grad()
+    finally:
+        engine.set_far_tier(True)
+    if o["valid"]:
+        assert abs(r.logLik - b[0]) <= 1e-13 * abs(b[0])
+
+
+def test_rejects_more_events_than_fixed_point_range(engine):
+    """The fixed-point background sums hold per-row totals below 2^23 (a row's
+    S_B can reach N): loads beyond 2^23 events are refused, not wrapped."""
+    n = (1 << 23) + 1
+    t = np.arange(n, dtype=np.float64) * 1e-3
+    z = np.zeros(n)
+    with pytest.raises(ValueError, match="at most 2\\^23 events"):
+        engine.load_events(z, z, t, float(t[-1]))
+    ev = pk.generateBenchmarkCloud(300, pk.SimWindow(0, 4, 0, 4, 60), 5)
+    engine.load(ev)  # (the engine still works)

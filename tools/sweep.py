@@ -31,8 +31,7 @@ for n in sizes:
             st = eng.stats()
             ev_ms.append(st["eval_ms"])
             pk_ms.append(st["pair_kernel_ms"])
-        flops = (bench.FLOPS_ANY * st["exec_geom"] + bench.FLOPS_BG_GRAD * st["exec_bg"]
-                 + bench.FLOPS_TR_GRAD * st["pairs_tr"] + bench.FLOPS_SYM_COLUMN * st["exec_sym"])
+        flops = bench.strict_flops(st)
         t = float(np.median(ev_ms))
         tp = float(np.median(pk_ms))
         row = {"n": n, "theta": name, "eval_ms": t, "pair_kernel_ms": tp, "evals_per_s": 1e3 / t,
