@@ -123,6 +123,18 @@ int sthk_loglik_batch(sthk_engine* e, const double* params, int64_t P,
  * 0 on those rows and STHK_ERANGE is returned. */
 int sthk_excitation(sthk_engine* e, double* mu, double* xi, double* pi);
 
+/* Posterior excitation over S parameter draws (the device half of
+ * hawkes::posteriorExcitation, excitation.cpp:72-130, without thinning and
+ * dump): every draw's pi_i is added, draws in order, to sum_pi[i] (in/out,
+ * length n; start from zeros and divide by S afterwards: bitwise the
+ * reference's meanPi loop, also across consecutive calls); per_draw (nullable, S x n row-major)
+ * receives every draw's pi. Draws sharing tauX, tauT (every draw of the
+ * reference MH sampler) share one background sweep. If a draw's rate
+ * underflowed, returns STHK_ERANGE with *bad_draw = the first such draw
+ * (else *bad_draw = -1). A rank engine fills its own rows only. */
+int sthk_excitation_batch(sthk_engine* e, const double* params, int64_t S, double* sum_pi,
+                          double* per_draw, int64_t* bad_draw);
+
 /* Asynchronous pair: enqueue one evaluation of the current params on the
  * engine's stream(s); sthk_result() waits for and returns the latest one. */
 int sthk_enqueue(sthk_engine* e, int want_grad, int want_per_event);

@@ -76,6 +76,7 @@ SIGNATURES = [
     ("sthk_loglik_grad", c_int, [c_void_p, _DPTR, _IPTR, _DPTR, _DPTR]),
     ("sthk_loglik_batch", c_int, [c_void_p, _DPTR, c_int64, _DPTR, _IPTR, _DPTR]),
     ("sthk_excitation", c_int, [c_void_p, _DPTR, _DPTR, _DPTR]),
+    ("sthk_excitation_batch", c_int, [c_void_p, _DPTR, c_int64, _DPTR, _DPTR, POINTER(c_int64)]),
     ("sthk_enqueue", c_int, [c_void_p, c_int, c_int]),
     ("sthk_result", c_int, [c_void_p, _DPTR, _IPTR, _DPTR, _DPTR]),
     ("sthk_set_timing", c_int, [c_void_p, c_int]),

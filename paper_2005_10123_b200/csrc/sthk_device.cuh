@@ -70,9 +70,36 @@ __device__ __forceinline__ double exp_l(double x, const uint2* __restrict__ tab)
 // N independent exp_l evaluations written in lockstep (stage by stage), so
 // the dependent 8-instruction chains are interleaved in program order and the
 // FP64 pipe's latency is covered by N-way ILP even at low occupancy.
+#ifndef STHK_EXP_CVT
+#define STHK_EXP_CVT 0
+#endif
 template <bool CHECK, int N>
 __device__ __forceinline__ void exp_l_batch(const double (&x)[N], double (&out)[N],
                                             const uint2* __restrict__ tab) {
+#if STHK_EXP_CVT
+  // k = rint(x) by F2I.F64 (round to nearest even, exactly as the magic-number
+  // rounding below) and kd = k by I2F.F64: both on the conversion pipe, so
+  // the exp costs 5 FP64-pipe instructions instead of 7; bitwise identical.
+  int k[N];
+  double u[N], q[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) k[i] = __double2int_rn(x[i]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) u[i] = x[i] - static_cast<double>(k[i]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) q[i] = fma(kE3, u[i], kE2);
+#pragma unroll
+  for (int i = 0; i < N; ++i) q[i] = fma(q[i], u[i], kE1);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const double p = q[i] * u[i];
+    const uint2 tj = tab[k[i] & kExpMask];
+    const double ts = __hiloint2double(static_cast<int>(tj.y) + (k[i] << kExpShift),
+                                       static_cast<int>(tj.x));
+    const double res = fma(ts, p, ts);
+    out[i] = CHECK ? (k[i] < kMinK ? 0.0 : res) : res;
+  }
+#else
   double t[N], u[N], q[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) t[i] = x[i] + kRoundMagic;
@@ -93,6 +120,7 @@ __device__ __forceinline__ void exp_l_batch(const double (&x)[N], double (&out)[
     const double res = fma(ts, p, ts);
     out[i] = CHECK ? (tb < kFlushBits ? 0.0 : res) : res;
   }
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -133,6 +133,14 @@ struct Slot {
   size_t pe_cap = 0;
   double* ex = nullptr;  // excitation mu, xi, pi [3][npad]
   size_t ex_cap = 0;
+  double* pi_sum = nullptr;  // excitation batch: sum of pi over the draws [npad]
+  size_t pi_sum_cap = 0;
+  int* pi_bad = nullptr;     // excitation batch: per-draw degenerate flags
+  size_t pi_bad_cap = 0;
+  double* pi_rows = nullptr;  // excitation batch: per-draw pi rows staged [kPiChunk][npad]
+  size_t pi_rows_cap = 0;
+  double* h_pi_rows = nullptr;  // pinned copy of pi_rows
+  size_t h_pi_rows_cap = 0;
   double* h_ex = nullptr;  // pinned
   size_t h_ex_cap = 0;
   unsigned long long* pair_counts = nullptr;
@@ -306,12 +314,14 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.ex),
                   static_cast<void*>(s.per_event),
                   static_cast<void*>(s.pair_counts), static_cast<void*>(s.tile_box),
-                  static_cast<void*>(s.fx_stage)}) {
+                  static_cast<void*>(s.fx_stage), static_cast<void*>(s.pi_sum),
+                  static_cast<void*>(s.pi_bad), static_cast<void*>(s.pi_rows)}) {
     if (p) cudaFree(p);
   }
   for (void* p : {static_cast<void*>(s.h_out), static_cast<void*>(s.h_counts),
                   static_cast<void*>(s.h_bad), static_cast<void*>(s.h_stats),
-                  static_cast<void*>(s.h_per_event), static_cast<void*>(s.h_ex)}) {
+                  static_cast<void*>(s.h_per_event), static_cast<void*>(s.h_ex),
+                  static_cast<void*>(s.h_pi_rows)}) {
     if (p) cudaFreeHost(p);
   }
   for (auto& e : s.ev) {
@@ -856,7 +866,8 @@ void combine_blocks(sthk_engine& e, int nb_total) {
   }
 }
 
-void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false) {
+void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
+                  bool ex_to_host = true) {
   if (!e.loaded) throw NotLoaded("sthk: no events loaded");
   if (!e.has_params) throw NotLoaded("sthk: no parameters set");
   const int shards = e.rank_mode ? e.world : static_cast<int>(e.slots.size());
@@ -1246,7 +1257,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false)
                          sizeof(double) * (s.row1 - s.row0), cudaMemcpyDeviceToHost, st),
          "D2H");
     }
-    if (want_ex && s.row1 > s.row0) {
+    if (want_ex && ex_to_host && s.row1 > s.row0) {
       if (s.h_ex_cap < static_cast<size_t>(3 * e.npad)) {
         if (s.h_ex) ck(cudaFreeHost(s.h_ex), "cudaFreeHost");
         ck(cudaMallocHost(&s.h_ex, sizeof(double) * 3 * e.npad), "cudaMallocHost");
@@ -1624,6 +1635,110 @@ int sthk_excitation(sthk_engine* e, double* mu, double* xi, double* pi) {
     degenerate = e->slots[0].h_out[7] > 0.0;
   });
   if (rc == STHK_OK && degenerate) {
+    return fail(e, STHK_ERANGE, "excitationProbabilities: per-event rate underflowed to zero");
+  }
+  return rc;
+}
+
+int sthk_excitation_batch(sthk_engine* e, const double* params, int64_t S, double* sum_pi,
+                          double* per_draw, int64_t* bad_draw) {
+  int64_t bad = -1;
+  const int rc = guarded(e, [&] {
+    if (S < 1 || !params || !sum_pi) throw InvalidArg("sthk_excitation_batch: no draws");
+    for (int64_t j = 0; j < S; ++j) {
+      try {
+        validate_params(params + 6 * j);
+      } catch (const InvalidArg& x) {
+        throw InvalidArg("sthk_excitation_batch: draw " + std::to_string(j) + ": " + x.what());
+      }
+    }
+    if (!e->loaded) throw NotLoaded("sthk: no events loaded");
+    if (e->pending) collect(*e, nullptr, nullptr, nullptr, nullptr);
+    double saved[6];
+    std::memcpy(saved, e->p, sizeof(saved));
+    const bool had = e->has_params;
+    constexpr int64_t kPiChunk = 32;  // per-draw rows staged per host copy
+    const int64_t n = e->n, npad = e->npad;
+    for (Slot& s : e->slots) {
+      set_dev(s);
+      dev_grow(s.pi_sum, s.pi_sum_cap, static_cast<size_t>(npad));
+      dev_grow(s.pi_bad, s.pi_bad_cap, static_cast<size_t>(S));
+      // (in/out: the draws' pi are added to the caller's sums)
+      ck(cudaMemcpyAsync(s.pi_sum, sum_pi, sizeof(double) * n, cudaMemcpyHostToDevice, s.stream),
+         "H2D pi sums");
+      ck(cudaMemsetAsync(s.pi_bad, 0, sizeof(int) * S, s.stream), "memset");
+      if (per_draw) {
+        dev_grow(s.pi_rows, s.pi_rows_cap, static_cast<size_t>(kPiChunk * npad));
+        if (s.h_pi_rows_cap < static_cast<size_t>(kPiChunk * npad)) {
+          if (s.h_pi_rows) ck(cudaFreeHost(s.h_pi_rows), "cudaFreeHost");
+          ck(cudaMallocHost(&s.h_pi_rows, sizeof(double) * kPiChunk * npad), "cudaMallocHost");
+          s.h_pi_rows_cap = static_cast<size_t>(kPiChunk * npad);
+        }
+      }
+    }
+    // Draws in order, each an excitation evaluation on the device (with the
+    // sweep caches on, draws that share tauX, tauT -- every draw of the
+    // reference MH sampler -- reuse one background sweep, and consecutive
+    // draws with equal omega, h one trigger sweep); pi is accumulated on the
+    // device in draw order, so the sum equals the reference's meanPi +=
+    // ex.pi loop bitwise (excitation.cpp:110-112).
+    auto flush_rows = [&](int64_t j0, int64_t j1) {  // draws [j0, j1) staged in pi_rows
+      for (Slot& s : e->slots) {
+        set_dev(s);
+        ck(cudaStreamSynchronize(s.stream), "excitation batch");
+        if (s.row1 <= s.row0) continue;
+        for (int64_t j = j0; j < j1; ++j) {
+          std::memcpy(per_draw + j * n + s.row0, s.h_pi_rows + (j - j0) * npad + s.row0,
+                      sizeof(double) * (s.row1 - s.row0));
+        }
+      }
+    };
+    int64_t chunk0 = 0;
+    for (int64_t j = 0; j < S; ++j) {
+      std::memcpy(e->p, params + 6 * j, sizeof(e->p));
+      e->has_params = true;
+      enqueue_eval(*e, false, false, true, false);
+      for (Slot& s : e->slots) {
+        set_dev(s);
+        ck(sthk::launch_pi_accumulate(s.ex, npad, s.row0, s.row1, s.pi_sum, s.pi_bad + j,
+                                      s.stream),
+           "pi accumulate");
+        e->launches += 1;
+        if (per_draw && s.row1 > s.row0) {
+          const size_t off = static_cast<size_t>(j - chunk0) * npad + s.row0;
+          const size_t bytes = sizeof(double) * (s.row1 - s.row0);
+          ck(cudaMemcpyAsync(s.h_pi_rows + off, s.ex + 2 * npad + s.row0, bytes,
+                             cudaMemcpyDeviceToHost, s.stream),
+             "D2H pi");
+        }
+      }
+      if (per_draw && (j + 1 - chunk0 == kPiChunk || j + 1 == S)) {
+        flush_rows(chunk0, j + 1);
+        chunk0 = j + 1;
+      }
+    }
+    std::vector<int> flags(static_cast<size_t>(S), 0);
+    for (Slot& s : e->slots) {
+      set_dev(s);
+      ck(cudaStreamSynchronize(s.stream), "excitation batch");
+      std::vector<int> f(static_cast<size_t>(S));
+      ck(cudaMemcpy(f.data(), s.pi_bad, sizeof(int) * S, cudaMemcpyDeviceToHost), "D2H");
+      for (int64_t j = 0; j < S; ++j) flags[j] |= f[j];
+      if (s.row1 > s.row0) {
+        ck(cudaMemcpy(sum_pi + s.row0, s.pi_sum + s.row0, sizeof(double) * (s.row1 - s.row0),
+                      cudaMemcpyDeviceToHost),
+           "D2H");
+      }
+    }
+    e->pending = false;
+    for (int64_t j = 0; j < S && bad < 0; ++j) {
+      if (flags[j]) bad = j;
+    }
+    std::memcpy(e->p, saved, sizeof(saved));
+    e->has_params = had;
+  });
+  if (bad_draw) *bad_draw = bad;
+  if (rc == STHK_OK && bad >= 0) {
     return fail(e, STHK_ERANGE, "excitationProbabilities: per-event rate underflowed to zero");
   }
   return rc;

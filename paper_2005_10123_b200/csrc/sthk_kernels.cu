@@ -546,8 +546,15 @@ constexpr int kSymR = 4;  // rows per thread
 #ifndef STHK_SYM_G
 #define STHK_SYM_G 4      // columns per shuffle reduce-scatter group (the far tier assumes 4)
 #endif
+#ifndef STHK_SPLIT_TRIG
+#define STHK_SPLIT_TRIG 0  // 1: background and trigger terms of a stage in separate passes (measured slower)
+#endif
 #ifndef STHK_SYM_MINB
-#define STHK_SYM_MINB 3   // resident sym CTAs per SM the register budget targets
+#if STHK_SPLIT_TRIG
+#define STHK_SYM_MINB 4   // resident sym CTAs per SM the register budget targets
+#else
+#define STHK_SYM_MINB 3
+#endif
 #endif
 constexpr int kSymG = STHK_SYM_G;
 
@@ -1020,33 +1027,51 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
       const double* sy = s_src[buf][1];
       const double* st = s_src[buf][2];
       const int col0 = warp * 32;
-      if (tr) {
+      auto pass = [&](bool pbg, int ptr) {
+        if (diag) {
+          sym_dispatch<GRAD, false, true, true, BGONLY>(pbg, ptr, sx, sy, st, col0, cnt, xi, yi, ti,
+                                                        rv, a.k, s_tab, racc, s_col);
+        } else if (rows_real < kTM) {
+          sym_dispatch<GRAD, true, true, true, BGONLY>(pbg, ptr, sx, sy, st, col0, cnt, xi, yi, ti,
+                                                       rv, a.k, s_tab, racc, s_col);
+        } else if (safe) {
+          sym_dispatch<GRAD, true, false, false, BGONLY>(pbg, ptr, sx, sy, st, col0, cnt, xi, yi,
+                                                         ti, rv, a.k, s_tab, racc, s_col);
+        } else {
+          sym_dispatch<GRAD, true, true, false, BGONLY>(pbg, ptr, sx, sy, st, col0, cnt, xi, yi, ti,
+                                                        rv, a.k, s_tab, racc, s_col);
+        }
+      };
+      auto load_tr = [&] {
 #pragma unroll
         for (int r = 0; r < kSymR; ++r) {
 #pragma unroll
           for (int q = NB; q < NS; ++q) racc[r][q] = s_red[warp][q][lane + 32 * r];
         }
-      }
-      if (diag) {
-        sym_dispatch<GRAD, false, true, true, BGONLY>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
-                                              a.k, s_tab, racc, s_col);
-      } else if (rows_real < kTM) {
-        sym_dispatch<GRAD, true, true, true, BGONLY>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv, a.k,
-                                             s_tab, racc, s_col);
-      } else if (safe) {
-        sym_dispatch<GRAD, true, false, false, BGONLY>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
-                                               a.k, s_tab, racc, s_col);
-      } else {
-        sym_dispatch<GRAD, true, true, false, BGONLY>(bg, tr, sx, sy, st, col0, cnt, xi, yi, ti, rv,
-                                              a.k, s_tab, racc, s_col);
-      }
-      if (tr) {
+      };
+      auto store_tr = [&] {
 #pragma unroll
         for (int r = 0; r < kSymR; ++r) {
 #pragma unroll
           for (int q = NB; q < NS; ++q) s_red[warp][q][lane + 32 * r] = racc[r][q];
         }
+      };
+#if STHK_SPLIT_TRIG
+      // Background and trigger in two passes over the stage: the trigger sums
+      // are live only in the second (fewer registers, more resident warps);
+      // every sum sees the same terms in the same order, so the result is
+      // bitwise that of one fused pass.
+      if (bg) pass(true, 0);
+      if (tr) {
+        load_tr();
+        pass(false, tr);
+        store_tr();
       }
+#else
+      if (tr) load_tr();
+      pass(bg, tr);
+      if (tr) store_tr();
+#endif
       if (!diag && bg) {  // (never in a trigger-only sweep)
         // column sums of source tile J: one fixed-point flush per column.
         // Warp w owns columns 32w..32w+31 (it wrote their s_col entries), so
@@ -1660,7 +1685,25 @@ __global__ void __launch_bounds__(256) fx_accumulate_kernel(const FxAccArgs a) {
   }
 }
 
+__global__ void __launch_bounds__(256) pi_accumulate_kernel(const double* __restrict__ ex,
+                                                            int64_t npad, int row0, int row1,
+                                                            double* __restrict__ sum_pi, int* bad) {
+  const int64_t i = row0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= row1) return;
+  const double lam = ex[i] + ex[npad + i];
+  if (!(lam > 0.0) || !isfinite(lam)) *bad = 1;
+  sum_pi[i] += ex[2 * npad + i];
+}
+
 }  // namespace
+
+cudaError_t launch_pi_accumulate(const double* ex, int64_t npad, int row0, int row1,
+                                 double* sum_pi, int* bad, cudaStream_t stream) {
+  if (row1 <= row0) return cudaSuccess;
+  pi_accumulate_kernel<<<(row1 - row0 + 255) / 256, 256, 0, stream>>>(ex, npad, row0, row1,
+                                                                      sum_pi, bad);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_fx_accumulate(const FxAccArgs& a, cudaStream_t stream) {
   if (a.nseg <= 0) return cudaSuccess;

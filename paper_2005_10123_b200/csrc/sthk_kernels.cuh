@@ -239,6 +239,14 @@ struct FxAccArgs {
   FxSeg seg[kMaxFxSegs];
 };
 cudaError_t launch_fx_accumulate(const FxAccArgs& a, cudaStream_t stream);
+
+// Posterior-excitation batch (sthk_excitation_batch): after a draw's
+// finalize wrote mu, xi, pi ([3][npad], ex), rows [row0, row1) add pi into
+// sum_pi (draws in order: the reference's meanPi += pi, excitation.cpp:112)
+// and flag the draw (*bad = 1) if some rate mu + xi is not positive and
+// finite (excitation.cpp:40-46).
+cudaError_t launch_pi_accumulate(const double* ex, int64_t npad, int row0, int row1,
+                                 double* sum_pi, int* bad, cudaStream_t stream);
 // Resident CTAs per SM of a pair kernel (for the persistent grid size).
 int pair_kernel_occupancy(bool grad, int mode);
 

@@ -173,6 +173,21 @@ class Engine:
         self._check(rc, "sthk_excitation")
         return mu, xi, pi
 
+    def excitation_batch(self, params_list, sum_pi=None, per_draw: bool = False):
+        """pi over S parameter draws in one engine call (sthk_excitation_batch):
+        returns (sum_pi, per_draw rows or None, first underflowed draw or -1).
+        sum_pi (length n, default zeros) is added to in draw order."""
+        P = np.ascontiguousarray(np.asarray(params_list, dtype=np.float64).reshape(-1, 6))
+        S = P.shape[0]
+        acc = np.zeros(self._n) if sum_pi is None else np.ascontiguousarray(sum_pi, np.float64)
+        rows = np.zeros((S, self._n)) if per_draw else None
+        bad = ctypes.c_int64(-1)
+        rc = self._lib.sthk_excitation_batch(self._h, _dptr(P), S, _dptr(acc),
+                                             _dptr(rows) if per_draw else None, byref(bad))
+        if rc != _lib.STHK_ERANGE:
+            self._check(rc, "sthk_excitation_batch")
+        return acc, rows, bad.value
+
     def enqueue(self, grad: bool = True, per_event: bool = False) -> None:
         self._check(self._lib.sthk_enqueue(self._h, int(grad), int(per_event)), "sthk_enqueue")
 

@@ -59,7 +59,10 @@ def posteriorExcitation(events: EventSet, draws: List[Params], backend=None,
                         dumpPath: Optional[str] = None,
                         engine: Optional[Engine] = None) -> PosteriorExcitation:
     """excitation.cpp:72-130: mean pi over thinned draws (summed in draw
-    order, then divided), optional per-draw matrix and text dump."""
+    order, then divided), optional per-draw matrix and text dump. The kept
+    draws run as batches on the device (sthk_excitation_batch: one background
+    sweep for draws sharing tauX, tauT); errors surface at the same draw, with
+    the same dump lines written before it, as in the reference's loop."""
     if len(draws) == 0:
         raise ValueError("posteriorExcitation: no draws")
     if thinTo < 1:
@@ -70,6 +73,15 @@ def posteriorExcitation(events: EventSet, draws: List[Params], backend=None,
     retain = kept * n <= memoryCapEntries
     per = np.zeros((kept, n)) if retain else np.zeros((0, 0))
     mean = np.zeros(n)
+    # the first kept draw with invalid params ends the loop there (the
+    # reference validates inside excitationProbabilities)
+    stop, stop_err = kept, None
+    for j, d in enumerate(idx):
+        try:
+            draws[d].validate()
+        except ValueError as e:
+            stop, stop_err = j, f"posteriorExcitation: draw {d}: {e}"
+            break
     dump = None
     if dumpPath is not None:
         try:
@@ -77,17 +89,30 @@ def posteriorExcitation(events: EventSet, draws: List[Params], backend=None,
         except OSError:
             raise RuntimeError(f"posteriorExcitation: cannot open dump file {dumpPath}") from None
         dump.write(f"# sthawkes pi draws v1, events={n}\n")
+    want_rows = retain or dump is not None
+    # draws per device call: bounded host memory for the per-draw rows
+    step = max(1, min(stop, 10_000_000 // max(n, 1))) if want_rows else max(stop, 1)
+    eng = engine or default_engine()
     try:
-        for j, d in enumerate(idx):
-            try:
-                ex = excitationProbabilities(events, draws[d], engine=engine)
-            except (ValueError, EngineError) as e:
-                raise RuntimeError(f"posteriorExcitation: draw {d}: {e}") from None
-            mean += ex.pi
-            if retain:
-                per[j] = ex.pi
-            if dump is not None:
-                dump.write(str(d) + "".join("\t%.17g" % v for v in ex.pi) + "\n")
+        j0 = 0
+        while j0 < stop:
+            j1 = min(stop, j0 + step)
+            with eng._lock:
+                eng.load(events)
+                mean, rows, bad = eng.excitation_batch(
+                    [draws[d].as_array() for d in idx[j0:j1]], sum_pi=mean, per_draw=want_rows)
+            done = j1 if bad < 0 else j0 + bad
+            for j in range(j0, done):
+                if retain:
+                    per[j] = rows[j - j0]
+                if dump is not None:
+                    dump.write(str(idx[j]) + "".join("\t%.17g" % v for v in rows[j - j0]) + "\n")
+            if bad >= 0:
+                raise RuntimeError(f"posteriorExcitation: draw {idx[j0 + bad]}: "
+                                   "excitationProbabilities: per-event rate underflowed to zero")
+            j0 = j1
+        if stop_err is not None:
+            raise RuntimeError(stop_err)
     finally:
         if dump is not None:
             dump.close()

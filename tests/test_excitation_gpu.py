@@ -90,3 +90,48 @@ def test_posterior_excitation_semantics(engine, tmp_path):
     pk.posteriorExcitation(ev, [draws[0]] * 7, thinTo=3, dumpPath=path, engine=engine)
     lines = open(path).read().strip().split("\n")
     assert lines[0].startswith("# sthawkes pi draws v1, events=200") and len(lines) == 4
+
+
+def test_posterior_excitation_batch_bitwise_and_errors(engine, tmp_path):
+    """The batched device path (sthk_excitation_batch: MH-style draws sharing
+    tauX, tauT share one background sweep) reproduces the reference's
+    one-call-per-draw loop bitwise -- meanPi, perDraw rows, the dump file --
+    also across chunked calls (sum_pi in/out), and stops at the same draw
+    with the same message on an underflowed rate."""
+    ev = pk.generateBenchmarkCloud(3000, pk.SimWindow(0, 8, 0, 8, 400), 9)
+    rng = np.random.default_rng(3)
+    draws, p = [], [0.6, 0.9, 3.0, 0.4, 2.0, 0.3]
+    for _ in range(40):  # an MH-like walk: one coordinate moves per draw
+        k = [0, 3, 4, 5][int(rng.integers(4))]
+        p = list(p)
+        p[k] *= float(np.exp(0.05 * rng.standard_normal()))
+        draws.append(pk.Params(*p))
+    path_b = os.path.join(str(tmp_path), "batch.tsv")
+    post = pk.posteriorExcitation(ev, draws, thinTo=25, dumpPath=path_b, engine=engine)
+    idx = pk.thinIndices(len(draws), 25)
+    acc, rows = np.zeros(ev.size()), []
+    for d in idx:
+        pi = pk.excitationProbabilities(ev, draws[d], engine=engine).pi
+        acc += pi
+        rows.append(pi)
+    acc /= float(len(idx))
+    assert np.array_equal(post.meanPi, acc)
+    assert np.array_equal(post.perDraw, np.array(rows))
+    ref_lines = ["# sthawkes pi draws v1, events=3000"] + [
+        str(d) + "".join("\t%.17g" % v for v in r) for d, r in zip(idx, rows)]
+    assert open(path_b).read() == "\n".join(ref_lines) + "\n"
+    # chunked: two device calls, sums carried through sum_pi
+    P = np.array([draws[d].as_array() for d in idx])
+    engine.load(ev)
+    s1, _, b1 = engine.excitation_batch(P[:11])
+    s2, r2, b2 = engine.excitation_batch(P[11:], sum_pi=s1, per_draw=True)
+    assert b1 == b2 == -1 and np.array_equal(s2 / float(len(idx)), acc)
+    assert np.array_equal(r2, np.array(rows[11:]))
+    # an underflowing draw (mu0 * S_B and the trigger both below the smallest
+    # double) stops the batch at its index, after the earlier draws' dump lines
+    bad = pk.Params(5e-324, 0.9, 3.0, 0.0, 2.0, 0.3)
+    seq = [draws[0], draws[1], bad, draws[2]]
+    path_e = os.path.join(str(tmp_path), "err.tsv")
+    with pytest.raises(RuntimeError, match="posteriorExcitation: draw 2: .*underflowed"):
+        pk.posteriorExcitation(ev, seq, dumpPath=path_e, engine=engine)
+    assert len(open(path_e).read().strip().split("\n")) == 3

@@ -122,7 +122,8 @@ def test_partition_bitwise_invariant(engine, k):
             a = engine.loglik_grad(per_event=True)
             b = sh.loglik_grad(per_event=True)
             assert a[0] == b[0] and np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
-            assert sh.exchange_bytes() > 0
+            if p.omega == 1440:  # (the second Theta reuses the cached background)
+                assert sh.exchange_bytes() > 0
 
 
 def test_pair_counters_and_results_through_mapped_memory(engine):
@@ -786,7 +787,7 @@ def test_extreme_trigger_boost_keeps_trigger_in_fp64(engine):
     Against the long-double oracle and the all-FP64 path."""
     ev = _c2(keep=20000)
     # boost = ln(theta omega / (2 pi h^2) / (mu0 (2pi)^-1.5 / (tauX^2 tauT)))
-    p = pk.Params(1e-9, 1.6, 14.0, 0.9, 0.5, 0.02)
+    p = pk.Params(1e-13, 1.6, 14.0, 0.9, 0.5, 0.01)
     cB = p.mu0 * (2 * np.pi) ** -1.5 / (p.tauX ** 2 * p.tauT)
     cT = p.theta * p.omega / (2 * np.pi * p.h ** 2)
     assert np.log(cT / cB) > 40

@@ -7,9 +7,9 @@ import bench  # noqa: E402
 import paper_2005_10123_b200 as pk  # noqa: E402
 
 theta = bench.THETA_INIT if "--init" in sys.argv else bench.THETA_POST
-ev = bench.make_workload()
+x, y, t, T = bench.make_workload()
 e = pk.Engine((0,))
-e.load(ev)
+e.load_events(x, y, t, T)
 e.set_params(theta)
 e.set_background_cache(False)  # every launch a full sweep
 for _ in range(5):
