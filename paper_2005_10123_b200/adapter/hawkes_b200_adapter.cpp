@@ -10,8 +10,10 @@
 //     when requested, 0 on degenerate rows.
 //   * logLikelihoodBatch rethrows "logLikelihoodBatch: entry i: ...".
 // Engine errors other than invalid arguments become std::runtime_error.
-// Linked in place of likelihood.cpp and excitation.cpp
-// (excitation semantics: proj/src/excitation.cpp:13-130).
+// Linked in place of likelihood.cpp; excitationProbabilities and
+// posteriorExcitation here take precedence over the reference's (whose
+// excitation.o is linked with those two symbols weakened, for thinIndices).
+// Excitation semantics: proj/src/excitation.cpp:13-130.
 //
 // State: one process-wide engine on the devices in $STHK_DEVICES (default
 // "0"), created on first use. The device copy of the events is reused only
@@ -366,16 +368,14 @@ ExcitationVector excitationProbabilities(const EventSet& events, const Params& p
   return out;
 }
 
-std::vector<Index> thinIndices(Index total, Index keep) {
-  if (total < 1 || keep < 1) {
-    throw std::invalid_argument("thinIndices: need total >= 1 and keep >= 1");
-  }
-  const Index k = keep < total ? keep : total;
-  std::vector<Index> idx(static_cast<size_t>(k));
-  for (Index j = 0; j < k; ++j) idx[static_cast<size_t>(j)] = j * total / k;
-  return idx;
-}
-
+// posteriorExcitation (excitation.hpp:43-47) on the batched device path. The
+// thinning is the reference's own thinIndices (excitation.cpp, linked from
+// the verbatim build with this file's two functions taking precedence); the
+// kept draws go to the engine in batches (sthk_excitation_batch: one
+// background sweep for draws sharing tauX, tauT, pi summed on the device in
+// draw order). Errors surface at the same draw, after the same dump lines,
+// with the same messages as the reference's draw-by-draw loop
+// (excitation.cpp:72-130).
 PosteriorExcitation posteriorExcitation(const EventSet& events, const std::vector<Params>& draws,
                                         const Backend& backend,
                                         const PosteriorExcitationOptions& options) {
@@ -387,40 +387,81 @@ PosteriorExcitation posteriorExcitation(const EventSet& events, const std::vecto
   PosteriorExcitation out;
   out.drawIndices = thinIndices(static_cast<Index>(draws.size()), options.thinTo);
   const Index kept = static_cast<Index>(out.drawIndices.size());
-  const bool keepRows = kept * n <= options.memoryCapEntries;
-  if (keepRows) out.perDraw.setZero(kept, n);
+  const bool retain = kept * n <= options.memoryCapEntries;
+  if (retain) out.perDraw.setZero(kept, n);
   out.meanPi.setZero(n);
 
   std::ofstream dump;
   if (options.dumpPath) {
     dump.open(*options.dumpPath);
     if (!dump) {
-      throw std::runtime_error("posteriorExcitation: cannot open dump file " +
-                               *options.dumpPath);
+      throw std::runtime_error("posteriorExcitation: cannot open dump file " + *options.dumpPath);
     }
     dump << "# sthawkes pi draws v1, events=" << n << "\n";
   }
-  char num[40];
-  for (Index j = 0; j < kept; ++j) {
+  // the loop ends at the first kept draw the reference's
+  // excitationProbabilities would reject (params, backend)
+  Index stop = kept;
+  std::string stop_msg;
+  for (Index j = 0; j < kept && stop == kept; ++j) {
     const Index d = out.drawIndices[static_cast<size_t>(j)];
-    ExcitationVector ex;
     try {
-      ex = excitationProbabilities(events, draws[static_cast<size_t>(d)], backend);
+      draws[static_cast<size_t>(d)].validate();
+      backend.validate();
     } catch (const std::exception& err) {
-      throw std::runtime_error("posteriorExcitation: draw " + std::to_string(d) + ": " +
-                               err.what());
-    }
-    out.meanPi += ex.pi;  // draw order, then one division (bitwise as the reference)
-    if (keepRows) out.perDraw.row(j) = ex.pi.transpose();
-    if (dump.is_open()) {
-      dump << d;
-      for (Index i = 0; i < n; ++i) {
-        std::snprintf(num, sizeof num, "%.17g", ex.pi[i]);
-        dump << '\t' << num;
-      }
-      dump << '\n';
+      stop = j;
+      stop_msg = "posteriorExcitation: draw " + std::to_string(d) + ": " + err.what();
     }
   }
+  const bool rows_needed = retain || dump.is_open();
+  const Index step =
+      rows_needed ? std::max<Index>(1, std::min<Index>(std::max<Index>(stop, 1), 10000000 / n))
+                  : std::max<Index>(stop, 1);
+  std::vector<double> rows(rows_needed ? static_cast<size_t>(step * n) : 0);
+  std::vector<double> pv;
+  std::string line;
+  char num[40];
+  AdapterEngine& e = engine();
+  for (Index j0 = 0; j0 < stop; j0 += step) {
+    const Index j1 = std::min(stop, j0 + step);
+    pv.assign(static_cast<size_t>(6 * (j1 - j0)), 0.0);
+    for (Index j = j0; j < j1; ++j) {
+      const Params& p = draws[static_cast<size_t>(out.drawIndices[static_cast<size_t>(j)])];
+      const double v[6] = {p.mu0, p.tauX, p.tauT, p.theta, p.omega, p.h};
+      std::copy(v, v + 6, pv.begin() + 6 * (j - j0));
+    }
+    int64_t bad = -1;
+    {
+      std::lock_guard<std::mutex> lock(e.mu);
+      e.ensureLoadedExact(events);
+      const int rc = sthk_excitation_batch(e.h, pv.data(), j1 - j0, out.meanPi.data(),
+                                           rows_needed ? rows.data() : nullptr, &bad);
+      if (rc != STHK_ERANGE) e.check(rc);
+    }
+    const Index done = bad < 0 ? j1 : j0 + static_cast<Index>(bad);
+    for (Index j = j0; j < done; ++j) {
+      const double* pi = rows.data() + (j - j0) * n;
+      if (retain) {
+        for (Index i = 0; i < n; ++i) out.perDraw(j, i) = pi[i];
+      }
+      if (dump.is_open()) {
+        line = std::to_string(out.drawIndices[static_cast<size_t>(j)]);
+        for (Index i = 0; i < n; ++i) {
+          std::snprintf(num, sizeof num, "\t%.17g", pi[i]);
+          line += num;
+        }
+        line += '\n';
+        dump << line;
+      }
+    }
+    if (bad >= 0) {
+      throw std::runtime_error(
+          "posteriorExcitation: draw " +
+          std::to_string(out.drawIndices[static_cast<size_t>(j0 + bad)]) +
+          ": excitationProbabilities: per-event rate underflowed to zero");
+    }
+  }
+  if (!stop_msg.empty()) throw std::runtime_error(stop_msg);
   out.meanPi /= static_cast<double>(kept);
   if (dump.is_open() && !dump) {
     throw std::runtime_error("posteriorExcitation: failed writing dump file");

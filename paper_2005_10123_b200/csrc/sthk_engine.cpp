@@ -16,6 +16,7 @@
 //                            per device, partials combined in block order)
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -486,10 +487,20 @@ struct PlanInput {
   double ext_x = 0, ext_y = 0, tile_tspan = 0;
 };
 
+// (development knob: STHK_MIN_CHUNK_STAGES overrides the minimum item length)
+int min_chunk_stages() {
+  static const int v = [] {
+    const char* s = std::getenv("STHK_MIN_CHUNK_STAGES");
+    const int k = s ? std::atoi(s) : 0;
+    return k >= 1 && k <= 64 ? k : 4;
+  }();
+  return v;
+}
+
 int chunk_size(int64_t n, int64_t npad) {
   int64_t sc = (n + kChunksTarget - 1) / kChunksTarget;
   sc = (sc + kTS - 1) / kTS * kTS;
-  sc = std::max<int64_t>(sc, 4 * kTS);
+  sc = std::max<int64_t>(sc, static_cast<int64_t>(min_chunk_stages()) * kTS);
   sc = std::min<int64_t>(sc, npad);
   return static_cast<int>(sc);
 }
@@ -1217,6 +1228,18 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
       fa.bgNorm = std::pow(2.0 * kPi, -1.5) / (p[1] * p[1] * p[2]);
       fa.trNorm = p[3] * p[4] / (2.0 * kPi * p[5] * p[5]);
       fa.cT = p[4] / (2.0 * kPi * p[5] * p[5]);
+      {  // gradient constants (FinArgs::gB, gT), folded in long double
+        const long double mb = static_cast<long double>(p[0]) * fa.bgNorm;
+        const long double tx = p[1], tt = p[2], om = p[4], h = p[5], tn = fa.trNorm;
+        fa.gB[0] = static_cast<double>(-2.0L * mb / tx);
+        fa.gB[1] = static_cast<double>(mb / (tx * tx * tx) / fxq[1]);
+        fa.gB[2] = static_cast<double>(-mb / tt);
+        fa.gB[3] = static_cast<double>(mb / (tt * tt * tt) / fxq[2]);
+        fa.gT[0] = static_cast<double>(tn / om);
+        fa.gT[1] = static_cast<double>(-tn);
+        fa.gT[2] = static_cast<double>(-2.0L * tn / h);
+        fa.gT[3] = static_cast<double>(tn / (h * h * h) * (sym ? 1.0L / (static_cast<long double>(pl.sx) * pl.sx) : 1.0L));
+      }
       fa.fx = s.fx;
       fa.tpart = s.tpart;
       fa.tr_r2_scale = sym ? 1.0 / (pl.sx * pl.sx) : 1.0;

@@ -1545,6 +1545,8 @@ __device__ __forceinline__ void final_sum_block(const double* __restrict__ bp, i
 template <bool GRAD>
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) {
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
+  constexpr int NB = GRAD ? 3 : 1;
+  constexpr int NT = NS - NB;
   __shared__ double s_red[kNOut][kFinThreads];
   const int tid = threadIdx.x;
   const int64_t base = static_cast<int64_t>(a.row0) + static_cast<int64_t>(blockIdx.x) * kFB;
@@ -1555,40 +1557,54 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
   do {  // one row per thread; `continue` / `break` skip to the reduction
     const int64_t r = base + tid;
     if (r >= a.row1) break;
-    constexpr int NB = GRAD ? 3 : 1;
-    double s[NS];
-#pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      s[k] = fx_value(a.fx[static_cast<size_t>(2 * k) * a.npad + r],
-                      a.fx[static_cast<size_t>(2 * k + 1) * a.npad + r]) /
-             a.fxq[k];
-    }
+    // every independent load first (the row is latency-bound at small N)
     const int2 cr = a.crange[r / kTM];
+    const int2 cf = a.tpart_far ? a.crange_far[r / kTM] : make_int2(0, -1);
+    unsigned long long fw[2 * NB];
 #pragma unroll
-    for (int k = NB; k < NS; ++k) s[k] = 0.0;
-    for (int c = cr.x; c <= cr.y; ++c) {
-      const double* p = a.tpart + static_cast<size_t>(c) * (NS - NB) * a.npad + r;
-#pragma unroll
-      for (int k = NB; k < NS; ++k) s[k] += p[static_cast<size_t>(k - NB) * a.npad];
+    for (int k = 0; k < 2 * NB; ++k) fw[k] = a.fx[static_cast<size_t>(k) * a.npad + r];
+    const double dPhi = a.comp[r];
+    const double em1 = a.comp[2 * a.npad + r];
+    double dL2c = 0.0, dec = 0.0;
+    if constexpr (GRAD) {
+      dL2c = a.comp[a.npad + r];
+      dec = a.comp[3 * a.npad + r];
     }
-    if (a.tpart_far) {  // then the far kernel's partials, in chunk order
-      const int2 cf = a.crange_far[r / kTM];
-      for (int c = cf.x; c <= cf.y; ++c) {
-        const double* p = a.tpart_far + static_cast<size_t>(c) * (NS - NB) * a.npad + r;
+    // trigger partials: chunks in order (then the far kernel's), four
+    // chunks' loads in flight at a time; the additions keep chunk order
+    double st[NT];
 #pragma unroll
-        for (int k = NB; k < NS; ++k) s[k] += p[static_cast<size_t>(k - NB) * a.npad];
+    for (int k = 0; k < NT; ++k) st[k] = 0.0;
+    auto sum_chunks = [&](const double* tp, int2 c) {
+      for (int c0 = c.x; c0 <= c.y; c0 += 4) {
+        double v[4][NT];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double* q = tp + static_cast<size_t>(c0 + u) * NT * a.npad + r;
+#pragma unroll
+          for (int k = 0; k < NT; ++k) v[u][k] = c0 + u <= c.y ? q[static_cast<size_t>(k) * a.npad] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (c0 + u <= c.y) {
+#pragma unroll
+            for (int k = 0; k < NT; ++k) st[k] += v[u][k];
+          }
+        }
       }
-    }
-    if constexpr (GRAD) s[5] *= a.tr_r2_scale;  // kSym: sum of e * (-cxL) r^2
-    const double sB = s[0];
-    const double sT = GRAD ? s[3] : s[1];
+    };
+    sum_chunks(a.tpart, cr);
+    if (a.tpart_far) sum_chunks(a.tpart_far, cf);  // (after the near ones: fixed order)
+    double xb[NB];  // background sums, fixed-point word values (S_B; S_Br, S_Bt scaled)
+#pragma unroll
+    for (int k = 0; k < NB; ++k) xb[k] = fx_value(fw[2 * k], fw[2 * k + 1]);
+    const double sB = xb[0];  // (fxq[0] = 1)
+    const double sT = st[0];
     const double B = a.bgNorm * sB;
     const double Tr = a.trNorm * sT;
     const double lam = a.mu0 * B + Tr;  // likelihood.cpp:35
 
     // compensatorTerm, kernels.hpp:54-65, from the prepared terms (prep_kernel)
-    const double dPhi = a.comp[r];
-    const double em1 = a.comp[2 * a.npad + r];
     const double Lam = a.mu0 * dPhi + (-a.theta * em1);
 
     if (a.ex_out) {  // excitation split, excitation.cpp:31-51
@@ -1606,24 +1622,19 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
     if (a.per_event) a.per_event[r] = term;
     if constexpr (GRAD) {
       const double inv = 1.0 / lam;
-      const double tx3 = a.tauX * a.tauX * a.tauX;
-      const double tt3 = a.tauT * a.tauT * a.tauT;
-      const double h3 = a.h * a.h * a.h;
-      const double mb = a.mu0 * a.bgNorm;
-      // d lambda / d p
-      const double dl1 = mb * (-2.0 * sB / a.tauX + s[1] / tx3);
-      const double dl2 = mb * (-sB / a.tauT + s[2] / tt3);
+      // d lambda / d p with host-folded constants
+      const double dl1 = fma(a.gB[0], sB, a.gB[1] * xb[1]);
+      const double dl2 = fma(a.gB[2], sB, a.gB[3] * xb[2]);
       const double dl3 = a.cT * sT;
-      const double dl4 = a.trNorm * (sT / a.omega - s[4]);
-      const double dl5 = a.trNorm * (-2.0 * sT / a.h + s[5] / h3);
+      const double dl4 = fma(a.gT[0], sT, a.gT[1] * st[1]);
+      const double dl5 = fma(a.gT[2], sT, a.gT[3] * st[2]);
       // d Lambda / d p (prepared: dPhi, em1, (phi1 D + phi0 t) / tauT^2, D e^(-omega D))
-      const double dL2 = -a.mu0 * a.comp[a.npad + r];
-      acc[1] += B * inv - dPhi;
-      acc[2] += dl1 * inv;
-      acc[3] += dl2 * inv - dL2;
-      acc[4] += dl3 * inv + em1;
-      acc[5] += dl4 * inv - a.theta * a.comp[3 * a.npad + r];
-      acc[6] += dl5 * inv;
+      acc[1] = fma(B, inv, acc[1]) - dPhi;
+      acc[2] = fma(dl1, inv, acc[2]);
+      acc[3] = fma(dl2, inv, acc[3]) + a.mu0 * dL2c;
+      acc[4] = fma(dl3, inv, acc[4]) + em1;
+      acc[5] = fma(dl4, inv, acc[5]) - a.theta * dec;
+      acc[6] = fma(dl5, inv, acc[6]);
     }
   } while (false);
 

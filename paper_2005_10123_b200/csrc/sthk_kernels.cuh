@@ -141,6 +141,13 @@ struct FinArgs {
   double bgNorm;        // (2pi)^-1.5 / (tauX^2 tauT)       kernels.hpp:79
   double trNorm;        // theta omega / (2 pi h^2)          kernels.hpp:82
   double cT;            // omega / (2 pi h^2)  (d lambda / d theta)
+  // gradient constants folded on the host (no divisions per row), applied to
+  // the raw fixed-point / trigger sums: with mb = mu0 bgNorm,
+  //   d lambda / d tauX  = gB[0] S_B + gB[1] X_Br   (X_Br = fixed-point S_Br word value)
+  //   d lambda / d tauT  = gB[2] S_B + gB[3] X_Bt
+  //   d lambda / d omega = gT[0] S_T + gT[1] S_Tt
+  //   d lambda / d h     = gT[2] S_T + gT[3] S_Tr'
+  double gB[4], gT[4];
   const unsigned long long* fx;
   double fxq[kNSumGrad];
   const double* tpart;

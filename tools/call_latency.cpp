@@ -1,13 +1,15 @@
-// Per-call wall latency of the C ABI for MH-style moves at C2 (N=85k):
+// Per-call wall latency of the C ABI for MH-style moves on C2 data (first N
+// events, argv[1], default 85k):
 // mu0 move (trigger cache hit: finalize only), h move (plan cached, trigger
 // sweep), omega move (plan + trigger sweep), full eval (caches off).
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include <cuda_runtime.h>
 #include "../include/sthk.h"
 #include "../include/sthk_sim.h"
-int main() {
+int main(int argc, char** argv) {
   const int64_t cap = 90000;
   std::vector<double> x(cap), y(cap), t(cap);
   std::vector<int> par(cap);
@@ -15,7 +17,8 @@ int main() {
   const double truth[6] = {1, 1.6, 14, 0.344, 1440, 0.0695};
   const double win[5] = {0, 15, 0, 15, 4750};
   sthk_sim_cluster(truth, win, 0.053217, 2005, cap, x.data(), y.data(), t.data(), par.data(), &cnt);
-  const int64_t n = 85000;
+  const int64_t n = argc > 1 ? std::atoll(argv[1]) : 85000;
+  printf("N = %lld\n", static_cast<long long>(n));
   sthk_engine* e = nullptr;
   int dev = 0;
   sthk_create(&dev, 1, &e);
@@ -72,7 +75,7 @@ int main() {
       printf("raw 3 x H2D pinned + sync     %8.1f us/call\n", std::chrono::duration<double, std::micro>(a1 - a0).count() / reps);
       cudaFree(d);
     }
-    printf("load_events (pinned, N=85k)  %8.1f us/call\n", std::chrono::duration<double, std::micro>(t1 - t0).count() / reps);
+    printf("load_events (pinned)         %8.1f us/call\n", std::chrono::duration<double, std::micro>(t1 - t0).count() / reps);
     printf("loglik_grad (caches off)     %8.1f us/call\n", std::chrono::duration<double, std::micro>(t2 - t1).count() / reps);
   }
   sthk_destroy(e);
