@@ -376,15 +376,20 @@ def main():
             "pairs": {"ordered_bg": st2["pairs_bg"], "trigger": st2["pairs_tr"],
                       "bg_exps_executed": st2["exec_bg"]},
             "loglik": sec_run["loglik"]}
-        # the precision policy's cost: every pair in FP64 (far tier off)
-        eng.set_far_tier(False)
-        fp64 = timed_device(THETA_POST, k2, 3)
-        eng.set_far_tier(True)
-        secondary["all_fp64"] = {
-            "what": "C2 at Theta_post with the FP32 far tier off (every evaluated pair in FP64)",
-            "evals_per_s": 1e3 * k2 / fp64["total_ms"], "pair_kernel_ms": fp64["pair_ms"],
-            "loglik": fp64["loglik"], "grad": fp64["grad"],
-            "loglik_rel_diff_vs_far_tier": abs(fp64["loglik"] - main_run["loglik"]) / abs(fp64["loglik"])}
+        # the precision policy's cost: the far list in FP64 (same culling
+        # windows), and no far tier at all (exact-underflow windows, FP64)
+        for name, mode, what in (
+                ("all_fp64", 2, "C2 at Theta_post, every evaluated pair in FP64: the FP32 far "
+                                "tier's list run by the FP64 kernel with the same windows"),
+                ("no_far_tier", 0, "C2 at Theta_post without the far tier: every pair inside the "
+                                   "exact-underflow windows (|dt| <= 540 d) in FP64")):
+            eng.set_far_tier(mode)
+            fp64 = timed_device(THETA_POST, k2, 3)
+            secondary[name] = {
+                "what": what, "evals_per_s": 1e3 * k2 / fp64["total_ms"],
+                "pair_kernel_ms": fp64["pair_ms"], "loglik": fp64["loglik"], "grad": fp64["grad"],
+                "loglik_rel_diff_vs_headline": abs(fp64["loglik"] - main_run["loglik"]) / abs(fp64["loglik"])}
+        eng.set_far_tier(1)
 
         # MH-chain-style steps (wall clock): tauX/tauT fixed, one of (mu0,
         # theta, omega, h) moves per step, sweep caches on
@@ -409,6 +414,57 @@ def main():
             "evals_per_s": args.steps / mh_s, "unit": "evals/s", "cache_hits": hits,
             "what": "wall-clock loglik calls, one of mu0/theta/omega/h perturbed per step (tauX, "
                     "tauT fixed as in the reference sampler): cached background, trigger band swept"}
+
+        # f3: logLikelihoodBatch (likelihood.cpp:57-75), 16 entries per call --
+        # distinct (tauX, tauT) (no sweep shared) vs mu0 / theta variants of
+        # one Theta (one sweep, then finalize passes)
+        def batch_rate(plist, reps=5):
+            eng.set_background_cache(True)
+            eng.loglik_batch(plist, grad=True)
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                eng.set_background_cache(False)  # (drop every cache between calls)
+                eng.set_background_cache(True)
+                eng.loglik_batch(plist, grad=True)
+            el = reduce_over_ranks(time.perf_counter() - t0)
+            eng.set_background_cache(False)
+            return reps * len(plist) / el
+        tau_grid = [[0.66, tx, tt, 0.344, 1440.0, 0.0695] for tx in (1.2, 1.4, 1.6, 1.8)
+                    for tt in (10.0, 12.0, 14.0, 16.0)]
+        mt_grid = [[m, 1.6, 14.0, th, 1440.0, 0.0695] for m in (0.5, 0.6, 0.66, 0.8)
+                   for th in (0.2, 0.3, 0.344, 0.4)]
+        secondary["f3_batch16"] = {
+            "what": "loglik+grad batches of 16 parameter vectors per call (wall clock, caches "
+                    "dropped between calls); entries sharing (tauX, tauT) share the background "
+                    "sweep, sharing (omega, h) too the trigger sweep",
+            "distinct_tau_evals_per_s": batch_rate(tau_grid),
+            "mu0_theta_variants_evals_per_s": batch_rate(mt_grid)}
+
+        # f2: posterior excitation over 1,000 MH-style draws at N=55,000 (the
+        # paper's workload): one device batch
+        ex55 = pk.simulateClusterProcess(pk.Params(*SIM_TRUTH), pk.SimWindow(*SIM_WINDOW), SIM_RATE,
+                                         SIM_SEED, keep=55000)[0]
+        rng2 = np.random.default_rng(7)
+        dr, cur = [], list(THETA_POST)
+        for _ in range(1000):
+            k = [0, 3, 4, 5][int(rng2.integers(4))]
+            cur = list(cur)
+            cur[k] *= float(np.exp(0.01 * rng2.standard_normal()))
+            dr.append(cur)
+        eng.load_events(ex55.xs(), ex55.ys(), ex55.ts(), ex55.windowEnd())
+        eng.set_background_cache(True)
+        eng.excitation_batch(dr[:4])
+        barrier()
+        t0 = time.perf_counter()
+        _, _, bad = eng.excitation_batch(dr)
+        f2_s = reduce_over_ranks(time.perf_counter() - t0)
+        eng.set_background_cache(False)
+        secondary["f2_posterior_excitation"] = {
+            "what": "pi over 1,000 MH-style draws (one of mu0/theta/omega/h moves per draw), "
+                    "N=55,000 C2-shaped events, one sthk_excitation_batch call (device sums)",
+            "seconds": f2_s, "draws_per_s": 1000 / f2_s, "underflow_draw": bad}
+        del ex55
 
         # C4: N = 1,000,000 (generateBenchmarkCloud, Rng(1e6)) on the same ranks
         c4 = pk.generateBenchmarkCloud(N_C4, pk.SimWindow(*SIM_WINDOW), N_C4)
@@ -475,7 +531,7 @@ def main():
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "precision_note": "results FP64 (secondary.all_fp64 gives the every-pair-FP64 line); pairs "
+        "precision_note": "results FP64 (secondary.all_fp64: every pair in FP64, same windows); pairs "
                           "whose every term is provably < e^-A of the row's self term run on the "
                           "FP32 far tier, A chosen so the tier moves each row's background sum by "
                           "<= 1e-13 relative, and terms whose total is provably below half an ulp "

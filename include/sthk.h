@@ -192,9 +192,12 @@ int sthk_set_dense(sthk_engine* e, int dense);
  * chunk grid, same kernels). Benchmarks of full evaluations turn them off. */
 int sthk_set_background_cache(sthk_engine* e, int enable);
 
-/* Far tier of the symmetric kernel (default on): stages whose every exponent
- * is provably below -40 (terms < 4.3e-18 of the self term) run in FP32 on the
- * MUFU/FP32 pipes; 0 = every pair in FP64 (testing / accuracy comparisons). */
+/* Far tier of the symmetric kernel. 1 (default): source stages whose every
+ * term is provably below e^-A of the row's self term (A in [30, 40]) run in
+ * FP32 on the FMA/MUFU pipes, and far terms whose total is provably below
+ * half an ulp of lambda are not evaluated. 2: the same far
+ * list and windows evaluated by the FP64 kernel (what the FP32 tier saves).
+ * 0: no far tier -- every pair within the exact-underflow windows in FP64. */
 int sthk_set_far_tier(sthk_engine* e, int enable);
 /* Trigger-free near kernel (default on): in full symmetric sweeps whose
  * trigger window dT is narrower than the near band, near stages of sources

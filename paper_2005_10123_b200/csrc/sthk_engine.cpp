@@ -188,7 +188,8 @@ struct sthk_engine {
   bool loaded = false, has_params = false;
   bool timing = false, dense = false;
   int mode = sthk::kSym;   // pair-kernel variant (sthk_set_kernel)
-  bool far_tier = true;    // FP32 far tier of the symmetric kernel (sthk_set_far_tier)
+  bool far_tier = true;    // far tier of the symmetric kernel (sthk_set_far_tier)
+  bool far_fp64 = false;   // ... its list evaluated by the FP64 kernel (same windows)
   bool bg_split = true;    // trigger-free near kernel for stages beyond the trigger window
   // The far kernel runs concurrently with the near (FP64) sweep on a second
   // stream: the near kernel is limited to near_ctas CTAs per SM so that
@@ -224,6 +225,7 @@ struct sthk_engine {
   int cache_mode = -1;
   bool cache_dense = false;
   bool cache_far_full = false;
+  bool cache_far_fp64 = false;
   double cache_tfar = 0.0;
   int cache_bg_adj = 0;
   std::vector<int> cache_cuts;  // shard cuts the cached sums were combined under
@@ -924,6 +926,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
   const bool cached = e.bg_cache && e.cache_valid && e.cache_gen == e.load_gen &&
                       e.cache_tx == e.p[1] && e.cache_tt == e.p[2] && e.cache_mode == e.mode &&
                       e.cache_far_full == far_full && e.cache_tfar == (far_full ? pl.tfar : 0.0) &&
+                      e.cache_far_fp64 == e.far_fp64 &&
                       e.cache_bg_adj == bg_adj && e.cache_dense == e.dense &&
                       e.cache_cuts == pl.cuts && (e.cache_grad || !grad);
   e.last_cache_hit = cached;
@@ -1169,6 +1172,19 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
       fa_.work_counter = s.scalars + 7;
       fa_.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 8);
       fa_.tpart = far_tr ? s.tpart_far : nullptr;
+      // far list in FP64 (sthk_set_far_tier(2)): the general near kernel over
+      // the same list with the far tier's windows -- the precision policy's
+      // cost measured with identical culling
+      auto launch_far_list = [&](int grid_far, cudaStream_t fs) {
+        if (e.far_fp64) {
+          sthk::PairArgs f64 = fa_;
+          f64.k.dB = pl.k.dBf;
+          f64.k.dT = pl.k.dTf;
+          f64.tpart = s.tpart_far;  // (read by finalize only when far_tr)
+          return sthk::launch_pairs(f64, grad, e.mode, s.sms * s.occ[e.mode][grad ? 1 : 0], fs);
+        }
+        return sthk::launch_far(fa_, grad, grid_far, fs);
+      };
       if (conc) {  // forked onto the second stream, joined before finalize
         ck(cudaEventRecord(s.fork, st), "event");
         ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
@@ -1176,11 +1192,11 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
           launch_bg();
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
           e.launches += 1;
-          ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
+          ck(launch_far_list(s.sms * e.far_ctas, s.stream2), "far kernel");
           e.launches += 1;
         } else {
           launch_bg();
-          ck(sthk::launch_far(fa_, grad, s.sms * e.far_ctas, s.stream2), "far kernel");
+          ck(launch_far_list(s.sms * e.far_ctas, s.stream2), "far kernel");
           e.launches += 1;
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
           e.launches += 1;
@@ -1191,7 +1207,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
         launch_bg();
         ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
         e.launches += 1;
-        ck(sthk::launch_far(fa_, grad, s.sms * s.occ_far[grad ? 1 : 0], st), "far kernel");
+        ck(launch_far_list(s.sms * s.occ_far[grad ? 1 : 0], st), "far kernel");
         e.launches += 1;
       }
     } else {
@@ -1306,6 +1322,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
     e.cache_mode = e.mode;
     e.cache_dense = e.dense;
     e.cache_far_full = far_full;
+    e.cache_far_fp64 = e.far_fp64;
     e.cache_tfar = far_full ? pl.tfar : 0.0;
     e.cache_bg_adj = bg_adj;
     e.cache_cuts = pl.cuts;
@@ -1862,7 +1879,11 @@ int sthk_set_bgonly_kernel(sthk_engine* e, int enable) {
 }
 
 int sthk_set_far_tier(sthk_engine* e, int enable) {
-  return guarded(e, [&] { e->far_tier = enable != 0; });
+  return guarded(e, [&] {
+    if (enable < 0 || enable > 2) throw InvalidArg("sthk_set_far_tier: mode must be 0, 1 or 2");
+    e->far_tier = enable != 0;
+    e->far_fp64 = enable == 2;
+  });
 }
 
 int sthk_set_kernel(sthk_engine* e, int mode) {

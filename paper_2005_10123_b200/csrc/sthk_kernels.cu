@@ -189,63 +189,91 @@ constexpr int kPlanBins = 1024;  // item-size classes (stages, clamped)
 // ones (less idle time in the tail); resets the pair kernel's work counter.
 // The order only affects scheduling: every partial has a fixed destination
 // and integer (fixed-point) accumulation, so results do not depend on it.
-// Work list of one kind (near or far) ordered by decreasing item size: a
-// histogram of the items' stage counts, an exclusive scan over the bins in
-// decreasing size, then placement (1024 threads, one CTA).
-// (my_rg / my_cr: this thread's first tile, kept in registers since phase 1)
-__device__ void plan_list(const PlanArgs& a, int sc, const int2* ranges, const int2* crange,
-                          int2 my_rg, int2 my_cr, int2* items, int* n_items, int* work_counter,
-                          int* s_hist, int* s_warp) {
+// The work lists (near, far, trigger-free) ordered by decreasing item size,
+// all in one pass: per list a histogram of the items' stage counts, one
+// exclusive scan over the bins in decreasing size for every list at once,
+// then placement (1024 threads, one CTA; five barriers whatever the number
+// of lists).
+struct PlanList {
+  int sc;
+  const int2* ranges;
+  const int2* crange;
+  int2* items;
+  int* n_items;
+  int* work_counter;
+};
+constexpr int kPlanLists = 3;
+
+// (my_rg / my_cr: this thread's first tile per list, kept in registers since
+// the range phase)
+__device__ __forceinline__ void plan_lists(const PlanArgs& a, const PlanList (&pl)[kPlanLists],
+                                                  const bool (&on)[kPlanLists],
+                           const int2 (&my_rg)[kPlanLists], const int2 (&my_cr)[kPlanLists],
+                           int (*s_hist)[kPlanBins], int (*s_warp)[32]) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ntiles = a.tile1 - a.tile0;
-  for (int b = tid; b < kPlanBins; b += 1024) s_hist[b] = 0;
+  _Pragma("unroll") for (int l = 0; l < kPlanLists; ++l) {
+    if (!on[l]) continue;
+    for (int b = tid; b < kPlanBins; b += 1024) s_hist[l][b] = 0;
+  }
   __syncthreads();
   for (int i = tid; i < ntiles; i += 1024) {
-    const int2 rg = i == tid ? my_rg : ranges[a.tile0 + i];
-    const int2 cr = i == tid ? my_cr : crange[a.tile0 + i];
-    for (int c = cr.x; c <= cr.y; ++c) {
-      atomicAdd(&s_hist[min(item_stages(sc, rg, c), kPlanBins - 1)], 1);
+    _Pragma("unroll") for (int l = 0; l < kPlanLists; ++l) {
+    if (!on[l]) continue;
+      const int2 rg = i == tid ? my_rg[l] : pl[l].ranges[a.tile0 + i];
+      const int2 cr = i == tid ? my_cr[l] : pl[l].crange[a.tile0 + i];
+      for (int c = cr.x; c <= cr.y; ++c) {
+        atomicAdd(&s_hist[l][min(item_stages(pl[l].sc, rg, c), kPlanBins - 1)], 1);
+      }
     }
   }
   __syncthreads();
-  const int bin = kPlanBins - 1 - tid;  // thread t owns bin kPlanBins - 1 - t
-  const int c = s_hist[bin];
-  int v = c;
+  const int bin = kPlanBins - 1 - tid;  // thread t owns bin kPlanBins - 1 - t of every list
+  int cnt[kPlanLists], v[kPlanLists];
+  _Pragma("unroll") for (int l = 0; l < kPlanLists; ++l) {
+    if (!on[l]) continue;
+    cnt[l] = s_hist[l][bin];
+    v[l] = cnt[l];
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int u = __shfl_up_sync(0xffffffffu, v, off);
-    if (lane >= off) v += u;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v[l], off);
+      if (lane >= off) v[l] += u;
+    }
+    if (lane == 31) s_warp[l][warp] = v[l];
   }
-  if (lane == 31) s_warp[warp] = v;
   __syncthreads();
-  if (warp == 0) {
-    int w = s_warp[lane];
+  if (warp < kPlanLists && on[warp]) {  // warp l scans list l's 32 warp totals
+    int w = s_warp[warp][lane];
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const int u = __shfl_up_sync(0xffffffffu, w, off);
       if (lane >= off) w += u;
     }
-    s_warp[lane] = w;
+    s_warp[warp][lane] = w;
   }
   __syncthreads();
-  const int incl = v + (warp > 0 ? s_warp[warp - 1] : 0);
-  if (tid == 1023) {
-    *n_items = incl;
-    *work_counter = 0;
+  _Pragma("unroll") for (int l = 0; l < kPlanLists; ++l) {
+    if (!on[l]) continue;
+    const int incl = v[l] + (warp > 0 ? s_warp[l][warp - 1] : 0);
+    if (tid == 1023) {
+      *pl[l].n_items = incl;
+      *pl[l].work_counter = 0;
+    }
+    s_hist[l][bin] = incl - cnt[l];  // start offset of the bin
   }
-  __syncthreads();
-  s_hist[bin] = incl - c;  // start offset of the bin
   __syncthreads();
   for (int i = tid; i < ntiles; i += 1024) {
     const int tile = a.tile0 + i;
-    const int2 rg = i == tid ? my_rg : ranges[tile];
-    const int2 cr = i == tid ? my_cr : crange[tile];
-    for (int ch = cr.x; ch <= cr.y; ++ch) {
-      const int pos = atomicAdd(&s_hist[min(item_stages(sc, rg, ch), kPlanBins - 1)], 1);
-      items[pos] = make_int2(tile, ch);
+    _Pragma("unroll") for (int l = 0; l < kPlanLists; ++l) {
+    if (!on[l]) continue;
+      const int2 rg = i == tid ? my_rg[l] : pl[l].ranges[tile];
+      const int2 cr = i == tid ? my_cr[l] : pl[l].crange[tile];
+      for (int ch = cr.x; ch <= cr.y; ++ch) {
+        const int pos = atomicAdd(&s_hist[l][min(item_stages(pl[l].sc, rg, ch), kPlanBins - 1)], 1);
+        pl[l].items[pos] = make_int2(tile, ch);
+      }
     }
   }
-  __syncthreads();
 }
 
 // Single CTA: per-tile near / far ranges, then each work list ordered by
@@ -255,8 +283,8 @@ __device__ void plan_list(const PlanArgs& a, int sc, const int2* ranges, const i
 // has a fixed destination and integer (fixed-point) accumulation, so results
 // do not depend on it.
 __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
-  __shared__ int s_hist[kPlanBins];
-  __shared__ int s_warp[32];
+  __shared__ int s_hist[kPlanLists][kPlanBins];
+  __shared__ int s_warp[kPlanLists][32];
   __shared__ __align__(8) uint64_t s_bar;
   extern __shared__ __align__(128) double s_piv[];  // kPivots (dynamic: 64 KB)
   const int tid = threadIdx.x;
@@ -298,16 +326,15 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
     }
   }
   __syncthreads();
-  plan_list(a, a.sc, a.ranges, a.crange, my[0], my[1], a.items, a.n_items, a.work_counter,
-            s_hist, s_warp);
-  if (a.ranges_far) {
-    plan_list(a, a.sc, a.ranges_far, a.crange_far, my[2], my[3], a.items_far, a.n_items_far,
-              a.work_counter_far, s_hist, s_warp);
-  }
-  if (a.ranges_bg) {
-    plan_list(a, a.sc_bg, a.ranges_bg, a.crange_bg, my[4], my[5], a.items_bg, a.n_items_bg,
-              a.work_counter_bg, s_hist, s_warp);
-  }
+  // fixed slots: 0 near, 1 far, 2 trigger-free (inactive lists are skipped)
+  const PlanList pl[kPlanLists] = {
+      PlanList{a.sc, a.ranges, a.crange, a.items, a.n_items, a.work_counter},
+      PlanList{a.sc, a.ranges_far, a.crange_far, a.items_far, a.n_items_far, a.work_counter_far},
+      PlanList{a.sc_bg, a.ranges_bg, a.crange_bg, a.items_bg, a.n_items_bg, a.work_counter_bg}};
+  const bool on[kPlanLists] = {true, a.ranges_far != nullptr, a.ranges_bg != nullptr};
+  const int2 mrg[kPlanLists] = {my[0], my[2], my[4]};
+  const int2 mcr[kPlanLists] = {my[1], my[3], my[5]};
+  plan_lists(a, pl, on, mrg, mcr, s_hist, s_warp);
 }
 
 // ---------------------------------------------------------------------------
@@ -557,6 +584,10 @@ constexpr int kSymR = 4;  // rows per thread
 #endif
 #endif
 constexpr int kSymG = STHK_SYM_G;
+#ifndef STHK_G_UNROLL
+#define STHK_G_UNROLL 1  // column groups per unrolled step of the stage loop (register-bound)
+#endif
+constexpr int kGUnroll = STHK_G_UNROLL;
 
 template <bool GRAD, bool SYM, bool BG, int TR, bool CHECK, bool VALID>
 __device__ __forceinline__ void sym_pairs(int g, int perm, const double* __restrict__ sx,
@@ -693,7 +724,7 @@ __device__ __forceinline__ void sym_block(const double* __restrict__ sx,
                                           double* __restrict__ s_col) {
   const int lane = threadIdx.x & 31;
   const int perm = kSymG == 4 ? (((lane >> 4) & 1) << 1) | ((lane >> 3) & 1) : (lane >> 4) & 1;
-#pragma unroll 1
+#pragma unroll kGUnroll
   for (int g = 0; g < 32 / kSymG; ++g) {
     double cp[kSymG][GRAD ? 3 : 1];
     sym_pairs<GRAD, SYM, BG, TR, CHECK, VALID>(g, perm, sx, sy, st, col0, cnt, xi, yi, ti, rv, k,

@@ -203,9 +203,10 @@ class Engine:
         """Trigger-free near kernel for stages beyond the trigger window (default on)."""
         self._check(self._lib.sthk_set_bgonly_kernel(self._h, int(on)), "sthk_set_bgonly_kernel")
 
-    def set_far_tier(self, on: bool) -> None:
-        """FP32 far tier of the symmetric kernel (default on; include/sthk.h)."""
-        self._check(self._lib.sthk_set_far_tier(self._h, int(on)), "sthk_set_far_tier")
+    def set_far_tier(self, mode) -> None:
+        """Far tier of the symmetric kernel (include/sthk.h): True / 1 = FP32 far
+        tier (default), 2 = the far list in FP64 (same windows), False / 0 = off."""
+        self._check(self._lib.sthk_set_far_tier(self._h, int(mode)), "sthk_set_far_tier")
 
     def set_far_schedule(self, concurrent: bool, near_ctas: int = 3, far_ctas: int = 6) -> None:
         self._check(self._lib.sthk_set_far_schedule(self._h, int(concurrent), near_ctas, far_ctas),

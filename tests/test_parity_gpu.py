@@ -811,3 +811,28 @@ def test_rejects_more_events_than_fixed_point_range(engine):
         engine.load_events(z, z, t, float(t[-1]))
     ev = pk.generateBenchmarkCloud(300, pk.SimWindow(0, 4, 0, 4, 60), 5)
     engine.load(ev)  # (the engine still works)
+
+
+def test_far_list_in_fp64_same_windows(engine):
+    """sthk_set_far_tier(2): the far list evaluated by the FP64 kernel with the
+    far tier's windows. Against the FP32 far tier it differs only by the far
+    terms' FP32 rounding (<= 1e-13 on loglik); against no far tier at all only
+    by terms below half an ulp of lambda."""
+    ev = _c2(keep=40000)
+    engine.load(ev)
+    for theta in ([0.66, 1.6, 14, 0.344, 1440, 0.0695], [1, 1.6, 14, 0.1, 1, 1]):
+        engine.set_params(theta)
+        res = {}
+        try:
+            for mode in (1, 2, 0):
+                engine.set_far_tier(mode)
+                engine.set_timing(True)
+                res[mode] = (engine.loglik_grad(), engine.stats()["exec_far"])
+                engine.set_timing(False)
+        finally:
+            engine.set_far_tier(1)
+        (a, fa), (b, fb), (c, fc) = res[1], res[2], res[0]
+        assert fa > 0 and fb == 0 and fc == 0
+        assert abs(a[0] - b[0]) <= 1e-13 * abs(b[0]) and abs(b[0] - c[0]) <= 1e-14 * abs(c[0])
+        o = og.oracle_loglik_grad(ev.xs(), ev.ys(), ev.ts(), ev.windowEnd(), np.array(theta))
+        assert np.all(np.abs(b[2] - c[2]) <= 1e-12 * o["grad_abs"])
