@@ -191,6 +191,12 @@ struct sthk_engine {
   bool far_tier = true;    // far tier of the symmetric kernel (sthk_set_far_tier)
   bool far_fp64 = false;   // ... its list evaluated by the FP64 kernel (same windows)
   bool bg_split = true;    // trigger-free near kernel for stages beyond the trigger window
+  // ... its list merged into the general kernel's launch (development knob
+  // STHK_MERGE_BG=0/1 at creation)
+  bool merge_bg = [] {
+    const char* v = std::getenv("STHK_MERGE_BG");
+    return v ? *v == '1' : false;
+  }();
   // The far kernel runs concurrently with the near (FP64) sweep on a second
   // stream: the near kernel is limited to near_ctas CTAs per SM so that
   // far_ctas_resident far CTAs fit beside it (FP64 and FP32/MUFU pipes busy
@@ -1144,8 +1150,17 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
     qa.pair_counts = e.timing ? s.pair_counts : nullptr;
     // a trigger-only sweep runs the same kernel with the background switched
     // off, so its trigger partials are summed exactly as in a full sweep
+    // merged: the general kernel takes the background-only list's items first
+    // (one launch; the general items fill the tail), else a separate launch
+    // of the trigger-free kernel
+    if (bg_split && e.merge_bg) {
+      qa.pre_ranges = s.ranges_bg;
+      qa.pre_items = s.items_bg;
+      qa.pre_n_items = s.scalars + 9;
+      qa.pre_sc = pl.sc_bg;
+    }
     auto launch_bg = [&] {  // the trigger-free kernel over the background-only list
-      if (!bg_split) return;
+      if (!bg_split || e.merge_bg) return;
       sthk::PairArgs ba = qa;
       ba.ranges = s.ranges_bg;
       ba.sc = pl.sc_bg;
@@ -1166,6 +1181,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
     ck(cudaEventRecord(s.ev[1], st), "event");
     if (far_on) {  // the far work list in FP32
       sthk::PairArgs fa_ = qa;
+      fa_.pre_items = nullptr;
       fa_.ranges = s.ranges_far;
       fa_.items = s.items_far;
       fa_.n_items = s.scalars + 6;

@@ -128,6 +128,14 @@ struct PairArgs {
   double* tpart;        // trigger partials [nchunks][3 or 1][npad]
   int bg_off;           // trigger-only sweep (background sums come from a cache)
   unsigned long long* pair_counts;  // [kNCounts] (tile granularity)
+  // merged trigger-free list (general sym_kernel only; nullptr: none): work
+  // items [0, *pre_n_items) are the background-only list's -- its ranges,
+  // items and chunk size, no trigger, fixed-point row sums only -- and the
+  // rest the general list's, all from the general list's work counter
+  const int2* pre_ranges;
+  const int2* pre_items;
+  const int* pre_n_items;
+  int pre_sc;
 };
 
 struct FinArgs {
