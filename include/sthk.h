@@ -168,12 +168,21 @@ typedef struct sthk_stats {
   int64_t exec_far;          /* pairs evaluated in the FP32 far tier (every exponent
                                 provably < -A, A in [30, 40]) */
   int64_t kernel_launches;   /* kernels the last evaluation launched (all devices) */
+  double far_threshold;      /* far tier's threshold A of the last evaluation */
+  double far_split_days;     /* its split tfar (sources further back run in FP32) */
 } sthk_stats;
 
 int sthk_set_timing(sthk_engine* e, int enable);
 int sthk_get_stats(sthk_engine* e, sthk_stats* out);
 /* cudaStream_t of local device slot `slot` (for event-based timing). */
 int sthk_get_stream(sthk_engine* e, int slot, void** stream);
+/* Development: the pair-kernel work-item trace of the last evaluation on a
+ * slot (only with STHK_ITEM_TRACE=<entries> in the environment at create
+ * time; else *count = 0). Four words per item: (kernel << 48 | smid << 32 |
+ * item), (stages << 8 | contains the diagonal stage), start ns, end ns
+ * (%globaltimer); kernel 1 general near, 2 trigger-free near, 3 far. */
+int sthk_debug_item_trace(sthk_engine* e, int slot, unsigned long long* out, int64_t cap,
+                          int64_t* count);
 /* Debug/testing knob: 0 = exact tile culling on (default), 1 = evaluate the
  * dense pair set (results are bitwise identical either way). */
 int sthk_set_dense(sthk_engine* e, int dense);

@@ -44,6 +44,8 @@ class StatsStruct(ctypes.Structure):
         ("trigger_cache_hit", ctypes.c_int32),
         ("exec_far", c_int64),
         ("kernel_launches", c_int64),
+        ("far_threshold", c_double),
+        ("far_split_days", c_double),
     ]
 
 
@@ -82,6 +84,7 @@ SIGNATURES = [
     ("sthk_set_timing", c_int, [c_void_p, c_int]),
     ("sthk_get_stats", c_int, [c_void_p, POINTER(StatsStruct)]),
     ("sthk_get_stream", c_int, [c_void_p, c_int, POINTER(c_void_p)]),
+    ("sthk_debug_item_trace", c_int, [c_void_p, c_int, c_void_p, c_int64, POINTER(c_int64)]),
     ("sthk_set_dense", c_int, [c_void_p, c_int]),
     ("sthk_get_exchange_bytes", c_int, [c_void_p, POINTER(c_int64)]),
     ("sthk_set_kernel", c_int, [c_void_p, c_int]),

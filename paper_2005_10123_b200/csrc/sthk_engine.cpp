@@ -95,7 +95,8 @@ struct Slot {
   size_t trange_cap = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;    // far kernel, concurrent with the near sweep
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t stream3 = nullptr;    // general near kernel beside the trigger-free one
+  cudaEvent_t fork = nullptr, join = nullptr, join3 = nullptr;
   cudaEvent_t pairs_done = nullptr, fin_done = nullptr;  // cross-slot ordering (local transport)
   ncclComm_t comm = nullptr;
   int shard = 0;                     // this slot's shard (= rank)
@@ -105,6 +106,8 @@ struct Slot {
   size_t x_cap = 0, y_cap = 0, t_cap = 0;
   double *xs = nullptr, *ys = nullptr;  // kSym: x, y scaled by sqrt(-cxL) (per evaluation)
   size_t xs_cap = 0, ys_cap = 0;
+  double* tsl = nullptr;  // kSym trigger-free kernel: (t - t_tile0) * sqrt(-ctL) (per evaluation)
+  size_t tsl_cap = 0;
   float *xf = nullptr, *yf = nullptr, *tf = nullptr;  // kSym far tier: FP32 coordinates
   size_t xf_cap = 0, yf_cap = 0, tf_cap = 0;
   double* h_stats = nullptr;  // pinned, device-mapped: load statistics (sthk::kLoadStats)
@@ -160,7 +163,19 @@ struct Slot {
   int plan_key[7] = {0, 0, 0, 0, 0, 0, 0};  // tile0, tile1, sc, dense, sym, trig_only, bg split
   double plan_tfar = 0, plan_dfar = 0;
   std::vector<std::pair<int, int>> runs;  // row ranges run on this slot
+  unsigned long long* trace = nullptr;     // development item trace (STHK_ITEM_TRACE)
 };
+
+// (development knob: STHK_ITEM_TRACE=<entries> records every pair-kernel work
+// item's SM and start / end time, sthk_debug_item_trace)
+int item_trace_cap() {
+  static const int v = [] {
+    const char* s = std::getenv("STHK_ITEM_TRACE");
+    const int k = s ? std::atoi(s) : 0;
+    return k > 0 ? std::min(k, 1 << 22) : 0;
+  }();
+  return v;
+}
 
 }  // namespace
 
@@ -203,6 +218,16 @@ struct sthk_engine {
   // at once); extra far CTAs queue until near CTAs retire.
   bool far_concurrent = true;
   int far_order = 1;  // 1: far launched first, 2: near first
+  // Launch order of the concurrent pair kernels (development knob
+  // STHK_PAIR_ORDER at creation): 0 trigger-free then general on one stream,
+  // far beside them; 1 trigger-free, general (third stream), far -- the
+  // general kernel's CTAs fill in as trigger-free CTAs retire; 2 general
+  // first. Without a trigger-free list, 1 and 2 launch the near kernel ahead
+  // of the far one.
+  int pair_order = [] {
+    const char* v = std::getenv("STHK_PAIR_ORDER");
+    return v ? std::atoi(v) : 0;
+  }();
   int near_ctas = 3, far_ctas = 6;
   double ext_x = 0, ext_y = 0;  // max |x - x[0]|, |y - y[0]| of the loaded set
   double tile_tspan = 0;        // max time span of a 128-event tile
@@ -210,6 +235,9 @@ struct sthk_engine {
   // from a tile's first event back to the last source before its k preceding
   // stages (the trigger-free split keeps those k stages with the tile)
   std::vector<double> adj_gap;
+  // span_min[L]: min time span of 2^L consecutive whole tiles (load
+  // statistics): bounds the number of events in any time window (far tier)
+  std::vector<double> span_min;
   // Background-sum cache: S_B (and S_Br, S_Bt) depend only on the events,
   // tauX, tauT -- fixed for a whole MH chain (sampler.cpp:48-49) -- so while
   // they are unchanged an evaluation sweeps only the trigger band. The
@@ -238,6 +266,7 @@ struct sthk_engine {
   std::string err;
   bool pending = false, last_grad = false, last_pe = false, last_ex = false;
   int last_sc = 0, last_items_est = 0;
+  double last_far_a = 0.0, last_tfar = 0.0;
 };
 
 namespace {
@@ -263,9 +292,19 @@ void init_slot(Slot& s, int dev) {
   set_dev(s);
   ck(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
   ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
-  ck(cudaStreamCreateWithFlags(&s.stream2, cudaStreamNonBlocking), "stream");
+  {
+    // (development knob STHK_STREAM_PRIO=1: far kernel stream at the lowest
+    // priority, the general near kernel's at the highest)
+    const char* pv = std::getenv("STHK_STREAM_PRIO");
+    int lo = 0, hi = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    const bool prio = pv && *pv == '1';
+    ck(cudaStreamCreateWithPriority(&s.stream2, cudaStreamNonBlocking, prio ? lo : 0), "stream");
+    ck(cudaStreamCreateWithPriority(&s.stream3, cudaStreamNonBlocking, prio ? hi : 0), "stream");
+  }
   ck(cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&s.join3, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.prepped, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.pairs_done, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.fin_done, cudaEventDisableTiming), "event");
@@ -282,6 +321,10 @@ void init_slot(Slot& s, int dev) {
   ck(cudaMemset(s.scalars + 4, 0xff, sizeof(unsigned long long)), "memset");
   ck(cudaMalloc(&s.pair_counts, sthk::kNCounts * sizeof(unsigned long long)), "cudaMalloc");
   ck(cudaMemset(s.pair_counts, 0, sthk::kNCounts * sizeof(unsigned long long)), "memset");
+  if (item_trace_cap() > 0) {
+    ck(cudaMalloc(&s.trace, (4 + 4 * static_cast<size_t>(item_trace_cap())) * sizeof(unsigned long long)),
+       "cudaMalloc");
+  }
   // results and counters are written by the last kernel straight into
   // device-mapped pinned memory: no D2H copy on the evaluation's stream
   constexpr unsigned kMapped = cudaHostAllocMapped | cudaHostAllocPortable;
@@ -308,7 +351,7 @@ void free_slot(Slot& s) {
   if (s.stream) cudaStreamSynchronize(s.stream);
   if (s.comm) ncclCommDestroy(s.comm);
   for (void* p : {static_cast<void*>(s.x), static_cast<void*>(s.y), static_cast<void*>(s.t),
-                  static_cast<void*>(s.xs), static_cast<void*>(s.ys),
+                  static_cast<void*>(s.xs), static_cast<void*>(s.ys), static_cast<void*>(s.tsl),
                   static_cast<void*>(s.xf), static_cast<void*>(s.yf), static_cast<void*>(s.tf),
                   static_cast<void*>(s.ranges_far), static_cast<void*>(s.crange_far),
                   static_cast<void*>(s.items_far), static_cast<void*>(s.tpart_far),
@@ -324,7 +367,8 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.per_event),
                   static_cast<void*>(s.pair_counts), static_cast<void*>(s.tile_box),
                   static_cast<void*>(s.fx_stage), static_cast<void*>(s.pi_sum),
-                  static_cast<void*>(s.pi_bad), static_cast<void*>(s.pi_rows)}) {
+                  static_cast<void*>(s.pi_bad), static_cast<void*>(s.pi_rows),
+                  static_cast<void*>(s.trace)}) {
     if (p) cudaFree(p);
   }
   for (void* p : {static_cast<void*>(s.h_out), static_cast<void*>(s.h_counts),
@@ -337,8 +381,11 @@ void free_slot(Slot& s) {
     if (e) cudaEventDestroy(e);
   }
   if (s.stream2) cudaStreamSynchronize(s.stream2);
+  if (s.stream3) cudaStreamSynchronize(s.stream3);
   if (s.fork) cudaEventDestroy(s.fork);
   if (s.join) cudaEventDestroy(s.join);
+  if (s.join3) cudaEventDestroy(s.join3);
+  if (s.stream3) cudaStreamDestroy(s.stream3);
   if (s.prepped) cudaEventDestroy(s.prepped);
   if (s.pairs_done) cudaEventDestroy(s.pairs_done);
   if (s.fin_done) cudaEventDestroy(s.fin_done);
@@ -387,6 +434,7 @@ void validate_window_end(const double* t, int64_t n, double window_end) {
 struct EvalPlan {
   sthk::PairConsts k;
   double sx = 1.0;  // kSym coordinate scale sqrt(-cxL)
+  double stl = 1.0;  // kSym trigger-free kernel time scale sqrt(-ctL)
   double sxf = 1.0, stf = 1.0;  // far-tier FP32 coordinate scales
   double tfar = 0.0;            // far split time gap (days)
   double boost = 0.0;           // ln(trNorm / (mu0 bgNorm)) when > 0
@@ -493,7 +541,23 @@ struct PlanInput {
   bool far;  // far tier enabled (partition cost)
   // load statistics (far-tier error bound): max |x - x0|, |y - y0|, tile time span
   double ext_x = 0, ext_y = 0, tile_tspan = 0;
+  const std::vector<double>* span_min = nullptr;  // (see sthk_engine::span_min)
 };
+
+// Upper bound on the number of events in any time window of length w, from
+// the load statistics: a window holding (2^L + 1) * 128 events contains 2^L
+// consecutive whole tiles, whose span is then <= w; so if every such run
+// spans more than w, the window holds fewer.
+int64_t max_events_in_window(const std::vector<double>* span_min, int64_t n, double w) {
+  if (span_min) {
+    for (size_t L = 0; L < span_min->size(); ++L) {
+      if ((*span_min)[L] > w) {
+        return std::min<int64_t>(n, ((int64_t{1} << L) + 1) * sthk::kTS - 1);
+      }
+    }
+  }
+  return n;
+}
 
 // (development knob: STHK_MIN_CHUNK_STAGES overrides the minimum item length)
 int min_chunk_stages() {
@@ -505,8 +569,19 @@ int min_chunk_stages() {
   return v;
 }
 
+// (development knob: STHK_CHUNKS_TARGET overrides the chunk count target)
+int chunks_target() {
+  static const int v = [] {
+    const char* s = std::getenv("STHK_CHUNKS_TARGET");
+    const int k = s ? std::atoi(s) : 0;
+    return k >= 1 && k <= 65536 ? k : kChunksTarget;
+  }();
+  return v;
+}
+
 int chunk_size(int64_t n, int64_t npad) {
-  int64_t sc = (n + kChunksTarget - 1) / kChunksTarget;
+  const int64_t ct = chunks_target();
+  int64_t sc = (n + ct - 1) / ct;
   sc = (sc + kTS - 1) / kTS * kTS;
   sc = std::max<int64_t>(sc, static_cast<int64_t>(min_chunk_stages()) * kTS);
   sc = std::min<int64_t>(sc, npad);
@@ -534,6 +609,7 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   pl.k.chL = static_cast<double>(-0.5L * L / (static_cast<long double>(p[5]) * p[5]));
   // symmetric kernel: coordinates scaled by sx so that r2 = sx^2 r^2 ~ -cxL r^2
   pl.sx = std::sqrt(-pl.k.cxL);
+  pl.stl = static_cast<double>(std::sqrt(0.5L * L) / static_cast<long double>(p[2]));
   pl.k.chS = pl.k.chL / (pl.sx * pl.sx);
   // far tier (FP32, log2 units): xf = (x - x0) sxf, tf = (t - t0) stf
   const double kLn2 = 0.693147180559945309417232121458176568;
@@ -570,7 +646,13 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
     const double dd = (2.0 * cc + dmax) * u + dmax * u;
     const double dE = 3.0 * (2.0 * dmax * dd + dmax * dmax * u) + 3.0 * dmax * dmax * u;
     const double eps = kLn2 * dE + 4.0 * u + static_cast<double>(chunk_size(e.n, e.npad)) * u;
-    const double a_need = std::log(static_cast<double>(std::max<int64_t>(e.n, 2)) * eps / kFarRowBound);
+    // far terms in one event's S_B: its far sources (rows) plus the later
+    // rows it is a far source of (columns), each within dfar + one tile's
+    // span of it, so at most twice the events of such a window (<= N)
+    const int64_t far_terms = std::min<int64_t>(
+        e.n, 2 * max_events_in_window(e.span_min, e.n, dfar + e.tile_tspan));
+    const double a_need =
+        std::log(static_cast<double>(std::max<int64_t>(far_terms, 2)) * eps / kFarRowBound);
     pl.far_a = std::min(kFarExponent, std::max(kFarExponentMin, a_need));
     pl.tfar = std::max(p[2] * std::sqrt(2.0 * pl.far_a), (pl.far_a + boost) / p[4]) *
               (1.0 + 1e-9);
@@ -901,9 +983,11 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
     e.ht_valid = true;
   }
   const EvalPlan pl = make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym, sym && e.far_tier,
-                                          e.ext_x, e.ext_y, e.tile_tspan},
+                                          e.ext_x, e.ext_y, e.tile_tspan, &e.span_min},
                                 shards);
   e.last_sc = pl.sc;
+  e.last_far_a = pl.far_a;
+  e.last_tfar = pl.tfar;
   e.exch_bytes = 0;
   e.launches = 0;
   // Split structure of a full sweep (it fixes how the background sums are
@@ -921,7 +1005,11 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
   // launch and per-CTA setup: measured break-even between N = 30k and 40k)
   int bg_adj = 0;
   if (sym && e.bg_split && !e.adj_gap.empty() && e.n >= kBgSplitMinEvents) {
-    const double dT_phys = sthk::kCullExponent / e.p[4] * (1.0 + 1e-9);
+    static const bool use_dT = [] {  // (development knob STHK_BGADJ_WINDOW=1: the half-ulp window)
+      const char* v = std::getenv("STHK_BGADJ_WINDOW");
+      return v && *v == '1';
+    }();
+    const double dT_phys = use_dT ? pl.k.dT : sthk::kCullExponent / e.p[4] * (1.0 + 1e-9);
     for (int k = 1; k <= kMaxAdj; ++k) {
       if (e.adj_gap[k - 1] > dT_phys) {
         bg_adj = k;
@@ -1019,6 +1107,11 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
       pr.sx = pl.sx;
       pr.xs = s.xs;
       pr.ys = s.ys;
+      if (bg_split) {
+        dev_grow(s.tsl, s.tsl_cap, static_cast<size_t>(e.npad));
+        pr.tsl = s.tsl;
+        pr.stl = pl.stl;
+      }
       if (far_on) {
         pr.sxf = pl.sxf;
         pr.stf = pl.stf;
@@ -1128,6 +1221,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
     qa.t = s.t;
     qa.xs = s.xs;
     qa.ys = s.ys;
+    qa.tsl = s.tsl;
+    qa.stl = pl.stl;
     qa.xf = s.xf;
     qa.yf = s.yf;
     qa.tf = s.tf;
@@ -1148,6 +1243,12 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
     for (int k = 0; k < sthk::kNSumGrad; ++k) qa.fxq[k] = fxq[k];
     if (sym) qa.fxq[1] = fxq[1] / (pl.sx * pl.sx);  // S_Br accumulates sx^2 r^2
     qa.pair_counts = e.timing ? s.pair_counts : nullptr;
+    if (s.trace) {
+      ck(cudaMemsetAsync(s.trace, 0, sizeof(unsigned long long), st), "memset");
+      qa.trace = s.trace;
+      qa.trace_cap = item_trace_cap();
+      qa.trace_kernel = 1;
+    }
     // a trigger-only sweep runs the same kernel with the background switched
     // off, so its trigger partials are summed exactly as in a full sweep
     // merged: the general kernel takes the background-only list's items first
@@ -1168,6 +1269,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
       ba.n_items = s.scalars + 9;
       ba.work_counter = s.scalars + 10;
       ba.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 11);
+      ba.trace_kernel = 2;
       ck(sthk::launch_bgonly(ba, grad, s.sms * s.occ_bg[grad ? 1 : 0], st), "bg-only kernel");
       e.launches += 1;
     };
@@ -1188,6 +1290,7 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
       fa_.work_counter = s.scalars + 7;
       fa_.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 8);
       fa_.tpart = far_tr ? s.tpart_far : nullptr;
+      fa_.trace_kernel = 3;
       // far list in FP64 (sthk_set_far_tier(2)): the general near kernel over
       // the same list with the far tier's windows -- the precision policy's
       // cost measured with identical culling
@@ -1201,10 +1304,29 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
         }
         return sthk::launch_far(fa_, grad, grid_far, fs);
       };
-      if (conc) {  // forked onto the second stream, joined before finalize
+      if (conc && e.pair_order > 0 && bg_split && !e.merge_bg) {
+        // three streams: trigger-free (st), general (stream3), far (stream2)
         ck(cudaEventRecord(s.fork, st), "event");
         ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
-        if (e.far_order == 2) {  // near first: its CTAs are resident before far CTAs fill in
+        ck(cudaStreamWaitEvent(s.stream3, s.fork, 0), "wait");
+        if (e.pair_order == 2) {
+          ck(sthk::launch_pairs(qa, grad, e.mode, grid, s.stream3), "pair kernel");
+          launch_bg();
+        } else {
+          launch_bg();
+          ck(sthk::launch_pairs(qa, grad, e.mode, grid, s.stream3), "pair kernel");
+        }
+        e.launches += 1;
+        ck(launch_far_list(s.sms * e.far_ctas, s.stream2), "far kernel");
+        e.launches += 1;
+        ck(cudaEventRecord(s.join, s.stream2), "event");
+        ck(cudaEventRecord(s.join3, s.stream3), "event");
+        ck(cudaStreamWaitEvent(st, s.join, 0), "wait");
+        ck(cudaStreamWaitEvent(st, s.join3, 0), "wait");
+      } else if (conc) {  // forked onto the second stream, joined before finalize
+        ck(cudaEventRecord(s.fork, st), "event");
+        ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
+        if (e.far_order == 2 || e.pair_order > 0) {  // near first: its CTAs are resident before far CTAs fill in
           launch_bg();
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
           e.launches += 1;
@@ -1622,6 +1744,7 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       e->ext_y = st[1];
       e->tile_tspan = st[2];
       e->adj_gap.assign(st + 3, st + 3 + kMaxAdj);
+      e->span_min.assign(st + 3 + kMaxAdj, st + 3 + kMaxAdj + sthk::kLoadSpan);
     }
     e->n = n;
     e->npad = npad;
@@ -1918,6 +2041,29 @@ int sthk_get_exchange_bytes(sthk_engine* e, int64_t* bytes) {
   });
 }
 
+int sthk_debug_item_trace(sthk_engine* e, int slot, unsigned long long* out, int64_t cap,
+                          int64_t* count) {
+  return guarded(e, [&] {
+    if (slot < 0 || slot >= static_cast<int>(e->slots.size()) || !count) {
+      throw InvalidArg("sthk_debug_item_trace: bad slot or count pointer");
+    }
+    Slot& s = e->slots[slot];
+    *count = 0;
+    if (!s.trace) return;
+    set_dev(s);
+    ck(cudaStreamSynchronize(s.stream), "sync");
+    ck(cudaStreamSynchronize(s.stream2), "sync");
+    unsigned long long n = 0;
+    ck(cudaMemcpy(&n, s.trace, sizeof(n), cudaMemcpyDeviceToHost), "D2H");
+    n = std::min<unsigned long long>(n, static_cast<unsigned long long>(item_trace_cap()));
+    *count = static_cast<int64_t>(n);
+    const size_t k = std::min<size_t>(static_cast<size_t>(n), static_cast<size_t>(std::max<int64_t>(cap, 0)));
+    if (out && k) {
+      ck(cudaMemcpy(out, s.trace + 4, 4 * k * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "D2H");
+    }
+  });
+}
+
 int sthk_get_stream(sthk_engine* e, int slot, void** stream) {
   return guarded(e, [&] {
     if (slot < 0 || slot >= static_cast<int>(e->slots.size()) || !stream) {
@@ -1937,6 +2083,8 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
     out->rank = e->rank;
     out->world = e->world;
     out->source_chunk = e->last_sc;
+    out->far_threshold = e->last_far_a;
+    out->far_split_days = e->last_tfar;
     out->kernel_mode = e->mode;
     out->cache_hit = e->last_cache_hit ? 1 : 0;
     out->trigger_cache_hit = e->last_tr_cache_hit ? 1 : 0;

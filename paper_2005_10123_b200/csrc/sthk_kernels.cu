@@ -46,6 +46,23 @@ namespace sthk {
 namespace {
 
 constexpr double kInvSqrt2 = 0.7071067811865475244;     // kernels.hpp:14
+
+// Work-item hand-out of the persistent pair kernels. STHK_STATIC_FIRST: a
+// CTA's first item is its block index (consecutive blocks are dispatched to
+// different SMs, so with fewer items than CTAs -- small N -- the items spread
+// over the SMs instead of piling onto the first CTAs to arrive), later items
+// come from the atomic counter. Scheduling only: every item's partials have
+// fixed destinations, so results do not depend on it.
+#ifndef STHK_STATIC_FIRST
+#define STHK_STATIC_FIRST 1
+#endif
+__device__ __forceinline__ int next_item(int* counter, int iter) {
+#if STHK_STATIC_FIRST
+  return iter == 0 ? static_cast<int>(blockIdx.x) : static_cast<int>(gridDim.x) + atomicAdd(counter, 1);
+#else
+  return atomicAdd(counter, 1);
+#endif
+}
 constexpr double kInvSqrt2Pi = 0.3989422804014326779;   // kernels.hpp:13
 
 // Sorted-time searches in two levels: kPivots evenly spaced pivots
@@ -455,7 +472,7 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
   unsigned long long cBg = 0, cTr = 0, cAny = 0;
 
   for (int iter = 0;; ++iter) {
-    if (tid == 0) s_item[iter & 1] = atomicAdd(a.work_counter, 1);
+    if (tid == 0) s_item[iter & 1] = next_item(a.work_counter, iter);
     __syncthreads();
     const int item = s_item[iter & 1];
     if (item >= n_items) break;
@@ -589,7 +606,7 @@ constexpr int kSymG = STHK_SYM_G;
 #endif
 constexpr int kGUnroll = STHK_G_UNROLL;
 
-template <bool GRAD, bool SYM, bool BG, int TR, bool CHECK, bool VALID>
+template <bool GRAD, bool SYM, bool BG, int TR, bool CHECK, bool VALID, bool TS>
 __device__ __forceinline__ void sym_pairs(int g, int perm, const double* __restrict__ sx,
                                           const double* __restrict__ sy,
                                           const double* __restrict__ st, int col0, int cnt,
@@ -618,10 +635,18 @@ __device__ __forceinline__ void sym_pairs(int g, int perm, const double* __restr
       r2[r] = fma(dx, dx, dy * dy);
     }
     if constexpr (BG) {
+      // TS (trigger-free kernel, scaled times): the exponent is -(r2 + dts^2)
+      // in one DFMA and the third sum weights each term by the exponent itself
+      // (S_Bt = -sum - S_Br at the flush); else dt^2 is formed and weighted
 #pragma unroll
       for (int r = 0; r < kSymR; ++r) {
-        dt2[r] = dt[r] * dt[r];
-        arg[r] = fma(k.ctL, dt2[r], -r2[r]);
+        if constexpr (TS) {
+          arg[r] = fma(-dt[r], dt[r], -r2[r]);
+          dt2[r] = arg[r];
+        } else {
+          dt2[r] = dt[r] * dt[r];
+          arg[r] = fma(k.ctL, dt2[r], -r2[r]);
+        }
       }
       exp_l_batch<CHECK>(arg, e, tab);
 #pragma unroll
@@ -713,7 +738,7 @@ __device__ __forceinline__ void sym_reduce(int g, int perm, int col0,
 // kSymG columns, each group's column partials reduce-scattered right away.
 // (Interleaving group g's reduction with group g+1's pair math doubles the
 // live registers and spills; measured slower.)
-template <bool GRAD, bool SYM, bool BG, int TR, bool CHECK, bool VALID>
+template <bool GRAD, bool SYM, bool BG, int TR, bool CHECK, bool VALID, bool TS>
 __device__ __forceinline__ void sym_block(const double* __restrict__ sx,
                                           const double* __restrict__ sy,
                                           const double* __restrict__ st, int col0, int cnt,
@@ -727,8 +752,8 @@ __device__ __forceinline__ void sym_block(const double* __restrict__ sx,
 #pragma unroll kGUnroll
   for (int g = 0; g < 32 / kSymG; ++g) {
     double cp[kSymG][GRAD ? 3 : 1];
-    sym_pairs<GRAD, SYM, BG, TR, CHECK, VALID>(g, perm, sx, sy, st, col0, cnt, xi, yi, ti, rv, k,
-                                               tab, racc, cp);
+    sym_pairs<GRAD, SYM, BG, TR, CHECK, VALID, TS>(g, perm, sx, sy, st, col0, cnt, xi, yi, ti, rv,
+                                                   k, tab, racc, cp);
     sym_reduce<GRAD, SYM, BG>(g, perm, col0, cp, s_col);
   }
 }
@@ -909,7 +934,7 @@ __device__ __forceinline__ void sym_dispatch(bool bg, int tr, const double* sx, 
                                              double (&racc)[kSymR][GRAD ? kNSumGrad : kNSumVal],
                                              double* s_col) {
 #define STHK_SYM_CALL(B, T) \
-  sym_block<GRAD, SYM, B, T, CHECK, VALID>(sx, sy, st, col0, cnt, xi, yi, ti, rv, k, tab, racc, s_col)
+  sym_block<GRAD, SYM, B, T, CHECK, VALID, BGONLY>(sx, sy, st, col0, cnt, xi, yi, ti, rv, k, tab, racc, s_col)
   if constexpr (BGONLY) {  // (the plan guarantees no live trigger term)
     if (bg) STHK_SYM_CALL(true, 0);
     return;
@@ -943,8 +968,12 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
   __shared__ double s_col[kTS * NSC];
   __shared__ double s_red[4][NS][kTM];
   __shared__ __align__(32) double4 s_box[2];  // bounding box of the staged source tile
+  __shared__ __align__(16) double2 s_tr[2];   // its first / last time (BGONLY: the staged times are scaled)
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ int s_item[2];
+  // BGONLY stages carry tile-relative scaled times (PairArgs::tsl)
+  const double* __restrict__ src_t = BGONLY ? a.tsl : a.t;
+  constexpr uint32_t kTrBytesS = BGONLY ? sizeof(double2) : 0;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -971,10 +1000,12 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
   unsigned long long cBg = 0, cTr = 0, cAny = 0, xBg = 0, xGeo = 0, xSym = 0;
 
   for (int iter = 0;; ++iter) {
-    if (tid == 0) s_item[iter & 1] = atomicAdd(a.work_counter, 1);
+    if (tid == 0) s_item[iter & 1] = next_item(a.work_counter, iter);
     __syncthreads();
     const int item = s_item[iter & 1];
     if (item >= n_items) break;
+    __shared__ unsigned long long s_trace_t0;  // (development trace: kept out of registers)
+    if (a.trace && tid == 0) s_trace_t0 = global_ns();
 
     // (merged lists: the trigger-free items first, the general items after)
     const bool pre = BGONLY || item < n_pre;
@@ -994,7 +1025,7 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
       const int64_t row = first + lane + 32 * r;
       xi[r] = a.xs[row];
       yi[r] = a.ys[row];
-      ti[r] = a.t[row];
+      ti[r] = BGONLY ? a.tsl[row] : a.t[row];
       rv[r] = row < n;
     }
     // Background row sums live in registers for the whole item; the trigger
@@ -1018,11 +1049,12 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
 
     constexpr uint32_t kStageBytes = kTS * sizeof(double);
     if (tid == 0 && nst > 0) {
-      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes + kBoxBytes);
+      mbar_arrive_expect_tx(&s_bar[0], 3 * kStageBytes + kBoxBytes + kTrBytesS);
       tma_load_1d(&s_box[0], a.tile_box + s_begin / kTS, kBoxBytes, &s_bar[0]);
+      if constexpr (BGONLY) tma_load_1d(&s_tr[0], a.tile_trange + s_begin / kTS, kTrBytesS, &s_bar[0]);
       tma_load_1d(s_src[0][0], a.xs + s_begin, kStageBytes, &s_bar[0]);
       tma_load_1d(s_src[0][1], a.ys + s_begin, kStageBytes, &s_bar[0]);
-      tma_load_1d(s_src[0][2], a.t + s_begin, kStageBytes, &s_bar[0]);
+      tma_load_1d(s_src[0][2], src_t + s_begin, kStageBytes, &s_bar[0]);
     }
     for (int s = 0; s < nst; ++s) {
       const int buf = s & 1;
@@ -1031,11 +1063,12 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
       if (tid == 0 && s + 1 < nst) {
         const int nb = buf ^ 1;
         const int64_t s0n = s_begin + static_cast<int64_t>(s + 1) * kTS;
-        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes + kBoxBytes);
+        mbar_arrive_expect_tx(&s_bar[nb], 3 * kStageBytes + kBoxBytes + kTrBytesS);
         tma_load_1d(&s_box[nb], a.tile_box + s0n / kTS, kBoxBytes, &s_bar[nb]);
+        if constexpr (BGONLY) tma_load_1d(&s_tr[nb], a.tile_trange + s0n / kTS, kTrBytesS, &s_bar[nb]);
         tma_load_1d(s_src[nb][0], a.xs + s0n, kStageBytes, &s_bar[nb]);
         tma_load_1d(s_src[nb][1], a.ys + s0n, kStageBytes, &s_bar[nb]);
-        tma_load_1d(s_src[nb][2], a.t + s0n, kStageBytes, &s_bar[nb]);
+        tma_load_1d(s_src[nb][2], src_t + s0n, kStageBytes, &s_bar[nb]);
       }
       const int64_t s0 = s_begin + static_cast<int64_t>(s) * kTS;
       const int cnt = static_cast<int>(min(static_cast<int64_t>(kTS), n - s0));
@@ -1044,7 +1077,8 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
       phase ^= 1u << buf;
       // stage metadata from the staged copy (no global-memory round trip)
       const double4 bs = s_box[buf];
-      const double smin = s_src[buf][2][0], smax = s_src[buf][2][cnt - 1];
+      const double smin = BGONLY ? s_tr[buf].x : s_src[buf][2][0];
+      const double smax = BGONLY ? s_tr[buf].y : s_src[buf][2][cnt - 1];
 
       const bool bg = !a.bg_off && !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
       int tr;
@@ -1062,18 +1096,27 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
       const double* sy = s_src[buf][1];
       const double* st = s_src[buf][2];
       const int col0 = warp * 32;
+      // BGONLY: row times relative to this stage's tile origin (scaled), so
+      // dts = tv - tsl_j; otherwise the raw times
+      double tsh[kSymR];
+      if constexpr (BGONLY) {
+        const double D = (tmin - smin) * a.stl;
+#pragma unroll
+        for (int r = 0; r < kSymR; ++r) tsh[r] = ti[r] + D;
+      }
+      const double(&tv)[kSymR] = BGONLY ? tsh : ti;
       auto pass = [&](bool pbg, int ptr) {
         if (diag) {
-          sym_dispatch<GRAD, false, true, true, BGONLY>(pbg, ptr, sx, sy, st, col0, cnt, xi, yi, ti,
+          sym_dispatch<GRAD, false, true, true, BGONLY>(pbg, ptr, sx, sy, st, col0, cnt, xi, yi, tv,
                                                         rv, a.k, s_tab, racc, s_col);
         } else if (rows_real < kTM) {
-          sym_dispatch<GRAD, true, true, true, BGONLY>(pbg, ptr, sx, sy, st, col0, cnt, xi, yi, ti,
+          sym_dispatch<GRAD, true, true, true, BGONLY>(pbg, ptr, sx, sy, st, col0, cnt, xi, yi, tv,
                                                        rv, a.k, s_tab, racc, s_col);
         } else if (safe) {
           sym_dispatch<GRAD, true, false, false, BGONLY>(pbg, ptr, sx, sy, st, col0, cnt, xi, yi,
-                                                         ti, rv, a.k, s_tab, racc, s_col);
+                                                         tv, rv, a.k, s_tab, racc, s_col);
         } else {
-          sym_dispatch<GRAD, true, true, false, BGONLY>(pbg, ptr, sx, sy, st, col0, cnt, xi, yi, ti,
+          sym_dispatch<GRAD, true, true, false, BGONLY>(pbg, ptr, sx, sy, st, col0, cnt, xi, yi, tv,
                                                         rv, a.k, s_tab, racc, s_col);
         }
       };
@@ -1116,9 +1159,15 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
         const int64_t col = s0 + jc;
 #pragma unroll
         for (int c = 0; c < NSC; ++c) {
+          double cv = s_col[jc * NSC + c], cq = a.fxq[c];
+          if constexpr (BGONLY && GRAD) {  // third sum: -(sum e * exponent) - S_Br = sum e dts^2
+            if (c == 2) {
+              cv = -cv - s_col[jc * NSC + 1];
+              cq = a.fxq[1];
+            }
+          }
           fx_add(a.fx + static_cast<size_t>(2 * c) * a.npad + col,
-                 a.fx + static_cast<size_t>(2 * c + 1) * a.npad + col,
-                 s_col[jc * NSC + c] * a.fxq[c]);
+                 a.fx + static_cast<size_t>(2 * c + 1) * a.npad + col, cv * cq);
         }
       }
       if (tid == 0) {
@@ -1156,13 +1205,21 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
       if (first + tid < n && !a.bg_off) {
 #pragma unroll
         for (int q = 0; q < NB; ++q) {
+          double rv_ = v[q], rq = a.fxq[q];
+          if constexpr (BGONLY && GRAD) {  // (as the column flush)
+            if (q == 2) {
+              rv_ = -v[2] - v[1];
+              rq = a.fxq[1];
+            }
+          }
           fx_add(a.fx + static_cast<size_t>(2 * q) * a.npad + first + tid,
-                 a.fx + static_cast<size_t>(2 * q + 1) * a.npad + first + tid, v[q] * a.fxq[q]);
+                 a.fx + static_cast<size_t>(2 * q + 1) * a.npad + first + tid, rv_ * rq);
         }
       }
     } else {
       store_row_sums<GRAD>(a, chunk, first + tid, v);
     }
+    if (a.trace && tid == 0) trace_item(a, item, nst, s_begin <= first && first < s_end, s_trace_t0);
   }
 
   if (tid == 0) {  // the last CTA out re-arms the work counter for the next launch
@@ -1229,10 +1286,12 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
   constexpr uint32_t kTrBytes = sizeof(double2);
 
   for (int iter = 0;; ++iter) {
-    if (tid == 0) s_item[iter & 1] = atomicAdd(a.work_counter, 1);
+    if (tid == 0) s_item[iter & 1] = next_item(a.work_counter, iter);
     __syncthreads();
     const int item = s_item[iter & 1];
     if (item >= n_items) break;
+    __shared__ unsigned long long s_trace_t0;  // (development trace: kept out of registers)
+    if (a.trace && tid == 0) s_trace_t0 = global_ns();
 
     const int2 it = a.items[item];
     const int tile = it.x, chunk = it.y;
@@ -1354,6 +1413,7 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
         out[static_cast<size_t>(q) * a.npad] = static_cast<double>(v[NB + q]) * tscale[q];
       }
     }
+    if (a.trace && tid == 0) trace_item(a, item, -1, 0, s_trace_t0);
   }
 
   if (tid == 0) {  // the last CTA out re-arms the work counter for the next launch
@@ -1464,6 +1524,11 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
     for (int a = 1; a <= kLoadAdj; ++a) {
       if (k >= a + 1) v[2 + a] = fmin(v[2 + a], tr.x - __ldcg(&trange[k - a - 1]).y);
     }
+#pragma unroll
+    for (int L = 0; L < kLoadSpan; ++L) {
+      const int64_t kl = k + (int64_t{1} << L) - 1;
+      if (kl < nt) v[3 + kLoadAdj + L] = fmin(v[3 + kLoadAdj + L], __ldcg(&trange[kl]).y - tr.x);
+    }
   }
 #pragma unroll
   for (int q = 0; q < kLoadStats; ++q) {
@@ -1512,6 +1577,7 @@ __global__ void prep_kernel(const PrepArgs a) {
     const double xv = a.x[i], yv = a.y[i];  // (the pad tail of x, y, t is zero)
     a.xs[i] = xv * a.sx;
     a.ys[i] = yv * a.sx;
+    if (a.tsl) a.tsl[i] = (a.t[i] - a.t[i - i % kTS]) * a.stl;
     if (a.xf) {
       a.xf[i] = static_cast<float>((xv - a.x[0]) * a.sxf);
       a.yf[i] = static_cast<float>((yv - a.y[0]) * a.sxf);

@@ -136,7 +136,44 @@ struct PairArgs {
   const int2* pre_items;
   const int* pre_n_items;
   int pre_sc;
+  // trigger-free kernel: tile-relative times scaled by stl = sqrt(-ctL), so
+  // the background exponent is -(r2 + dts^2) (one DFMA) and S_Bt is
+  // recovered per flush as -(sum e * exponent) - S_Br
+  const double* tsl;
+  double stl;
+  // development trace (nullptr: off): trace[0] counts entries, entry e at
+  // trace[4 + 4e ..]: (kernel << 48 | smid << 32 | item), (stages << 8 | diag),
+  // globaltimer at item start, at item end
+  unsigned long long* trace;
+  int trace_kernel;
+  int trace_cap;
 };
+
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned int sm_id() {
+  unsigned int r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void trace_item(const PairArgs& a, int item, int nst, int diag,
+                                           unsigned long long t0) {
+  const unsigned long long t1 = global_ns();
+  const unsigned long long e = atomicAdd(a.trace, 1ULL);
+  if (e < static_cast<unsigned long long>(a.trace_cap)) {
+    unsigned long long* p = a.trace + 4 + 4 * e;
+    p[0] = (static_cast<unsigned long long>(a.trace_kernel) << 48) |
+           (static_cast<unsigned long long>(sm_id()) << 32) | static_cast<unsigned int>(item);
+    p[1] = (static_cast<unsigned long long>(nst) << 8) | static_cast<unsigned>(diag);
+    p[2] = t0;
+    p[3] = t1;
+  }
+}
+#endif
 
 struct FinArgs {
   const double* t;
@@ -183,9 +220,13 @@ struct FinArgs {
 // Load-time statistics of an event set (tile_box_kernel, host-mapped):
 // [0] max |x - x[0]|, [1] max |y - y[0]|, [2] max time span of a 128-event
 // tile, [3 + k - 1] (k = 1..kLoadAdj) min over tiles of t[first] -
-// t[first - 128 k - 1] (the gap k stages ahead of a tile's first event).
+// t[first - 128 k - 1] (the gap k stages ahead of a tile's first event),
+// [3 + kLoadAdj + L] (L = 0..kLoadSpan-1) min over runs of 2^L consecutive
+// whole tiles of their time span (+inf: no such run): a time window shorter
+// than level L's span holds fewer than (2^L + 1) * 128 events.
 constexpr int kLoadAdj = 16;
-constexpr int kLoadStats = 3 + kLoadAdj;
+constexpr int kLoadSpan = 16;
+constexpr int kLoadStats = 3 + kLoadAdj + kLoadSpan;
 
 // Per-tile bounding boxes and time ranges, and the plan's search pivots
 // (PlanArgs::piv); also zeroes the pad tail [n, npad)
@@ -216,6 +257,9 @@ struct PrepArgs {
   unsigned long long* fx;
   double* comp;
   double window_end, tauT, omega;
+  // trigger-free kernel: tile-relative scaled times tsl = (t - t_tile0) * stl
+  double stl;
+  double* tsl;
 };
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);

@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
-from ctypes import byref, c_double, c_int, c_void_p
+from ctypes import byref, c_double, c_int, c_int64, c_void_p
 from typing import Optional, Sequence
 
 import numpy as np
@@ -237,6 +237,27 @@ class Engine:
         s = _lib.StatsStruct()
         self._check(self._lib.sthk_get_stats(self._h, byref(s)), "sthk_get_stats")
         return {name: getattr(s, name) for name, _ in _lib.StatsStruct._fields_}
+
+    def item_trace(self, slot: int = 0) -> np.ndarray:
+        """Development: the last evaluation's pair-kernel work items (needs
+        STHK_ITEM_TRACE=<entries> at engine creation), rows of (kernel, sm,
+        item, stages, diag, start_ns, end_ns)."""
+        cnt = c_int64()
+        self._check(self._lib.sthk_debug_item_trace(self._h, slot, None, 0, byref(cnt)),
+                    "sthk_debug_item_trace")
+        raw = np.zeros((cnt.value, 4), dtype=np.uint64)
+        if cnt.value:
+            self._check(self._lib.sthk_debug_item_trace(self._h, slot, raw.ctypes.data, cnt.value,
+                                                        byref(cnt)), "sthk_debug_item_trace")
+        out = np.zeros((len(raw), 7), dtype=np.int64)
+        out[:, 0] = (raw[:, 0] >> np.uint64(48)).astype(np.int64)
+        out[:, 1] = ((raw[:, 0] >> np.uint64(32)) & np.uint64(0xFFFF)).astype(np.int64)
+        out[:, 2] = (raw[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        out[:, 3] = (raw[:, 1] >> np.uint64(8)).astype(np.int64)
+        out[:, 4] = (raw[:, 1] & np.uint64(0xFF)).astype(np.int64)
+        out[:, 5] = raw[:, 2].astype(np.int64)
+        out[:, 6] = raw[:, 3].astype(np.int64)
+        return out
 
     def stream(self, slot: int = 0) -> int:
         p = c_void_p()

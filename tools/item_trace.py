@@ -1,0 +1,64 @@
+"""Per-item timeline of the pair kernels of one evaluation (development
+tool; needs STHK_ITEM_TRACE=<entries>): item durations by kernel, stage count
+and diagonal flag, the kernel spans, SM busy fraction and the tail.
+usage: STHK_ITEM_TRACE=200000 python tools/item_trace.py [N|c2] [post|init]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import paper_2005_10123_b200 as pk  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "c2"
+th = sys.argv[2] if len(sys.argv) > 2 else "post"
+theta = [0.66, 1.6, 14, 0.344, 1440, 0.0695] if th == "post" else [1, 1.6, 14, 0.1, 1, 1]
+if which == "c2":
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005, keep=85000)
+else:
+    n = int(which)
+    ev = pk.generateBenchmarkCloud(n, pk.SimWindow(0, 15, 0, 15, 4750), n)
+e = pk.Engine((0,))
+e.set_background_cache(False)
+e.set_timing(True)
+e.load(ev)
+e.set_params(theta)
+for _ in range(5):
+    e.loglik_grad()
+st = e.stats()
+tr = e.item_trace()
+print(f"{which} {th}: eval {st['eval_ms'] * 1e3:.1f} us, pair phase {st['pair_kernel_ms'] * 1e3:.1f} us, "
+      f"{len(tr)} items, far threshold A {st['far_threshold']:.2f} split {st['far_split_days']:.1f} d")
+t00 = tr[:, 5].min()
+names = {1: "general", 2: "trigger-free", 3: "far"}
+for k in (2, 1, 3):
+    m = tr[:, 0] == k
+    if not m.any():
+        continue
+    d = (tr[m, 6] - tr[m, 5]) / 1e3
+    s0, s1 = (tr[m, 5].min() - t00) / 1e3, (tr[m, 6].max() - t00) / 1e3
+    sms = len(np.unique(tr[m, 1]))
+    busy = d.sum() / (sms * (s1 - s0)) if s1 > s0 else 0
+    print(f"  {names[k]:12s} items {m.sum():5d} span {s0:7.1f}..{s1:7.1f} us  SMs {sms}  "
+          f"item us: mean {d.mean():6.2f} p50 {np.median(d):6.2f} max {d.max():6.2f}  "
+          f"sum {d.sum():8.1f} (per-SM busy {busy:.2f})")
+    for stg in np.unique(tr[m, 3]):
+        for dg in (0, 1):
+            mm = m & (tr[:, 3] == stg) & (tr[:, 4] == dg)
+            if mm.sum() == 0:
+                continue
+            dd = (tr[mm, 6] - tr[mm, 5]) / 1e3
+            print(f"      stages {stg:3d} diag {dg}: {mm.sum():5d} items, us mean {dd.mean():6.2f} "
+                  f"max {dd.max():6.2f}")
+    # tail: when do the last 10% of items end vs the first end
+    ends = np.sort(tr[m, 6] - t00) / 1e3
+    print(f"      ends: p10 {ends[len(ends) // 10]:.1f} p50 {ends[len(ends) // 2]:.1f} "
+          f"p90 {ends[9 * len(ends) // 10]:.1f} max {ends[-1]:.1f} us")
+# concurrency profile: items in flight per 2 us bin
+t1 = (tr[:, 6].max() - t00) / 1e3
+bins = np.arange(0, t1 + 2, 2.0)
+line = []
+for b in bins:
+    live = ((tr[:, 5] - t00) / 1e3 <= b + 1) & ((tr[:, 6] - t00) / 1e3 > b + 1)
+    line.append(int(live.sum()))
+print("  items in flight per 2 us:", line)

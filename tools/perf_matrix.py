@@ -34,4 +34,5 @@ for sc in scheds:
             ev_ms.append(st["eval_ms"])
             pk_ms.append(st["pair_kernel_ms"])
         print(f"{tag} sched={sc} {name} eval_ms={np.median(ev_ms):.4f} pair_ms={np.median(pk_ms):.4f} "
+              f"A={st['far_threshold']:.2f} tfar={st['far_split_days']:.1f} "
               f"ll={r[0]!r} g={r[2][0]!r}", flush=True)
