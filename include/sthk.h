@@ -172,6 +172,10 @@ typedef struct sthk_stats {
   double far_split_days;     /* its split tfar (sources further back run in FP32) */
 } sthk_stats;
 
+/* Timing and pair counters (sthk_get_stats): 0 off, 1 whole evaluation and
+ * pair phase (device events), 2 whole evaluation only (no events between the
+ * kernels: the one-shard evaluation graph keeps its kernel-to-kernel
+ * dependencies, as with timing off). */
 int sthk_set_timing(sthk_engine* e, int enable);
 int sthk_get_stats(sthk_engine* e, sthk_stats* out);
 /* cudaStream_t of local device slot `slot` (for event-based timing). */

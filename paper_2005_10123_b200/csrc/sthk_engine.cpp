@@ -187,11 +187,73 @@ enum class Xport {
   kHosted,  // rank engine with caller-supplied host callbacks (sthk_host_comm)
 };
 
+// One stream operation of an evaluation (graph mode records these and
+// replays them as a CUDA graph).
+struct GraphOp {
+  enum Kind : int { kKernel, kRecord, kRecordTimed, kWait, kMemset, kMemcpy } kind = kKernel;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev = nullptr;
+  const void* func = nullptr;
+  dim3 grid, block;
+  size_t smem = 0;
+  std::vector<unsigned char> args;
+  void* dst = nullptr;
+  const void* src = nullptr;
+  size_t bytes = 0;
+  int value = 0;
+  cudaMemcpyKind ckind = cudaMemcpyDefault;
+};
+
+struct OpSink final : sthk::LaunchSink {
+  std::vector<GraphOp>* ops;
+  explicit OpSink(std::vector<GraphOp>* o) : ops(o) {}
+  void launch(const void* func, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+              const void* args, size_t arg_bytes) override {
+    GraphOp op;
+    op.kind = GraphOp::kKernel;
+    op.st = st;
+    op.func = func;
+    op.grid = grid;
+    op.block = block;
+    op.smem = smem;
+    op.args.assign(static_cast<const unsigned char*>(args),
+                   static_cast<const unsigned char*>(args) + arg_bytes);
+    ops->push_back(std::move(op));
+  }
+};
+
+// An instantiated evaluation graph: its topology signature, the template
+// graph (owner of the kernel nodes) and the kernel nodes in issue order with
+// the arguments they were last set to.
+struct GraphEntry {
+  uint64_t sig = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaGraphNode_t> knodes;
+  std::vector<std::vector<unsigned char>> kargs;
+};
+
 struct sthk_engine {
   std::vector<Slot> slots;
   bool rank_mode = false;
   int rank = 0, world = 1;
   Xport xport = Xport::kSingle;
+  // One-shard evaluations are captured into a CUDA graph and launched as one
+  // (the instantiated graph is updated in place while its topology holds):
+  // one host submission instead of ~20 launch / event calls, and device-side
+  // dependencies between the kernels (development knob STHK_GRAPH=0: off).
+  bool use_graph = [] {
+    const char* v = std::getenv("STHK_GRAPH");
+    return !(v && *v == '0');
+  }();
+  bool recording = false;
+  std::vector<GraphOp> ops;    // the evaluation's stream operations, in issue order
+  OpSink sink{&ops};
+  // instantiated graphs by topology signature (an MH chain alternates a few
+  // evaluation shapes: finalize only, trigger sweep, full sweep), most
+  // recently used first
+  std::vector<GraphEntry> graphs;
+  int64_t graph_updates = 0, graph_instantiations = 0;
   sthk_host_comm hcomm{};
   int64_t exch_bytes = 0;  // fx bytes sent to other owners by the last evaluation
   int64_t launches = 0;    // kernels launched by the last evaluation (all slots)
@@ -202,6 +264,7 @@ struct sthk_engine {
   double p[6] = {0, 0, 0, 0, 0, 0};
   bool loaded = false, has_params = false;
   bool timing = false, dense = false;
+  bool timing_pairs = true;  // timing: also the pair-phase events (sthk_set_timing 1; 2: whole evaluation only)
   int mode = sthk::kSym;   // pair-kernel variant (sthk_set_kernel)
   bool far_tier = true;    // far tier of the symmetric kernel (sthk_set_far_tier)
   bool far_fp64 = false;   // ... its list evaluated by the FP64 kernel (same windows)
@@ -579,7 +642,17 @@ int chunks_target() {
   return v;
 }
 
+// Small event sets (N <= kOneStageChunkMaxN): one-stage chunks. With few row
+// tiles the pair kernels hold fewer items than CTA slots, so an evaluation
+// lasts as long as its longest item: measured N = 10k 80.8 -> 56 us, 20k
+// 97 -> 75 us per loglik+grad evaluation; neutral at 30-40k, slower from 50k.
+constexpr int64_t kOneStageChunkMaxN = 24 * 1024;
+
 int chunk_size(int64_t n, int64_t npad) {
+  static const bool target_set = std::getenv("STHK_CHUNKS_TARGET") != nullptr;
+  if (n <= kOneStageChunkMaxN && !target_set) {
+    return static_cast<int>(std::min<int64_t>(sthk::kTS, npad));
+  }
   const int64_t ct = chunks_target();
   int64_t sc = (n + ct - 1) / ct;
   sc = (sc + kTS - 1) / kTS * kTS;
@@ -967,8 +1040,237 @@ void combine_blocks(sthk_engine& e, int nb_total) {
   }
 }
 
+// Stream operations of an evaluation: issued directly, or recorded while
+// the engine builds / replays its evaluation graph.
+cudaError_t op_record(sthk_engine& e, cudaEvent_t ev, cudaStream_t st) {
+  if (!e.recording) return cudaEventRecord(ev, st);
+  GraphOp op;
+  op.kind = GraphOp::kRecord;
+  op.st = st;
+  op.ev = ev;
+  e.ops.push_back(std::move(op));
+  return cudaSuccess;
+}
+// (timing events: event-record nodes in a graph)
+cudaError_t record_timing(sthk_engine& e, cudaEvent_t ev, cudaStream_t st) {
+  if (!e.recording) return cudaEventRecord(ev, st);
+  GraphOp op;
+  op.kind = GraphOp::kRecordTimed;
+  op.st = st;
+  op.ev = ev;
+  e.ops.push_back(std::move(op));
+  return cudaSuccess;
+}
+cudaError_t op_wait(sthk_engine& e, cudaStream_t st, cudaEvent_t ev) {
+  if (!e.recording) return cudaStreamWaitEvent(st, ev, 0);
+  GraphOp op;
+  op.kind = GraphOp::kWait;
+  op.st = st;
+  op.ev = ev;
+  e.ops.push_back(std::move(op));
+  return cudaSuccess;
+}
+cudaError_t op_memset(sthk_engine& e, void* dst, int value, size_t bytes, cudaStream_t st) {
+  if (!e.recording) return cudaMemsetAsync(dst, value, bytes, st);
+  GraphOp op;
+  op.kind = GraphOp::kMemset;
+  op.st = st;
+  op.dst = dst;
+  op.value = value;
+  op.bytes = bytes;
+  e.ops.push_back(std::move(op));
+  return cudaSuccess;
+}
+cudaError_t op_memcpy(sthk_engine& e, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                      cudaStream_t st) {
+  if (!e.recording) return cudaMemcpyAsync(dst, src, bytes, kind, st);
+  GraphOp op;
+  op.kind = GraphOp::kMemcpy;
+  op.st = st;
+  op.dst = dst;
+  op.src = src;
+  op.bytes = bytes;
+  op.ckind = kind;
+  e.ops.push_back(std::move(op));
+  return cudaSuccess;
+}
+
+// Topology signature of a recorded evaluation: every operation's kind,
+// stream, event, and for kernels the function and launch shape, for copies
+// and memsets their operands (FNV-1a). Kernel arguments are not part of it:
+// they are updated in place on a matching graph.
+uint64_t ops_signature(const std::vector<GraphOp>& ops) {
+  uint64_t h = 1469598103934665603ULL;
+  auto mix = [&](uint64_t v) {
+    for (int b = 0; b < 8; ++b) {
+      h ^= (v >> (8 * b)) & 0xff;
+      h *= 1099511628211ULL;
+    }
+  };
+  mix(ops.size());
+  for (const GraphOp& op : ops) {
+    mix(static_cast<uint64_t>(op.kind));
+    mix(reinterpret_cast<uint64_t>(op.st));
+    mix(reinterpret_cast<uint64_t>(op.ev));
+    if (op.kind == GraphOp::kKernel) {
+      mix(reinterpret_cast<uint64_t>(op.func));
+      mix((static_cast<uint64_t>(op.grid.x) << 32) | op.block.x);
+      mix(op.smem);
+      mix(op.args.size());
+    } else if (op.kind == GraphOp::kMemset || op.kind == GraphOp::kMemcpy) {
+      mix(reinterpret_cast<uint64_t>(op.dst));
+      mix(reinterpret_cast<uint64_t>(op.src));
+      mix(op.bytes);
+      mix(static_cast<uint64_t>(op.value));
+      mix(static_cast<uint64_t>(op.ckind));
+    }
+  }
+  return h;
+}
+
+// The graph of a recorded operation list: a node per kernel, memset, copy and
+// timing-event record; dependencies follow stream order and event waits.
+GraphEntry build_graph(const std::vector<GraphOp>& ops) {
+  GraphEntry g;
+  ck(cudaGraphCreate(&g.graph, 0), "graph create");
+  try {
+    std::vector<std::pair<cudaStream_t, std::vector<cudaGraphNode_t>>> tail;
+    std::vector<std::pair<cudaEvent_t, std::vector<cudaGraphNode_t>>> evn;
+    auto tail_of = [&](cudaStream_t st) -> std::vector<cudaGraphNode_t>& {
+      for (auto& kv : tail) {
+        if (kv.first == st) return kv.second;
+      }
+      tail.push_back({st, {}});
+      return tail.back().second;
+    };
+    auto ev_of = [&](cudaEvent_t ev) -> std::vector<cudaGraphNode_t>& {
+      for (auto& kv : evn) {
+        if (kv.first == ev) return kv.second;
+      }
+      evn.push_back({ev, {}});
+      return evn.back().second;
+    };
+    for (const GraphOp& op : ops) {
+      std::vector<cudaGraphNode_t>& deps = tail_of(op.st);
+      cudaGraphNode_t nd = nullptr;
+      switch (op.kind) {
+        case GraphOp::kKernel: {
+          cudaKernelNodeParams kp{};
+          kp.func = const_cast<void*>(op.func);
+          kp.gridDim = op.grid;
+          kp.blockDim = op.block;
+          kp.sharedMemBytes = static_cast<unsigned>(op.smem);
+          void* argp = const_cast<unsigned char*>(op.args.data());
+          kp.kernelParams = &argp;
+          ck(cudaGraphAddKernelNode(&nd, g.graph, deps.data(), deps.size(), &kp), "graph kernel");
+          g.knodes.push_back(nd);
+          g.kargs.push_back(op.args);
+          break;
+        }
+        case GraphOp::kMemset: {
+          cudaMemsetParams mp{};
+          mp.dst = op.dst;
+          mp.value = static_cast<unsigned>(op.value);
+          mp.elementSize = 1;
+          mp.width = op.bytes;
+          mp.height = 1;
+          ck(cudaGraphAddMemsetNode(&nd, g.graph, deps.data(), deps.size(), &mp), "graph memset");
+          break;
+        }
+        case GraphOp::kMemcpy:
+          ck(cudaGraphAddMemcpyNode1D(&nd, g.graph, deps.data(), deps.size(), op.dst, op.src,
+                                      op.bytes, op.ckind),
+             "graph memcpy");
+          break;
+        case GraphOp::kRecordTimed:
+          ck(cudaGraphAddEventRecordNode(&nd, g.graph, deps.data(), deps.size(), op.ev),
+             "graph event");
+          break;
+        case GraphOp::kRecord:
+          ev_of(op.ev) = deps;
+          break;
+        case GraphOp::kWait: {
+          const std::vector<cudaGraphNode_t>& w = ev_of(op.ev);
+          for (cudaGraphNode_t x : w) {
+            if (std::find(deps.begin(), deps.end(), x) == deps.end()) deps.push_back(x);
+          }
+          break;
+        }
+      }
+      if (nd) {
+        deps.assign(1, nd);
+        if (op.kind == GraphOp::kRecordTimed) ev_of(op.ev) = deps;
+      }
+    }
+    ck(cudaGraphInstantiate(&g.exec, g.graph, 0), "graph instantiate");
+  } catch (...) {
+    cudaGraphDestroy(g.graph);
+    throw;
+  }
+  return g;
+}
+
+// End the recording of a one-shard evaluation and launch it: a graph of the
+// same topology gets the new kernel arguments in place (only those that
+// changed), else one is built, instantiated and kept (LRU, at most 16).
+void launch_recorded(sthk_engine& e, cudaStream_t st) {
+  constexpr size_t kMaxGraphs = 16;
+  e.recording = false;
+  sthk::set_launch_sink(nullptr);
+  const uint64_t sig = ops_signature(e.ops);
+  auto it = std::find_if(e.graphs.begin(), e.graphs.end(),
+                         [&](const GraphEntry& g) { return g.sig == sig; });
+  if (it != e.graphs.end()) {
+    std::rotate(e.graphs.begin(), it, it + 1);  // most recently used first
+    GraphEntry& g = e.graphs.front();
+    size_t k = 0;
+    for (const GraphOp& op : e.ops) {
+      if (op.kind != GraphOp::kKernel) continue;
+      if (op.args != g.kargs[k]) {
+        cudaKernelNodeParams kp{};
+        kp.func = const_cast<void*>(op.func);
+        kp.gridDim = op.grid;
+        kp.blockDim = op.block;
+        kp.sharedMemBytes = static_cast<unsigned>(op.smem);
+        void* argp = const_cast<unsigned char*>(op.args.data());
+        kp.kernelParams = &argp;
+        ck(cudaGraphExecKernelNodeSetParams(g.exec, g.knodes[k], &kp), "graph kernel update");
+        g.kargs[k] = op.args;
+      }
+      ++k;
+    }
+    ++e.graph_updates;
+  } else {
+    GraphEntry g = build_graph(e.ops);
+    g.sig = sig;
+    ++e.graph_instantiations;
+    if (e.graphs.size() >= kMaxGraphs) {
+      cudaGraphExecDestroy(e.graphs.back().exec);
+      cudaGraphDestroy(e.graphs.back().graph);
+      e.graphs.pop_back();
+    }
+    e.graphs.insert(e.graphs.begin(), std::move(g));
+  }
+  ck(cudaGraphLaunch(e.graphs.front().exec, st), "graph launch");
+}
+
+void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bool ex_to_host);
+
 void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
                   bool ex_to_host = true) {
+  try {
+    enqueue_eval_body(e, grad, want_pe, want_ex, ex_to_host);
+  } catch (...) {
+    if (e.recording) {  // nothing of the recorded evaluation was issued
+      e.recording = false;
+      e.ops.clear();
+      sthk::set_launch_sink(nullptr);
+    }
+    throw;
+  }
+}
+
+void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bool ex_to_host) {
   if (!e.loaded) throw NotLoaded("sthk: no events loaded");
   if (!e.has_params) throw NotLoaded("sthk: no parameters set");
   const int shards = e.rank_mode ? e.world : static_cast<int>(e.slots.size());
@@ -1090,9 +1392,30 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
     dev_grow(s.comp, s.comp_cap, static_cast<size_t>(4) * e.npad);
     if (want_pe) dev_grow(s.per_event, s.pe_cap, static_cast<size_t>(e.npad));
     if (want_ex) dev_grow(s.ex, s.ex_cap, static_cast<size_t>(3) * e.npad);
+    if (sym && bg_split) dev_grow(s.tsl, s.tsl_cap, static_cast<size_t>(e.npad));
+    if (want_pe && s.h_pe_cap < static_cast<size_t>(e.npad)) {
+      if (s.h_per_event) ck(cudaFreeHost(s.h_per_event), "cudaFreeHost");
+      s.h_per_event = nullptr;
+      ck(cudaMallocHost(&s.h_per_event, sizeof(double) * e.npad), "cudaMallocHost");
+      s.h_pe_cap = static_cast<size_t>(e.npad);
+    }
+    if (want_ex && ex_to_host && s.h_ex_cap < static_cast<size_t>(3 * e.npad)) {
+      if (s.h_ex) ck(cudaFreeHost(s.h_ex), "cudaFreeHost");
+      s.h_ex = nullptr;
+      ck(cudaMallocHost(&s.h_ex, sizeof(double) * 3 * e.npad), "cudaMallocHost");
+      s.h_ex_cap = static_cast<size_t>(3 * e.npad);
+    }
 
     cudaStream_t st = s.stream;
-    if (e.timing) ck(cudaEventRecord(s.ev[0], st), "event");
+    // (one shard: every stream operation from here on is recorded and
+    // replayed as the evaluation graph)
+    if (e.use_graph && e.xport == Xport::kSingle && e.slots.size() == 1 && !e.recording) {
+      e.ops.clear();
+      e.recording = true;
+      sthk::set_launch_sink(&e.sink);
+    }
+    if (e.timing) ck(record_timing(e, s.ev[0], st), "event");
+    if (s.trace) ck(op_memset(e, s.trace, 0, sizeof(unsigned long long), st), "memset");
     // (pair counters, timing only, are zero here: the final kernel of the
     // previous timed evaluation re-zeroed them after copying them out)
     // one prep pass on stream 2, beside the plan (stream 1): scaled / FP32
@@ -1108,7 +1431,6 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
       pr.xs = s.xs;
       pr.ys = s.ys;
       if (bg_split) {
-        dev_grow(s.tsl, s.tsl_cap, static_cast<size_t>(e.npad));
         pr.tsl = s.tsl;
         pr.stl = pl.stl;
       }
@@ -1127,36 +1449,39 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
       pr.tauT = p[2];
       pr.omega = p[4];
     }
+    pr.trace = s.trace;
+    pr.trace_cap = item_trace_cap();
     if (pr.xs || pr.fx || pr.comp) {  // (launched right after the plan, see below)
-      ck(cudaEventRecord(s.fork, st), "event");
+      ck(op_record(e, s.fork, st), "event");
       prep_unlaunched = true;
     }
     if (shards > 1) {
-      ck(cudaMemsetAsync(s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
+      ck(op_memset(e, s.block_partial, 0, sizeof(double) * nb_total * kNOut, st), "memset");
     }
     // The plan kernel goes first: its few CTAs take whole SMs (1024 threads,
     // the full register file) before the prep pass spreads over the rest, so
     // the plan's latency-bound searches do not queue behind prep traffic.
     auto launch_prep_now = [&] {
       if (!prep_unlaunched) return;
-      ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
+      ck(op_wait(e, s.stream2, s.fork), "wait");
       ck(sthk::launch_prep(pr, s.stream2), "prep");
       e.launches += 1;
-      ck(cudaEventRecord(s.prepped, s.stream2), "event");
+      ck(op_record(e, s.prepped, s.stream2), "event");
       prep_unlaunched = false;
       prep_pending = true;
     };
     auto join_prep = [&] {
       if (!prep_pending) return;
-      ck(cudaStreamWaitEvent(st, s.prepped, 0), "wait");
+      ck(op_wait(e, st, s.prepped), "wait");
       prep_pending = false;
     };
     if (ntiles == 0 || tr_cached) {
       launch_prep_now();
       join_prep();
-      ck(cudaEventRecord(s.ev[1], st), "event");
-      if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
-      ck(cudaEventRecord(s.pairs_done, st), "event");
+      ck(e.timing && e.timing_pairs ? record_timing(e, s.ev[1], st) : op_record(e, s.ev[1], st),
+         "event");
+      if (e.timing && e.timing_pairs) ck(record_timing(e, s.ev[2], st), "event");
+      ck(op_record(e, s.pairs_done, st), "event");
       continue;  // (tr_cached: every pair sum is cached, finalize only)
     }
     sthk::PlanArgs pa{};
@@ -1179,6 +1504,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
     pa.n_items = s.scalars;
     pa.work_counter = s.scalars + 1;
     pa.tfar = far_on ? pl.tfar : 0.0;
+    pa.trace = s.trace;
+    pa.trace_cap = item_trace_cap();
     // far list start: the far tier's cull window (trigger-only sweeps: trigger only)
     // (only with a far list: its window then keys the plan cache)
     pa.dFar = !far_on ? 0.0 : cached ? pl.k.dTf : std::max(pl.k.dBf, pl.k.dTf);
@@ -1244,7 +1571,6 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
     if (sym) qa.fxq[1] = fxq[1] / (pl.sx * pl.sx);  // S_Br accumulates sx^2 r^2
     qa.pair_counts = e.timing ? s.pair_counts : nullptr;
     if (s.trace) {
-      ck(cudaMemsetAsync(s.trace, 0, sizeof(unsigned long long), st), "memset");
       qa.trace = s.trace;
       qa.trace_cap = item_trace_cap();
       qa.trace_kernel = 1;
@@ -1280,7 +1606,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
     // timing event here, between the prep join and the far fork, measurably
     // lets the near kernel's CTAs reach the SMs ahead of the far kernel's
     // (C2, Θ_post: 0.472 -> 0.444 ms with timing off; no effect at Θ_init)
-    ck(cudaEventRecord(s.ev[1], st), "event");
+    // (an event-record node in graph mode too: it has the same effect there)
+    ck(record_timing(e, s.ev[1], st), "event");
     if (far_on) {  // the far work list in FP32
       sthk::PairArgs fa_ = qa;
       fa_.pre_items = nullptr;
@@ -1306,9 +1633,9 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
       };
       if (conc && e.pair_order > 0 && bg_split && !e.merge_bg) {
         // three streams: trigger-free (st), general (stream3), far (stream2)
-        ck(cudaEventRecord(s.fork, st), "event");
-        ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
-        ck(cudaStreamWaitEvent(s.stream3, s.fork, 0), "wait");
+        ck(op_record(e, s.fork, st), "event");
+        ck(op_wait(e, s.stream2, s.fork), "wait");
+        ck(op_wait(e, s.stream3, s.fork), "wait");
         if (e.pair_order == 2) {
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, s.stream3), "pair kernel");
           launch_bg();
@@ -1319,13 +1646,13 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
         e.launches += 1;
         ck(launch_far_list(s.sms * e.far_ctas, s.stream2), "far kernel");
         e.launches += 1;
-        ck(cudaEventRecord(s.join, s.stream2), "event");
-        ck(cudaEventRecord(s.join3, s.stream3), "event");
-        ck(cudaStreamWaitEvent(st, s.join, 0), "wait");
-        ck(cudaStreamWaitEvent(st, s.join3, 0), "wait");
+        ck(op_record(e, s.join, s.stream2), "event");
+        ck(op_record(e, s.join3, s.stream3), "event");
+        ck(op_wait(e, st, s.join), "wait");
+        ck(op_wait(e, st, s.join3), "wait");
       } else if (conc) {  // forked onto the second stream, joined before finalize
-        ck(cudaEventRecord(s.fork, st), "event");
-        ck(cudaStreamWaitEvent(s.stream2, s.fork, 0), "wait");
+        ck(op_record(e, s.fork, st), "event");
+        ck(op_wait(e, s.stream2, s.fork), "wait");
         if (e.far_order == 2 || e.pair_order > 0) {  // near first: its CTAs are resident before far CTAs fill in
           launch_bg();
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
@@ -1339,8 +1666,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
           e.launches += 1;
         }
-        ck(cudaEventRecord(s.join, s.stream2), "event");
-        ck(cudaStreamWaitEvent(st, s.join, 0), "wait");
+        ck(op_record(e, s.join, s.stream2), "event");
+        ck(op_wait(e, st, s.join), "wait");
       } else {
         launch_bg();
         ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
@@ -1353,8 +1680,8 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
       ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
       e.launches += 1;
     }
-    if (e.timing) ck(cudaEventRecord(s.ev[2], st), "event");
-    ck(cudaEventRecord(s.pairs_done, st), "event");
+    if (e.timing && e.timing_pairs) ck(record_timing(e, s.ev[2], st), "event");
+    ck(op_record(e, s.pairs_done, st), "event");
   }
 
   // phase 2: symmetric sweeps add column sums to earlier rows, some owned by
@@ -1411,10 +1738,12 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
       fa.counts_out = s.d_hcounts;
       fa.nblocks_total = nb_total;
       fa.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 3);
+      fa.trace = s.trace;
+      fa.trace_cap = item_trace_cap();
       ck(sthk::launch_finalize(fa, grad, s.stream), "finalize");
       e.launches += 1;
     }
-    ck(cudaEventRecord(s.fin_done, s.stream), "event");
+    ck(op_record(e, s.fin_done, s.stream), "event");
   }
 
   // phase 4: exact combination of the block partials, fixed-order final sum
@@ -1425,28 +1754,19 @@ void enqueue_eval(sthk_engine& e, bool grad, bool want_pe, bool want_ex = false,
     cudaStream_t st = s.stream;
     if (!e.timing) std::fill(s.h_counts, s.h_counts + sthk::kNCounts, 0ULL);
     if (want_pe && s.row1 > s.row0) {
-      if (s.h_pe_cap < static_cast<size_t>(e.npad)) {
-        if (s.h_per_event) ck(cudaFreeHost(s.h_per_event), "cudaFreeHost");
-        ck(cudaMallocHost(&s.h_per_event, sizeof(double) * e.npad), "cudaMallocHost");
-        s.h_pe_cap = static_cast<size_t>(e.npad);
-      }
-      ck(cudaMemcpyAsync(s.h_per_event + s.row0, s.per_event + s.row0,
+      ck(op_memcpy(e, s.h_per_event + s.row0, s.per_event + s.row0,
                          sizeof(double) * (s.row1 - s.row0), cudaMemcpyDeviceToHost, st),
          "D2H");
     }
     if (want_ex && ex_to_host && s.row1 > s.row0) {
-      if (s.h_ex_cap < static_cast<size_t>(3 * e.npad)) {
-        if (s.h_ex) ck(cudaFreeHost(s.h_ex), "cudaFreeHost");
-        ck(cudaMallocHost(&s.h_ex, sizeof(double) * 3 * e.npad), "cudaMallocHost");
-        s.h_ex_cap = static_cast<size_t>(3 * e.npad);
-      }
       for (int k = 0; k < 3; ++k) {
-        ck(cudaMemcpyAsync(s.h_ex + k * e.npad + s.row0, s.ex + k * e.npad + s.row0,
+        ck(op_memcpy(e, s.h_ex + k * e.npad + s.row0, s.ex + k * e.npad + s.row0,
                            sizeof(double) * (s.row1 - s.row0), cudaMemcpyDeviceToHost, st),
            "D2H");
       }
     }
-    if (e.timing) ck(cudaEventRecord(s.ev[3], st), "event");
+    if (e.timing) ck(record_timing(e, s.ev[3], st), "event");
+    if (e.recording) launch_recorded(e, st);
   }
   e.pending = true;
   e.last_grad = grad;
@@ -1685,6 +2005,14 @@ int sthk_create_rank_hosted(int device, int rank, int world, const sthk_host_com
 
 int sthk_destroy(sthk_engine* e) {
   if (!e) return STHK_EINVAL;
+  if (!e->graphs.empty()) {
+    cudaSetDevice(e->slots[0].dev);
+    cudaStreamSynchronize(e->slots[0].stream);
+    for (auto& g : e->graphs) {
+      cudaGraphExecDestroy(g.exec);
+      cudaGraphDestroy(g.graph);
+    }
+  }
   for (auto& s : e->slots) free_slot(s);
   delete e;
   return STHK_OK;
@@ -1965,7 +2293,11 @@ int sthk_loglik_batch(sthk_engine* e, const double* params, int64_t P, double* l
 }
 
 int sthk_set_timing(sthk_engine* e, int enable) {
-  return guarded(e, [&] { e->timing = enable != 0; });
+  return guarded(e, [&] {
+    if (enable < 0 || enable > 2) throw InvalidArg("sthk_set_timing: enable must be 0, 1 or 2");
+    e->timing = enable != 0;
+    e->timing_pairs = enable == 1;
+  });
 }
 
 int sthk_set_dense(sthk_engine* e, int dense) {
@@ -2100,7 +2432,7 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
       if (e->timing && s.row1 > s.row0) {
         float a = 0, b = 0;
         set_dev(s);
-        if (cudaEventElapsedTime(&a, s.ev[1], s.ev[2]) == cudaSuccess) {
+        if (e->timing_pairs && cudaEventElapsedTime(&a, s.ev[1], s.ev[2]) == cudaSuccess) {
           out->pair_kernel_ms = std::max(out->pair_kernel_ms, static_cast<double>(a));
         }
         if (cudaEventElapsedTime(&b, s.ev[0], s.ev[3]) == cudaSuccess) {

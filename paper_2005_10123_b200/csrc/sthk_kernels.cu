@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   __shared__ __align__(8) uint64_t s_bar;
   extern __shared__ __align__(128) double s_piv[];  // kPivots (dynamic: 64 KB)
   const int tid = threadIdx.x;
+  const unsigned long long trace_t0 = (a.trace && tid == 0) ? global_ns() : 0ULL;
   const int ntiles = a.tile1 - a.tile0;
   Pivots pv;
   pv.stride = pivot_stride(a.n);
@@ -352,6 +353,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   const int2 mrg[kPlanLists] = {my[0], my[2], my[4]};
   const int2 mcr[kPlanLists] = {my[1], my[3], my[5]};
   plan_lists(a, pl, on, mrg, mcr, s_hist, s_warp);
+  if (a.trace && tid == 0) trace_cta(a.trace, a.trace_cap, 4, trace_t0);
 }
 
 // ---------------------------------------------------------------------------
@@ -452,6 +454,8 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
   __shared__ int s_item[2];
 
   const int tid = threadIdx.x;
+  __shared__ unsigned long long s_cta_t0;  // (development trace)
+  if (a.trace && tid == 0) s_cta_t0 = global_ns();
   __shared__ __align__(8) uint64_t s_tbar;
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
@@ -562,6 +566,7 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
       *a.work_counter = 0;
       *a.done_counter = 0u;
     }
+    if (a.trace) trace_cta(a.trace, a.trace_cap, a.trace_kernel, s_cta_t0);
   }
   if (tid == 0 && a.pair_counts) {
     atomicAdd(&a.pair_counts[0], cBg);
@@ -977,6 +982,8 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  __shared__ unsigned long long s_cta_t0;  // (development trace)
+  if (a.trace && tid == 0) s_cta_t0 = global_ns();
   __shared__ __align__(8) uint64_t s_tbar;
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
@@ -1228,6 +1235,7 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
       *a.work_counter = 0;
       *a.done_counter = 0u;
     }
+    if (a.trace) trace_cta(a.trace, a.trace_cap, a.trace_kernel, s_cta_t0);
   }
   if (tid == 0 && a.pair_counts) {
     atomicAdd(&a.pair_counts[0], cBg);
@@ -1268,6 +1276,8 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
   __shared__ int s_item[2];
 
   const int tid = threadIdx.x;
+  __shared__ unsigned long long s_cta_t0;  // (development trace)
+  if (a.trace && tid == 0) s_cta_t0 = global_ns();
   const int lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
@@ -1422,6 +1432,7 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
       *a.work_counter = 0;
       *a.done_counter = 0u;
     }
+    if (a.trace) trace_cta(a.trace, a.trace_cap, a.trace_kernel, s_cta_t0);
   }
   if (tid == 0 && a.pair_counts) {
     atomicAdd(&a.pair_counts[0], cBg);
@@ -1573,6 +1584,7 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
 __global__ void prep_kernel(const PrepArgs a) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= a.npad) return;
+  const unsigned long long trace_t0 = (a.trace && threadIdx.x == 0) ? global_ns() : 0ULL;
   if (a.xs) {
     const double xv = a.x[i], yv = a.y[i];  // (the pad tail of x, y, t is zero)
     a.xs[i] = xv * a.sx;
@@ -1603,6 +1615,7 @@ __global__ void prep_kernel(const PrepArgs a) {
     // exp(-omega D) directly: 1 + expm1 cancels when omega D is large
     a.comp[3 * a.npad + i] = D * exp(-a.omega * D);
   }
+  if (a.trace && threadIdx.x == 0) trace_cta(a.trace, a.trace_cap, 5, trace_t0);
 }
 
 // exp_l on a vector of natural-unit exponents (accuracy tests; the argument
@@ -1650,6 +1663,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
   constexpr int NT = NS - NB;
   __shared__ double s_red[kNOut][kFinThreads];
   const int tid = threadIdx.x;
+  __shared__ unsigned long long s_cta_t0;  // (development trace)
+  if (a.trace && tid == 0) s_cta_t0 = global_ns();
   const int64_t base = static_cast<int64_t>(a.row0) + static_cast<int64_t>(blockIdx.x) * kFB;
   double acc[kNOut];
 #pragma unroll
@@ -1770,6 +1785,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
       if (tid == 0) *a.done_counter = 0u;
     }
   }
+  if (a.trace && tid == 0) trace_cta(a.trace, a.trace_cap, 6, s_cta_t0);
 }
 
 __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict__ bp,
@@ -1809,6 +1825,25 @@ __global__ void __launch_bounds__(256) pi_accumulate_kernel(const double* __rest
 
 }  // namespace
 
+namespace {
+thread_local LaunchSink* t_sink = nullptr;
+
+// One single-struct-argument kernel launch, to the sink when one is set.
+template <typename A>
+cudaError_t launch_one(void (*kernel)(A), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       const A& args) {
+  if (t_sink) {
+    t_sink->launch(reinterpret_cast<const void*>(kernel), grid, block, smem, stream, &args,
+                   sizeof(A));
+    return cudaSuccess;
+  }
+  kernel<<<grid, block, smem, stream>>>(args);
+  return cudaGetLastError();
+}
+}  // namespace
+
+void set_launch_sink(LaunchSink* sink) { t_sink = sink; }
+
 cudaError_t launch_pi_accumulate(const double* ex, int64_t npad, int row0, int row1,
                                  double* sum_pi, int* bad, cudaStream_t stream) {
   if (row1 <= row0) return cudaSuccess;
@@ -1838,8 +1873,8 @@ cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_
 }
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t stream) {
-  prep_kernel<<<static_cast<unsigned>((a.npad + 255) / 256), 256, 0, stream>>>(a);
-  return cudaGetLastError();
+  return launch_one(prep_kernel, dim3(static_cast<unsigned>((a.npad + 255) / 256)), dim3(256), 0,
+                    stream, a);
 }
 
 cudaError_t launch_exp_probe(const double* x, int64_t n, double* out, cudaStream_t stream) {
@@ -1851,8 +1886,7 @@ cudaError_t launch_exp_probe(const double* x, int64_t n, double* out, cudaStream
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
   const int ntiles = a.tile1 - a.tile0;
   if (ntiles <= 0) return cudaSuccess;
-  plan_kernel<<<1, 1024, kPivots * sizeof(double), stream>>>(a);
-  return cudaGetLastError();
+  return launch_one(plan_kernel, dim3(1), dim3(1024), kPivots * sizeof(double), stream, a);
 }
 
 // The exp table (pair kernels) and the search pivots (plan) live in dynamic
@@ -1880,22 +1914,20 @@ cudaError_t prepare_pair_kernels() {
 
 cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaStream_t stream) {
   if (mode == kSym) {
-    if (grad) sym_kernel<true><<<grid, kTM, kTabBytes, stream>>>(a);
-    else sym_kernel<false><<<grid, kTM, kTabBytes, stream>>>(a);
+    return grad ? launch_one(sym_kernel<true>, dim3(grid), dim3(kTM), kTabBytes, stream, a)
+                : launch_one(sym_kernel<false>, dim3(grid), dim3(kTM), kTabBytes, stream, a);
   } else {
-    if (grad) pair_kernel<true><<<grid, kTM, kTabBytes, stream>>>(a);
-    else pair_kernel<false><<<grid, kTM, kTabBytes, stream>>>(a);
+    return grad ? launch_one(pair_kernel<true>, dim3(grid), dim3(kTM), kTabBytes, stream, a)
+                : launch_one(pair_kernel<false>, dim3(grid), dim3(kTM), kTabBytes, stream, a);
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream) {
   const int nblocks = (a.row1 - a.row0 + kFB - 1) / kFB;
   if (nblocks <= 0) return cudaSuccess;
   static_assert(kFinThreads == 256, "fused final sum uses the 256-thread final_sum_block");
-  if (grad) finalize_kernel<true><<<nblocks, kFinThreads, 0, stream>>>(a);
-  else finalize_kernel<false><<<nblocks, kFinThreads, 0, stream>>>(a);
-  return cudaGetLastError();
+  return grad ? launch_one(finalize_kernel<true>, dim3(nblocks), dim3(kFinThreads), 0, stream, a)
+              : launch_one(finalize_kernel<false>, dim3(nblocks), dim3(kFinThreads), 0, stream, a);
 }
 
 cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,
@@ -1906,9 +1938,8 @@ cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* o
 }
 
 cudaError_t launch_bgonly(const PairArgs& a, bool grad, int grid, cudaStream_t stream) {
-  if (grad) sym_kernel<true, true><<<grid, kTM, kTabBytes, stream>>>(a);
-  else sym_kernel<false, true><<<grid, kTM, kTabBytes, stream>>>(a);
-  return cudaGetLastError();
+  return grad ? launch_one(sym_kernel<true, true>, dim3(grid), dim3(kTM), kTabBytes, stream, a)
+              : launch_one(sym_kernel<false, true>, dim3(grid), dim3(kTM), kTabBytes, stream, a);
 }
 
 int bgonly_kernel_occupancy(bool grad) {
@@ -1920,9 +1951,8 @@ int bgonly_kernel_occupancy(bool grad) {
 }
 
 cudaError_t launch_far(const PairArgs& a, bool grad, int grid, cudaStream_t stream) {
-  if (grad) far_kernel<true><<<grid, kTM, 0, stream>>>(a);
-  else far_kernel<false><<<grid, kTM, 0, stream>>>(a);
-  return cudaGetLastError();
+  return grad ? launch_one(far_kernel<true>, dim3(grid), dim3(kTM), 0, stream, a)
+              : launch_one(far_kernel<false>, dim3(grid), dim3(kTM), 0, stream, a);
 }
 
 int far_kernel_occupancy(bool grad) {

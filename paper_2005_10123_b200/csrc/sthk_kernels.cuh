@@ -97,6 +97,8 @@ struct PlanArgs {
   int2* items_bg;
   int* n_items_bg;
   int* work_counter_bg;
+  unsigned long long* trace;  // development trace (PairArgs::trace), nullptr: off
+  int trace_cap;
 };
 
 // Background sums (k = 0..2: S_B, S_Br, S_Bt) are fixed point,
@@ -160,6 +162,20 @@ __device__ __forceinline__ unsigned int sm_id() {
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
   return r;
 }
+// one entry per CTA (item field all ones): kernel id, SM, block, start, end
+__device__ __forceinline__ void trace_cta(unsigned long long* trace, int cap, int kernel,
+                                          unsigned long long t0) {
+  const unsigned long long t1 = global_ns();
+  const unsigned long long e = atomicAdd(trace, 1ULL);
+  if (e < static_cast<unsigned long long>(cap)) {
+    unsigned long long* p = trace + 4 + 4 * e;
+    p[0] = (static_cast<unsigned long long>(kernel) << 48) |
+           (static_cast<unsigned long long>(sm_id()) << 32) | 0xFFFFFFFFULL;
+    p[1] = static_cast<unsigned long long>(blockIdx.x) << 8;
+    p[2] = t0;
+    p[3] = t1;
+  }
+}
 __device__ __forceinline__ void trace_item(const PairArgs& a, int item, int nst, int diag,
                                            unsigned long long t0) {
   const unsigned long long t1 = global_ns();
@@ -214,7 +230,20 @@ struct FinArgs {
   // and re-zeroed for the next evaluation; nullptr: untouched
   unsigned long long* counts;
   unsigned long long* counts_out;
+  unsigned long long* trace;  // development trace (PairArgs::trace), nullptr: off
+  int trace_cap;
 };
+
+// Launch sink: while set (per host thread), the evaluation-path launch
+// wrappers (plan, prep, pair, trigger-free, far, finalize) hand their launch
+// to the sink instead of issuing it -- the engine records an evaluation's
+// kernels and replays them as a CUDA graph (sthk_engine.cpp).
+struct LaunchSink {
+  virtual void launch(const void* func, dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                      const void* args, size_t arg_bytes) = 0;
+  virtual ~LaunchSink() = default;
+};
+void set_launch_sink(LaunchSink* sink);
 
 // Launch wrappers (sthk_kernels.cu). All enqueue on `stream`.
 // Load-time statistics of an event set (tile_box_kernel, host-mapped):
@@ -260,6 +289,8 @@ struct PrepArgs {
   // trigger-free kernel: tile-relative scaled times tsl = (t - t_tile0) * stl
   double stl;
   double* tsl;
+  unsigned long long* trace;  // development trace (PairArgs::trace), nullptr: off
+  int trace_cap;
 };
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);

@@ -212,7 +212,8 @@ class Engine:
         self._check(self._lib.sthk_set_far_schedule(self._h, int(concurrent), near_ctas, far_ctas),
                     "sthk_set_far_schedule")
 
-    def set_timing(self, on: bool) -> None:
+    def set_timing(self, on: "bool | int") -> None:
+        """0 off, 1 whole evaluation + pair phase, 2 whole evaluation only."""
         self._check(self._lib.sthk_set_timing(self._h, int(on)), "sthk_set_timing")
 
     def set_dense(self, on: bool) -> None:

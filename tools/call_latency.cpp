@@ -75,6 +75,21 @@ int main(int argc, char** argv) {
       printf("raw 3 x H2D pinned + sync     %8.1f us/call\n", std::chrono::duration<double, std::micro>(a1 - a0).count() / reps);
       cudaFree(d);
     }
+    {  // host time of the enqueue alone (full evaluation, caches off), then the wait
+      double enq = 0, tot = 0;
+      for (int i = 0; i < reps; ++i) {
+        p[0] *= (i & 1) ? 1.0 / 1.01 : 1.01;
+        sthk_set_params(e, p);
+        auto b0 = std::chrono::steady_clock::now();
+        sthk_enqueue(e, 1, 0);
+        auto b1 = std::chrono::steady_clock::now();
+        sthk_result(e, &ll, &valid, g, nullptr);
+        auto b2 = std::chrono::steady_clock::now();
+        enq += std::chrono::duration<double, std::micro>(b1 - b0).count();
+        tot += std::chrono::duration<double, std::micro>(b2 - b0).count();
+      }
+      printf("enqueue host time (full eval) %8.1f us/call of %8.1f us\n", enq / reps, tot / reps);
+    }
     printf("load_events (pinned)         %8.1f us/call\n", std::chrono::duration<double, std::micro>(t1 - t0).count() / reps);
     printf("loglik_grad (caches off)     %8.1f us/call\n", std::chrono::duration<double, std::micro>(t2 - t1).count() / reps);
   }

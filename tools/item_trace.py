@@ -20,17 +20,24 @@ else:
     ev = pk.generateBenchmarkCloud(n, pk.SimWindow(0, 15, 0, 15, 4750), n)
 e = pk.Engine((0,))
 e.set_background_cache(False)
-e.set_timing(True)
+e.set_timing(os.environ.get("IT_TIMING", "1") == "1")
 e.load(ev)
 e.set_params(theta)
 for _ in range(5):
     e.loglik_grad()
 st = e.stats()
-tr = e.item_trace()
+raw = e.item_trace()
+cta = raw[raw[:, 2] == 0xFFFFFFFF]
+tr = raw[raw[:, 2] != 0xFFFFFFFF]
 print(f"{which} {th}: eval {st['eval_ms'] * 1e3:.1f} us, pair phase {st['pair_kernel_ms'] * 1e3:.1f} us, "
       f"{len(tr)} items, far threshold A {st['far_threshold']:.2f} split {st['far_split_days']:.1f} d")
-t00 = tr[:, 5].min()
-names = {1: "general", 2: "trigger-free", 3: "far"}
+t00 = raw[:, 5].min()
+names = {1: "general", 2: "trigger-free", 3: "far", 4: "plan", 5: "prep", 6: "finalize"}
+print("  kernel timeline (first CTA start .. last CTA end, us from the first start):")
+for k in sorted(set(cta[:, 0].tolist()), key=lambda k: cta[cta[:, 0] == k, 5].min()):
+    m = cta[:, 0] == k
+    print(f"    {names.get(k, k):12s} {(cta[m, 5].min() - t00) / 1e3:7.1f} .. {(cta[m, 6].max() - t00) / 1e3:7.1f}"
+          f"   ({m.sum()} CTAs)")
 for k in (2, 1, 3):
     m = tr[:, 0] == k
     if not m.any():
