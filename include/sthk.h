@@ -170,6 +170,8 @@ typedef struct sthk_stats {
   int64_t kernel_launches;   /* kernels the last evaluation launched (all devices) */
   double far_threshold;      /* far tier's threshold A of the last evaluation */
   double far_split_days;     /* its split tfar (sources further back run in FP32) */
+  int64_t graph_launches;    /* evaluations launched as a cached CUDA graph (updated in place) */
+  int64_t graph_builds;      /* evaluation graphs built and instantiated */
 } sthk_stats;
 
 /* Timing and pair counters (sthk_get_stats): 0 off, 1 whole evaluation and
@@ -177,6 +179,11 @@ typedef struct sthk_stats {
  * kernels: the one-shard evaluation graph keeps its kernel-to-kernel
  * dependencies, as with timing off). */
 int sthk_set_timing(sthk_engine* e, int enable);
+/* One-shard evaluations as CUDA graphs (default on): the evaluation's stream
+ * operations are recorded and replayed as one graph launch; a graph of the
+ * same topology is kept and its kernel arguments updated in place. Results
+ * are bitwise identical either way (same kernels, same order of sums). */
+int sthk_set_graphs(sthk_engine* e, int enable);
 int sthk_get_stats(sthk_engine* e, sthk_stats* out);
 /* cudaStream_t of local device slot `slot` (for event-based timing). */
 int sthk_get_stream(sthk_engine* e, int slot, void** stream);

@@ -46,6 +46,8 @@ class StatsStruct(ctypes.Structure):
         ("kernel_launches", c_int64),
         ("far_threshold", c_double),
         ("far_split_days", c_double),
+        ("graph_launches", c_int64),
+        ("graph_builds", c_int64),
     ]
 
 
@@ -84,6 +86,7 @@ SIGNATURES = [
     ("sthk_set_timing", c_int, [c_void_p, c_int]),
     ("sthk_get_stats", c_int, [c_void_p, POINTER(StatsStruct)]),
     ("sthk_get_stream", c_int, [c_void_p, c_int, POINTER(c_void_p)]),
+    ("sthk_set_graphs", c_int, [c_void_p, c_int]),
     ("sthk_debug_item_trace", c_int, [c_void_p, c_int, c_void_p, c_int64, POINTER(c_int64)]),
     ("sthk_set_dense", c_int, [c_void_p, c_int]),
     ("sthk_get_exchange_bytes", c_int, [c_void_p, POINTER(c_int64)]),

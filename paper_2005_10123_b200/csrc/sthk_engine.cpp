@@ -2300,6 +2300,10 @@ int sthk_set_timing(sthk_engine* e, int enable) {
   });
 }
 
+int sthk_set_graphs(sthk_engine* e, int enable) {
+  return guarded(e, [&] { e->use_graph = enable != 0; });
+}
+
 int sthk_set_dense(sthk_engine* e, int dense) {
   return guarded(e, [&] { e->dense = dense != 0; });
 }
@@ -2416,6 +2420,8 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
     out->world = e->world;
     out->source_chunk = e->last_sc;
     out->far_threshold = e->last_far_a;
+    out->graph_launches = e->graph_updates;
+    out->graph_builds = e->graph_instantiations;
     out->far_split_days = e->last_tfar;
     out->kernel_mode = e->mode;
     out->cache_hit = e->last_cache_hit ? 1 : 0;

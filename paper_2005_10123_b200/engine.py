@@ -216,6 +216,10 @@ class Engine:
         """0 off, 1 whole evaluation + pair phase, 2 whole evaluation only."""
         self._check(self._lib.sthk_set_timing(self._h, int(on)), "sthk_set_timing")
 
+    def set_graphs(self, on: bool) -> None:
+        """One-shard evaluations as cached CUDA graphs (default on)."""
+        self._check(self._lib.sthk_set_graphs(self._h, int(on)), "sthk_set_graphs")
+
     def set_dense(self, on: bool) -> None:
         self._check(self._lib.sthk_set_dense(self._h, int(on)), "sthk_set_dense")
 
