@@ -1606,8 +1606,12 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     // timing event here, between the prep join and the far fork, measurably
     // lets the near kernel's CTAs reach the SMs ahead of the far kernel's
     // (C2, Θ_post: 0.472 -> 0.444 ms with timing off; no effect at Θ_init)
-    // (an event-record node in graph mode too: it has the same effect there)
-    ck(record_timing(e, s.ev[1], st), "event");
+    // (an event-record node in graph mode too, where it has the same effect
+    // with a trigger-free list; without one -- small N -- the node only adds
+    // latency: measured 5 us at N = 10k)
+    ck((e.timing && e.timing_pairs) || bg_split ? record_timing(e, s.ev[1], st)
+                                                : op_record(e, s.ev[1], st),
+       "event");
     if (far_on) {  // the far work list in FP32
       sthk::PairArgs fa_ = qa;
       fa_.pre_items = nullptr;
