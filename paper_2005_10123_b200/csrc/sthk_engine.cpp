@@ -582,10 +582,52 @@ std::vector<int> plan_cuts(const std::vector<double>& ht, int64_t n, const doubl
 // most N sources, to < 2^-54 lambda -- invisible in FP64. The
 // boost is a whole number (trigger_boost), so the window (and with it the
 // trigger sums, cached per window) moves only in whole steps.
-void culling_windows(const double* p, int64_t n, double& dB, double& dT) {
+int64_t max_events_in_window(const std::vector<double>* span_min, int64_t n, double w);
+
+// Half-ulp cull exponents, tighter than C = ln N + 54 ln 2
+// wherever the load statistics bound the events per time window. Culled
+// terms lie beyond a time cut d; split that region into shells of width w:
+// each holds at most M(w) events per side (max_events_in_window), and the
+// exponent grows by at least a = d w / tauT^2 (background, Gaussian in dt)
+// or omega w (trigger, exponential) per shell, so the culled terms of one
+// event total at most K e^-z with K = sides * M(w) / (1 - e^-a). With
+// z = ln K + 54 ln 2 that is below half an ulp of S_B (and of lambda for the
+// trigger, after its boost). zb: background (two-sided), zt: trigger (earlier
+// sources only, before adding the boost); both <= C.
+void cull_exponents(const std::vector<double>* span, int64_t n, const double* p, double& zb,
+                    double& zt) {
+  const double ln2 = 0.693147180559945309417232121458176568;
+  const double zN = far_cull_exponent(n);
+  const double tt2 = p[2] * p[2];
+  auto kb = [&](double d) {  // background K at cut d, minimised over shell widths
+    double best = static_cast<double>(n);
+    for (int k = -3; k <= 6; ++k) {
+      const double w = std::ldexp(tt2 / d, k);
+      const double a = d * w / tt2;
+      const double m = static_cast<double>(max_events_in_window(span, n, w));
+      best = std::min(best, 2.0 * m / -std::expm1(-a));
+    }
+    return std::max(best, 1.0);
+  };
+  // candidate from the cut of C, then made valid at its own (shorter) cut:
+  // K only shrinks as the cut moves out, so max(z_c, ln K(d_c) + 54 ln 2) holds
+  const double zc = std::min(zN, std::log(kb(p[2] * std::sqrt(2.0 * zN))) + 54.0 * ln2);
+  zb = std::min(zN, std::max(zc, std::log(kb(p[2] * std::sqrt(2.0 * zc))) + 54.0 * ln2));
+  double kt = static_cast<double>(n);
+  for (int k = -3; k <= 6; ++k) {
+    const double w = std::ldexp(1.0 / p[4], k);
+    const double m = static_cast<double>(max_events_in_window(span, n, w));
+    kt = std::min(kt, m / -std::expm1(-p[4] * w));
+  }
+  zt = std::min(zN, std::log(std::max(kt, 1.0)) + 54.0 * ln2);
+}
+
+void culling_windows(const double* p, int64_t n, const std::vector<double>* span, double& dB,
+                     double& dT) {
   dB = p[2] * std::sqrt(2.0 * sthk::kCullExponent) * (1.0 + 1e-9);
-  const double zt = std::min(sthk::kCullExponent, far_cull_exponent(n) + trigger_boost(p));
-  dT = zt / p[4] * (1.0 + 1e-9);
+  double zb, zt;
+  cull_exponents(span, n, p, zb, zt);
+  dT = std::min(sthk::kCullExponent, zt + trigger_boost(p)) / p[4] * (1.0 + 1e-9);
 }
 
 int64_t lb(const std::vector<double>& t, int64_t n, double v) {
@@ -674,7 +716,9 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   EvalPlan pl;
   const double* p = e.p;
   double dB, dT;
-  culling_windows(p, e.n, dB, dT);
+  culling_windows(p, e.n, e.span_min, dB, dT);
+  double zb = 0.0, zt = 0.0;
+  cull_exponents(e.span_min, e.n, p, zb, zt);
   // exponent constants in L units (x 2048/ln2), see exp_l (sthk_device.cuh)
   const long double L = 2048.0L / 0.693147180559945309417232121458176568L;
   pl.k.cxL = static_cast<double>(-0.5L * L / (static_cast<long double>(p[1]) * p[1]));
@@ -709,7 +753,7 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
     // FP32 accumulation of at most one chunk of terms; A is the smallest value
     // in [kFarExponentMin, kFarExponent] keeping N e^-A eps <= kFarRowBound of
     // every row's S_B (1e-13: the loglik moves by < 3e-13 relative at C2).
-    const double zc = far_cull_exponent(e.n);
+    const double zc = std::max(zb, zt);
     const double u = std::ldexp(1.0, -24);
     const double dmax = std::sqrt(zc / kLn2);  // max |coordinate difference| of a far pair
     const double sxf = 1.0 / (p[1] * std::sqrt(2.0 * kLn2));
@@ -745,9 +789,8 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   // The same windows apply with culling off (dense), so dense == culled.
   {
     const double zf = 126.0 * kLn2 + 1.0;
-    const double zc = far_cull_exponent(e.n);
-    pl.k.dBf = p[2] * std::sqrt(2.0 * zc) * (1.0 + 1e-9);
-    pl.k.dTf = std::min(zf, zc + pl.boost) / p[4] * (1.0 + 1e-9);
+    pl.k.dBf = p[2] * std::sqrt(2.0 * zb) * (1.0 + 1e-9);
+    pl.k.dTf = std::min(zf, zt + pl.boost) / p[4] * (1.0 + 1e-9);
     // (never beyond the FP64 culling windows)
     pl.k.dBf = std::min(pl.k.dBf, pl.k.dB);
     pl.k.dTf = std::min(pl.k.dTf, pl.k.dT);
@@ -755,7 +798,7 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
     // C + boost > 126 ln 2 + 1 (the far kernel's exponent omits the boost):
     // then every live trigger source stays in the FP64 near list, and the far
     // tier carries background terms only (its trigger window dTf <= tfar).
-    if (zc + pl.boost > zf) pl.tfar = std::max(pl.tfar, dT * (1.0 + 1e-9));
+    if (zt + pl.boost > zf) pl.tfar = std::max(pl.tfar, dT * (1.0 + 1e-9));
   }
 
   // Chunk size: a function of N only (never of the parameters, the device
