@@ -74,10 +74,18 @@ constexpr double kInvSqrt2Pi = 0.3989422804014326779;   // kernels.hpp:13
 constexpr int kPivots = kPlanPivots;
 __device__ __forceinline__ int64_t pivot_stride(int64_t n) { return (n + kPivots - 1) / kPivots; }
 
+// Tile pivots (N <= kPivots * 128): piv[k] = the last time of 128-event tile
+// k, and a search answers at tile granularity -- the start of the tile that
+// holds the exact answer, in shared memory only. Every consumer rounds its
+// range starts down to whole 128-source stages, so this changes no stage set
+// (the row kernel's upper bound is rounded up instead: the extra sources lie
+// beyond the exact-underflow window, exact zeros). Larger N: strided pivots
+// piv[k] = t[k * stride] and log2(stride) global rounds to the exact index.
 struct Pivots {
   const double* piv;  // shared memory, np entries
   int np;
   int64_t stride;
+  bool tiles;
 };
 
 // K independent searches in lockstep. Result: the first index in [0, n) whose
@@ -99,6 +107,11 @@ __device__ __forceinline__ void bounds_lockstep(const double* t, int64_t n, cons
   }
 #pragma unroll
   for (int k = 0; k < K; ++k) kp[k] = before(k, p.piv[kPivots - 1]) ? kPivots : kp[k];
+  if (p.tiles) {  // the first tile with an event not before v starts at kp * 128
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = min(static_cast<int64_t>(kp[k]) * kTS, n);
+    return;
+  }
   int lo[K], hi[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {  // (kp == 0: t[0] is not before v)
@@ -156,10 +169,12 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
     lo = min(static_cast<int>(b[0]), static_cast<int>(first));
     hi = static_cast<int>(last + 1);
   } else {
-    // the tile's own rows are always live (background self term)
+    // the tile's own rows are always live (background self term); (tile
+    // pivots: the row kernel's end rounded up to the end of its tile)
     lo = min(static_cast<int>(b[0]), static_cast<int>(first));
+    const int64_t b1 = pv.tiles ? min(b[1] + kTS, a.n) : b[1];
     hi = a.sym ? static_cast<int>(last + 1)
-               : max(static_cast<int>(b[1]), static_cast<int>(last + 1));
+               : max(static_cast<int>(b1), static_cast<int>(last + 1));
   }
   // symmetric mode: later tiles reach this one through their column sums
   if (a.sym || a.trig_only) hi = static_cast<int>(last + 1);
@@ -199,6 +214,20 @@ __device__ __forceinline__ int item_stages(int sc, int2 rg, int chunk) {
 }
 
 constexpr int kPlanBins = 1024;  // item-size classes (stages, clamped)
+
+// atomicAdd(&hist[bin], 1) aggregated over the active lanes of the warp that
+// hit the same bin (one shared-memory atomic per distinct bin: most items of
+// a list share a few sizes); returns this lane's old-value slot.
+__device__ __forceinline__ int warp_agg_add(int* hist, int bin) {
+  const unsigned active = __activemask();
+  const unsigned same = __match_any_sync(active, bin);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(same) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(&hist[bin], __popc(same));
+  base = __shfl_sync(active, base, leader);
+  return base + __popc(same & ((1u << lane) - 1u));
+}
 
 // Single CTA: per-tile ranges, then the (tile, chunk) work list ordered by
 // decreasing item size (a counting sort on the stage count), so the
@@ -240,7 +269,7 @@ __device__ __forceinline__ void plan_lists(const PlanArgs& a, const PlanList (&p
       const int2 rg = i == tid ? my_rg[l] : pl[l].ranges[a.tile0 + i];
       const int2 cr = i == tid ? my_cr[l] : pl[l].crange[a.tile0 + i];
       for (int c = cr.x; c <= cr.y; ++c) {
-        atomicAdd(&s_hist[l][min(item_stages(pl[l].sc, rg, c), kPlanBins - 1)], 1);
+        warp_agg_add(&s_hist[l][0], min(item_stages(pl[l].sc, rg, c), kPlanBins - 1));
       }
     }
   }
@@ -286,7 +315,7 @@ __device__ __forceinline__ void plan_lists(const PlanArgs& a, const PlanList (&p
       const int2 rg = i == tid ? my_rg[l] : pl[l].ranges[tile];
       const int2 cr = i == tid ? my_cr[l] : pl[l].crange[tile];
       for (int ch = cr.x; ch <= cr.y; ++ch) {
-        const int pos = atomicAdd(&s_hist[l][min(item_stages(pl[l].sc, rg, ch), kPlanBins - 1)], 1);
+        const int pos = warp_agg_add(&s_hist[l][0], min(item_stages(pl[l].sc, rg, ch), kPlanBins - 1));
         pl[l].items[pos] = make_int2(tile, ch);
       }
     }
@@ -308,7 +337,8 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   const unsigned long long trace_t0 = (a.trace && tid == 0) ? global_ns() : 0ULL;
   const int ntiles = a.tile1 - a.tile0;
   Pivots pv;
-  pv.stride = pivot_stride(a.n);
+  pv.tiles = (a.n + kTS - 1) / kTS <= kPivots;
+  pv.stride = pv.tiles ? kTS : pivot_stride(a.n);
   pv.np = static_cast<int>((a.n + pv.stride - 1) / pv.stride);
   pv.piv = s_piv;
   if (tid == 0) {  // the pivots (precomputed at load): one bulk copy
@@ -319,6 +349,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   }
   __syncthreads();
   mbar_wait(&s_bar, 0);
+  if (a.trace && tid == 0) trace_cta(a.trace, a.trace_cap, 7, trace_t0);  // (phase: pivots staged)
   int2 my[6] = {make_int2(0, 0), make_int2(0, -1), make_int2(0, 0), make_int2(0, -1),
                 make_int2(0, 0), make_int2(0, -1)};  // first tile: near, far, bg (range, chunks)
   for (int i = tid; i < ntiles; i += 1024) {
@@ -344,6 +375,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
     }
   }
   __syncthreads();
+  if (a.trace && tid == 0) trace_cta(a.trace, a.trace_cap, 8, trace_t0);  // (phase: tile ranges)
   // fixed slots: 0 near, 1 far, 2 trigger-free (inactive lists are skipped)
   const PlanList pl[kPlanLists] = {
       PlanList{a.sc, a.ranges, a.crange, a.items, a.n_items, a.work_counter},
@@ -1461,9 +1493,11 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
   }
   // the plan's search pivots t[k * stride], +inf padded to kPivots
   {
-    const int64_t stride = pivot_stride(n), np = (n + stride - 1) / stride;
+    const bool tiles = (n + kTS - 1) / kTS <= kPivots;  // (see Pivots)
+    const int64_t stride = tiles ? kTS : pivot_stride(n), np = (n + stride - 1) / stride;
     for (int64_t k = gid; k < kPivots; k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-      piv[k] = k < np ? t[k * stride] : __longlong_as_double(0x7ff0000000000000LL);
+      piv[k] = k >= np ? __longlong_as_double(0x7ff0000000000000LL)
+                       : t[tiles ? min(k * kTS + kTS - 1, n - 1) : k * stride];
     }
   }
   // one warp per tile: 4 coalesced loads per lane, then a shuffle min/max
