@@ -164,6 +164,10 @@ struct Slot {
   double plan_tfar = 0, plan_dfar = 0;
   std::vector<std::pair<int, int>> runs;  // row ranges run on this slot
   unsigned long long* trace = nullptr;     // development item trace (STHK_ITEM_TRACE)
+  unsigned long long* tstamp = nullptr;    // kernel timing stamps [4] (graph-mode timing)
+  unsigned long long* h_tstamp = nullptr;  // pinned, device-mapped copy written by finalize
+  unsigned long long* d_htstamp = nullptr;
+  bool last_stamps = false;                // the last evaluation was timed by stamps
 };
 
 // (development knob: STHK_ITEM_TRACE=<entries> records every pair-kernel work
@@ -384,6 +388,15 @@ void init_slot(Slot& s, int dev) {
   ck(cudaMemset(s.scalars + 4, 0xff, sizeof(unsigned long long)), "memset");
   ck(cudaMalloc(&s.pair_counts, sthk::kNCounts * sizeof(unsigned long long)), "cudaMalloc");
   ck(cudaMemset(s.pair_counts, 0, sthk::kNCounts * sizeof(unsigned long long)), "memset");
+  {
+    const unsigned long long init[4] = {~0ULL, 0ULL, ~0ULL, 0ULL};
+    ck(cudaMalloc(&s.tstamp, sizeof(init)), "cudaMalloc");
+    ck(cudaMemcpy(s.tstamp, init, sizeof(init), cudaMemcpyHostToDevice), "H2D");
+    ck(cudaHostAlloc(&s.h_tstamp, sizeof(init), cudaHostAllocMapped | cudaHostAllocPortable),
+       "cudaHostAlloc");
+    ck(cudaHostGetDevicePointer(&s.d_htstamp, s.h_tstamp, 0), "cudaHostGetDevicePointer");
+    std::fill(s.h_tstamp, s.h_tstamp + 4, 0ULL);
+  }
   if (item_trace_cap() > 0) {
     ck(cudaMalloc(&s.trace, (4 + 4 * static_cast<size_t>(item_trace_cap())) * sizeof(unsigned long long)),
        "cudaMalloc");
@@ -431,13 +444,13 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.pair_counts), static_cast<void*>(s.tile_box),
                   static_cast<void*>(s.fx_stage), static_cast<void*>(s.pi_sum),
                   static_cast<void*>(s.pi_bad), static_cast<void*>(s.pi_rows),
-                  static_cast<void*>(s.trace)}) {
+                  static_cast<void*>(s.trace), static_cast<void*>(s.tstamp)}) {
     if (p) cudaFree(p);
   }
   for (void* p : {static_cast<void*>(s.h_out), static_cast<void*>(s.h_counts),
                   static_cast<void*>(s.h_bad), static_cast<void*>(s.h_stats),
                   static_cast<void*>(s.h_per_event), static_cast<void*>(s.h_ex),
-                  static_cast<void*>(s.h_pi_rows)}) {
+                  static_cast<void*>(s.h_pi_rows), static_cast<void*>(s.h_tstamp)}) {
     if (p) cudaFreeHost(p);
   }
   for (auto& e : s.ev) {
@@ -1405,8 +1418,13 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
   const bool need_comp = !(e.bg_cache && e.comp_valid && e.comp_gen == e.load_gen &&
                            e.comp_tt == p[2] && e.comp_om == p[4]);
   if (need_comp) e.comp_valid = false;  // re-armed once the prep pass is enqueued
+  // Timing in graph mode: kernel-side %globaltimer stamps instead of event
+  // nodes, which would sit between the kernels and add their latency.
+  const bool graph_mode = e.use_graph && e.xport == Xport::kSingle && e.slots.size() == 1;
+  const bool stamps = graph_mode && e.timing;
   // phase 1: zero the accumulators, plan and run the pair kernels per shard
   for (Slot& s : e.slots) {
+    s.last_stamps = stamps;
     bool prep_pending = false, prep_unlaunched = false;
     sthk::PrepArgs pr{};
     set_dev(s);
@@ -1452,12 +1470,12 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     cudaStream_t st = s.stream;
     // (one shard: every stream operation from here on is recorded and
     // replayed as the evaluation graph)
-    if (e.use_graph && e.xport == Xport::kSingle && e.slots.size() == 1 && !e.recording) {
+    if (graph_mode && !e.recording) {
       e.ops.clear();
       e.recording = true;
       sthk::set_launch_sink(&e.sink);
     }
-    if (e.timing) ck(record_timing(e, s.ev[0], st), "event");
+    if (e.timing && !stamps) ck(record_timing(e, s.ev[0], st), "event");
     if (s.trace) ck(op_memset(e, s.trace, 0, sizeof(unsigned long long), st), "memset");
     // (pair counters, timing only, are zero here: the final kernel of the
     // previous timed evaluation re-zeroed them after copying them out)
@@ -1494,6 +1512,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     }
     pr.trace = s.trace;
     pr.trace_cap = item_trace_cap();
+    pr.tstamp = stamps ? s.tstamp : nullptr;
     if (pr.xs || pr.fx || pr.comp) {  // (launched right after the plan, see below)
       ck(op_record(e, s.fork, st), "event");
       prep_unlaunched = true;
@@ -1521,9 +1540,10 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     if (ntiles == 0 || tr_cached) {
       launch_prep_now();
       join_prep();
-      ck(e.timing && e.timing_pairs ? record_timing(e, s.ev[1], st) : op_record(e, s.ev[1], st),
+      ck(e.timing && e.timing_pairs && !stamps ? record_timing(e, s.ev[1], st)
+                                                : op_record(e, s.ev[1], st),
          "event");
-      if (e.timing && e.timing_pairs) ck(record_timing(e, s.ev[2], st), "event");
+      if (e.timing && e.timing_pairs && !stamps) ck(record_timing(e, s.ev[2], st), "event");
       ck(op_record(e, s.pairs_done, st), "event");
       continue;  // (tr_cached: every pair sum is cached, finalize only)
     }
@@ -1549,6 +1569,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     pa.tfar = far_on ? pl.tfar : 0.0;
     pa.trace = s.trace;
     pa.trace_cap = item_trace_cap();
+    pa.tstamp = stamps ? s.tstamp : nullptr;
     // far list start: the far tier's cull window (trigger-only sweeps: trigger only)
     // (only with a far list: its window then keys the plan cache)
     pa.dFar = !far_on ? 0.0 : cached ? pl.k.dTf : std::max(pl.k.dBf, pl.k.dTf);
@@ -1613,6 +1634,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     for (int k = 0; k < sthk::kNSumGrad; ++k) qa.fxq[k] = fxq[k];
     if (sym) qa.fxq[1] = fxq[1] / (pl.sx * pl.sx);  // S_Br accumulates sx^2 r^2
     qa.pair_counts = e.timing ? s.pair_counts : nullptr;
+    qa.tstamp = stamps ? s.tstamp : nullptr;
     if (s.trace) {
       qa.trace = s.trace;
       qa.trace_cap = item_trace_cap();
@@ -1652,8 +1674,16 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     // (an event-record node in graph mode too, where it has the same effect
     // with a trigger-free list; without one -- small N -- the node only adds
     // latency: measured 5 us at N = 10k)
-    ck((e.timing && e.timing_pairs) || bg_split ? record_timing(e, s.ev[1], st)
-                                                : op_record(e, s.ev[1], st),
+    // (graph mode: without this node the far kernel's CTAs reach the SMs
+    // first and the near kernel starts 20 us later -- measured 4.5% slower at
+    // C2; graph node priorities do not change that order)
+    static const bool ev1_node = [] {  // (development knob STHK_EV1_NODE=0/1)
+      const char* v = std::getenv("STHK_EV1_NODE");
+      return !(v && *v == '0');
+    }();
+    ck((e.timing && e.timing_pairs && !stamps) || (bg_split && ev1_node)
+           ? record_timing(e, s.ev[1], st)
+           : op_record(e, s.ev[1], st),
        "event");
     if (far_on) {  // the far work list in FP32
       sthk::PairArgs fa_ = qa;
@@ -1727,7 +1757,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
       e.launches += 1;
     }
-    if (e.timing && e.timing_pairs) ck(record_timing(e, s.ev[2], st), "event");
+    if (e.timing && e.timing_pairs && !stamps) ck(record_timing(e, s.ev[2], st), "event");
     ck(op_record(e, s.pairs_done, st), "event");
   }
 
@@ -1787,6 +1817,8 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       fa.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 3);
       fa.trace = s.trace;
       fa.trace_cap = item_trace_cap();
+      fa.tstamp = stamps ? s.tstamp : nullptr;
+      fa.tstamp_out = s.d_htstamp;
       ck(sthk::launch_finalize(fa, grad, s.stream), "finalize");
       e.launches += 1;
     }
@@ -1812,7 +1844,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
            "D2H");
       }
     }
-    if (e.timing) ck(record_timing(e, s.ev[3], st), "event");
+    if (e.timing && !stamps) ck(record_timing(e, s.ev[3], st), "event");
     if (e.recording) launch_recorded(e, st);
   }
   e.pending = true;
@@ -2482,7 +2514,13 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
       out->exec_geom += static_cast<int64_t>(s.h_counts[4]);
       out->exec_sym += static_cast<int64_t>(s.h_counts[5]);
       out->exec_far += static_cast<int64_t>(s.h_counts[6]);
-      if (e->timing && s.row1 > s.row0) {
+      if (e->timing && s.row1 > s.row0 && s.last_stamps) {
+        const unsigned long long* h = s.h_tstamp;
+        if (h[1] > h[0]) out->eval_ms = std::max(out->eval_ms, (h[1] - h[0]) * 1e-6);
+        if (e->timing_pairs && h[3] > h[2]) {
+          out->pair_kernel_ms = std::max(out->pair_kernel_ms, (h[3] - h[2]) * 1e-6);
+        }
+      } else if (e->timing && s.row1 > s.row0) {
         float a = 0, b = 0;
         set_dev(s);
         if (e->timing_pairs && cudaEventElapsedTime(&a, s.ev[1], s.ev[2]) == cudaSuccess) {

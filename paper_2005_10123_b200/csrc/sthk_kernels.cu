@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   extern __shared__ __align__(128) double s_piv[];  // kPivots (dynamic: 64 KB)
   const int tid = threadIdx.x;
   const unsigned long long trace_t0 = (a.trace && tid == 0) ? global_ns() : 0ULL;
+  if (tid == 0) stamp_min(a.tstamp, 0);
   const int ntiles = a.tile1 - a.tile0;
   Pivots pv;
   pv.tiles = (a.n + kTS - 1) / kTS <= kPivots;
@@ -488,6 +489,10 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
   const int tid = threadIdx.x;
   __shared__ unsigned long long s_cta_t0;  // (development trace)
   if (a.trace && tid == 0) s_cta_t0 = global_ns();
+  if (tid == 0) {
+    stamp_min(a.tstamp, 0);
+    stamp_min(a.tstamp, 2);
+  }
   __shared__ __align__(8) uint64_t s_tbar;
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
@@ -599,6 +604,7 @@ __global__ void __launch_bounds__(kTM, STHK_PAIR_MINB) pair_kernel(const PairArg
       *a.done_counter = 0u;
     }
     if (a.trace) trace_cta(a.trace, a.trace_cap, a.trace_kernel, s_cta_t0);
+    stamp_max(a.tstamp, 3);
   }
   if (tid == 0 && a.pair_counts) {
     atomicAdd(&a.pair_counts[0], cBg);
@@ -1016,6 +1022,10 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
   const int lane = tid & 31, warp = tid >> 5;
   __shared__ unsigned long long s_cta_t0;  // (development trace)
   if (a.trace && tid == 0) s_cta_t0 = global_ns();
+  if (tid == 0) {
+    stamp_min(a.tstamp, 0);
+    stamp_min(a.tstamp, 2);
+  }
   __shared__ __align__(8) uint64_t s_tbar;
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
@@ -1268,6 +1278,7 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
       *a.done_counter = 0u;
     }
     if (a.trace) trace_cta(a.trace, a.trace_cap, a.trace_kernel, s_cta_t0);
+    stamp_max(a.tstamp, 3);
   }
   if (tid == 0 && a.pair_counts) {
     atomicAdd(&a.pair_counts[0], cBg);
@@ -1311,6 +1322,10 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
   __shared__ unsigned long long s_cta_t0;  // (development trace)
   if (a.trace && tid == 0) s_cta_t0 = global_ns();
   const int lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    stamp_min(a.tstamp, 0);
+    stamp_min(a.tstamp, 2);
+  }
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
@@ -1465,6 +1480,7 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
       *a.done_counter = 0u;
     }
     if (a.trace) trace_cta(a.trace, a.trace_cap, a.trace_kernel, s_cta_t0);
+    stamp_max(a.tstamp, 3);
   }
   if (tid == 0 && a.pair_counts) {
     atomicAdd(&a.pair_counts[0], cBg);
@@ -1619,6 +1635,7 @@ __global__ void prep_kernel(const PrepArgs a) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= a.npad) return;
   const unsigned long long trace_t0 = (a.trace && threadIdx.x == 0) ? global_ns() : 0ULL;
+  if (threadIdx.x == 0) stamp_min(a.tstamp, 0);
   if (a.xs) {
     const double xv = a.x[i], yv = a.y[i];  // (the pad tail of x, y, t is zero)
     a.xs[i] = xv * a.sx;
@@ -1699,6 +1716,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
   const int tid = threadIdx.x;
   __shared__ unsigned long long s_cta_t0;  // (development trace)
   if (a.trace && tid == 0) s_cta_t0 = global_ns();
+  if (tid == 0) stamp_min(a.tstamp, 0);
   const int64_t base = static_cast<int64_t>(a.row0) + static_cast<int64_t>(blockIdx.x) * kFB;
   double acc[kNOut];
 #pragma unroll
@@ -1815,6 +1833,11 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
       if (a.counts && tid < kNCounts) {
         a.counts_out[tid] = a.counts[tid];
         a.counts[tid] = 0ULL;
+      }
+      if (a.tstamp && tid < 4) {  // timing stamps out (mapped), re-armed for the next evaluation
+        const unsigned long long v = tid == 1 ? max(a.tstamp[1], global_ns()) : a.tstamp[tid];
+        a.tstamp_out[tid] = v;
+        a.tstamp[tid] = (tid & 1) ? 0ULL : ~0ULL;
       }
       if (tid == 0) *a.done_counter = 0u;
     }

@@ -99,6 +99,7 @@ struct PlanArgs {
   int* work_counter_bg;
   unsigned long long* trace;  // development trace (PairArgs::trace), nullptr: off
   int trace_cap;
+  unsigned long long* tstamp;  // timing stamps (PairArgs::tstamp), nullptr: off
 };
 
 // Background sums (k = 0..2: S_B, S_Br, S_Bt) are fixed point,
@@ -149,6 +150,10 @@ struct PairArgs {
   unsigned long long* trace;
   int trace_kernel;
   int trace_cap;
+  // timing without events between kernels (graph mode): %globaltimer stamps,
+  // [0] first CTA start of the evaluation (min), [1] end (finalize, max),
+  // [2] first pair CTA start (min), [3] last pair CTA end (max); nullptr: off
+  unsigned long long* tstamp;
 };
 
 #ifdef __CUDACC__
@@ -175,6 +180,13 @@ __device__ __forceinline__ void trace_cta(unsigned long long* trace, int cap, in
     p[2] = t0;
     p[3] = t1;
   }
+}
+// (timing stamps: CTA start -> min into slot, CTA end -> max into slot)
+__device__ __forceinline__ void stamp_min(unsigned long long* ts, int slot) {
+  if (ts) atomicMin(ts + slot, global_ns());
+}
+__device__ __forceinline__ void stamp_max(unsigned long long* ts, int slot) {
+  if (ts) atomicMax(ts + slot, global_ns());
 }
 __device__ __forceinline__ void trace_item(const PairArgs& a, int item, int nst, int diag,
                                            unsigned long long t0) {
@@ -230,8 +242,10 @@ struct FinArgs {
   // and re-zeroed for the next evaluation; nullptr: untouched
   unsigned long long* counts;
   unsigned long long* counts_out;
+  unsigned long long* tstamp_out;  // with tstamp: the last block copies the stamps here (mapped) and re-arms them
   unsigned long long* trace;  // development trace (PairArgs::trace), nullptr: off
   int trace_cap;
+  unsigned long long* tstamp;  // timing stamps (PairArgs::tstamp), nullptr: off
 };
 
 // Launch sink: while set (per host thread), the evaluation-path launch
@@ -291,6 +305,7 @@ struct PrepArgs {
   double* tsl;
   unsigned long long* trace;  // development trace (PairArgs::trace), nullptr: off
   int trace_cap;
+  unsigned long long* tstamp;  // timing stamps (PairArgs::tstamp), nullptr: off
 };
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);

@@ -1,6 +1,9 @@
 {
-for n in c2 10000 250000; do STHK_ITEM_TRACE=400000 python tools/item_trace.py $n post | grep -A4 timeline; done
-QP_REPS=60 python tools/perf_matrix.py
-SN=2000,10000,20000 python tools/small_n.py 2>&1 | grep cloud
-timeout 1500 python -m pytest tests -q -m gpu -x -k "not c4_1m" 2>&1 | tail -3
+for v in "1 1" "0 1" "1 0" "0 0"; do set -- $v
+echo "== STHK_EV1_NODE=$1 STHK_NODE_PRIO=$2"
+STHK_EV1_NODE=$1 STHK_NODE_PRIO=$2 python bench.py --steps 300 --no-secondary --no-cpu-baseline 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['value'], d['e2e']['value'], d['roofline']['pair_kernel_ms'])"
+STHK_EV1_NODE=$1 STHK_NODE_PRIO=$2 STHK_ITEM_TRACE=400000 python tools/item_trace.py c2 post | grep -A9 timeline | grep "plan \|trigger\|far \|general \|finalize"
+STHK_EV1_NODE=$1 STHK_NODE_PRIO=$2 STHK_ITEM_TRACE=400000 python tools/item_trace.py c2 init | grep -A9 timeline | grep "plan \|trigger\|far \|general \|finalize"
+done
 } > gpurun_out/c.txt 2>&1
