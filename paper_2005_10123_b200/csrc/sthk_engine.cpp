@@ -1631,6 +1631,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     qa.fx = s.fx;
     qa.tpart = s.tpart;
     qa.bg_off = cached ? 1 : 0;
+    qa.bg_diag_only = bg_split ? 1 : 0;
     for (int k = 0; k < sthk::kNSumGrad; ++k) qa.fxq[k] = fxq[k];
     if (sym) qa.fxq[1] = fxq[1] / (pl.sx * pl.sx);  // S_Br accumulates sx^2 r^2
     qa.pair_counts = e.timing ? s.pair_counts : nullptr;
@@ -1660,6 +1661,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       ba.n_items = s.scalars + 9;
       ba.work_counter = s.scalars + 10;
       ba.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 11);
+      ba.bg_diag_only = 0;
       ba.trace_kernel = 2;
       ck(sthk::launch_bgonly(ba, grad, s.sms * s.occ_bg[grad ? 1 : 0], st), "bg-only kernel");
       e.launches += 1;
@@ -1694,6 +1696,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       fa_.work_counter = s.scalars + 7;
       fa_.done_counter = reinterpret_cast<unsigned int*>(s.scalars + 8);
       fa_.tpart = far_tr ? s.tpart_far : nullptr;
+      fa_.bg_diag_only = 0;
       fa_.trace_kernel = 3;
       // far list in FP64 (sthk_set_far_tier(2)): the general near kernel over
       // the same list with the far tier's windows -- the precision policy's

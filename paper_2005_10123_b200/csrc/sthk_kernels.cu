@@ -47,6 +47,7 @@ namespace {
 
 constexpr double kInvSqrt2 = 0.7071067811865475244;     // kernels.hpp:14
 
+
 // Work-item hand-out of the persistent pair kernels. STHK_STATIC_FIRST: a
 // CTA's first item is its block index (consecutive blocks are dispatched to
 // different SMs, so with fewer items than CTAs -- small N -- the items spread
@@ -200,8 +201,12 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
   cr = make_int2(fbt / a.sc, (hi - 1) / a.sc);
   rgf = make_int2(flo, fb);
   crf = fb > flo ? make_int2(flo / a.sc, (fb - 1) / a.sc) : make_int2(0, -1);
-  rgb = make_int2(fb, fbt);
-  crb = fbt > fb ? make_int2(fb / a.sc_bg, (fbt - 1) / a.sc_bg) : make_int2(0, -1);
+  // (the trigger-free kernel takes the background of every near stage before
+  // the diagonal one; the general kernel keeps the trigger terms of the
+  // bg_adj stages ahead of the tile and the diagonal stage)
+  const int fbe = a.ranges_bg ? static_cast<int>(first) : fbt;
+  rgb = make_int2(fb, fbe);
+  crb = fbe > fb ? make_int2(fb / a.sc_bg, (fbe - 1) / a.sc_bg) : make_int2(0, -1);
 }
 
 // Number of 128-source stages of work item (tile, chunk) -- the same bounds
@@ -1129,7 +1134,8 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
       const double smin = BGONLY ? s_tr[buf].x : s_src[buf][2][0];
       const double smax = BGONLY ? s_tr[buf].y : s_src[buf][2][cnt - 1];
 
-      const bool bg = !a.bg_off && !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
+      const bool bg = !a.bg_off && (!a.bg_diag_only || diag || pre) &&
+                      !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
       int tr;
       if (pre || smin >= tmax || smax < tmin - a.k.dT) tr = 0;
       else if (smax < tmin) tr = 1;

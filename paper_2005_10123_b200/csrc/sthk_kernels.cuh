@@ -130,6 +130,8 @@ struct PairArgs {
   double fxq[kNSumGrad];
   double* tpart;        // trigger partials [nchunks][3 or 1][npad]
   int bg_off;           // trigger-only sweep (background sums come from a cache)
+  int bg_diag_only;     // general kernel beside the trigger-free one: background on the
+                        // diagonal stage only (the trigger-free kernel has every earlier stage)
   unsigned long long* pair_counts;  // [kNCounts] (tile granularity)
   // merged trigger-free list (general sym_kernel only; nullptr: none): work
   // items [0, *pre_n_items) are the background-only list's -- its ranges,
