@@ -164,6 +164,7 @@ struct Slot {
   double plan_tfar = 0, plan_dfar = 0;
   std::vector<std::pair<int, int>> runs;  // row ranges run on this slot
   unsigned long long* trace = nullptr;     // development item trace (STHK_ITEM_TRACE)
+  unsigned long long* load_dstats = nullptr;  // load statistics accumulators (tile_box_kernel)
   unsigned long long* tstamp = nullptr;    // kernel timing stamps [4] (graph-mode timing)
   unsigned long long* h_tstamp = nullptr;  // pinned, device-mapped copy written by finalize
   unsigned long long* d_htstamp = nullptr;
@@ -389,6 +390,13 @@ void init_slot(Slot& s, int dev) {
   ck(cudaMalloc(&s.pair_counts, sthk::kNCounts * sizeof(unsigned long long)), "cudaMalloc");
   ck(cudaMemset(s.pair_counts, 0, sthk::kNCounts * sizeof(unsigned long long)), "memset");
   {
+    std::vector<unsigned long long> ls(sthk::kLoadStats, 0x7ff0000000000000ULL);
+    std::fill(ls.begin(), ls.begin() + 3, 0ULL);
+    ck(cudaMalloc(&s.load_dstats, sizeof(unsigned long long) * ls.size()), "cudaMalloc");
+    ck(cudaMemcpy(s.load_dstats, ls.data(), sizeof(unsigned long long) * ls.size(),
+                  cudaMemcpyHostToDevice), "H2D");
+  }
+  {
     const unsigned long long init[4] = {~0ULL, 0ULL, ~0ULL, 0ULL};
     ck(cudaMalloc(&s.tstamp, sizeof(init)), "cudaMalloc");
     ck(cudaMemcpy(s.tstamp, init, sizeof(init), cudaMemcpyHostToDevice), "H2D");
@@ -444,7 +452,8 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.pair_counts), static_cast<void*>(s.tile_box),
                   static_cast<void*>(s.fx_stage), static_cast<void*>(s.pi_sum),
                   static_cast<void*>(s.pi_bad), static_cast<void*>(s.pi_rows),
-                  static_cast<void*>(s.trace), static_cast<void*>(s.tstamp)}) {
+                  static_cast<void*>(s.trace), static_cast<void*>(s.tstamp),
+                  static_cast<void*>(s.load_dstats)}) {
     if (p) cudaFree(p);
   }
   for (void* p : {static_cast<void*>(s.h_out), static_cast<void*>(s.h_counts),
@@ -2137,7 +2146,7 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       ck(cudaHostGetDevicePointer(&d_hstats, s.h_stats, 0), "cudaHostGetDevicePointer");
       if (!s.piv) ck(cudaMalloc(&s.piv, sizeof(double) * sthk::kPlanPivots), "cudaMalloc");
       ck(sthk::launch_tile_boxes(s.x, s.y, s.t, n, npad, s.tile_box, s.tile_trange, s.piv, bad,
-                                 done, d_hbad, d_hstats, s.stream),
+                                 done, d_hbad, d_hstats, s.load_dstats, s.stream),
          "tile boxes + checks");
     }
     for (Slot& s : e->slots) {

@@ -1505,7 +1505,16 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
                                 double* __restrict__ t, int64_t n, int64_t npad, double4* box,
                                 double2* trange, double* __restrict__ piv,
                                 unsigned long long* bad, unsigned int* done,
-                                unsigned long long* h_bad, double* h_stats) {
+                                unsigned long long* h_bad, double* h_stats,
+                                unsigned long long* __restrict__ dstats) {
+  // load statistics (kLoadStats): per tile one value per lane, reduced over
+  // the block in shared memory, then one device atomic per statistic and
+  // block; every value is >= 0, so its bit pattern orders like the double
+  __shared__ unsigned long long s_st[kLoadStats];
+  for (int q = threadIdx.x; q < kLoadStats; q += blockDim.x) {
+    s_st[q] = q < 3 ? 0ULL : 0x7ff0000000000000ULL;
+  }
+  __syncthreads();
   // zero the pad tail [n, npad) of the coordinate arrays (never read as sources)
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid < npad - n) {
@@ -1560,12 +1569,41 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
       const double4 b = make_double4(x0, x1, y0, y1);
       box[tile] = b;
       trange[tile] = make_double2(t[first], t[last - 1]);
+      // extents relative to event 0, the tile's time span
+      const double x00 = x[0], y00 = y[0];
+      const double e[3] = {fmax(fabs(x0 - x00), fabs(x1 - x00)), fmax(fabs(y0 - y00), fabs(y1 - y00)),
+                           t[last - 1] - t[first]};
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        atomicMax(&s_st[q], static_cast<unsigned long long>(__double_as_longlong(fmax(e[q], 0.0))));
+      }
+    }
+    // lanes 0..15: the gap a = lane + 1 stages ahead of the tile's first event
+    // (t[first] - t[first - 128 a - 1]); lanes 16..31: the span of 2^L whole
+    // tiles from this one, L = lane - 16
+    const int64_t nt = (n + kTS - 1) / kTS;
+    double v = __longlong_as_double(0x7ff0000000000000LL);
+    if (lane < kLoadAdj) {
+      const int64_t a = lane + 1;
+      if (tile >= a + 1) v = t[first] - t[(tile - a) * kTS - 1];
+    } else {
+      const int64_t L = lane - kLoadAdj;
+      if (L < kLoadSpan && tile + (int64_t{1} << L) - 1 < nt) {
+        v = t[min((tile + (int64_t{1} << L)) * kTS, n) - 1] - t[first];
+      }
+    }
+    if (lane < kLoadAdj + kLoadSpan) {
+      atomicMin(&s_st[3 + lane], static_cast<unsigned long long>(__double_as_longlong(fmax(v, 0.0))));
     }
   }
+  __syncthreads();
+  for (int q = threadIdx.x; q < kLoadStats; q += blockDim.x) {
+    if (q < 3) atomicMax(&dstats[q], s_st[q]);
+    else atomicMin(&dstats[q], s_st[q]);
+  }
   // the last block out hands the first bad index and the load statistics to
-  // the host (mapped) and re-arms the device minimum for the next load
+  // the host (mapped) and re-arms the device copies for the next load
   __shared__ bool s_last;
-  __shared__ double s_w[8][kLoadStats];
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -1574,50 +1612,9 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int64_t nt = (n + kTS - 1) / kTS;
-  const double x00 = __ldcg(x), y00 = __ldcg(y);
-  double v[kLoadStats];  // maxima [0..2], minima [3..]
-#pragma unroll
-  for (int q = 0; q < kLoadStats; ++q) v[q] = q < 3 ? 0.0 : __longlong_as_double(0x7ff0000000000000LL);
-  for (int64_t k = threadIdx.x; k < nt; k += blockDim.x) {
-    const double2 bxy = __ldcg(reinterpret_cast<const double2*>(&box[k]));
-    const double2 bzw = __ldcg(reinterpret_cast<const double2*>(&box[k]) + 1);
-    const double4 b = make_double4(bxy.x, bxy.y, bzw.x, bzw.y);
-    const double2 tr = __ldcg(&trange[k]);
-    v[0] = fmax(v[0], fmax(fabs(b.x - x00), fabs(b.y - x00)));
-    v[1] = fmax(v[1], fmax(fabs(b.z - y00), fabs(b.w - y00)));
-    v[2] = fmax(v[2], tr.y - tr.x);
-#pragma unroll
-    for (int a = 1; a <= kLoadAdj; ++a) {
-      if (k >= a + 1) v[2 + a] = fmin(v[2 + a], tr.x - __ldcg(&trange[k - a - 1]).y);
-    }
-#pragma unroll
-    for (int L = 0; L < kLoadSpan; ++L) {
-      const int64_t kl = k + (int64_t{1} << L) - 1;
-      if (kl < nt) v[3 + kLoadAdj + L] = fmin(v[3 + kLoadAdj + L], __ldcg(&trange[kl]).y - tr.x);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < kLoadStats; ++q) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double o = __shfl_xor_sync(0xffffffffu, v[q], off);
-      v[q] = q < 3 ? fmax(v[q], o) : fmin(v[q], o);
-    }
-  }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-    for (int q = 0; q < kLoadStats; ++q) s_w[w][q] = v[q];
-  }
-  __syncthreads();
-  if (threadIdx.x < kLoadStats) {
-    const int q = threadIdx.x;
-    double r = s_w[0][q];
-    for (int ww = 1; ww < static_cast<int>(blockDim.x >> 5); ++ww) {
-      r = q < 3 ? fmax(r, s_w[ww][q]) : fmin(r, s_w[ww][q]);
-    }
-    h_stats[q] = r;
+  for (int q = threadIdx.x; q < kLoadStats; q += blockDim.x) {
+    h_stats[q] = __longlong_as_double(static_cast<long long>(atomicAdd(&dstats[q], 0ULL)));
+    dstats[q] = q < 3 ? 0ULL : 0x7ff0000000000000ULL;
   }
   if (threadIdx.x == 0) {
     *h_bad = atomicExch(bad, ~0ULL);
@@ -1928,10 +1925,11 @@ cudaError_t launch_fx_accumulate(const FxAccArgs& a, cudaStream_t stream) {
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
                               double4* box, double2* trange, double* piv,
                               unsigned long long* bad, unsigned int* done,
-                              unsigned long long* h_bad, double* h_stats, cudaStream_t stream) {
+                              unsigned long long* h_bad, double* h_stats,
+                              unsigned long long* dstats, cudaStream_t stream) {
   const int64_t ntiles = (n + kTS - 1) / kTS;
   tile_box_kernel<<<static_cast<unsigned>((ntiles + 7) / 8), 256, 0, stream>>>(
-      x, y, t, n, npad, box, trange, piv, bad, done, h_bad, h_stats);
+      x, y, t, n, npad, box, trange, piv, bad, done, h_bad, h_stats, dstats);
   return cudaGetLastError();
 }
 

@@ -274,6 +274,8 @@ constexpr int kLoadSpan = 16;
 constexpr int kLoadStats = 3 + kLoadAdj + kLoadSpan;
 
 // Per-tile bounding boxes and time ranges, and the plan's search pivots
+// (dstats: kLoadStats device words, maxima 0 / minima +inf bits, re-armed by
+// the kernel)
 // (PlanArgs::piv); also zeroes the pad tail [n, npad)
 // of x, y, t and runs the EventSet checks (finite, t >= 0, sorted). The
 // kernel's last block writes the first failing index (all ones: none) to
@@ -282,7 +284,8 @@ constexpr int kLoadStats = 3 + kLoadAdj + kLoadSpan;
 cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
                               double4* box, double2* trange, double* piv,
                               unsigned long long* bad, unsigned int* done,
-                              unsigned long long* h_bad, double* h_stats, cudaStream_t stream);
+                              unsigned long long* h_bad, double* h_stats,
+                              unsigned long long* dstats, cudaStream_t stream);
 // Per-evaluation preparation (prep_kernel); every output optional (nullptr):
 // kSym coordinates xs, ys = (x, y) * sx and the far tier's FP32 copies
 // xf, yf = (x - x[0], y - y[0]) * sxf, tf = (t - t[tile start]) * stf; zeroed
