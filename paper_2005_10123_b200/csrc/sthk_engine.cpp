@@ -302,6 +302,7 @@ struct sthk_engine {
   // adj_gap[k-1]: min over tiles of t[first] - t[first - 128k - 1], the time
   // from a tile's first event back to the last source before its k preceding
   // stages (the trigger-free split keeps those k stages with the tile)
+  bool tile_pivots = true;  // plan searches on tile pivots (set at load)
   std::vector<double> adj_gap;
   // span_min[L]: min time span of 2^L consecutive whole tiles (load
   // statistics): bounds the number of events in any time window (far tier)
@@ -1576,6 +1577,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     pa.n_items = s.scalars;
     pa.work_counter = s.scalars + 1;
     pa.tfar = far_on ? pl.tfar : 0.0;
+    pa.tile_pivots = e.tile_pivots ? 1 : 0;
     pa.trace = s.trace;
     pa.trace_cap = item_trace_cap();
     pa.tstamp = stamps ? s.tstamp : nullptr;
@@ -2116,6 +2118,13 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
     if (e->pending) collect(*e, nullptr, nullptr, nullptr, nullptr);
     e->loaded = false;  // until the device-side checks pass
     const int64_t npad = (n + kTM - 1) / kTM * kTM;
+    // (development knob STHK_PLAN_STRIDED=1: strided pivots at any N, to
+    // check that tile-granular plan searches change no result)
+    static const bool force_strided = [] {
+      const char* v = std::getenv("STHK_PLAN_STRIDED");
+      return v && *v == '1';
+    }();
+    e->tile_pivots = sthk::use_tile_pivots(n) && !force_strided;
     const bool multi = e->slots.size() > 1 || e->rank_mode;
     if (multi) e->ht.assign(t, t + n);
     e->ht_valid = multi;
@@ -2146,7 +2155,7 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       ck(cudaHostGetDevicePointer(&d_hstats, s.h_stats, 0), "cudaHostGetDevicePointer");
       if (!s.piv) ck(cudaMalloc(&s.piv, sizeof(double) * sthk::kPlanPivots), "cudaMalloc");
       ck(sthk::launch_tile_boxes(s.x, s.y, s.t, n, npad, s.tile_box, s.tile_trange, s.piv, bad,
-                                 done, d_hbad, d_hstats, s.load_dstats, s.stream),
+                                 done, d_hbad, d_hstats, s.load_dstats, e->tile_pivots, s.stream),
          "tile boxes + checks");
     }
     for (Slot& s : e->slots) {

@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   if (tid == 0) stamp_min(a.tstamp, 0);
   const int ntiles = a.tile1 - a.tile0;
   Pivots pv;
-  pv.tiles = (a.n + kTS - 1) / kTS <= kPivots;
+  pv.tiles = a.tile_pivots != 0;
   pv.stride = pv.tiles ? kTS : pivot_stride(a.n);
   pv.np = static_cast<int>((a.n + pv.stride - 1) / pv.stride);
   pv.piv = s_piv;
@@ -1506,7 +1506,7 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
                                 double2* trange, double* __restrict__ piv,
                                 unsigned long long* bad, unsigned int* done,
                                 unsigned long long* h_bad, double* h_stats,
-                                unsigned long long* __restrict__ dstats) {
+                                unsigned long long* __restrict__ dstats, bool tiles) {
   // load statistics (kLoadStats): per tile one value per lane, reduced over
   // the block in shared memory, then one device atomic per statistic and
   // block; every value is >= 0, so its bit pattern orders like the double
@@ -1524,7 +1524,7 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
   }
   // the plan's search pivots t[k * stride], +inf padded to kPivots
   {
-    const bool tiles = (n + kTS - 1) / kTS <= kPivots;  // (see Pivots)
+    // (see Pivots)
     const int64_t stride = tiles ? kTS : pivot_stride(n), np = (n + stride - 1) / stride;
     for (int64_t k = gid; k < kPivots; k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
       piv[k] = k >= np ? __longlong_as_double(0x7ff0000000000000LL)
@@ -1926,10 +1926,10 @@ cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_
                               double4* box, double2* trange, double* piv,
                               unsigned long long* bad, unsigned int* done,
                               unsigned long long* h_bad, double* h_stats,
-                              unsigned long long* dstats, cudaStream_t stream) {
+                              unsigned long long* dstats, bool tile_pivots, cudaStream_t stream) {
   const int64_t ntiles = (n + kTS - 1) / kTS;
   tile_box_kernel<<<static_cast<unsigned>((ntiles + 7) / 8), 256, 0, stream>>>(
-      x, y, t, n, npad, box, trange, piv, bad, done, h_bad, h_stats, dstats);
+      x, y, t, n, npad, box, trange, piv, bad, done, h_bad, h_stats, dstats, tile_pivots);
   return cudaGetLastError();
 }
 

@@ -90,6 +90,7 @@ struct PlanArgs {
   // background-only split of the near range (kSym full sweeps): near stages
   // before first - bg_adj * 128 (no live trigger, host-checked) go to a third
   // list for the trigger-free FP64 kernel; nullptr: off
+  int tile_pivots;      // piv holds tile last times (see use_tile_pivots), else strided times
   int bg_adj;           // near stages kept with the tile for the general kernel (>= 1)
   int sc_bg;            // sources per chunk of the background-only list (multiple of kTS)
   int2* ranges_bg;
@@ -285,7 +286,10 @@ cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_
                               double4* box, double2* trange, double* piv,
                               unsigned long long* bad, unsigned int* done,
                               unsigned long long* h_bad, double* h_stats,
-                              unsigned long long* dstats, cudaStream_t stream);
+                              unsigned long long* dstats, bool tile_pivots, cudaStream_t stream);
+// Tile pivots (tile last times, tile-granular plan searches) are used up to
+// kPlanPivots tiles; above, strided pivots t[k ceil(n / kPlanPivots)].
+inline bool use_tile_pivots(int64_t n) { return (n + kTS - 1) / kTS <= kPlanPivots; }
 // Per-evaluation preparation (prep_kernel); every output optional (nullptr):
 // kSym coordinates xs, ys = (x, y) * sx and the far tier's FP32 copies
 // xf, yf = (x - x[0], y - y[0]) * sxf, tf = (t - t[tile start]) * stf; zeroed

@@ -880,3 +880,42 @@ def test_graph_replay_bitwise_equals_direct_launches(n):
             assert st["graph_builds"] <= 10, st["graph_builds"]
         e.close()
     assert out[True] == out[False]
+
+
+_PIVOT_SCRIPT = r"""
+import hashlib, json, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import paper_2005_10123_b200 as pk
+out = []
+for n, th in ((85000, [0.66, 1.6, 14, 0.344, 1440, 0.0695]), (85000, [1, 1.6, 14, 0.1, 1, 1]),
+              (6000, [0.66, 1.6, 14, 0.344, 1440, 0.0695])):
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005, keep=n)
+    e = pk.Engine((0,))
+    e.set_background_cache(False)
+    e.load(ev)
+    e.set_params(th)
+    ll, ok, g, pe = e.loglik_grad(per_event=True)
+    out.append([ll.hex(), [float(v).hex() for v in g], hashlib.sha256(pe.tobytes()).hexdigest()])
+    e.close()
+print(json.dumps(out))
+"""
+
+
+def test_tile_pivot_plan_bitwise_equals_strided_plan():
+    """The plan's tile-granular searches (tile last times as pivots, no global
+    rounds) and the exact strided-pivot searches give the same stage sets,
+    hence bitwise-identical loglik, gradient and per-event terms."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for strided in ("0", "1"):
+        env = dict(os.environ, STHK_PLAN_STRIDED=strided)
+        r = subprocess.run([sys.executable, "-c", _PIVOT_SCRIPT, root], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[strided] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["0"] == res["1"]
