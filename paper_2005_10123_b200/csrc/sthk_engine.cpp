@@ -95,8 +95,7 @@ struct Slot {
   size_t trange_cap = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;    // far kernel, concurrent with the near sweep
-  cudaStream_t stream3 = nullptr;    // general near kernel beside the trigger-free one
-  cudaEvent_t fork = nullptr, join = nullptr, join3 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
   cudaEvent_t pairs_done = nullptr, fin_done = nullptr;  // cross-slot ordering (local transport)
   ncclComm_t comm = nullptr;
   int shard = 0;                     // this slot's shard (= rank)
@@ -286,16 +285,6 @@ struct sthk_engine {
   // at once); extra far CTAs queue until near CTAs retire.
   bool far_concurrent = true;
   int far_order = 1;  // 1: far launched first, 2: near first
-  // Launch order of the concurrent pair kernels (development knob
-  // STHK_PAIR_ORDER at creation): 0 trigger-free then general on one stream,
-  // far beside them; 1 trigger-free, general (third stream), far -- the
-  // general kernel's CTAs fill in as trigger-free CTAs retire; 2 general
-  // first. Without a trigger-free list, 1 and 2 launch the near kernel ahead
-  // of the far one.
-  int pair_order = [] {
-    const char* v = std::getenv("STHK_PAIR_ORDER");
-    return v ? std::atoi(v) : 0;
-  }();
   int near_ctas = 3, far_ctas = 6;
   double ext_x = 0, ext_y = 0;  // max |x - x[0]|, |y - y[0]| of the loaded set
   double tile_tspan = 0;        // max time span of a 128-event tile
@@ -361,19 +350,9 @@ void init_slot(Slot& s, int dev) {
   set_dev(s);
   ck(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
   ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
-  {
-    // (development knob STHK_STREAM_PRIO=1: far kernel stream at the lowest
-    // priority, the general near kernel's at the highest)
-    const char* pv = std::getenv("STHK_STREAM_PRIO");
-    int lo = 0, hi = 0;
-    ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
-    const bool prio = pv && *pv == '1';
-    ck(cudaStreamCreateWithPriority(&s.stream2, cudaStreamNonBlocking, prio ? lo : 0), "stream");
-    ck(cudaStreamCreateWithPriority(&s.stream3, cudaStreamNonBlocking, prio ? hi : 0), "stream");
-  }
+  ck(cudaStreamCreateWithFlags(&s.stream2, cudaStreamNonBlocking), "stream");
   ck(cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming), "event");
-  ck(cudaEventCreateWithFlags(&s.join3, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.prepped, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.pairs_done, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.fin_done, cudaEventDisableTiming), "event");
@@ -467,11 +446,8 @@ void free_slot(Slot& s) {
     if (e) cudaEventDestroy(e);
   }
   if (s.stream2) cudaStreamSynchronize(s.stream2);
-  if (s.stream3) cudaStreamSynchronize(s.stream3);
   if (s.fork) cudaEventDestroy(s.fork);
   if (s.join) cudaEventDestroy(s.join);
-  if (s.join3) cudaEventDestroy(s.join3);
-  if (s.stream3) cudaStreamDestroy(s.stream3);
   if (s.prepped) cudaEventDestroy(s.prepped);
   if (s.pairs_done) cudaEventDestroy(s.pairs_done);
   if (s.fin_done) cudaEventDestroy(s.fin_done);
@@ -1373,11 +1349,10 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
   // launch and per-CTA setup: measured break-even between N = 30k and 40k)
   int bg_adj = 0;
   if (sym && e.bg_split && !e.adj_gap.empty() && e.n >= kBgSplitMinEvents) {
-    static const bool use_dT = [] {  // (development knob STHK_BGADJ_WINDOW=1: the half-ulp window)
-      const char* v = std::getenv("STHK_BGADJ_WINDOW");
-      return v && *v == '1';
-    }();
-    const double dT_phys = use_dT ? pl.k.dT : sthk::kCullExponent / e.p[4] * (1.0 + 1e-9);
+    // (choosing it from the half-ulp window pl.k.dT instead was measured: 6%
+    // slower at Theta_init, where the general kernel's fused background +
+    // trigger stages beat a trigger-only pass beside the trigger-free kernel)
+    const double dT_phys = sthk::kCullExponent / e.p[4] * (1.0 + 1e-9);
     for (int k = 1; k <= kMaxAdj; ++k) {
       if (e.adj_gap[k - 1] > dT_phys) {
         bg_adj = k;
@@ -1690,11 +1665,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     // (graph mode: without this node the far kernel's CTAs reach the SMs
     // first and the near kernel starts 20 us later -- measured 4.5% slower at
     // C2; graph node priorities do not change that order)
-    static const bool ev1_node = [] {  // (development knob STHK_EV1_NODE=0/1)
-      const char* v = std::getenv("STHK_EV1_NODE");
-      return !(v && *v == '0');
-    }();
-    ck((e.timing && e.timing_pairs && !stamps) || (bg_split && ev1_node)
+    ck((e.timing && e.timing_pairs && !stamps) || bg_split
            ? record_timing(e, s.ev[1], st)
            : op_record(e, s.ev[1], st),
        "event");
@@ -1722,29 +1693,10 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
         }
         return sthk::launch_far(fa_, grad, grid_far, fs);
       };
-      if (conc && e.pair_order > 0 && bg_split && !e.merge_bg) {
-        // three streams: trigger-free (st), general (stream3), far (stream2)
+      if (conc) {  // forked onto the second stream, joined before finalize
         ck(op_record(e, s.fork, st), "event");
         ck(op_wait(e, s.stream2, s.fork), "wait");
-        ck(op_wait(e, s.stream3, s.fork), "wait");
-        if (e.pair_order == 2) {
-          ck(sthk::launch_pairs(qa, grad, e.mode, grid, s.stream3), "pair kernel");
-          launch_bg();
-        } else {
-          launch_bg();
-          ck(sthk::launch_pairs(qa, grad, e.mode, grid, s.stream3), "pair kernel");
-        }
-        e.launches += 1;
-        ck(launch_far_list(s.sms * e.far_ctas, s.stream2), "far kernel");
-        e.launches += 1;
-        ck(op_record(e, s.join, s.stream2), "event");
-        ck(op_record(e, s.join3, s.stream3), "event");
-        ck(op_wait(e, st, s.join), "wait");
-        ck(op_wait(e, st, s.join3), "wait");
-      } else if (conc) {  // forked onto the second stream, joined before finalize
-        ck(op_record(e, s.fork, st), "event");
-        ck(op_wait(e, s.stream2, s.fork), "wait");
-        if (e.far_order == 2 || e.pair_order > 0) {  // near first: its CTAs are resident before far CTAs fill in
+        if (e.far_order == 2) {  // near first: its CTAs are resident before far CTAs fill in
           launch_bg();
           ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
           e.launches += 1;
