@@ -1501,78 +1501,116 @@ __global__ void __launch_bounds__(kTM, STHK_FAR_MINB) far_kernel(const PairArgs 
 
 // Per 128-event tile bounding box of the (x, y) coordinates (params
 // independent; computed once per load). Feeds the no-underflow proofs.
-__global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
-                                double* __restrict__ t, int64_t n, int64_t npad, double4* box,
-                                double2* trange, double* __restrict__ piv,
-                                unsigned long long* bad, unsigned int* done,
-                                unsigned long long* h_bad, double* h_stats,
-                                unsigned long long* __restrict__ dstats, bool tiles) {
-  // load statistics (kLoadStats): per tile one value per lane, reduced over
-  // the block in shared memory, then one device atomic per statistic and
-  // block; every value is >= 0, so its bit pattern orders like the double
+// Event load, pass 1 (one warp per 128-event tile): reads the tile from its
+// source -- the caller's pinned host arrays over PCIe (zero-copy: this pass
+// is the host-to-device copy) or the device arrays themselves after a
+// cudaMemcpy -- writes the device copy, and computes the tile's bounding box
+// and (first, last) time and the EventSet checks (types.hpp:85-109: finite,
+// t >= 0, nondecreasing; the predecessor of each element from a shuffle, one
+// source read per tile for the element before it). Also zeroes the pad tail
+// and writes the tile pivots (PlanArgs::piv).
+__global__ void tile_load_kernel(const double* __restrict__ sx, const double* __restrict__ sy,
+                                 const double* __restrict__ st, double* __restrict__ x,
+                                 double* __restrict__ y, double* __restrict__ t, int64_t n,
+                                 int64_t npad, double4* box, double2* trange,
+                                 double* __restrict__ piv, unsigned long long* bad, bool tiles) {
+  const bool copy = sx != x;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid < npad - n) {  // pad tail [n, npad): never read as sources
+    x[n + gid] = 0.0;
+    y[n + gid] = 0.0;
+    t[n + gid] = 0.0;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t tile = gid >> 5;
+  const int64_t first = tile * kTS;
+  if (first >= n) return;
+  const int64_t last = min(first + kTS, n);
+  double x0 = __longlong_as_double(0x7ff0000000000000LL), x1 = -x0, y0 = x0, y1 = -x0;
+  double carry = (lane == 0 && first > 0) ? st[first - 1] : 0.0;  // element before the tile
+  double tfirst = 0.0, tlast = 0.0;
+  int64_t first_bad = INT64_MAX;
+#pragma unroll
+  for (int it = 0; it < kTS / 32; ++it) {
+    const int64_t i = first + lane + 32 * it;
+    const bool live = i < last;
+    double xv = 0.0, yv = 0.0, tv = 0.0;
+    if (live) {
+      xv = sx[i];
+      yv = sy[i];
+      tv = st[i];
+      if (copy) {
+        x[i] = xv;
+        y[i] = yv;
+        t[i] = tv;
+      }
+      x0 = fmin(x0, xv);
+      x1 = fmax(x1, xv);
+      y0 = fmin(y0, yv);
+      y1 = fmax(y1, yv);
+    }
+    const double up = __shfl_up_sync(0xffffffffu, tv, 1);
+    const double prev = lane == 0 ? carry : up;
+    carry = __shfl_sync(0xffffffffu, tv, 31);  // (lane 0 of the next round)
+    const bool ok = isfinite(xv) && isfinite(yv) && isfinite(tv) && tv >= prev;
+    if (live && !ok && i < first_bad) first_bad = i;
+    if (it == 0) tfirst = __shfl_sync(0xffffffffu, tv, 0);
+    const int64_t lk = last - 1 - first - 32 * it;  // lane holding t[last - 1] in this round
+    const double tl = __shfl_sync(0xffffffffu, tv, static_cast<int>(lk < 0 ? 0 : (lk > 31 ? 31 : lk)));
+    if (lk >= 0 && lk < 32) tlast = tl;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    first_bad = min(first_bad, static_cast<int64_t>(__shfl_xor_sync(
+                                   0xffffffffu, static_cast<long long>(first_bad), off)));
+    x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+    x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+    y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, off));
+    y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, off));
+  }
+  if (lane == 0) {
+    if (first_bad != INT64_MAX) atomicMin(bad, static_cast<unsigned long long>(first_bad));
+    box[tile] = make_double4(x0, x1, y0, y1);
+    trange[tile] = make_double2(tfirst, tlast);
+    if (tiles) piv[tile] = tlast;  // (see Pivots)
+  }
+}
+
+// Event load, pass 2 (one warp per tile, after pass 1): the remaining plan
+// pivots, and the load statistics (kLoadStats) -- per tile one value per
+// lane, reduced over the block in shared memory, then one device atomic per
+// statistic and block (every value is >= 0, so its bit pattern orders like
+// the double). The last block out hands the first bad index and the
+// statistics to the host (mapped) and re-arms the device copies.
+__global__ void tile_stats_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                  const double* __restrict__ t, int64_t n, const double4* box,
+                                  const double2* trange, double* __restrict__ piv, bool tiles,
+                                  unsigned long long* bad, unsigned int* done,
+                                  unsigned long long* h_bad, double* h_stats,
+                                  unsigned long long* __restrict__ dstats) {
   __shared__ unsigned long long s_st[kLoadStats];
   for (int q = threadIdx.x; q < kLoadStats; q += blockDim.x) {
     s_st[q] = q < 3 ? 0ULL : 0x7ff0000000000000ULL;
   }
   __syncthreads();
-  // zero the pad tail [n, npad) of the coordinate arrays (never read as sources)
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (gid < npad - n) {
-    x[n + gid] = 0.0;
-    y[n + gid] = 0.0;
-    t[n + gid] = 0.0;
-  }
-  // the plan's search pivots t[k * stride], +inf padded to kPivots
-  {
-    // (see Pivots)
+  const int64_t nt = (n + kTS - 1) / kTS;
+  {  // pivots: +inf beyond the tiles (tile pivots), or strided t[k * stride]
     const int64_t stride = tiles ? kTS : pivot_stride(n), np = (n + stride - 1) / stride;
     for (int64_t k = gid; k < kPivots; k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-      piv[k] = k >= np ? __longlong_as_double(0x7ff0000000000000LL)
-                       : t[tiles ? min(k * kTS + kTS - 1, n - 1) : k * stride];
+      if (k >= np) piv[k] = __longlong_as_double(0x7ff0000000000000LL);
+      else if (!tiles) piv[k] = t[k * stride];
     }
   }
-  // one warp per tile: 4 coalesced loads per lane, then a shuffle min/max
   const int lane = threadIdx.x & 31;
   const int64_t tile = gid >> 5;
-  const int64_t first = tile * kTS;
-  if (first < n) {
-    const int64_t last = min(first + kTS, n);
-    double x0 = x[first], x1 = x0, y0 = y[first], y1 = y0;
-    int64_t first_bad = INT64_MAX;
-    for (int64_t i = first + lane; i < last; i += 32) {
-      const double xv = x[i], yv = y[i], tv = t[i];
-      x0 = fmin(x0, xv);
-      x1 = fmax(x1, xv);
-      y0 = fmin(y0, yv);
-      y1 = fmax(y1, yv);
-      // EventSet checks (types.hpp:85-109): finite, t >= 0, nondecreasing
-      const double prev = i > 0 ? t[i - 1] : 0.0;
-      const bool ok = isfinite(xv) && isfinite(yv) && isfinite(tv) && tv >= prev;
-      if (!ok && i < first_bad) first_bad = i;
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      first_bad = min(first_bad, static_cast<int64_t>(__shfl_xor_sync(
-                                     0xffffffffu, static_cast<long long>(first_bad), off)));
-    }
-    if (lane == 0 && first_bad != INT64_MAX) {
-      atomicMin(bad, static_cast<unsigned long long>(first_bad));
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, off));
-      x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, off));
-      y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, off));
-      y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, off));
-    }
-    if (lane == 0) {
-      const double4 b = make_double4(x0, x1, y0, y1);
-      box[tile] = b;
-      trange[tile] = make_double2(t[first], t[last - 1]);
-      // extents relative to event 0, the tile's time span
+  if (tile < nt) {
+    const double2 tr = trange[tile];
+    if (lane == 0) {  // extents relative to event 0, the tile's time span
+      const double4 b = box[tile];
       const double x00 = x[0], y00 = y[0];
-      const double e[3] = {fmax(fabs(x0 - x00), fabs(x1 - x00)), fmax(fabs(y0 - y00), fabs(y1 - y00)),
-                           t[last - 1] - t[first]};
+      const double e[3] = {fmax(fabs(b.x - x00), fabs(b.y - x00)), fmax(fabs(b.z - y00), fabs(b.w - y00)),
+                           tr.y - tr.x};
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         atomicMax(&s_st[q], static_cast<unsigned long long>(__double_as_longlong(fmax(e[q], 0.0))));
@@ -1581,15 +1619,14 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
     // lanes 0..15: the gap a = lane + 1 stages ahead of the tile's first event
     // (t[first] - t[first - 128 a - 1]); lanes 16..31: the span of 2^L whole
     // tiles from this one, L = lane - 16
-    const int64_t nt = (n + kTS - 1) / kTS;
     double v = __longlong_as_double(0x7ff0000000000000LL);
     if (lane < kLoadAdj) {
       const int64_t a = lane + 1;
-      if (tile >= a + 1) v = t[first] - t[(tile - a) * kTS - 1];
+      if (tile >= a + 1) v = tr.x - trange[tile - a - 1].y;
     } else {
       const int64_t L = lane - kLoadAdj;
       if (L < kLoadSpan && tile + (int64_t{1} << L) - 1 < nt) {
-        v = t[min((tile + (int64_t{1} << L)) * kTS, n) - 1] - t[first];
+        v = trange[tile + (int64_t{1} << L) - 1].y - tr.x;
       }
     }
     if (lane < kLoadAdj + kLoadSpan) {
@@ -1601,8 +1638,6 @@ __global__ void tile_box_kernel(double* __restrict__ x, double* __restrict__ y,
     if (q < 3) atomicMax(&dstats[q], s_st[q]);
     else atomicMin(&dstats[q], s_st[q]);
   }
-  // the last block out hands the first bad index and the load statistics to
-  // the host (mapped) and re-arms the device copies for the next load
   __shared__ bool s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1922,14 +1957,17 @@ cudaError_t launch_fx_accumulate(const FxAccArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
-                              double4* box, double2* trange, double* piv,
-                              unsigned long long* bad, unsigned int* done,
-                              unsigned long long* h_bad, double* h_stats,
+cudaError_t launch_tile_boxes(const double* sx, const double* sy, const double* st, double* x,
+                              double* y, double* t, int64_t n, int64_t npad, double4* box,
+                              double2* trange, double* piv, unsigned long long* bad,
+                              unsigned int* done, unsigned long long* h_bad, double* h_stats,
                               unsigned long long* dstats, bool tile_pivots, cudaStream_t stream) {
   const int64_t ntiles = (n + kTS - 1) / kTS;
-  tile_box_kernel<<<static_cast<unsigned>((ntiles + 7) / 8), 256, 0, stream>>>(
-      x, y, t, n, npad, box, trange, piv, bad, done, h_bad, h_stats, dstats, tile_pivots);
+  const unsigned blocks = static_cast<unsigned>((ntiles + 7) / 8);
+  tile_load_kernel<<<blocks, 256, 0, stream>>>(sx, sy, st, x, y, t, n, npad, box, trange, piv, bad,
+                                               tile_pivots);
+  tile_stats_kernel<<<blocks, 256, 0, stream>>>(x, y, t, n, box, trange, piv, tile_pivots, bad, done,
+                                                h_bad, h_stats, dstats);
   return cudaGetLastError();
 }
 

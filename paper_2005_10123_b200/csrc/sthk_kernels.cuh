@@ -274,18 +274,19 @@ constexpr int kLoadAdj = 16;
 constexpr int kLoadSpan = 16;
 constexpr int kLoadStats = 3 + kLoadAdj + kLoadSpan;
 
-// Per-tile bounding boxes and time ranges, and the plan's search pivots
-// (dstats: kLoadStats device words, maxima 0 / minima +inf bits, re-armed by
-// the kernel)
-// (PlanArgs::piv); also zeroes the pad tail [n, npad)
-// of x, y, t and runs the EventSet checks (finite, t >= 0, sorted). The
-// kernel's last block writes the first failing index (all ones: none) to
-// *h_bad and the load statistics to h_stats (both host-mapped), and re-arms
-// *bad (device, all ones between loads) and *done (0).
-cudaError_t launch_tile_boxes(double* x, double* y, double* t, int64_t n, int64_t npad,
-                              double4* box, double2* trange, double* piv,
-                              unsigned long long* bad, unsigned int* done,
-                              unsigned long long* h_bad, double* h_stats,
+// Event load into x, y, t from sources sx, sy, st -- the caller's pinned
+// host arrays (device-mapped: the load kernel itself is the H2D copy) or x,
+// y, t themselves after a cudaMemcpy -- with the per-tile bounding boxes and
+// time ranges, the plan's search pivots (PlanArgs::piv), the pad tail zeroed
+// and the EventSet checks (finite, t >= 0, sorted). The second kernel's last
+// block writes the first failing index (all ones: none) to *h_bad and the
+// load statistics to h_stats (both host-mapped), and re-arms *bad (device,
+// all ones between loads), *done (0) and dstats (kLoadStats device words,
+// maxima 0 / minima +inf bits).
+cudaError_t launch_tile_boxes(const double* sx, const double* sy, const double* st, double* x,
+                              double* y, double* t, int64_t n, int64_t npad, double4* box,
+                              double2* trange, double* piv, unsigned long long* bad,
+                              unsigned int* done, unsigned long long* h_bad, double* h_stats,
                               unsigned long long* dstats, bool tile_pivots, cudaStream_t stream);
 // Tile pivots (tile last times, tile-granular plan searches) are used up to
 // kPlanPivots tiles; above, strided pivots t[k ceil(n / kPlanPivots)].

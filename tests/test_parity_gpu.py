@@ -409,9 +409,15 @@ def test_engine_event_checks_match_reference_messages(engine):
     big_t = np.sort(np.random.default_rng(1).uniform(0, 100, 5000))
     big_t[4321] = big_t[4320] - 1e-9
     cases.append(((np.zeros(5000), np.zeros(5000), big_t, 200.0), "times not sorted at index 4321"))
+    import torch
+
+    def pinned(a):  # (pinned host arrays take the zero-copy load kernel)
+        return torch.from_numpy(np.asarray(a, float)).pin_memory().numpy()
+
     for (x, y, t, we), msg in cases:
-        with pytest.raises(ValueError, match=msg):
-            engine.load_events(np.asarray(x, float), np.asarray(y, float), np.asarray(t, float), we)
+        for conv in (lambda a: np.asarray(a, float), pinned):
+            with pytest.raises(ValueError, match=msg):
+                engine.load_events(conv(x), conv(y), conv(t), we)
     # a failed load leaves the engine without events; a good load recovers
     ev = pk.generateBenchmarkCloud(300, pk.SimWindow(0, 4, 0, 4, 60), 5)
     engine.load(ev)
@@ -950,3 +956,25 @@ def test_shell_bound_culls_bursty_against_oracle(engine, seed):
         assert ok and o["valid"]
         assert abs(ll - o["loglik"]) <= 1e-12 * abs(o["loglik"]), (theta, ll, o["loglik"], st["exec_far"])
         assert np.all(np.abs(g - o["grad"]) <= 1e-10 * o["grad_abs"]), (theta, g, o["grad"])
+
+
+def test_pinned_zero_copy_load_bitwise_equals_pageable_load(engine):
+    """Pinned host arrays are read by the load kernel itself over PCIe
+    (zero-copy); pageable ones are copied first. Same device data, same load
+    statistics, bitwise-identical results (C2 at both Theta and a partial tile)."""
+    import torch
+    for keep in (85000, 85000 - 77):
+        ev = _c2(keep)
+        res = []
+        for pin in (False, True):
+            x, y, t = ev.xs(), ev.ys(), ev.ts()
+            if pin:
+                x, y, t = (torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for a in (x, y, t))
+            engine.load_events(x, y, t, ev.windowEnd())
+            out = []
+            for th in ([0.66, 1.6, 14, 0.344, 1440, 0.0695], [1, 1.6, 14, 0.1, 1, 1]):
+                engine.set_params(th)
+                ll, ok, g, pe = engine.loglik_grad(per_event=True)
+                out.append((ll, ok, tuple(g), pe.tobytes()))
+            res.append(out)
+        assert res[0] == res[1]
