@@ -206,6 +206,10 @@ struct GraphOp {
   size_t bytes = 0;
   int value = 0;
   cudaMemcpyKind ckind = cudaMemcpyDefault;
+  // kernels: 1 = programmatic dependency on the previous kernel of the same
+  // stream (the kernel waits with griddepcontrol.wait; it may launch while
+  // that one drains)
+  int dep_kind = 0;
 };
 
 struct OpSink final : sthk::LaunchSink {
@@ -1137,6 +1141,13 @@ cudaError_t op_memcpy(sthk_engine& e, void* dst, const void* src, size_t bytes, 
   return cudaSuccess;
 }
 
+// (graph mode: annotate the kernel just recorded with a dependency kind, see
+// GraphOp::dep_kind; no effect with direct launches)
+void mark_last_kernel(sthk_engine& e, int kind) {
+  if (!e.recording || e.ops.empty() || e.ops.back().kind != GraphOp::kKernel) return;
+  e.ops.back().dep_kind = kind;
+}
+
 // Topology signature of a recorded evaluation: every operation's kind,
 // stream, event, and for kernels the function and launch shape, for copies
 // and memsets their operands (FNV-1a). Kernel arguments are not part of it:
@@ -1159,6 +1170,7 @@ uint64_t ops_signature(const std::vector<GraphOp>& ops) {
       mix((static_cast<uint64_t>(op.grid.x) << 32) | op.block.x);
       mix(op.smem);
       mix(op.args.size());
+      mix(static_cast<uint64_t>(op.dep_kind));
     } else if (op.kind == GraphOp::kMemset || op.kind == GraphOp::kMemcpy) {
       mix(reinterpret_cast<uint64_t>(op.dst));
       mix(reinterpret_cast<uint64_t>(op.src));
@@ -1192,6 +1204,13 @@ GraphEntry build_graph(const std::vector<GraphOp>& ops) {
       evn.push_back({ev, {}});
       return evn.back().second;
     };
+    std::vector<std::pair<cudaStream_t, cudaGraphNode_t>> last_kernel;
+    auto last_kernel_of = [&](cudaStream_t st) -> cudaGraphNode_t {
+      for (auto& kv : last_kernel) {
+        if (kv.first == st) return kv.second;
+      }
+      return nullptr;
+    };
     for (const GraphOp& op : ops) {
       std::vector<cudaGraphNode_t>& deps = tail_of(op.st);
       cudaGraphNode_t nd = nullptr;
@@ -1204,7 +1223,33 @@ GraphEntry build_graph(const std::vector<GraphOp>& ops) {
           kp.sharedMemBytes = static_cast<unsigned>(op.smem);
           void* argp = const_cast<unsigned char*>(op.args.data());
           kp.kernelParams = &argp;
-          ck(cudaGraphAddKernelNode(&nd, g.graph, deps.data(), deps.size(), &kp), "graph kernel");
+          // programmatic edge from the previous kernel of this stream (taken
+          // out of the full-completion dependencies)
+          cudaGraphNode_t prog_from = nullptr;
+          std::vector<cudaGraphNode_t> full = deps;
+          if (op.dep_kind == 1) {
+            cudaGraphNode_t prev = last_kernel_of(op.st);
+            auto it = std::find(full.begin(), full.end(), prev);
+            if (prev && it != full.end()) {
+              full.erase(it);
+              prog_from = prev;
+            }
+          }
+          ck(cudaGraphAddKernelNode(&nd, g.graph, full.data(), full.size(), &kp), "graph kernel");
+          if (prog_from) {
+            cudaGraphEdgeData ed{};
+            ed.type = cudaGraphDependencyTypeProgrammatic;
+            ed.from_port = cudaGraphKernelNodePortProgrammatic;
+            ck(cudaGraphAddDependencies_v2(g.graph, &prog_from, &nd, &ed, 1), "graph edge");
+          }
+          bool found = false;
+          for (auto& kv : last_kernel) {
+            if (kv.first == op.st) {
+              kv.second = nd;
+              found = true;
+            }
+          }
+          if (!found) last_kernel.push_back({op.st, nd});
           g.knodes.push_back(nd);
           g.kargs.push_back(op.args);
           break;
@@ -1664,7 +1709,9 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     // latency: measured 5 us at N = 10k)
     // (graph mode: without this node the far kernel's CTAs reach the SMs
     // first and the near kernel starts 20 us later -- measured 4.5% slower at
-    // C2; graph node priorities do not change that order)
+    // C2; graph node priorities do not change that order, and a
+    // launch-completion edge from the trigger-free kernel to the far kernel
+    // defers the far kernel behind the general one: 1.5% slower)
     ck((e.timing && e.timing_pairs && !stamps) || bg_split
            ? record_timing(e, s.ev[1], st)
            : op_record(e, s.ev[1], st),
@@ -1786,6 +1833,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       fa.tstamp = stamps ? s.tstamp : nullptr;
       fa.tstamp_out = s.d_htstamp;
       ck(sthk::launch_finalize(fa, grad, s.stream), "finalize");
+      mark_last_kernel(e, 1);  // (graph mode: launched while the last pair kernel drains)
       e.launches += 1;
     }
     ck(op_record(e, s.fin_done, s.stream), "event");

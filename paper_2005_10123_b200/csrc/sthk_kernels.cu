@@ -1277,6 +1277,9 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
     if (a.trace && tid == 0) trace_item(a, item, nst, s_begin <= first && first < s_end, s_trace_t0);
   }
 
+  // (no more items for this CTA: a programmatically dependent kernel may
+  // start launching -- it still waits for this grid's completion)
+  asm volatile("griddepcontrol.launch_dependents;");
   if (tid == 0) {  // the last CTA out re-arms the work counter for the next launch
     __threadfence();
     if (atomicAdd(a.done_counter, 1u) == gridDim.x - 1) {
@@ -1753,6 +1756,9 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
   __shared__ double s_red[kNOut][kFinThreads];
   const int tid = threadIdx.x;
   __shared__ unsigned long long s_cta_t0;  // (development trace)
+  // (graph mode: launched by a programmatic edge while the last pair kernel
+  // drains; wait for its completion and memory -- a no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (a.trace && tid == 0) s_cta_t0 = global_ns();
   if (tid == 0) stamp_min(a.tstamp, 0);
   const int64_t base = static_cast<int64_t>(a.row0) + static_cast<int64_t>(blockIdx.x) * kFB;
