@@ -969,7 +969,7 @@ def test_pinned_zero_copy_load_bitwise_equals_pageable_load(engine):
         for pin in (False, True):
             x, y, t = ev.xs(), ev.ys(), ev.ts()
             if pin:
-                x, y, t = (torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for a in (x, y, t))
+                x, y, t = (torch.from_numpy(np.array(a, dtype=np.float64)).pin_memory().numpy() for a in (x, y, t))
             engine.load_events(x, y, t, ev.windowEnd())
             out = []
             for th in ([0.66, 1.6, 14, 0.344, 1440, 0.0695], [1, 1.6, 14, 0.1, 1, 1]):
