@@ -74,15 +74,15 @@ SIGNATURES = [
     ("sthk_create_rank_hosted", c_int,
      [c_int, c_int, c_int, POINTER(HostCommStruct), POINTER(c_void_p)]),
     ("sthk_destroy", c_int, [c_void_p]),
-    ("sthk_load_events", c_int, [c_void_p, _DPTR, _DPTR, _DPTR, c_int64, c_double]),
-    ("sthk_set_params", c_int, [c_void_p, _DPTR]),
-    ("sthk_loglik", c_int, [c_void_p, _DPTR, _IPTR, _DPTR]),
-    ("sthk_loglik_grad", c_int, [c_void_p, _DPTR, _IPTR, _DPTR, _DPTR]),
+    ("sthk_load_events", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_double]),
+    ("sthk_set_params", c_int, [c_void_p, c_void_p]),
+    ("sthk_loglik", c_int, [c_void_p, _DPTR, _IPTR, c_void_p]),
+    ("sthk_loglik_grad", c_int, [c_void_p, _DPTR, _IPTR, c_void_p, c_void_p]),
     ("sthk_loglik_batch", c_int, [c_void_p, _DPTR, c_int64, _DPTR, _IPTR, _DPTR]),
     ("sthk_excitation", c_int, [c_void_p, _DPTR, _DPTR, _DPTR]),
     ("sthk_excitation_batch", c_int, [c_void_p, _DPTR, c_int64, _DPTR, _DPTR, POINTER(c_int64)]),
     ("sthk_enqueue", c_int, [c_void_p, c_int, c_int]),
-    ("sthk_result", c_int, [c_void_p, _DPTR, _IPTR, _DPTR, _DPTR]),
+    ("sthk_result", c_int, [c_void_p, _DPTR, _IPTR, c_void_p, c_void_p]),
     ("sthk_set_timing", c_int, [c_void_p, c_int]),
     ("sthk_get_stats", c_int, [c_void_p, POINTER(StatsStruct)]),
     ("sthk_get_stream", c_int, [c_void_p, c_int, POINTER(c_void_p)]),

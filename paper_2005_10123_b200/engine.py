@@ -28,6 +28,10 @@ def _dptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.POINTER(c_double))
 
 
+def _vptr(a):  # (c_void_p arguments of the per-evaluation calls: cheaper than data_as)
+    return None if a is None else a.ctypes.data
+
+
 class Engine:
     """Stateful device engine: events stay resident in HBM across calls.
 
@@ -119,7 +123,7 @@ class Engine:
         if x.size != n or y.size != n:
             raise ValueError("EventSet: coordinate/time length mismatch")
         self._events_key = None  # (a failed load leaves the engine without events)
-        self._check(self._lib.sthk_load_events(self._h, _dptr(x), _dptr(y), _dptr(t), n,
+        self._check(self._lib.sthk_load_events(self._h, _vptr(x), _vptr(y), _vptr(t), n,
                                                float(window_end)), "sthk_load_events")
         self._n = n
 
@@ -135,21 +139,19 @@ class Engine:
     def set_params(self, params) -> None:
         p = params.as_array() if isinstance(params, Params) else np.asarray(params, np.float64)
         p = np.ascontiguousarray(p, dtype=np.float64)
-        self._check(self._lib.sthk_set_params(self._h, _dptr(p)), "sthk_set_params")
+        self._check(self._lib.sthk_set_params(self._h, _vptr(p)), "sthk_set_params")
 
     def loglik(self, per_event: bool = False):
         ll, ok = c_double(), c_int()
         pe = np.zeros(self._n) if per_event else None
-        self._check(self._lib.sthk_loglik(self._h, byref(ll), byref(ok),
-                                          _dptr(pe) if pe is not None else None), "sthk_loglik")
+        self._check(self._lib.sthk_loglik(self._h, byref(ll), byref(ok), _vptr(pe)), "sthk_loglik")
         return ll.value, bool(ok.value), pe
 
     def loglik_grad(self, per_event: bool = False):
         ll, ok = c_double(), c_int()
         g = np.zeros(6)
         pe = np.zeros(self._n) if per_event else None
-        self._check(self._lib.sthk_loglik_grad(self._h, byref(ll), byref(ok), _dptr(g),
-                                               _dptr(pe) if pe is not None else None),
+        self._check(self._lib.sthk_loglik_grad(self._h, byref(ll), byref(ok), _vptr(g), _vptr(pe)),
                     "sthk_loglik_grad")
         return ll.value, bool(ok.value), g, pe
 
@@ -195,8 +197,8 @@ class Engine:
         ll, ok = c_double(), c_int()
         g = np.zeros(6)
         pe = np.zeros(self._n) if per_event else None
-        self._check(self._lib.sthk_result(self._h, byref(ll), byref(ok), _dptr(g),
-                                          _dptr(pe) if pe is not None else None), "sthk_result")
+        self._check(self._lib.sthk_result(self._h, byref(ll), byref(ok), _vptr(g), _vptr(pe)),
+                    "sthk_result")
         return ll.value, bool(ok.value), g, pe
 
     def set_bgonly_kernel(self, on: bool) -> None:
