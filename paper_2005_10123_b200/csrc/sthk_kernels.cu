@@ -1725,8 +1725,33 @@ __global__ void exp_probe_kernel(const double* __restrict__ x, int64_t n, double
 // ---------------------------------------------------------------------------
 // Fixed-order sum of the block partials by one 256-thread block: thread t
 // sums blocks t, t+256, ... in order, then a fixed tree over the threads.
+// Fixed-order sum of kNOut values over a 256-thread block: a butterfly
+// within each warp (every lane ends with the same bits: each add is
+// commutative), then the 8 warp totals in warp order. Two barriers instead
+// of a shared-memory tree's eight.
+__device__ __forceinline__ void block_sum8(double (&v)[kNOut], double (*s_w)[kNOut]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int q = 0; q < kNOut; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < kNOut; ++q) s_w[warp][q] = v[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < kNOut) {
+    const int q = threadIdx.x;
+    double r = s_w[0][q];
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) r += s_w[w][q];
+    v[0] = r;  // (thread q holds the block total of output q)
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void final_sum_block(const double* __restrict__ bp, int nblocks,
-                                                double* out, double (*s_red)[256]) {
+                                                double* out, double (*s_w)[kNOut]) {
   const int tid = threadIdx.x;
   double acc[kNOut];
 #pragma unroll
@@ -1735,17 +1760,8 @@ __device__ __forceinline__ void final_sum_block(const double* __restrict__ bp, i
 #pragma unroll
     for (int q = 0; q < kNOut; ++q) acc[q] += bp[static_cast<size_t>(b) * kNOut + q];
   }
-#pragma unroll
-  for (int q = 0; q < kNOut; ++q) s_red[q][tid] = acc[q];
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (tid < w) {
-#pragma unroll
-      for (int q = 0; q < kNOut; ++q) s_red[q][tid] += s_red[q][tid + w];
-    }
-    __syncthreads();
-  }
-  if (tid < kNOut) out[tid] = s_red[tid][0];
+  block_sum8(acc, s_w);
+  if (tid < kNOut) out[tid] = acc[0];
 }
 
 template <bool GRAD>
@@ -1753,7 +1769,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   constexpr int NB = GRAD ? 3 : 1;
   constexpr int NT = NS - NB;
-  __shared__ double s_red[kNOut][kFinThreads];
+  __shared__ double s_w[kFinThreads / 32][kNOut];
   const int tid = threadIdx.x;
   __shared__ unsigned long long s_cta_t0;  // (development trace)
   // (graph mode: launched by a programmatic edge while the last pair kernel
@@ -1850,19 +1866,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
     }
   } while (false);
 
-#pragma unroll
-  for (int q = 0; q < kNOut; ++q) s_red[q][tid] = acc[q];
-  __syncthreads();
-  for (int w = kFinThreads / 2; w > 0; w >>= 1) {
-    if (tid < w) {
-#pragma unroll
-      for (int q = 0; q < kNOut; ++q) s_red[q][tid] += s_red[q][tid + w];
-    }
-    __syncthreads();
-  }
-  if (tid < kNOut) {
-    a.block_partial[(base / kFB) * kNOut + tid] = s_red[tid][0];
-  }
+  block_sum8(acc, s_w);
+  if (tid < kNOut) a.block_partial[(base / kFB) * kNOut + tid] = acc[0];
   if (a.fused_out) {  // single shard: the last block to finish does the final sum
     __shared__ bool s_last;
     __syncthreads();
@@ -1873,7 +1878,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
     __syncthreads();
     if (s_last) {
       __threadfence();
-      final_sum_block(a.block_partial, a.nblocks_total, a.fused_out, s_red);
+      final_sum_block(a.block_partial, a.nblocks_total, a.fused_out, s_w);
       if (a.counts && tid < kNCounts) {
         a.counts_out[tid] = a.counts[tid];
         a.counts[tid] = 0ULL;
@@ -1893,8 +1898,8 @@ __global__ void __launch_bounds__(256) final_sum_kernel(const double* __restrict
                                                         int nblocks, double* out,
                                                         unsigned long long* counts,
                                                         unsigned long long* counts_out) {
-  __shared__ double s_red[kNOut][256];
-  if (out) final_sum_block(bp, nblocks, out, s_red);
+  __shared__ double s_w[8][kNOut];
+  if (out) final_sum_block(bp, nblocks, out, s_w);
   if (counts && threadIdx.x < kNCounts) {
     counts_out[threadIdx.x] = counts[threadIdx.x];
     counts[threadIdx.x] = 0ULL;

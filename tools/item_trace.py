@@ -19,12 +19,20 @@ else:
     n = int(which)
     ev = pk.generateBenchmarkCloud(n, pk.SimWindow(0, 15, 0, 15, 4750), n)
 e = pk.Engine((0,))
-e.set_background_cache(False)
+move = os.environ.get("IT_MOVE")  # (h / omega / mu0: a cached MH-style move from theta)
+e.set_background_cache(move is not None)
 e.set_timing(os.environ.get("IT_TIMING", "1") == "1")
 e.load(ev)
 e.set_params(theta)
 for _ in range(5):
     e.loglik_grad()
+if move:
+    k = {"mu0": 0, "theta": 3, "omega": 4, "h": 5}[move]
+    for i in range(5):
+        th2 = list(theta)
+        th2[k] *= 1.0 + 0.01 * (i + 1)
+        e.set_params(th2)
+        e.loglik_grad()
 st = e.stats()
 raw = e.item_trace()
 cta = raw[raw[:, 2] == 0xFFFFFFFF]
@@ -62,6 +70,8 @@ for k in (2, 1, 3):
     print(f"      ends: p10 {ends[len(ends) // 10]:.1f} p50 {ends[len(ends) // 2]:.1f} "
           f"p90 {ends[9 * len(ends) // 10]:.1f} max {ends[-1]:.1f} us")
 # concurrency profile: items in flight per 2 us bin
+if len(tr) == 0:
+    sys.exit(0)
 t1 = (tr[:, 6].max() - t00) / 1e3
 bins = np.arange(0, t1 + 2, 2.0)
 line = []
