@@ -235,6 +235,7 @@ struct OpSink final : sthk::LaunchSink {
 // the arguments they were last set to.
 struct GraphEntry {
   uint64_t sig = 0;
+  std::vector<uint64_t> key;  // full topology (ops_topology)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   std::vector<cudaGraphNode_t> knodes;
@@ -1148,35 +1149,42 @@ void mark_last_kernel(sthk_engine& e, int kind) {
   e.ops.back().dep_kind = kind;
 }
 
-// Topology signature of a recorded evaluation: every operation's kind,
-// stream, event, and for kernels the function and launch shape, for copies
-// and memsets their operands (FNV-1a). Kernel arguments are not part of it:
-// they are updated in place on a matching graph.
-uint64_t ops_signature(const std::vector<GraphOp>& ops) {
+// Topology of a recorded evaluation: every operation's kind, stream, event,
+// and for kernels the function, launch shape and dependency kind, for copies
+// and memsets their operands. Kernel arguments are not part of it: they are
+// updated in place on a graph of the same topology (looked up by its FNV-1a
+// hash, confirmed by comparing the full key).
+std::vector<uint64_t> ops_topology(const std::vector<GraphOp>& ops) {
+  std::vector<uint64_t> key;
+  key.reserve(8 * ops.size() + 1);
+  key.push_back(ops.size());
+  for (const GraphOp& op : ops) {
+    key.push_back(static_cast<uint64_t>(op.kind));
+    key.push_back(reinterpret_cast<uint64_t>(op.st));
+    key.push_back(reinterpret_cast<uint64_t>(op.ev));
+    if (op.kind == GraphOp::kKernel) {
+      key.push_back(reinterpret_cast<uint64_t>(op.func));
+      key.push_back((static_cast<uint64_t>(op.grid.x) << 32) | op.block.x);
+      key.push_back(op.smem);
+      key.push_back(op.args.size());
+      key.push_back(static_cast<uint64_t>(op.dep_kind));
+    } else if (op.kind == GraphOp::kMemset || op.kind == GraphOp::kMemcpy) {
+      key.push_back(reinterpret_cast<uint64_t>(op.dst));
+      key.push_back(reinterpret_cast<uint64_t>(op.src));
+      key.push_back(op.bytes);
+      key.push_back(static_cast<uint64_t>(op.value));
+      key.push_back(static_cast<uint64_t>(op.ckind));
+    }
+  }
+  return key;
+}
+
+uint64_t fnv1a(const std::vector<uint64_t>& key) {
   uint64_t h = 1469598103934665603ULL;
-  auto mix = [&](uint64_t v) {
+  for (const uint64_t v : key) {
     for (int b = 0; b < 8; ++b) {
       h ^= (v >> (8 * b)) & 0xff;
       h *= 1099511628211ULL;
-    }
-  };
-  mix(ops.size());
-  for (const GraphOp& op : ops) {
-    mix(static_cast<uint64_t>(op.kind));
-    mix(reinterpret_cast<uint64_t>(op.st));
-    mix(reinterpret_cast<uint64_t>(op.ev));
-    if (op.kind == GraphOp::kKernel) {
-      mix(reinterpret_cast<uint64_t>(op.func));
-      mix((static_cast<uint64_t>(op.grid.x) << 32) | op.block.x);
-      mix(op.smem);
-      mix(op.args.size());
-      mix(static_cast<uint64_t>(op.dep_kind));
-    } else if (op.kind == GraphOp::kMemset || op.kind == GraphOp::kMemcpy) {
-      mix(reinterpret_cast<uint64_t>(op.dst));
-      mix(reinterpret_cast<uint64_t>(op.src));
-      mix(op.bytes);
-      mix(static_cast<uint64_t>(op.value));
-      mix(static_cast<uint64_t>(op.ckind));
     }
   }
   return h;
@@ -1304,9 +1312,10 @@ void launch_recorded(sthk_engine& e, cudaStream_t st) {
   constexpr size_t kMaxGraphs = 16;
   e.recording = false;
   sthk::set_launch_sink(nullptr);
-  const uint64_t sig = ops_signature(e.ops);
+  std::vector<uint64_t> key = ops_topology(e.ops);
+  const uint64_t sig = fnv1a(key);
   auto it = std::find_if(e.graphs.begin(), e.graphs.end(),
-                         [&](const GraphEntry& g) { return g.sig == sig; });
+                         [&](const GraphEntry& g) { return g.sig == sig && g.key == key; });
   if (it != e.graphs.end()) {
     std::rotate(e.graphs.begin(), it, it + 1);  // most recently used first
     GraphEntry& g = e.graphs.front();
@@ -1330,6 +1339,7 @@ void launch_recorded(sthk_engine& e, cudaStream_t st) {
   } else {
     GraphEntry g = build_graph(e.ops);
     g.sig = sig;
+    g.key = std::move(key);
     ++e.graph_instantiations;
     if (e.graphs.size() >= kMaxGraphs) {
       cudaGraphExecDestroy(e.graphs.back().exec);
