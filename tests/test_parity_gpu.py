@@ -978,3 +978,27 @@ def test_pinned_zero_copy_load_bitwise_equals_pageable_load(engine):
                 out.append((ll, ok, tuple(g), pe.tobytes()))
             res.append(out)
         assert res[0] == res[1]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 127, 128, 129, 255, 256, 257, 1023, 1025])
+def test_tile_boundary_sizes_against_oracle(engine, n):
+    """Event counts around the 128-event tile and 1024-row block boundaries
+    (partial tiles, a single event, one row per block): loglik and gradient
+    against the long-double oracle, through the graph path and both load
+    paths (pinned zero-copy and pageable)."""
+    import torch
+    rng = np.random.default_rng(n)
+    t = np.sort(rng.uniform(0, 40, n))
+    x, y = rng.uniform(0, 3, n), rng.uniform(0, 3, n)
+    p = np.array([0.7, 0.8, 4.0, 0.4, 1.5, 0.3])
+    o = og.oracle_loglik_grad(x, y, t, float(t[-1]) + 1.0, p)
+    for pin in (False, True):
+        arrs = [np.array(a) for a in (x, y, t)]
+        if pin:
+            arrs = [torch.from_numpy(a).pin_memory().numpy() for a in arrs]
+        engine.load_events(*arrs, float(t[-1]) + 1.0)
+        engine.set_params(p)
+        ll, ok, g, _ = engine.loglik_grad()
+        assert ok == o["valid"]
+        assert abs(ll - o["loglik"]) <= 1e-12 * abs(o["loglik"]), (n, pin, ll, o["loglik"])
+        assert np.all(np.abs(g - o["grad"]) <= 1e-10 * o["grad_abs"] + 1e-300), (n, pin, g, o["grad"])
