@@ -1002,3 +1002,59 @@ def test_tile_boundary_sizes_against_oracle(engine, n):
         assert ok == o["valid"]
         assert abs(ll - o["loglik"]) <= 1e-12 * abs(o["loglik"]), (n, pin, ll, o["loglik"])
         assert np.all(np.abs(g - o["grad"]) <= 1e-10 * o["grad_abs"] + 1e-300), (n, pin, g, o["grad"])
+
+
+def test_full_size_metamorphic_identities(engine):
+    """Size-independent identities of the model, checked on the C2 workload
+    itself (85,000 events) without an oracle:
+      * translation and rotation of space leave loglik and gradient unchanged;
+      * scaling space by s with tauX, h scaled alike: loglik - 2 N ln s, and
+        d/dtauX, d/dh scale by 1/s;
+      * scaling time by s (t, T, tauT scaled; omega / s): loglik - N ln s,
+        d/dtauT by 1/s, d/domega by s.
+    (to 1e-11 relative: the inputs are rounded differently)"""
+    ev = _c2()
+    x, y, t, T = ev.xs(), ev.ys(), ev.ts(), ev.windowEnd()
+    n = t.size
+    for theta in ([0.66, 1.6, 14, 0.344, 1440, 0.0695], [1, 1.6, 14, 0.1, 1, 1]):
+        p = np.array(theta)
+
+        def run(xx, yy, tt, TT, pp):
+            engine.load_events(np.ascontiguousarray(xx), np.ascontiguousarray(yy),
+                               np.ascontiguousarray(tt), TT)
+            engine.set_params(pp)
+            ll, ok, g, _ = engine.loglik_grad()
+            assert ok
+            return ll, g.copy()
+
+        ll0, g0 = run(x, y, t, T, p)
+        gs = np.abs(g0) + 1e-300
+
+        ang = 0.7
+        xr = np.cos(ang) * x - np.sin(ang) * y + 123.456
+        yr = np.sin(ang) * x + np.cos(ang) * y - 78.9
+        ll1, g1 = run(xr, yr, t, T, p)
+        assert abs(ll1 - ll0) <= 1e-11 * abs(ll0), (theta, ll0, ll1)
+        assert np.all(np.abs(g1 - g0) <= 1e-9 * gs), (theta, g0, g1)
+
+        s = 1.7
+        ps = p.copy()
+        ps[1] *= s
+        ps[5] *= s
+        ll2, g2 = run(s * x, s * y, t, T, ps)
+        assert abs(ll2 - (ll0 - 2 * n * np.log(s))) <= 1e-11 * abs(ll0), (theta, ll0, ll2)
+        want = g0.copy()
+        want[1] /= s
+        want[5] /= s
+        assert np.all(np.abs(g2 - want) <= 1e-9 * gs), (theta, want, g2)
+
+        st = 2.3
+        pt = p.copy()
+        pt[2] *= st
+        pt[4] /= st
+        ll3, g3 = run(x, y, st * t, st * T, pt)
+        assert abs(ll3 - (ll0 - n * np.log(st))) <= 1e-11 * abs(ll0), (theta, ll0, ll3)
+        want = g0.copy()
+        want[2] /= st
+        want[4] *= st
+        assert np.all(np.abs(g3 - want) <= 1e-9 * gs), (theta, want, g3)
