@@ -1058,3 +1058,32 @@ def test_full_size_metamorphic_identities(engine):
         want[2] /= st
         want[4] *= st
         assert np.all(np.abs(g3 - want) <= 1e-9 * gs), (theta, want, g3)
+
+
+def test_c4_1m_scaling_identities(engine):
+    """The space and time scaling identities (see the C2 test above) on the C4
+    workload, N = 1,000,000: loglik - 2 N ln s and - N ln s, to 1e-11."""
+    ev = pk.generateBenchmarkCloud(1_000_000, pk.SimWindow(0, 15, 0, 15, 4750), 1_000_000)
+    x, y, t, T = ev.xs(), ev.ys(), ev.ts(), ev.windowEnd()
+    n = t.size
+    p = np.array([0.66, 1.6, 14, 0.344, 1440, 0.0695])
+
+    def run(xx, yy, tt, TT, pp):
+        engine.load_events(np.ascontiguousarray(xx), np.ascontiguousarray(yy),
+                           np.ascontiguousarray(tt), TT)
+        engine.set_params(pp)
+        ll, ok = engine.loglik()[:2]
+        assert ok
+        return ll
+
+    ll0 = run(x, y, t, T, p)
+    s = 1.7
+    ps = p.copy()
+    ps[1] *= s
+    ps[5] *= s
+    assert abs(run(s * x, s * y, t, T, ps) - (ll0 - 2 * n * np.log(s))) <= 1e-11 * abs(ll0)
+    st = 2.3
+    pt = p.copy()
+    pt[2] *= st
+    pt[4] /= st
+    assert abs(run(x, y, st * t, st * T, pt) - (ll0 - n * np.log(st))) <= 1e-11 * abs(ll0)
