@@ -220,19 +220,6 @@ __device__ __forceinline__ int item_stages(int sc, int2 rg, int chunk) {
 
 constexpr int kPlanBins = 1024;  // item-size classes (stages, clamped)
 
-// atomicAdd(&hist[bin], 1) aggregated over the active lanes of the warp that
-// hit the same bin (one shared-memory atomic per distinct bin: most items of
-// a list share a few sizes); returns this lane's old-value slot.
-__device__ __forceinline__ int warp_agg_add(int* hist, int bin) {
-  const unsigned active = __activemask();
-  const unsigned same = __match_any_sync(active, bin);
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(same) - 1;
-  int base = 0;
-  if (lane == leader) base = atomicAdd(&hist[bin], __popc(same));
-  base = __shfl_sync(active, base, leader);
-  return base + __popc(same & ((1u << lane) - 1u));
-}
 
 // Single CTA: per-tile ranges, then the (tile, chunk) work list ordered by
 // decreasing item size (a counting sort on the stage count), so the
@@ -257,10 +244,14 @@ constexpr int kPlanLists = 3;
 
 // (my_rg / my_cr: this thread's first tile per list, kept in registers since
 // the range phase)
+// (per tile and list the first and the last chunk may be partial; every chunk
+// between them is a full chunk of sc / 128 stages, counted and placed with one
+// shared atomic per warp)
 __device__ __forceinline__ void plan_lists(const PlanArgs& a, const PlanList (&pl)[kPlanLists],
-                                                  const bool (&on)[kPlanLists],
-                           const int2 (&my_rg)[kPlanLists], const int2 (&my_cr)[kPlanLists],
-                           int (*s_hist)[kPlanBins], int (*s_warp)[32]) {
+                                           const bool (&on)[kPlanLists],
+                                           const int2 (&my_rg)[kPlanLists],
+                                           const int2 (&my_cr)[kPlanLists],
+                                           int (*s_hist)[kPlanBins], int (*s_warp)[32]) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ntiles = a.tile1 - a.tile0;
   _Pragma("unroll") for (int l = 0; l < kPlanLists; ++l) {
@@ -268,14 +259,28 @@ __device__ __forceinline__ void plan_lists(const PlanArgs& a, const PlanList (&p
     for (int b = tid; b < kPlanBins; b += 1024) s_hist[l][b] = 0;
   }
   __syncthreads();
-  for (int i = tid; i < ntiles; i += 1024) {
+  auto tile_lists = [&](int l, int i, int2& rg, int2& cr) {
+    rg = make_int2(0, 0);
+    cr = make_int2(0, -1);
+    if (i < ntiles) {
+      rg = i == tid ? my_rg[l] : pl[l].ranges[a.tile0 + i];
+      cr = i == tid ? my_cr[l] : pl[l].crange[a.tile0 + i];
+    }
+  };
+  auto bin_of = [&](int l, int2 rg, int c) { return min(item_stages(pl[l].sc, rg, c), kPlanBins - 1); };
+  for (int i0 = 0; i0 < ntiles; i0 += 1024) {  // (warp-uniform trip count)
     _Pragma("unroll") for (int l = 0; l < kPlanLists; ++l) {
-    if (!on[l]) continue;
-      const int2 rg = i == tid ? my_rg[l] : pl[l].ranges[a.tile0 + i];
-      const int2 cr = i == tid ? my_cr[l] : pl[l].crange[a.tile0 + i];
-      for (int c = cr.x; c <= cr.y; ++c) {
-        warp_agg_add(&s_hist[l][0], min(item_stages(pl[l].sc, rg, c), kPlanBins - 1));
+      if (!on[l]) continue;
+      int2 rg, cr;
+      tile_lists(l, i0 + tid, rg, cr);
+      int nfull = 0;
+      if (cr.y >= cr.x) {
+        atomicAdd(&s_hist[l][bin_of(l, rg, cr.x)], 1);
+        if (cr.y > cr.x) atomicAdd(&s_hist[l][bin_of(l, rg, cr.y)], 1);
+        nfull = max(cr.y - cr.x - 1, 0);
       }
+      const int wsum = __reduce_add_sync(0xffffffffu, nfull);
+      if (lane == 0 && wsum) atomicAdd(&s_hist[l][min(pl[l].sc / kTS, kPlanBins - 1)], wsum);
     }
   }
   __syncthreads();
@@ -313,16 +318,30 @@ __device__ __forceinline__ void plan_lists(const PlanArgs& a, const PlanList (&p
     s_hist[l][bin] = incl - cnt[l];  // start offset of the bin
   }
   __syncthreads();
-  for (int i = tid; i < ntiles; i += 1024) {
-    const int tile = a.tile0 + i;
+  for (int i0 = 0; i0 < ntiles; i0 += 1024) {
+    const int tile = a.tile0 + i0 + tid;
     _Pragma("unroll") for (int l = 0; l < kPlanLists; ++l) {
-    if (!on[l]) continue;
-      const int2 rg = i == tid ? my_rg[l] : pl[l].ranges[tile];
-      const int2 cr = i == tid ? my_cr[l] : pl[l].crange[tile];
-      for (int ch = cr.x; ch <= cr.y; ++ch) {
-        const int pos = warp_agg_add(&s_hist[l][0], min(item_stages(pl[l].sc, rg, ch), kPlanBins - 1));
-        pl[l].items[pos] = make_int2(tile, ch);
+      if (!on[l]) continue;
+      int2 rg, cr;
+      tile_lists(l, i0 + tid, rg, cr);
+      int nfull = 0;
+      if (cr.y >= cr.x) {
+        pl[l].items[atomicAdd(&s_hist[l][bin_of(l, rg, cr.x)], 1)] = make_int2(tile, cr.x);
+        if (cr.y > cr.x) pl[l].items[atomicAdd(&s_hist[l][bin_of(l, rg, cr.y)], 1)] = make_int2(tile, cr.y);
+        nfull = max(cr.y - cr.x - 1, 0);
       }
+      // the full chunks: one reservation per warp, lanes at their prefix offsets
+      int incl = nfull;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += u;
+      }
+      int base = 0;
+      if (lane == 31 && incl) base = atomicAdd(&s_hist[l][min(pl[l].sc / kTS, kPlanBins - 1)], incl);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      int pos = base + incl - nfull;
+      for (int c = cr.x + 1; c < cr.y; ++c) pl[l].items[pos++] = make_int2(tile, c);
     }
   }
 }
