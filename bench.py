@@ -57,6 +57,7 @@ METRIC = "loglik+gradient evals/sec and pair-interactions/sec at N=85k"
 FLOPS_ANY, FLOPS_BG_GRAD, FLOPS_TR_GRAD = 6, 38, 38
 NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 64 DFMA/clk x 2 x 1.965 GHz
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+SPIN_CYCLES = 400_000  # ~0.2 ms at 1.9 GHz: covers the host's enqueue (tens of us)
 REF_MAX_STEPS = 150  # reference arm: full evaluations (~1.1 s each on 16 cores)
 
 
@@ -116,6 +117,9 @@ def config_dict(world):
         "parallelism": (f"row partition over {world} ranks (owner-directed fx exchange + "
                         "NCCL all-reduce of block partials)") if world > 1 else "1 GPU",
         "l2": "flushed between timed steps (256 MiB write); inputs (2 MB) are L2-resident within a step",
+        "timed_region": ("device events around one evaluation, recorded after an untimed spin that "
+                         "covers the host's enqueue: device time, not host launch latency (the "
+                         "end-to-end arm pays it)"),
     }
 
 
@@ -279,8 +283,10 @@ def main():
         obj = [pk.Engine.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         eng = pk.Engine((local_rank,), rank=rank, world=world, nccl_id=obj[0])
+        eng2 = None  # (ranks exchange over NCCL: the end-to-end arm stays serial)
     else:
         eng = pk.Engine((local_rank,))
+        eng2 = pk.Engine((local_rank,))  # second event set of the pipelined end-to-end arm
 
     x, y, t, T = make_workload()
     n = t.size
@@ -292,6 +298,9 @@ def main():
     eng.set_timing(True)
     # every timed step is a full evaluation: no sweep caches
     eng.set_background_cache(False)
+    if eng2 is not None:
+        eng2.set_timing(True)
+        eng2.set_background_cache(False)
     stream = torch.cuda.ExternalStream(eng.stream(0))
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
@@ -320,6 +329,9 @@ def main():
         for _ in range(steps):
             with torch.cuda.stream(stream):
                 flush.zero_()  # untimed L2 flush between steps
+                # untimed spin (~0.2 ms) while the host enqueues the evaluation,
+                # so e0 -> e1 times the evaluation, not the host's launch latency
+                torch.cuda._sleep(SPIN_CYCLES)
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -347,7 +359,7 @@ def main():
     clocks = sampler.stop() if sampler else None
 
     # end to end through the public API: pinned host inputs -> H2D -> eval -> results
-    def e2e(theta, steps):
+    def e2e_serial(theta, steps):
         for _ in range(2):
             eng.load_events(hx.numpy(), hy.numpy(), ht.numpy(), T)
             eng.set_params(theta)
@@ -362,7 +374,38 @@ def main():
         barrier()
         return reduce_over_ranks(el)
 
-    e2e_s = e2e(THETA_POST, args.steps)
+    # Pipelined: two engines (two event sets) alternate, so step k+1's load --
+    # its pinned x, y, t copied by the copy engines -- runs while step k
+    # evaluates; every step still copies its inputs and reads its result.
+    def e2e_pipelined(theta, steps):
+        engs = (eng, eng2)
+        lls = []
+
+        def run(k_steps):
+            engs[0].load_events(hx.numpy(), hy.numpy(), ht.numpy(), T)
+            engs[0].set_params(theta)
+            engs[0].enqueue(grad=True)
+            for k in range(k_steps):
+                if k + 1 < k_steps:
+                    nxt = engs[(k + 1) % 2]
+                    nxt.load_events(hx.numpy(), hy.numpy(), ht.numpy(), T)
+                    nxt.set_params(theta)
+                    nxt.enqueue(grad=True)
+                lls.append(engs[k % 2].result()[0])
+
+        run(4)
+        barrier()
+        t0 = time.perf_counter()
+        run(steps)
+        el = time.perf_counter() - t0
+        barrier()
+        return reduce_over_ranks(el), lls
+
+    e2e_serial_s = e2e_serial(THETA_POST, args.steps)
+    if eng2 is not None:
+        e2e_s, e2e_lls = e2e_pipelined(THETA_POST, args.steps)
+    else:
+        e2e_s, e2e_lls = e2e_serial_s, []
 
     secondary = {}
     if not args.no_secondary:
@@ -551,8 +594,13 @@ def main():
         "e2e": {"value": K / e2e_s, "unit": "evals/s",
                 "h2d_bytes_per_step": 3 * 8 * n * world,
                 "d2h_bytes_per_step": 8 * 8 * world,
-                "path": "Engine.load_events(pinned x,y,t) + set_params + loglik_grad (C ABI), "
-                        "every rank"},
+                "path": ("Engine.load_events(pinned x,y,t) + set_params + enqueue / result (C ABI); "
+                         "two engines alternate so step k+1's H2D overlaps step k" if eng2 is not None
+                         else "Engine.load_events(pinned x,y,t) + set_params + loglik_grad (C ABI), "
+                              "every rank"),
+                "serial": {"value": K / e2e_serial_s,
+                           "path": "one engine: load_events + set_params + loglik_grad per step"},
+                "results_bitwise_equal_device_run": len(set(e2e_lls + [main_run["loglik"]])) == 1},
         "gpu_launches": main_run["launches"],
         "roofline": {
             "bound": "fp64",

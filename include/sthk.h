@@ -172,6 +172,9 @@ typedef struct sthk_stats {
   double far_split_days;     /* its split tfar (sources further back run in FP32) */
   int64_t graph_launches;    /* evaluations launched as a cached CUDA graph (updated in place) */
   int64_t graph_builds;      /* evaluation graphs built and instantiated */
+  int32_t load_zero_copy;    /* 1 if the last load read pinned caller arrays in place
+                                (0: copied first -- pageable arrays, several devices,
+                                or another engine's evaluation running on the device) */
 } sthk_stats;
 
 /* Timing and pair counters (sthk_get_stats): 0 off, 1 whole evaluation and

@@ -48,6 +48,7 @@ class StatsStruct(ctypes.Structure):
         ("far_split_days", c_double),
         ("graph_launches", c_int64),
         ("graph_builds", c_int64),
+        ("load_zero_copy", ctypes.c_int32),
     ]
 
 

@@ -181,6 +181,7 @@ int item_trace_cap() {
   return v;
 }
 
+struct EvalPlan;  // (defined with the planner below)
 }  // namespace
 
 // How the shards of one evaluation are combined.
@@ -318,6 +319,14 @@ struct sthk_engine {
   double tr_cache_omega = 0, tr_cache_h = 0, tr_cache_dT = 0, tr_cache_dTf = 0;
   bool tr_cache_far_tr = false;  // the cached sweep stored far-tier trigger partials
   uint64_t load_gen = 0, cache_gen = 0;
+  bool load_zero_copy = false;  // the last load read pinned caller arrays in place
+  // last evaluation plan and its inputs (make_plan is a pure function of
+  // them; repeated evaluations at the same parameters skip ~1.5 us of host work)
+  std::unique_ptr<EvalPlan> plan_memo;
+  double plan_memo_p[6] = {};
+  uint64_t plan_memo_gen = 0;
+  int plan_memo_shards = 0;
+  int plan_memo_flags = -1;
   double cache_tx = 0, cache_tt = 0;
   int cache_mode = -1;
   bool cache_dense = false;
@@ -350,12 +359,47 @@ constexpr int64_t kBgSplitMinEvents = 36 * 1024;  // trigger-free split only fro
 
 void set_dev(const Slot& s) { ck(cudaSetDevice(s.dev), "cudaSetDevice"); }
 
+// Main streams of every live engine slot, by device. A load whose device is
+// running another engine's evaluation copies the caller's arrays with the
+// copy engines instead of the zero-copy gather: the gather kernel would wait
+// for SM slots until that evaluation ends, the copies overlap it.
+std::mutex g_streams_mu;
+std::vector<std::pair<int, cudaStream_t>> g_streams;
+
+void register_stream(int dev, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  g_streams.emplace_back(dev, st);
+}
+
+void unregister_stream(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  g_streams.erase(std::remove_if(g_streams.begin(), g_streams.end(),
+                                 [&](const std::pair<int, cudaStream_t>& v) {
+                                   return v.second == st;
+                                 }),
+                  g_streams.end());
+}
+
+bool device_busy_elsewhere(int dev, cudaStream_t own) {
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  bool busy = false;
+  for (const auto& v : g_streams) {
+    if (v.first == dev && v.second != own && cudaStreamQuery(v.second) == cudaErrorNotReady) {
+      busy = true;
+      break;
+    }
+  }
+  (void)cudaGetLastError();
+  return busy;
+}
+
 void init_slot(Slot& s, int dev) {
   s.dev = dev;
   set_dev(s);
   ck(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
   ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&s.stream2, cudaStreamNonBlocking), "stream");
+  register_stream(dev, s.stream);
   ck(cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.prepped, cudaEventDisableTiming), "event");
@@ -417,7 +461,10 @@ void init_slot(Slot& s, int dev) {
 
 void free_slot(Slot& s) {
   cudaSetDevice(s.dev);
-  if (s.stream) cudaStreamSynchronize(s.stream);
+  if (s.stream) {
+    cudaStreamSynchronize(s.stream);
+    unregister_stream(s.stream);
+  }
   if (s.comm) ncclCommDestroy(s.comm);
   for (void* p : {static_cast<void*>(s.x), static_cast<void*>(s.y), static_cast<void*>(s.t),
                   static_cast<void*>(s.xs), static_cast<void*>(s.ys), static_cast<void*>(s.tsl),
@@ -1381,9 +1428,21 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     ck(cudaStreamSynchronize(s0.stream), "D2H");
     e.ht_valid = true;
   }
-  const EvalPlan pl = make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym, sym && e.far_tier,
-                                          e.ext_x, e.ext_y, e.tile_tspan, &e.span_min},
-                                shards);
+  const int plan_flags = (e.dense ? 1 : 0) | (sym ? 2 : 0) | (sym && e.far_tier ? 4 : 0) |
+                         (e.ht_valid ? 8 : 0);
+  if (!e.plan_memo || e.plan_memo_gen != e.load_gen || e.plan_memo_shards != shards ||
+      e.plan_memo_flags != plan_flags || std::memcmp(e.plan_memo_p, e.p, sizeof e.plan_memo_p)) {
+    e.plan_memo.reset();  // (stays empty if make_plan throws)
+    e.plan_memo = std::make_unique<EvalPlan>(
+        make_plan(PlanInput{e.ht, e.n, e.npad, e.p, e.dense, sym, sym && e.far_tier, e.ext_x,
+                            e.ext_y, e.tile_tspan, &e.span_min},
+                  shards));
+    std::memcpy(e.plan_memo_p, e.p, sizeof e.plan_memo_p);
+    e.plan_memo_gen = e.load_gen;
+    e.plan_memo_shards = shards;
+    e.plan_memo_flags = plan_flags;
+  }
+  const EvalPlan& pl = *e.plan_memo;
   e.last_sc = pl.sc;
   e.last_far_a = pl.far_a;
   e.last_tfar = pl.tfar;
@@ -2154,12 +2213,13 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
       dev_grow(s.tf, s.tf_cap, static_cast<size_t>(npad));
       // Pinned (device-mapped) caller arrays on one device: the load kernel
       // reads them over PCIe itself -- one pass instead of three copies and a
-      // kernel (measured 69 -> 57 us at C2). Otherwise copy first.
+      // kernel (measured 69 -> 57 us at C2). Otherwise, or while another
+      // engine's evaluation occupies the device, copy first.
       const double* srcx = s.x;
       const double* srcy = s.y;
       const double* srct = s.t;
       const double* mapped[3] = {nullptr, nullptr, nullptr};
-      if (e->slots.size() == 1) {
+      if (e->slots.size() == 1 && !device_busy_elsewhere(s.dev, s.stream)) {
         const double* hp[3] = {x, y, t};
         for (int k = 0; k < 3; ++k) {
           cudaPointerAttributes at{};
@@ -2170,7 +2230,8 @@ int sthk_load_events(sthk_engine* e, const double* x, const double* y, const dou
         }
         (void)cudaGetLastError();
       }
-      if (mapped[0] && mapped[1] && mapped[2]) {
+      e->load_zero_copy = mapped[0] && mapped[1] && mapped[2];
+      if (e->load_zero_copy) {
         srcx = mapped[0];
         srcy = mapped[1];
         srct = mapped[2];
@@ -2556,6 +2617,7 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
     out->far_threshold = e->last_far_a;
     out->graph_launches = e->graph_updates;
     out->graph_builds = e->graph_instantiations;
+    out->load_zero_copy = e->load_zero_copy ? 1 : 0;
     out->far_split_days = e->last_tfar;
     out->kernel_mode = e->mode;
     out->cache_hit = e->last_cache_hit ? 1 : 0;

@@ -980,6 +980,42 @@ def test_pinned_zero_copy_load_bitwise_equals_pageable_load(engine):
         assert res[0] == res[1]
 
 
+def test_load_beside_a_running_evaluation_copies_and_matches(engine):
+    """A load issued while another engine's evaluation runs on the device
+    copies the pinned arrays with the copy engines (the zero-copy gather
+    would wait for SM slots); an idle device gets the zero-copy gather.
+    Both loads give bitwise-identical results, and the pipelined two-engine
+    pattern of bench.py's end-to-end arm returns every step's result."""
+    import torch
+    import paper_2005_10123_b200 as pk
+    ev = _c2(85000)
+    x, y, t = (torch.from_numpy(np.array(a, dtype=np.float64)).pin_memory().numpy()
+               for a in (ev.xs(), ev.ys(), ev.ts()))
+    th = [0.66, 1.6, 14, 0.344, 1440, 0.0695]
+    engine.set_background_cache(False)
+    engine.load_events(x, y, t, ev.windowEnd())
+    assert engine.stats()["load_zero_copy"] == 1
+    engine.set_params(th)
+    ref = engine.loglik_grad()
+    with pk.Engine((0,)) as other:
+        other.set_background_cache(False)
+        other.load_events(x, y, t, ev.windowEnd())
+        other.set_params(th)
+        copied = 0
+        for _ in range(4):
+            other.enqueue(grad=True)
+            engine.load_events(x, y, t, ev.windowEnd())
+            copied += 1 - engine.stats()["load_zero_copy"]
+            engine.set_params(th)
+            engine.enqueue(grad=True)
+            r_other = other.result()
+            r_eng = engine.result()
+            for r in (r_other, r_eng):
+                assert r[0] == ref[0] and r[1] == ref[1] and tuple(r[2]) == tuple(ref[2])
+        assert copied >= 1  # (the first evaluation of 85k events lasts ~0.4 ms)
+    engine.set_background_cache(True)
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 127, 128, 129, 255, 256, 257, 1023, 1025])
 def test_tile_boundary_sizes_against_oracle(engine, n):
     """Event counts around the 128-event tile and 1024-row block boundaries
