@@ -175,6 +175,9 @@ typedef struct sthk_stats {
   int32_t load_zero_copy;    /* 1 if the last load read pinned caller arrays in place
                                 (0: copied first -- pageable arrays, several devices,
                                 or another engine's evaluation running on the device) */
+  int32_t trigger_rows;      /* 1 if the last evaluation summed its trigger terms by row
+                                windows (trigger window shorter than every 128-event
+                                tile: trig_rows_kernel), 0 if by the tiled sweep */
 } sthk_stats;
 
 /* Timing and pair counters (sthk_get_stats): 0 off, 1 whole evaluation and

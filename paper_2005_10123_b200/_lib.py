@@ -49,6 +49,7 @@ class StatsStruct(ctypes.Structure):
         ("graph_launches", c_int64),
         ("graph_builds", c_int64),
         ("load_zero_copy", ctypes.c_int32),
+        ("trigger_rows", ctypes.c_int32),
     ]
 
 

@@ -128,6 +128,9 @@ struct Slot {
   size_t fx_cap = 0;
   double* tpart = nullptr;           // trigger partials [nchunks][3][npad]
   size_t tpart_cap = 0;
+  double* trow = nullptr;            // trigger sums per row [3][npad] (trig_rows_kernel)
+  size_t trow_cap = 0;
+  cudaEvent_t trow_ev = nullptr;     // trig_rows_kernel done (second stream)
   int2* crange = nullptr;
   size_t crange_cap = 0;
   double* block_partial = nullptr;
@@ -290,6 +293,14 @@ struct sthk_engine {
   // far_ctas_resident far CTAs fit beside it (FP64 and FP32/MUFU pipes busy
   // at once); extra far CTAs queue until near CTAs retire.
   bool far_concurrent = true;
+  // trigger sums by row windows when the window is shorter than every tile
+  // (development knob STHK_TRIG_ROWS=0 at creation: always the tiled sweep)
+  bool trig_rows = [] {
+    const char* v = std::getenv("STHK_TRIG_ROWS");
+    return v ? *v != '0' : true;
+  }();
+  bool last_trig_rows = false;
+  bool tr_cache_rows = false;
   int far_order = 1;  // 1: far launched first, 2: near first
   int near_ctas = 3, far_ctas = 6;
   double ext_x = 0, ext_y = 0;  // max |x - x[0]|, |y - y[0]| of the loaded set
@@ -404,6 +415,7 @@ void init_slot(Slot& s, int dev) {
   ck(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.prepped, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.pairs_done, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&s.trow_ev, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s.fin_done, cudaEventDisableTiming), "event");
   for (auto& e : s.ev) ck(cudaEventCreate(&e), "event");
   ck(cudaMalloc(&s.scalars, 16 * sizeof(int)), "cudaMalloc");
@@ -479,6 +491,7 @@ void free_slot(Slot& s) {
                   static_cast<void*>(s.items), static_cast<void*>(s.scalars),
                   static_cast<void*>(s.fx), static_cast<void*>(s.block_partial),
                   static_cast<void*>(s.tpart), static_cast<void*>(s.crange),
+                  static_cast<void*>(s.trow),
                   static_cast<void*>(s.ex),
                   static_cast<void*>(s.per_event),
                   static_cast<void*>(s.pair_counts), static_cast<void*>(s.tile_box),
@@ -502,6 +515,7 @@ void free_slot(Slot& s) {
   if (s.join) cudaEventDestroy(s.join);
   if (s.prepped) cudaEventDestroy(s.prepped);
   if (s.pairs_done) cudaEventDestroy(s.pairs_done);
+  if (s.trow_ev) cudaEventDestroy(s.trow_ev);
   if (s.fin_done) cudaEventDestroy(s.fin_done);
   if (s.stream2) cudaStreamDestroy(s.stream2);
   if (s.stream) cudaStreamDestroy(s.stream);
@@ -1493,9 +1507,22 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
   // Trigger sums cached from the last sweep: same omega, h and trigger
   // windows, and the same far-tier trigger split (which fixes whether far
   // trigger partials exist and which chunks finalize sums).
+  // Trigger sums by row windows (trig_rows_kernel) when the trigger's exact
+  // underflow window 709/omega -- beyond it every trigger term is +0, in the
+  // reference's exp as in ours -- is shorter than every 128-event tile's time
+  // span (load statistics) and no trigger term goes to the far tier. Each row
+  // then sums every trigger term that is not +0, exactly the reference's set,
+  // at a few pairs per row. A function of omega and the load only -- never
+  // of the cache state, the shard count or the culling mode -- so every
+  // evaluation path sums the same terms alike.
+  const double dT_rows = sthk::kCullExponent / e.p[4] * (1.0 + 1e-9);
+  const bool tr_rows = sym && e.trig_rows && !e.span_min.empty() && dT_rows < e.span_min[0] &&
+                       !(far_full && pl.k.dTf > pl.tfar);
+  e.last_trig_rows = tr_rows;
   const bool tr_cached = cached && e.tr_cache_valid && e.tr_cache_omega == e.p[4] &&
                          e.tr_cache_h == e.p[5] && e.tr_cache_dT == pl.k.dT &&
                          e.tr_cache_dTf == pl.k.dTf && e.tr_cache_far_tr == far_tr &&
+                         e.tr_cache_rows == tr_rows &&
                          e.tr_cache_grad == grad;  // (tpart layout)
   e.last_tr_cache_hit = tr_cached;
   e.cache_valid = false;  // re-armed below once the sweep is enqueued
@@ -1534,6 +1561,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     dev_grow(s.items, s.items_cap, static_cast<size_t>(std::max(ntiles, 1)) * pl.nchunks);
     dev_grow(s.fx, s.fx_cap, static_cast<size_t>(kFxRows) * e.npad);
     dev_grow(s.tpart, s.tpart_cap, static_cast<size_t>(pl.nchunks) * 3 * e.npad);
+    if (tr_rows) dev_grow(s.trow, s.trow_cap, static_cast<size_t>(3) * e.npad);
     dev_grow(s.crange, s.crange_cap, static_cast<size_t>(ntiles_total));
     if (bg_split) {
       dev_grow(s.ranges_bg, s.ranges_bg_cap, static_cast<size_t>(ntiles_total));
@@ -1636,6 +1664,35 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       ck(op_wait(e, st, s.prepped), "wait");
       prep_pending = false;
     };
+    auto launch_trig_rows = [&](cudaStream_t ts) {
+      sthk::TrigRowsArgs ra{};
+      ra.xs = s.xs;
+      ra.ys = s.ys;
+      ra.t = s.t;
+      ra.npad = e.npad;
+      ra.row0 = s.row0;
+      ra.row1 = s.row1;
+      ra.nomL = pl.k.nomL;
+      ra.chS = pl.k.chS;
+      ra.dT = dT_rows;
+      ra.trow = s.trow;
+      ra.pair_counts = e.timing ? s.pair_counts : nullptr;
+      ra.tstamp = stamps ? s.tstamp : nullptr;
+      ck(sthk::launch_trig_rows(ra, grad, ts), "trigger rows");
+      e.launches += 1;
+    };
+    if (ntiles > 0 && tr_rows && cached && !tr_cached) {
+      // trigger-only sweep by row windows: no plan, no pair kernels
+      launch_prep_now();  // (compensator terms when tauT / omega moved)
+      ck(e.timing && e.timing_pairs && !stamps ? record_timing(e, s.ev[1], st)
+                                                : op_record(e, s.ev[1], st),
+         "event");
+      launch_trig_rows(st);
+      join_prep();
+      if (e.timing && e.timing_pairs && !stamps) ck(record_timing(e, s.ev[2], st), "event");
+      ck(op_record(e, s.pairs_done, st), "event");
+      continue;
+    }
     if (ntiles == 0 || tr_cached) {
       launch_prep_now();
       join_prep();
@@ -1704,6 +1761,15 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       std::copy(key, key + 7, s.plan_key);
     }
     launch_prep_now();
+    const bool rows_forked = tr_rows && !cached;
+    if (rows_forked) {  // beside the pair kernels, after prep (scaled coordinates)
+      if (!prep_pending) {
+        ck(op_record(e, s.fork, st), "event");
+        ck(op_wait(e, s.stream2, s.fork), "wait");
+      }
+      launch_trig_rows(s.stream2);
+      ck(op_record(e, s.trow_ev, s.stream2), "event");
+    }
     join_prep();  // pair kernels need the prepared coordinates / zeroed sums
 
     sthk::PairArgs qa{};
@@ -1731,6 +1797,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     qa.fx = s.fx;
     qa.tpart = s.tpart;
     qa.bg_off = cached ? 1 : 0;
+    qa.tr_off = tr_rows ? 1 : 0;
     qa.bg_diag_only = bg_split ? 1 : 0;
     for (int k = 0; k < sthk::kNSumGrad; ++k) qa.fxq[k] = fxq[k];
     if (sym) qa.fxq[1] = fxq[1] / (pl.sx * pl.sx);  // S_Br accumulates sx^2 r^2
@@ -1839,6 +1906,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
       e.launches += 1;
     }
+    if (rows_forked) ck(op_wait(e, st, s.trow_ev), "wait");
     if (e.timing && e.timing_pairs && !stamps) ck(record_timing(e, s.ev[2], st), "event");
     ck(op_record(e, s.pairs_done, st), "event");
   }
@@ -1886,6 +1954,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       fa.crange = s.crange;
       fa.comp = s.comp;
       fa.tpart_far = far_tr ? s.tpart_far : nullptr;
+      fa.trow = tr_rows ? s.trow : nullptr;
       fa.crange_far = s.crange_far;
       for (int k = 0; k < sthk::kNSumGrad; ++k) fa.fxq[k] = fxq[k];
       fa.per_event = want_pe ? s.per_event : nullptr;
@@ -1955,6 +2024,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     e.tr_cache_dT = pl.k.dT;
     e.tr_cache_dTf = pl.k.dTf;
     e.tr_cache_far_tr = far_tr;
+    e.tr_cache_rows = tr_rows;
   }
   e.tr_cache_valid = e.bg_cache;
   e.comp_valid = e.bg_cache;
@@ -2618,6 +2688,7 @@ int sthk_get_stats(sthk_engine* e, sthk_stats* out) {
     out->graph_launches = e->graph_updates;
     out->graph_builds = e->graph_instantiations;
     out->load_zero_copy = e->load_zero_copy ? 1 : 0;
+    out->trigger_rows = e->last_trig_rows ? 1 : 0;
     out->far_split_days = e->last_tfar;
     out->kernel_mode = e->mode;
     out->cache_hit = e->last_cache_hit ? 1 : 0;

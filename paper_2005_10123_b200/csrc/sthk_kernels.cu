@@ -493,6 +493,7 @@ __device__ __forceinline__ void store_row_sums(const PairArgs& a, int chunk, int
     fx_add(a.fx + static_cast<size_t>(2 * q) * a.npad + row,
            a.fx + static_cast<size_t>(2 * q + 1) * a.npad + row, acc[q] * a.fxq[q]);
   }
+  if (a.tr_off) return;
   double* out = a.tpart + static_cast<size_t>(chunk) * NT * a.npad + row;
 #pragma unroll
   for (int q = 0; q < NT; ++q) out[static_cast<size_t>(q) * a.npad] = acc[NB + q];
@@ -1156,7 +1157,7 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
       const bool bg = !a.bg_off && (!a.bg_diag_only || diag || pre) &&
                       !(smin > tmax + a.k.dB || smax < tmin - a.k.dB);
       int tr;
-      if (pre || smin >= tmax || smax < tmin - a.k.dT) tr = 0;
+      if (pre || a.tr_off || smin >= tmax || smax < tmin - a.k.dT) tr = 0;
       else if (smax < tmin) tr = 1;
       else tr = 2;
       const double dxm = fmax(bt.y - bs.x, bs.y - bt.x);
@@ -1640,14 +1641,15 @@ __global__ void tile_stats_kernel(const double* __restrict__ x, const double* __
     }
     // lanes 0..15: the gap a = lane + 1 stages ahead of the tile's first event
     // (t[first] - t[first - 128 a - 1]); lanes 16..31: the span of 2^L whole
-    // tiles from this one, L = lane - 16
+    // tiles from this one, L = lane - 16 (whole: a partial last tile holds
+    // fewer than 128 events, so its short span bounds nothing)
     double v = __longlong_as_double(0x7ff0000000000000LL);
     if (lane < kLoadAdj) {
       const int64_t a = lane + 1;
       if (tile >= a + 1) v = tr.x - trange[tile - a - 1].y;
     } else {
       const int64_t L = lane - kLoadAdj;
-      if (L < kLoadSpan && tile + (int64_t{1} << L) - 1 < nt) {
+      if (L < kLoadSpan && (tile + (int64_t{1} << L)) * kTS <= n) {
         v = trange[tile + (int64_t{1} << L) - 1].y - tr.x;
       }
     }
@@ -1783,6 +1785,66 @@ __device__ __forceinline__ void final_sum_block(const double* __restrict__ bp, i
   if (tid < kNOut) out[tid] = acc[0];
 }
 
+// ---------------------------------------------------------------------------
+// Trigger sums over each row's own time window (short windows: every tile
+// spans more than dT = 709 / omega, beyond which every trigger term is +0).
+// The tiled sweep gives a row all 128-256 sources of the stages its window
+// touches; here a thread walks back from j = i - 1 while t_i - t_j <= dT, so
+// the work is the pairs in the window only -- at Θ_post (ω = 1440, half a
+// day) about ten per row instead of ~200 -- and every term that is not +0 is
+// summed, as in the reference. Same term as the general kernel (exponent
+// nomL dt + chS r2 on scaled coordinates, strict t_j < t_i), sums added in
+// descending j. Every evaluation whose window qualifies -- full sweep or
+// trigger-only, cached or not, any shard count, dense or culled -- takes this
+// path, so those stay bitwise identical.
+// ---------------------------------------------------------------------------
+constexpr int kTrigRowsThreads = 128;
+
+template <bool GRAD>
+__global__ void __launch_bounds__(kTrigRowsThreads) trig_rows_kernel(const TrigRowsArgs a) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    stamp_min(a.tstamp, 0);
+    stamp_min(a.tstamp, 2);
+  }
+  const int64_t i = static_cast<int64_t>(a.row0) + static_cast<int64_t>(blockIdx.x) * kTrigRowsThreads + tid;
+  unsigned long long pairs = 0;
+  if (i < a.row1) {
+    const double ti = a.t[i], xi = a.xs[i], yi = a.ys[i];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int64_t j = i - 1; j >= 0; --j) {
+      const double tj = __ldg(a.t + j);
+      const double dt = ti - tj;
+      if (dt > a.dT) break;
+      if (!(dt > 0.0)) continue;  // ties: strict t_j < t_i
+      const double dx = xi - __ldg(a.xs + j);
+      const double dy = yi - __ldg(a.ys + j);
+      const double r2 = fma(dx, dx, dy * dy);
+      const double e = exp_l<true>(fma(a.nomL, dt, a.chS * r2), kExpTable);
+      s0 += e;
+      if constexpr (GRAD) {
+        s1 = fma(e, dt, s1);
+        s2 = fma(e, r2, s2);
+      }
+      ++pairs;
+    }
+    a.trow[i] = s0;
+    if constexpr (GRAD) {
+      a.trow[a.npad + i] = s1;
+      a.trow[2 * a.npad + i] = s2;
+    }
+  }
+  if (a.pair_counts) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, off);
+    if ((tid & 31) == 0 && pairs) {
+      atomicAdd(&a.pair_counts[1], pairs);
+      atomicAdd(&a.pair_counts[4], pairs);
+    }
+  }
+  if (tid == 0) stamp_max(a.tstamp, 3);
+}
+
 template <bool GRAD>
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) {
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
@@ -1805,7 +1867,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
     const int64_t r = base + tid;
     if (r >= a.row1) break;
     // every independent load first (the row is latency-bound at small N)
-    const int2 cr = a.crange[r / kTM];
+    const int2 cr = a.trow ? make_int2(0, -1) : a.crange[r / kTM];
     const int2 cf = a.tpart_far ? a.crange_far[r / kTM] : make_int2(0, -1);
     unsigned long long fw[2 * NB];
 #pragma unroll
@@ -1840,7 +1902,12 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
         }
       }
     };
-    sum_chunks(a.tpart, cr);
+    if (a.trow) {  // (trig_rows_kernel: one sum per row)
+#pragma unroll
+      for (int k = 0; k < NT; ++k) st[k] = a.trow[static_cast<size_t>(k) * a.npad + r];
+    } else {
+      sum_chunks(a.tpart, cr);
+    }
     if (a.tpart_far) sum_chunks(a.tpart_far, cf);  // (after the near ones: fixed order)
     double xb[NB];  // background sums, fixed-point word values (S_B; S_Br, S_Bt scaled)
 #pragma unroll
@@ -2057,6 +2124,13 @@ cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream) {
   static_assert(kFinThreads == 256, "fused final sum uses the 256-thread final_sum_block");
   return grad ? launch_one(finalize_kernel<true>, dim3(nblocks), dim3(kFinThreads), 0, stream, a)
               : launch_one(finalize_kernel<false>, dim3(nblocks), dim3(kFinThreads), 0, stream, a);
+}
+
+cudaError_t launch_trig_rows(const TrigRowsArgs& a, bool grad, cudaStream_t stream) {
+  const int nblocks = (a.row1 - a.row0 + kTrigRowsThreads - 1) / kTrigRowsThreads;
+  if (nblocks <= 0) return cudaSuccess;
+  return grad ? launch_one(trig_rows_kernel<true>, dim3(nblocks), dim3(kTrigRowsThreads), 0, stream, a)
+              : launch_one(trig_rows_kernel<false>, dim3(nblocks), dim3(kTrigRowsThreads), 0, stream, a);
 }
 
 cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,

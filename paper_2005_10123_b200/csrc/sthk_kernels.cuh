@@ -131,6 +131,7 @@ struct PairArgs {
   double fxq[kNSumGrad];
   double* tpart;        // trigger partials [nchunks][3 or 1][npad]
   int bg_off;           // trigger-only sweep (background sums come from a cache)
+  int tr_off;           // no trigger terms: trig_rows_kernel computes them (sparse window)
   int bg_diag_only;     // general kernel beside the trigger-free one: background on the
                         // diagonal stage only (the trigger-free kernel has every earlier stage)
   unsigned long long* pair_counts;  // [kNCounts] (tile granularity)
@@ -206,6 +207,22 @@ __device__ __forceinline__ void trace_item(const PairArgs& a, int item, int nst,
 }
 #endif
 
+// Trigger sums over each row's own window (trig_rows_kernel): every source
+// j < i with 0 < t_i - t_j <= dT (the exact underflow window 709/omega), for
+// windows shorter than every 128-event tile's time span (at most 254 sources
+// per row, usually a handful).
+struct TrigRowsArgs {
+  const double* xs;     // scaled coordinates (prep_kernel): r2 = sx^2 r^2
+  const double* ys;
+  const double* t;
+  int64_t npad;
+  int row0, row1;
+  double nomL, chS, dT;  // PairConsts::nomL, chS; the window (709 / omega)
+  double* trow;         // [NT][npad]: S_T (, S_Tt, S_Tr') per row
+  unsigned long long* pair_counts;  // nullable (timing): [1] trigger pairs, [4] geometries
+  unsigned long long* tstamp;
+};
+
 struct FinArgs {
   const double* t;
   int64_t n;
@@ -232,6 +249,7 @@ struct FinArgs {
   const double* comp;   // prepared compensator terms [4][npad] (prep_kernel)
   const double* tpart_far;  // far kernel's trigger partials (same layout), chunks crange_far
   const int2* crange_far;
+  const double* trow;   // non-null: trigger sums per row (trig_rows_kernel) instead of tpart
   double* per_event;    // nullable
   double* ex_out;       // nullable: excitation mu, xi, pi as [3][npad]
   double* block_partial;  // [ceil(n / kFB)][kNOut]
@@ -330,6 +348,7 @@ int bgonly_kernel_occupancy(bool grad);
 cudaError_t launch_far(const PairArgs& a, bool grad, int grid, cudaStream_t stream);
 int far_kernel_occupancy(bool grad);
 cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream);
+cudaError_t launch_trig_rows(const TrigRowsArgs& a, bool grad, cudaStream_t stream);
 // (out and counts_out may be host-mapped; counts, if non-null, are copied to
 // counts_out and re-zeroed; out == nullptr: counters only)
 cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,

@@ -1123,3 +1123,85 @@ def test_c4_1m_scaling_identities(engine):
     pt[2] *= st
     pt[4] /= st
     assert abs(run(x, y, st * t, st * T, pt) - (ll0 - n * np.log(st))) <= 1e-11 * abs(ll0)
+
+
+_ROWS_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import paper_2005_10123_b200 as pk
+out = []
+for n, th in ((85000, [0.66, 1.6, 14, 0.344, 1440, 0.0695]), (85000, [0.66, 1.6, 14, 0.344, 300, 0.2]),
+              (85000, [1, 1.6, 14, 0.1, 1, 1]), (4000, [0.66, 1.6, 14, 0.344, 1440, 0.0695])):
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005, keep=n)
+    e = pk.Engine((0,))
+    e.set_background_cache(False)
+    e.load(ev)
+    e.set_params(th)
+    ll, ok, g, pe = e.loglik_grad(per_event=True)
+    out.append([ll, list(map(float, g)), e.stats()["trigger_rows"]])
+    e.close()
+print(json.dumps(out))
+"""
+
+
+def test_trigger_rows_match_tiled_sweep_and_oracle(engine):
+    """Trigger underflow windows 709/ω shorter than every 128-event tile's
+    time span (Θ_post, ω = 1440: half a day) are summed by row windows
+    (trig_rows_kernel): taken at Θ_post, not at Θ_init (ω = 1); the results
+    match the tiled sweep (STHK_TRIG_ROWS=0) to 1e-13 relative (loglik) and
+    1e-10 scale-aware (gradient), and the oracle with tied timestamps; a
+    trigger-only sweep over a cached background (h, ω moves) is bitwise the
+    full sweep."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for rows in ("0", "1"):
+        env = dict(os.environ, STHK_TRIG_ROWS=rows)
+        r = subprocess.run([sys.executable, "-c", _ROWS_SCRIPT, root], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[rows] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert [c[2] for c in res["0"]] == [0, 0, 0, 0]
+    assert [c[2] for c in res["1"]][0::2] == [1, 0] and res["1"][3][2] == 1
+    for a, b in zip(res["0"], res["1"]):
+        assert abs(a[0] - b[0]) <= 1e-13 * abs(a[0])
+        scale = max(abs(v) for v in a[1])
+        for ga, gb in zip(a[1], b[1]):
+            assert abs(ga - gb) <= 1e-10 * scale
+    # ties (strict t_j < t_i) against the oracle, on the row-window path
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=3000)
+    t = np.floor(ev.ts() * 86400.0) / 86400.0
+    ev2 = pk.EventSet(ev.xs(), ev.ys(), t)
+    p = pk.Params(0.66, 1.6, 14, 0.344, 1440, 0.0695)
+    _check(engine, ev2, p)
+    engine.set_params(p)
+    engine.loglik_grad()
+    assert engine.stats()["trigger_rows"] == 1
+    # cached trigger-only sweeps (h, omega moves and back) == full sweeps, bitwise
+    ev, _ = pk.simulateClusterProcess(pk.Params(1, 1.6, 14, 0.344, 1440, 0.0695),
+                                      pk.SimWindow(0, 15, 0, 15, 4750), 0.053217, 2005,
+                                      keep=40000)
+    engine.load(ev)
+    seq = [[0.66, 1.6, 14, 0.344, 1440, 0.0695], [0.66, 1.6, 14, 0.344, 1440, 0.072],
+           [0.66, 1.6, 14, 0.344, 1300, 0.072], [0.7, 1.6, 14, 0.3, 1300, 0.072],
+           [0.66, 1.6, 14, 0.344, 1440, 0.0695]]
+    out = {}
+    for cache in (False, True):
+        engine.set_background_cache(cache)
+        rr = []
+        for th in seq:
+            engine.set_params(th)
+            r = engine.loglik_grad(per_event=True)
+            st = engine.stats()
+            rr.append((r[0], tuple(r[2]), r[3].tobytes(), st["trigger_rows"], st["cache_hit"]))
+        out[cache] = rr
+    engine.set_background_cache(True)
+    for a, b in zip(out[False], out[True]):
+        assert a[:4] == b[:4] and a[3] == 1
+    assert sum(b[4] for b in out[True]) >= 3

@@ -37,7 +37,20 @@ int main(int argc, char** argv) {
     }
     double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() / reps;
     sthk_stats st; sthk_get_stats(e, &st);
-    printf("%-28s %8.1f us/call  (cache_hit %d, trigger_cache_hit %d)\n", name, us, st.cache_hit, st.trigger_cache_hit);
+    // device time of the same move (timing level 2: kernel stamps, no events)
+    sthk_set_timing(e, 2);
+    double dev_ms = 0;
+    for (int i = 0; i < 40; ++i) {
+      p[k] *= (i & 1) ? 1.0 / f : f;
+      sthk_set_params(e, p);
+      sthk_loglik(e, &ll, &valid, nullptr);
+      sthk_stats s2; sthk_get_stats(e, &s2);
+      dev_ms += s2.eval_ms;
+    }
+    sthk_set_timing(e, 0);
+    printf("%-28s %8.1f us/call  device %6.1f us  launches %lld  (cache_hit %d, trigger_cache_hit %d)\n",
+           name, us, dev_ms / 40 * 1e3, static_cast<long long>(st.kernel_launches), st.cache_hit,
+           st.trigger_cache_hit);
   };
   run("mu0 move", 0, 1.01);
   run("theta move", 3, 1.01);
