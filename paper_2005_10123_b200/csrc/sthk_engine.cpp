@@ -1473,10 +1473,29 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
   const bool far_guard = sym && e.far_tier && e.ext_x * pl.sxf <= kFarCoordMax &&
                          e.ext_y * pl.sxf <= kFarCoordMax && e.tile_tspan * pl.stf <= kFarCoordMax;
   const bool far_full = far_guard && !(std::max(pl.k.dB, pl.k.dT) <= pl.tfar);
+  // Trigger sums by row windows (trig_rows_kernel) when the trigger's exact
+  // underflow window 709/omega -- beyond it every trigger term is +0, in the
+  // reference's exp as in ours -- is shorter than every 128-event tile's time
+  // span (load statistics) and no trigger term goes to the far tier. Each row
+  // then sums every trigger term that is not +0, exactly the reference's set,
+  // at a few pairs per row. A function of omega and the load only -- never
+  // of the cache state, the shard count or the culling mode -- so every
+  // evaluation path sums the same terms alike.
+  const double dT_rows = sthk::kCullExponent / e.p[4] * (1.0 + 1e-9);
+  const bool tr_rows = sym && e.trig_rows && !e.span_min.empty() && dT_rows < e.span_min[0] &&
+                       !(far_full && pl.k.dTf > pl.tfar);
+  e.last_trig_rows = tr_rows;
+  // With the trigger sums by row windows no near stage has a trigger term:
+  // every near stage, the diagonal one included, goes to the trigger-free
+  // kernel and the general kernel is not launched (bg_adj -1 in the cache
+  // and plan keys: the split fixes each background term's rounding).
+  const bool bg_all_struct = tr_rows && e.bg_split && !e.merge_bg;
   // (a third kernel only pays off with enough row tiles to amortise its
   // launch and per-CTA setup: measured break-even between N = 30k and 40k)
   int bg_adj = 0;
-  if (sym && e.bg_split && !e.adj_gap.empty() && e.n >= kBgSplitMinEvents) {
+  if (bg_all_struct) {
+    bg_adj = -1;
+  } else if (sym && e.bg_split && !e.adj_gap.empty() && e.n >= kBgSplitMinEvents) {
     // (choosing it from the half-ulp window pl.k.dT instead was measured: 6%
     // slower at Theta_init, where the general kernel's fused background +
     // trigger stages beat a trigger-only pass beside the trigger-free kernel)
@@ -1495,7 +1514,8 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
                       e.cache_bg_adj == bg_adj && e.cache_dense == e.dense &&
                       e.cache_cuts == pl.cuts && (e.cache_grad || !grad);
   e.last_cache_hit = cached;
-  const bool bg_split = !cached && bg_adj > 0;
+  const bool bg_all = !cached && bg_all_struct;
+  const bool bg_split = !cached && (bg_adj > 0 || bg_all);
   // (a far list that is provably empty -- every live source within tfar of
   // its tile, e.g. a trigger-only sweep at large omega -- is not planned or
   // launched; results are the same either way)
@@ -1507,18 +1527,6 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
   // Trigger sums cached from the last sweep: same omega, h and trigger
   // windows, and the same far-tier trigger split (which fixes whether far
   // trigger partials exist and which chunks finalize sums).
-  // Trigger sums by row windows (trig_rows_kernel) when the trigger's exact
-  // underflow window 709/omega -- beyond it every trigger term is +0, in the
-  // reference's exp as in ours -- is shorter than every 128-event tile's time
-  // span (load statistics) and no trigger term goes to the far tier. Each row
-  // then sums every trigger term that is not +0, exactly the reference's set,
-  // at a few pairs per row. A function of omega and the load only -- never
-  // of the cache state, the shard count or the culling mode -- so every
-  // evaluation path sums the same terms alike.
-  const double dT_rows = sthk::kCullExponent / e.p[4] * (1.0 + 1e-9);
-  const bool tr_rows = sym && e.trig_rows && !e.span_min.empty() && dT_rows < e.span_min[0] &&
-                       !(far_full && pl.k.dTf > pl.tfar);
-  e.last_trig_rows = tr_rows;
   const bool tr_cached = cached && e.tr_cache_valid && e.tr_cache_omega == e.p[4] &&
                          e.tr_cache_h == e.p[5] && e.tr_cache_dT == pl.k.dT &&
                          e.tr_cache_dTf == pl.k.dTf && e.tr_cache_far_tr == far_tr &&
@@ -1731,7 +1739,8 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     // (only with a far list: its window then keys the plan cache)
     pa.dFar = !far_on ? 0.0 : cached ? pl.k.dTf : std::max(pl.k.dBf, pl.k.dTf);
     if (bg_split) {
-      pa.bg_adj = bg_adj;
+      pa.bg_adj = std::max(bg_adj, 0);
+      pa.bg_all = bg_all ? 1 : 0;
       pa.sc_bg = pl.sc_bg;
       pa.ranges_bg = s.ranges_bg;
       pa.crange_bg = s.crange_bg;
@@ -1746,7 +1755,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       pa.n_items_far = s.scalars + 6;
       pa.work_counter_far = s.scalars + 7;
     }
-    const int key[7] = {tile0, tile1, pl.sc, pa.dense, pa.sym, pa.trig_only, bg_split ? bg_adj : 0};
+    const int key[7] = {tile0, tile1, pl.sc, pa.dense, pa.sym, pa.trig_only, bg_split ? bg_adj : 0};  // (-1: bg_all)
     const bool plan_hit = e.bg_cache && s.plan_valid && s.plan_dB == pa.dB &&
                           s.plan_dT == pa.dT && s.plan_tfar == pa.tfar && s.plan_dfar == pa.dFar &&
                           std::equal(key, key + 7, s.plan_key);
@@ -1836,6 +1845,11 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     const int occ = s.occ[e.mode][grad ? 1 : 0];
     const bool conc = far_on && e.far_concurrent;
     const int grid = s.sms * (conc ? std::min(e.near_ctas, occ) : occ);
+    auto launch_general = [&] {  // (bg_all: its list is empty, not launched)
+      if (bg_all) return;
+      ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
+      e.launches += 1;
+    };
     // ev[1] (pair-phase start) is recorded whether or not timing is on: a
     // timing event here, between the prep join and the far fork, measurably
     // lets the near kernel's CTAs reach the SMs ahead of the far kernel's
@@ -1881,30 +1895,26 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
         ck(op_wait(e, s.stream2, s.fork), "wait");
         if (e.far_order == 2) {  // near first: its CTAs are resident before far CTAs fill in
           launch_bg();
-          ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
-          e.launches += 1;
+          launch_general();
           ck(launch_far_list(s.sms * e.far_ctas, s.stream2), "far kernel");
           e.launches += 1;
         } else {
           launch_bg();
           ck(launch_far_list(s.sms * e.far_ctas, s.stream2), "far kernel");
           e.launches += 1;
-          ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
-          e.launches += 1;
+          launch_general();
         }
         ck(op_record(e, s.join, s.stream2), "event");
         ck(op_wait(e, st, s.join), "wait");
       } else {
         launch_bg();
-        ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
-        e.launches += 1;
+        launch_general();
         ck(launch_far_list(s.sms * s.occ_far[grad ? 1 : 0], st), "far kernel");
         e.launches += 1;
       }
     } else {
       launch_bg();
-      ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
-      e.launches += 1;
+      launch_general();
     }
     if (rows_forked) ck(op_wait(e, st, s.trow_ev), "wait");
     if (e.timing && e.timing_pairs && !stamps) ck(record_timing(e, s.ev[2], st), "event");

@@ -204,9 +204,13 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
   // (the trigger-free kernel takes the background of every near stage before
   // the diagonal one; the general kernel keeps the trigger terms of the
   // bg_adj stages ahead of the tile and the diagonal stage)
-  const int fbe = a.ranges_bg ? static_cast<int>(first) : fbt;
+  const int fbe = !a.ranges_bg ? fbt : a.bg_all ? hi : static_cast<int>(first);
   rgb = make_int2(fb, fbe);
   crb = fbe > fb ? make_int2(fb / a.sc_bg, (fbe - 1) / a.sc_bg) : make_int2(0, -1);
+  if (a.bg_all && a.ranges_bg) {  // (the general list is empty)
+    rg = make_int2(hi, hi);
+    cr = make_int2(0, -1);
+  }
 }
 
 // Number of 128-source stages of work item (tile, chunk) -- the same bounds

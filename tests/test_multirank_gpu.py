@@ -218,4 +218,7 @@ def test_hosted_gloo_ranks_bitwise(engine, world):
                 assert np.array_equal(np.array(pe)[lo:hi], r[3][lo:hi])
             if j == 0 and rank > 0:
                 assert extra > 0  # (fx bytes sent to earlier owners)
-        assert out[2][4] == 1 and out[3][4] == 1  # background cached across the moves
+        # background cached across the omega move (the theta move before it
+        # re-sweeps: from Θ_init's tiled trigger terms to row windows, the
+        # near split -- hence the background's grouping -- changes)
+        assert out[3][4] == 1
