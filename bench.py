@@ -443,18 +443,21 @@ def main():
         eng.loglik()
         barrier()
         t0 = time.perf_counter()
-        hits = 0
+        hits = rows = 0
         for _ in range(args.steps):
             k = [0, 3, 4, 5][int(rng.integers(4))]
             cand = list(theta)
             cand[k] = theta[k] * float(np.exp(0.01 * rng.standard_normal()))
             eng.set_params(cand)
             eng.loglik()
-            hits += eng.stats()["cache_hit"]
+            st = eng.stats()
+            hits += st["cache_hit"]
+            rows += st["trigger_rows"]
         mh_s = reduce_over_ranks(time.perf_counter() - t0)
         eng.set_background_cache(False)
         secondary["mh_style_loglik"] = {
             "evals_per_s": args.steps / mh_s, "unit": "evals/s", "cache_hits": hits,
+            "trigger_rows_evals": rows,
             "what": "wall-clock loglik calls, one of mu0/theta/omega/h perturbed per step (tauX, "
                     "tauT fixed as in the reference sampler): cached background, trigger band swept"}
 

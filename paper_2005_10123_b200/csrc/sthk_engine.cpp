@@ -1551,6 +1551,10 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
   // compensator terms: cached (exact) while tauT and omega are unchanged
   const bool need_comp = !(e.bg_cache && e.comp_valid && e.comp_gen == e.load_gen &&
                            e.comp_tt == p[2] && e.comp_om == p[4]);
+  // trigger-only sweep by row windows over the cached background (h, omega
+  // moves): finalize computes each row's trigger sums -- and, when tauT or
+  // omega moved, its compensator terms -- itself: one kernel per evaluation
+  const bool fin_rows = tr_rows && cached && !tr_cached;
   if (need_comp) e.comp_valid = false;  // re-armed once the prep pass is enqueued
   // Timing in graph mode: kernel-side %globaltimer stamps instead of event
   // nodes, which would sit between the kernels and add their latency.
@@ -1639,7 +1643,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       }
     }
     if (!cached) pr.fx = s.fx;
-    if (need_comp) {
+    if (need_comp && !fin_rows) {
       pr.comp = s.comp;
       pr.window_end = e.window_end;
       pr.tauT = p[2];
@@ -1689,19 +1693,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       ck(sthk::launch_trig_rows(ra, grad, ts), "trigger rows");
       e.launches += 1;
     };
-    if (ntiles > 0 && tr_rows && cached && !tr_cached) {
-      // trigger-only sweep by row windows: no plan, no pair kernels
-      launch_prep_now();  // (compensator terms when tauT / omega moved)
-      ck(e.timing && e.timing_pairs && !stamps ? record_timing(e, s.ev[1], st)
-                                                : op_record(e, s.ev[1], st),
-         "event");
-      launch_trig_rows(st);
-      join_prep();
-      if (e.timing && e.timing_pairs && !stamps) ck(record_timing(e, s.ev[2], st), "event");
-      ck(op_record(e, s.pairs_done, st), "event");
-      continue;
-    }
-    if (ntiles == 0 || tr_cached) {
+    if (ntiles == 0 || tr_cached || fin_rows) {
       launch_prep_now();
       join_prep();
       ck(e.timing && e.timing_pairs && !stamps ? record_timing(e, s.ev[1], st)
@@ -1965,6 +1957,20 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       fa.comp = s.comp;
       fa.tpart_far = far_tr ? s.tpart_far : nullptr;
       fa.trow = tr_rows ? s.trow : nullptr;
+      if (fin_rows) {
+        fa.rows.xs = s.xs;
+        fa.rows.ys = s.ys;
+        fa.rows.t = s.t;
+        fa.rows.npad = e.npad;
+        fa.rows.row0 = s.row0;
+        fa.rows.row1 = s.row1;
+        fa.rows.nomL = pl.k.nomL;
+        fa.rows.chS = pl.k.chS;
+        fa.rows.dT = dT_rows;
+        fa.rows.trow = s.trow;
+        fa.rows.pair_counts = e.timing ? s.pair_counts : nullptr;
+        fa.comp_inline = need_comp ? 1 : 0;
+      }
       fa.crange_far = s.crange_far;
       for (int k = 0; k < sthk::kNSumGrad; ++k) fa.fxq[k] = fxq[k];
       fa.per_event = want_pe ? s.per_event : nullptr;

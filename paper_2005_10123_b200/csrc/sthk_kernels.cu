@@ -1697,6 +1697,25 @@ __global__ void tile_stats_kernel(const double* __restrict__ x, const double* __
 //    Phi(-t/tauT), comp[1] = (phi(z1) D + phi(z0) t) / tauT^2 (d Lambda / d tauT
 //    = -mu0 comp[1]), comp[2] = expm1(-omega D), comp[3] = D exp(-omega D),
 //    D = T - t; finalize combines them with mu0 and theta.
+// One event's compensator terms (compensatorTerm, kernels.hpp:54-65, and its
+// tauT / omega derivatives): shared by prep_kernel and the fused
+// trigger-only finalize, so both produce the same bits.
+__device__ __forceinline__ void comp_terms(double ti, double window_end, double tauT, double omega,
+                                           double (&c)[4]) {
+  const double D = window_end - ti;
+  // normalCdf = 0.5 erfc(-z/sqrt2), kernels.hpp:21
+  const double Phi1 = 0.5 * erfc(-(D / tauT) * kInvSqrt2);
+  const double Phi0 = 0.5 * erfc(-(-ti / tauT) * kInvSqrt2);
+  const double z1 = D / tauT, z0 = ti / tauT;
+  const double phi1 = kInvSqrt2Pi * exp(-0.5 * z1 * z1);
+  const double phi0 = kInvSqrt2Pi * exp(-0.5 * z0 * z0);
+  c[0] = Phi1 - Phi0;
+  c[1] = (phi1 * D + phi0 * ti) / (tauT * tauT);
+  c[2] = expm1(-omega * D);
+  // exp(-omega D) directly: 1 + expm1 cancels when omega D is large
+  c[3] = D * exp(-omega * D);
+}
+
 __global__ void prep_kernel(const PrepArgs a) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= a.npad) return;
@@ -1718,19 +1737,10 @@ __global__ void prep_kernel(const PrepArgs a) {
     for (int k = 0; k < 6; ++k) a.fx[static_cast<size_t>(k) * a.npad + i] = 0ULL;
   }
   if (a.comp && i < a.n) {
-    const double ti = a.t[i];
-    const double D = a.window_end - ti;
-    // normalCdf = 0.5 erfc(-z/sqrt2), kernels.hpp:21
-    const double Phi1 = 0.5 * erfc(-(D / a.tauT) * kInvSqrt2);
-    const double Phi0 = 0.5 * erfc(-(-ti / a.tauT) * kInvSqrt2);
-    const double z1 = D / a.tauT, z0 = ti / a.tauT;
-    const double phi1 = kInvSqrt2Pi * exp(-0.5 * z1 * z1);
-    const double phi0 = kInvSqrt2Pi * exp(-0.5 * z0 * z0);
-    a.comp[i] = Phi1 - Phi0;
-    a.comp[a.npad + i] = (phi1 * D + phi0 * ti) / (a.tauT * a.tauT);
-    a.comp[2 * a.npad + i] = expm1(-a.omega * D);
-    // exp(-omega D) directly: 1 + expm1 cancels when omega D is large
-    a.comp[3 * a.npad + i] = D * exp(-a.omega * D);
+    double c[4];
+    comp_terms(a.t[i], a.window_end, a.tauT, a.omega, c);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a.comp[static_cast<size_t>(k) * a.npad + i] = c[k];
   }
   if (a.trace && threadIdx.x == 0) trace_cta(a.trace, a.trace_cap, 5, trace_t0);
 }
@@ -1804,6 +1814,55 @@ __device__ __forceinline__ void final_sum_block(const double* __restrict__ bp, i
 // ---------------------------------------------------------------------------
 constexpr int kTrigRowsThreads = 128;
 
+// Row i's trigger sums (S_T, and for GRAD S_Tt, S_Tr') over its window,
+// written to trow; returns the pairs evaluated. Shared by trig_rows_kernel
+// and the fused trigger-only finalize, so both produce the same bits.
+template <bool GRAD>
+__device__ __forceinline__ unsigned long long trig_row_sums(const TrigRowsArgs& a, int64_t i,
+                                                            double (&st)[GRAD ? 3 : 1]) {
+  unsigned long long pairs = 0;
+  const double ti = a.t[i], xi = a.xs[i], yi = a.ys[i];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  // two sources per step (j, j - 1), their exps in lockstep; a source outside
+  // the window or tied with t_i adds an exact 0 (s + 0 == s: every sum >= 0),
+  // so the sums are those of the one-at-a-time loop, bit for bit
+  for (int64_t j = i - 1; j >= 0; j -= 2) {
+    const int64_t j1 = j >= 1 ? j - 1 : j;
+    const double tj0 = __ldg(a.t + j);
+    const double tj1 = j >= 1 ? __ldg(a.t + j1) : ti;  // (no second source: dt 0, masked)
+    const double dt0 = ti - tj0, dt1 = ti - tj1;
+    if (dt0 > a.dT) break;
+    const bool v0 = dt0 > 0.0;  // ties: strict t_j < t_i
+    const bool v1 = dt1 > 0.0 && dt1 <= a.dT;
+    const double dx0 = xi - __ldg(a.xs + j), dy0 = yi - __ldg(a.ys + j);
+    const double dx1 = xi - __ldg(a.xs + j1), dy1 = yi - __ldg(a.ys + j1);
+    const double r20 = fma(dx0, dx0, dy0 * dy0), r21 = fma(dx1, dx1, dy1 * dy1);
+    const double x[2] = {fma(a.nomL, dt0, a.chS * r20), fma(a.nomL, dt1, a.chS * r21)};
+    double e[2];
+    exp_l_batch<true, 2>(x, e, kExpTable);
+    const double e0 = v0 ? e[0] : 0.0, e1 = v1 ? e[1] : 0.0;
+    s0 += e0;
+    s0 += e1;
+    if constexpr (GRAD) {
+      s1 = fma(e0, dt0, s1);
+      s1 = fma(e1, dt1, s1);
+      s2 = fma(e0, r20, s2);
+      s2 = fma(e1, r21, s2);
+    }
+    pairs += static_cast<unsigned long long>(v0) + static_cast<unsigned long long>(v1);
+    if (!(dt1 <= a.dT)) break;  // (time-sorted: every earlier source is outside too)
+  }
+  st[0] = s0;
+  a.trow[i] = s0;
+  if constexpr (GRAD) {
+    st[1] = s1;
+    st[2] = s2;
+    a.trow[a.npad + i] = s1;
+    a.trow[2 * a.npad + i] = s2;
+  }
+  return pairs;
+}
+
 template <bool GRAD>
 __global__ void __launch_bounds__(kTrigRowsThreads) trig_rows_kernel(const TrigRowsArgs a) {
   const int tid = threadIdx.x;
@@ -1814,29 +1873,8 @@ __global__ void __launch_bounds__(kTrigRowsThreads) trig_rows_kernel(const TrigR
   const int64_t i = static_cast<int64_t>(a.row0) + static_cast<int64_t>(blockIdx.x) * kTrigRowsThreads + tid;
   unsigned long long pairs = 0;
   if (i < a.row1) {
-    const double ti = a.t[i], xi = a.xs[i], yi = a.ys[i];
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int64_t j = i - 1; j >= 0; --j) {
-      const double tj = __ldg(a.t + j);
-      const double dt = ti - tj;
-      if (dt > a.dT) break;
-      if (!(dt > 0.0)) continue;  // ties: strict t_j < t_i
-      const double dx = xi - __ldg(a.xs + j);
-      const double dy = yi - __ldg(a.ys + j);
-      const double r2 = fma(dx, dx, dy * dy);
-      const double e = exp_l<true>(fma(a.nomL, dt, a.chS * r2), kExpTable);
-      s0 += e;
-      if constexpr (GRAD) {
-        s1 = fma(e, dt, s1);
-        s2 = fma(e, r2, s2);
-      }
-      ++pairs;
-    }
-    a.trow[i] = s0;
-    if constexpr (GRAD) {
-      a.trow[a.npad + i] = s1;
-      a.trow[2 * a.npad + i] = s2;
-    }
+    double st[GRAD ? 3 : 1];
+    pairs = trig_row_sums<GRAD>(a, i, st);
   }
   if (a.pair_counts) {
 #pragma unroll
@@ -1849,7 +1887,11 @@ __global__ void __launch_bounds__(kTrigRowsThreads) trig_rows_kernel(const TrigR
   if (tid == 0) stamp_max(a.tstamp, 3);
 }
 
-template <bool GRAD>
+// ROWS: trigger-only evaluation by row windows over cached background sums
+// (h, omega, theta moves): the row's trigger sums (trig_row_sums) and, if
+// a.comp_inline, its compensator terms (comp_terms) are computed here and
+// stored for the caches -- one kernel for the whole evaluation.
+template <bool GRAD, bool ROWS>
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) {
   constexpr int NS = GRAD ? kNSumGrad : kNSumVal;
   constexpr int NB = GRAD ? 3 : 1;
@@ -1866,22 +1908,36 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
   double acc[kNOut];
 #pragma unroll
   for (int q = 0; q < kNOut; ++q) acc[q] = 0.0;
+  unsigned long long rows_pairs = 0;  // (ROWS: trigger pairs evaluated, timing counters)
 
   do {  // one row per thread; `continue` / `break` skip to the reduction
     const int64_t r = base + tid;
     if (r >= a.row1) break;
     // every independent load first (the row is latency-bound at small N)
-    const int2 cr = a.trow ? make_int2(0, -1) : a.crange[r / kTM];
+    const int2 cr = (ROWS || a.trow) ? make_int2(0, -1) : a.crange[r / kTM];
     const int2 cf = a.tpart_far ? a.crange_far[r / kTM] : make_int2(0, -1);
     unsigned long long fw[2 * NB];
 #pragma unroll
     for (int k = 0; k < 2 * NB; ++k) fw[k] = a.fx[static_cast<size_t>(k) * a.npad + r];
-    const double dPhi = a.comp[r];
-    const double em1 = a.comp[2 * a.npad + r];
+    double cc[4];
+    if (ROWS && a.comp_inline) {
+      comp_terms(a.t[r], a.window_end, a.tauT, a.omega, cc);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) a.comp[static_cast<size_t>(k) * a.npad + r] = cc[k];
+    } else {
+      cc[0] = a.comp[r];
+      cc[2] = a.comp[2 * a.npad + r];
+      if constexpr (GRAD) {
+        cc[1] = a.comp[a.npad + r];
+        cc[3] = a.comp[3 * a.npad + r];
+      }
+    }
+    const double dPhi = cc[0];
+    const double em1 = cc[2];
     double dL2c = 0.0, dec = 0.0;
     if constexpr (GRAD) {
-      dL2c = a.comp[a.npad + r];
-      dec = a.comp[3 * a.npad + r];
+      dL2c = cc[1];
+      dec = cc[3];
     }
     // trigger partials: chunks in order (then the far kernel's), four
     // chunks' loads in flight at a time; the additions keep chunk order
@@ -1906,7 +1962,9 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
         }
       }
     };
-    if (a.trow) {  // (trig_rows_kernel: one sum per row)
+    if constexpr (ROWS) {
+      rows_pairs = trig_row_sums<GRAD>(a.rows, r, st);
+    } else if (a.trow) {  // (trig_rows_kernel: one sum per row)
 #pragma unroll
       for (int k = 0; k < NT; ++k) st[k] = a.trow[static_cast<size_t>(k) * a.npad + r];
     } else {
@@ -1956,6 +2014,14 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
     }
   } while (false);
 
+  if (ROWS && a.rows.pair_counts) {  // (one atomic per warp)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) rows_pairs += __shfl_xor_sync(0xffffffffu, rows_pairs, off);
+    if ((tid & 31) == 0 && rows_pairs) {
+      atomicAdd(&a.rows.pair_counts[1], rows_pairs);
+      atomicAdd(&a.rows.pair_counts[4], rows_pairs);
+    }
+  }
   block_sum8(acc, s_w);
   if (tid < kNOut) a.block_partial[(base / kFB) * kNOut + tid] = acc[0];
   if (a.fused_out) {  // single shard: the last block to finish does the final sum
@@ -2126,8 +2192,12 @@ cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream) {
   const int nblocks = (a.row1 - a.row0 + kFB - 1) / kFB;
   if (nblocks <= 0) return cudaSuccess;
   static_assert(kFinThreads == 256, "fused final sum uses the 256-thread final_sum_block");
-  return grad ? launch_one(finalize_kernel<true>, dim3(nblocks), dim3(kFinThreads), 0, stream, a)
-              : launch_one(finalize_kernel<false>, dim3(nblocks), dim3(kFinThreads), 0, stream, a);
+  if (a.rows.trow) {
+    return grad ? launch_one(finalize_kernel<true, true>, dim3(nblocks), dim3(kFinThreads), 0, stream, a)
+                : launch_one(finalize_kernel<false, true>, dim3(nblocks), dim3(kFinThreads), 0, stream, a);
+  }
+  return grad ? launch_one(finalize_kernel<true, false>, dim3(nblocks), dim3(kFinThreads), 0, stream, a)
+              : launch_one(finalize_kernel<false, false>, dim3(nblocks), dim3(kFinThreads), 0, stream, a);
 }
 
 cudaError_t launch_trig_rows(const TrigRowsArgs& a, bool grad, cudaStream_t stream) {

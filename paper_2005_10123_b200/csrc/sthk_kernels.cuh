@@ -248,10 +248,15 @@ struct FinArgs {
   const double* tpart;
   double tr_r2_scale;   // 1 (kRows) or 1/sx^2 (kSym: trigger r^2 sums on scaled coordinates)
   const int2* crange;
-  const double* comp;   // prepared compensator terms [4][npad] (prep_kernel)
+  double* comp;         // prepared compensator terms [4][npad] (prep_kernel)
   const double* tpart_far;  // far kernel's trigger partials (same layout), chunks crange_far
   const int2* crange_far;
   const double* trow;   // non-null: trigger sums per row (trig_rows_kernel) instead of tpart
+  // rows.trow non-null: trigger-only evaluation by row windows, the trigger
+  // sums computed (and stored to rows.trow) by finalize itself; comp_inline:
+  // the compensator terms too (stored to comp)
+  TrigRowsArgs rows;
+  int comp_inline;
   double* per_event;    // nullable
   double* ex_out;       // nullable: excitation mu, xi, pi as [3][npad]
   double* block_partial;  // [ceil(n / kFB)][kNOut]
