@@ -607,9 +607,10 @@ def main():
         "gpu_launches": main_run["launches"],
         "roofline": {
             "bound": "fp64",
-            "kernel": ("sym_kernel<GRAD=true> (FP64 near, trigger-free + general) || "
-                       "far_kernel<GRAD=true> (FP32 far tier), concurrent"
-                       if st["exec_far"] else "sym_kernel<GRAD=true>"),
+            "kernel": (("sym_kernel<GRAD=true, BGONLY> (FP64 near: every near stage; trigger sums by "
+                        "row windows, trig_rows_kernel)" if st["trigger_rows"] else
+                        "sym_kernel<GRAD=true> (FP64 near, trigger-free + general)")
+                       + (" || far_kernel<GRAD=true> (FP32 far tier), concurrent" if st["exec_far"] else "")),
             "achieved": achieved,
             "peak": peak_best,
             "unit": "TFLOP/s",

@@ -739,6 +739,20 @@ int min_chunk_stages() {
   return v;
 }
 
+// Row-window evaluations run every near stage in the trigger-free kernel from
+// this many events; below it the general kernel (trigger terms off) keeps them
+// (measured, whole evaluation at Θ_post: 1.5k-5k events 29.6 vs 23.8 us,
+// 10k 34.8 vs 29.7, 20k 49.8 vs 46.4, 36k 88.5 vs 90.0; development knob
+// STHK_BG_ALL_MIN overrides it)
+constexpr int64_t kBgAllMinEvents = 32 * 1024;
+int64_t bg_all_min_events() {
+  static const int64_t v = [] {
+    const char* s = std::getenv("STHK_BG_ALL_MIN");
+    return s ? static_cast<int64_t>(std::atoll(s)) : kBgAllMinEvents;
+  }();
+  return v;
+}
+
 // (development knob: STHK_CHUNKS_TARGET overrides the chunk count target)
 int chunks_target() {
   static const int v = [] {
@@ -1489,7 +1503,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
   // every near stage, the diagonal one included, goes to the trigger-free
   // kernel and the general kernel is not launched (bg_adj -1 in the cache
   // and plan keys: the split fixes each background term's rounding).
-  const bool bg_all_struct = tr_rows && e.bg_split && !e.merge_bg;
+  const bool bg_all_struct = tr_rows && e.bg_split && !e.merge_bg && e.n >= bg_all_min_events();
   // (a third kernel only pays off with enough row tiles to amortise its
   // launch and per-CTA setup: measured break-even between N = 30k and 40k)
   int bg_adj = 0;

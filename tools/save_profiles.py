@@ -29,7 +29,7 @@ if os.path.exists(lc):
         agg[name][0] += 1
         agg[name][1] += float(r[vi].replace(",", ""))
     ours = {k: v for k, v in agg.items() if any(s in k for s in
-            ("pair_kernel", "sym_kernel", "far_kernel", "finalize", "plan_", "final_sum", "tile_box",
+            ("pair_kernel", "sym_kernel", "far_kernel", "finalize", "plan_", "final_sum", "tile_box", "tile_load", "tile_stats", "trig_rows",
              "prep_kernel"))}
     tot = sum(v[1] for v in ours.values())
     with open(f"{p}/{tag}_launch_list_summary.txt", "w") as f:
