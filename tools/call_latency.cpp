@@ -22,6 +22,10 @@ int main(int argc, char** argv) {
   sthk_engine* e = nullptr;
   int dev = 0;
   sthk_create(&dev, 1, &e);
+  if (argc > 2 && std::atoi(argv[2]) == 0) {
+    sthk_set_graphs(e, 0);
+    printf("(graphs off)\n");
+  }
   sthk_load_events(e, x.data(), y.data(), t.data(), n, t[n - 1]);
   double p[6] = {0.66, 1.6, 14, 0.344, 1440, 0.0695};
   double ll; int valid;
@@ -102,6 +106,27 @@ int main(int argc, char** argv) {
         tot += std::chrono::duration<double, std::micro>(b2 - b0).count();
       }
       printf("enqueue host time (full eval) %8.1f us/call of %8.1f us\n", enq / reps, tot / reps);
+    }
+    {  // the same split for a mu0 move over the cached sums (finalize only)
+      sthk_set_background_cache(e, 1);
+      sthk_loglik(e, &ll, &valid, nullptr);
+      double enq = 0, tot = 0, sp = 0;
+      for (int i = 0; i < 4 * reps; ++i) {
+        p[0] *= (i & 1) ? 1.0 / 1.01 : 1.01;
+        auto a0 = std::chrono::steady_clock::now();
+        sthk_set_params(e, p);
+        auto b0 = std::chrono::steady_clock::now();
+        sthk_enqueue(e, 0, 0);
+        auto b1 = std::chrono::steady_clock::now();
+        sthk_result(e, &ll, &valid, nullptr, nullptr);
+        auto b2 = std::chrono::steady_clock::now();
+        sp += std::chrono::duration<double, std::micro>(b0 - a0).count();
+        enq += std::chrono::duration<double, std::micro>(b1 - b0).count();
+        tot += std::chrono::duration<double, std::micro>(b2 - a0).count();
+      }
+      printf("mu0 move: set_params %.1f + enqueue %.1f us of %.1f us/call\n", sp / (4 * reps),
+             enq / (4 * reps), tot / (4 * reps));
+      sthk_set_background_cache(e, 0);
     }
     printf("load_events (pinned)         %8.1f us/call\n", std::chrono::duration<double, std::micro>(t1 - t0).count() / reps);
     printf("loglik_grad (caches off)     %8.1f us/call\n", std::chrono::duration<double, std::micro>(t2 - t1).count() / reps);
