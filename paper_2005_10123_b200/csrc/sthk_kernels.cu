@@ -362,6 +362,9 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   __shared__ __align__(8) uint64_t s_bar;
   extern __shared__ __align__(128) double s_piv[];  // kPivots (dynamic: 64 KB)
   const int tid = threadIdx.x;
+  // (graph mode: the trigger-free kernel is launched by a programmatic edge
+  // from here; its CTAs set up while the plan runs and wait for its lists)
+  asm volatile("griddepcontrol.launch_dependents;");
   const unsigned long long trace_t0 = (a.trace && tid == 0) ? global_ns() : 0ULL;
   if (tid == 0) stamp_min(a.tstamp, 0);
   const int ntiles = a.tile1 - a.tile0;
@@ -1069,6 +1072,9 @@ __global__ void __launch_bounds__(kTM, BGONLY ? STHK_SYMBG_MINB : STHK_SYM_MINB)
   }
   mbar_wait(&s_tbar, 0);
 
+  // (launched by a programmatic edge from the plan: wait for its work lists
+  // and counters -- a no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int n_pre = (!BGONLY && a.pre_items) ? *a.pre_n_items : 0;
   const int n_items = *a.n_items + n_pre;
   const int64_t n = a.n;
@@ -1866,6 +1872,7 @@ __device__ __forceinline__ unsigned long long trig_row_sums(const TrigRowsArgs& 
 template <bool GRAD>
 __global__ void __launch_bounds__(kTrigRowsThreads) trig_rows_kernel(const TrigRowsArgs a) {
   const int tid = threadIdx.x;
+  const unsigned long long trace_t0 = (a.trace && tid == 0) ? global_ns() : 0ULL;
   if (tid == 0) {
     stamp_min(a.tstamp, 0);
     stamp_min(a.tstamp, 2);
@@ -1884,6 +1891,7 @@ __global__ void __launch_bounds__(kTrigRowsThreads) trig_rows_kernel(const TrigR
       atomicAdd(&a.pair_counts[4], pairs);
     }
   }
+  if (a.trace && tid == 0) trace_cta(a.trace, a.trace_cap, 11, trace_t0);
   if (tid == 0) stamp_max(a.tstamp, 3);
 }
 
@@ -2175,6 +2183,30 @@ cudaError_t prepare_pair_kernels() {
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(kPivots * sizeof(double)));
   if (e != cudaSuccess) err = e;
+  // Kernels that run beside the pair kernels (or just before them) ask for
+  // the pair kernels' shared-memory carveout: an SM changes its L1 / shared
+  // split only when idle, so a small kernel configured for the largest L1
+  // holds whole SMs away from the pair kernels' CTAs until it drains
+  // (measured: trig_rows_kernel beside the trigger-free kernel delayed its
+  // first CTA from 7.5 to 14.5 us into the evaluation).
+  auto carve = [&](const void* f) {
+    const cudaError_t c = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                               cudaSharedmemCarveoutMaxShared);
+    if (c != cudaSuccess) err = c;
+  };
+  carve(reinterpret_cast<const void*>(&trig_rows_kernel<true>));
+  carve(reinterpret_cast<const void*>(&trig_rows_kernel<false>));
+  carve(reinterpret_cast<const void*>(&prep_kernel));
+  carve(reinterpret_cast<const void*>(&far_kernel<true>));
+  carve(reinterpret_cast<const void*>(&far_kernel<false>));
+  carve(reinterpret_cast<const void*>(&finalize_kernel<true, false>));
+  carve(reinterpret_cast<const void*>(&finalize_kernel<false, false>));
+  for (const void* f : {reinterpret_cast<const void*>(&sym_kernel<true>),
+                        reinterpret_cast<const void*>(&sym_kernel<false>),
+                        reinterpret_cast<const void*>(&sym_kernel<true, true>),
+                        reinterpret_cast<const void*>(&sym_kernel<false, true>)}) {
+    carve(f);
+  }
   return err;
 }
 

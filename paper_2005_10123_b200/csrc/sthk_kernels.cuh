@@ -223,6 +223,8 @@ struct TrigRowsArgs {
   double* trow;         // [NT][npad]: S_T (, S_Tt, S_Tr') per row
   unsigned long long* pair_counts;  // nullable (timing): [1] trigger pairs, [4] geometries
   unsigned long long* tstamp;
+  unsigned long long* trace;  // development trace (PairArgs::trace), nullptr: off
+  int trace_cap;
 };
 
 struct FinArgs {

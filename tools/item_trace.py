@@ -40,7 +40,7 @@ tr = raw[raw[:, 2] != 0xFFFFFFFF]
 print(f"{which} {th}: eval {st['eval_ms'] * 1e3:.1f} us, pair phase {st['pair_kernel_ms'] * 1e3:.1f} us, "
       f"{len(tr)} items, far threshold A {st['far_threshold']:.2f} split {st['far_split_days']:.1f} d")
 t00 = raw[:, 5].min()
-names = {1: "general", 2: "trigger-free", 3: "far", 4: "plan", 5: "prep", 6: "finalize", 7: "plan:pivots", 8: "plan:ranges", 9: "plan:histogram", 10: "plan:scan"}
+names = {1: "general", 2: "trigger-free", 3: "far", 4: "plan", 5: "prep", 6: "finalize", 7: "plan:pivots", 8: "plan:ranges", 9: "plan:histogram", 10: "plan:scan", 11: "trig_rows"}
 print("  kernel timeline (first CTA start .. last CTA end, us from the first start):")
 for k in sorted(set(cta[:, 0].tolist()), key=lambda k: cta[cta[:, 0] == k, 5].min()):
     m = cta[:, 0] == k
