@@ -1205,3 +1205,30 @@ def test_trigger_rows_match_tiled_sweep_and_oracle(engine):
     for a, b in zip(out[False], out[True]):
         assert a[:4] == b[:4] and a[3] == 1
     assert sum(b[4] for b in out[True]) >= 3
+
+
+def test_trigger_rows_long_windows_against_oracle(engine):
+    """Row windows near their limit: ω chosen so that 709/ω is 0.9 of the
+    shortest tile's time span, ≈ 115 sources per row in the window (uniform
+    times, 6,000 events), against the long-double oracle; and a bursty
+    variant (half the events packed into short bursts)."""
+    rng = np.random.default_rng(77)
+    n, T = 6000, 100.0
+    t = np.sort(rng.uniform(0, T, n))
+    x, y = rng.uniform(0, 4, n), rng.uniform(0, 4, n)
+    span = min(t[k + 127] - t[k] for k in range(0, n - 127, 128))
+    omega = 709.0 / (0.9 * span)
+    for p in ([0.7, 1.2, 6.0, 0.5, omega, 1.0], [0.7, 1.2, 6.0, 0.5, omega, 0.2]):
+        ev = pk.EventSet(x, y, t)
+        _check(engine, ev, pk.Params(*p))
+        engine.set_params(p)
+        engine.loglik_grad()
+        assert engine.stats()["trigger_rows"] == 1
+    # bursty: 40 bursts of 75 events within 0.01 days each, plus a uniform half
+    tb = np.concatenate([rng.uniform(0, T, 3000)] +
+                        [c + rng.uniform(0, 0.01, 75) for c in rng.uniform(0, T, 40)])
+    tb = np.sort(tb)
+    ev = pk.EventSet(rng.uniform(0, 4, tb.size), rng.uniform(0, 4, tb.size), tb)
+    for omega_b in (2000.0, 20000.0):
+        p = pk.Params(0.7, 1.2, 6.0, 0.5, omega_b, 0.5)
+        _check(engine, ev, p)
