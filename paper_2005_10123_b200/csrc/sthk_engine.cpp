@@ -85,7 +85,7 @@ struct Slot {
   size_t ranges_bg_cap = 0, crange_bg_cap = 0, items_bg_cap = 0;
   int2 *ranges_far = nullptr, *crange_far = nullptr, *items_far = nullptr;
   size_t ranges_far_cap = 0, crange_far_cap = 0, items_far_cap = 0;
-  double* tpart_far = nullptr;       // far kernel trigger partials [nchunks][3][npad]
+  double* tpart_far = nullptr;       // far kernel trigger partials [nchunks_far][3][npad]
   size_t tpart_far_cap = 0;
   double2* tile_trange = nullptr;    // per tile: t first, t last
   double* comp = nullptr;            // compensator terms [4][npad] (prep_kernel)
@@ -571,6 +571,8 @@ struct EvalPlan {
   int nchunks = 0;
   int sc_bg = 0;       // chunk size of the background-only list (finer: a function of N only)
   int nchunks_bg = 0;
+  int sc_far = 0;      // chunk size of the far list (finer: a function of N only)
+  int nchunks_far = 0;
   std::vector<int> cuts;  // shard row boundaries (size shards+1)
 };
 
@@ -782,6 +784,22 @@ int chunk_size(int64_t n, int64_t npad) {
   return static_cast<int>(sc);
 }
 
+// Far list chunk: a quarter of the trigger partials' chunk grid (a function
+// of N only), so the far kernel's tail is finer and each FP32 row partial sums
+// fewer terms (the far tier's error bound counts them: A 30.27 -> 30.00 at
+// C2). Measured whole evaluation (Θ_post) with sc, sc/2, sc/4: 50k 130.6 /
+// 129.5 / 127.0 us, C2 308.1 / 306.5 / 307.2 us, 250k 2.377 / 2.371 / 2.364
+// ms, 1M 36.98 / 36.81 / 36.66 ms. Development knob STHK_FAR_DIV.
+int far_chunk_size(int64_t n, int64_t npad) {
+  static const int div = [] {
+    const char* s = std::getenv("STHK_FAR_DIV");
+    const int k = s ? std::atoi(s) : 0;
+    return k >= 1 && k <= 16 ? k : 4;
+  }();
+  const int sc = chunk_size(n, npad);
+  return std::max(static_cast<int>(kTS), sc / div / kTS * kTS);
+}
+
 // Far-tier cull exponent C = ln N + 54 ln 2, capped by the FP32 flush point
 // 126 ln 2 + 1: far terms below e^-C sum to < 2^-54 of every row's S_B
 // (DESIGN.md §3).
@@ -841,7 +859,7 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
     const double cc = std::max({e.ext_x * sxf, e.ext_y * sxf, (e.tile_tspan + dfar) * stf});
     const double dd = (2.0 * cc + dmax) * u + dmax * u;
     const double dE = 3.0 * (2.0 * dmax * dd + dmax * dmax * u) + 3.0 * dmax * dmax * u;
-    const double eps = kLn2 * dE + 4.0 * u + static_cast<double>(chunk_size(e.n, e.npad)) * u;
+    const double eps = kLn2 * dE + 4.0 * u + static_cast<double>(far_chunk_size(e.n, e.npad)) * u;
     // far terms in one event's S_B: its far sources (rows) plus the later
     // rows it is a far source of (columns), each within dfar + one tile's
     // span of it, so at most twice the events of such a window (<= N)
@@ -896,6 +914,8 @@ EvalPlan make_plan(const PlanInput& e, int shards) {
   // cloud; at C2 (85k) and above the full chunk is as fast or faster)
   const int bg_div = n < 64 * 1024 ? 2 : 1;
   pl.sc_bg = std::max(kTS, (pl.sc / bg_div + kTS - 1) / kTS * kTS);
+  pl.sc_far = far_chunk_size(n, e.npad);
+  pl.nchunks_far = static_cast<int>((n + pl.sc_far - 1) / pl.sc_far);
   pl.nchunks_bg = static_cast<int>((n + pl.sc_bg - 1) / pl.sc_bg);
   pl.cuts = plan_cuts(e.ht, n, p, e.dense, e.sym, e.far, shards);
 
@@ -1600,8 +1620,10 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       dev_grow(s.ranges_far, s.ranges_far_cap, static_cast<size_t>(ntiles_total));
       dev_grow(s.crange_far, s.crange_far_cap, static_cast<size_t>(ntiles_total));
       dev_grow(s.items_far, s.items_far_cap,
-               static_cast<size_t>(std::max(ntiles, 1)) * pl.nchunks);
-      dev_grow(s.tpart_far, s.tpart_far_cap, static_cast<size_t>(pl.nchunks) * 3 * e.npad);
+               static_cast<size_t>(std::max(ntiles, 1)) * pl.nchunks_far);
+      if (far_tr || e.far_fp64) {
+        dev_grow(s.tpart_far, s.tpart_far_cap, static_cast<size_t>(pl.nchunks_far) * 3 * e.npad);
+      }
     }
     dev_grow(s.block_partial, s.bp_cap, static_cast<size_t>(nb_total) * kNOut);
     dev_grow(s.comp, s.comp_cap, static_cast<size_t>(4) * e.npad);
@@ -1731,6 +1753,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     pa.sym = sym ? 1 : 0;
     pa.trig_only = cached ? 1 : 0;
     pa.sc = pl.sc;
+    pa.sc_far = pl.sc_far;
     pa.nchunks = pl.nchunks;
     pa.ranges = s.ranges;
     pa.crange = s.crange;
@@ -1881,6 +1904,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     if (far_on) {  // the far work list in FP32
       sthk::PairArgs fa_ = qa;
       fa_.pre_items = nullptr;
+      fa_.sc = pl.sc_far;
       fa_.ranges = s.ranges_far;
       fa_.items = s.items_far;
       fa_.n_items = s.scalars + 6;

@@ -200,7 +200,7 @@ __device__ __forceinline__ void tile_plan(const PlanArgs& a, const Pivots& pv, i
   rg = make_int2(fbt, hi);
   cr = make_int2(fbt / a.sc, (hi - 1) / a.sc);
   rgf = make_int2(flo, fb);
-  crf = fb > flo ? make_int2(flo / a.sc, (fb - 1) / a.sc) : make_int2(0, -1);
+  crf = fb > flo ? make_int2(flo / a.sc_far, (fb - 1) / a.sc_far) : make_int2(0, -1);
   // (the trigger-free kernel takes the background of every near stage before
   // the diagonal one; the general kernel keeps the trigger terms of the
   // bg_adj stages ahead of the tile and the diagonal stage)
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   // fixed slots: 0 near, 1 far, 2 trigger-free (inactive lists are skipped)
   const PlanList pl[kPlanLists] = {
       PlanList{a.sc, a.ranges, a.crange, a.items, a.n_items, a.work_counter},
-      PlanList{a.sc, a.ranges_far, a.crange_far, a.items_far, a.n_items_far, a.work_counter_far},
+      PlanList{a.sc_far, a.ranges_far, a.crange_far, a.items_far, a.n_items_far, a.work_counter_far},
       PlanList{a.sc_bg, a.ranges_bg, a.crange_bg, a.items_bg, a.n_items_bg, a.work_counter_bg}};
   const bool on[kPlanLists] = {true, a.ranges_far != nullptr, a.ranges_bg != nullptr};
   const int2 mrg[kPlanLists] = {my[0], my[2], my[4]};

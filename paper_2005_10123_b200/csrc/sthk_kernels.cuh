@@ -95,6 +95,7 @@ struct PlanArgs {
   int bg_all;           // no near trigger term (trig_rows_kernel): every near stage,
                         // the diagonal one included, to the trigger-free list
   int sc_bg;            // sources per chunk of the background-only list (multiple of kTS)
+  int sc_far;           // sources per chunk of the far list (multiple of kTS)
   int2* ranges_bg;
   int2* crange_bg;
   int2* items_bg;
