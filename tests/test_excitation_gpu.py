@@ -135,3 +135,28 @@ def test_posterior_excitation_batch_bitwise_and_errors(engine, tmp_path):
     with pytest.raises(RuntimeError, match="posteriorExcitation: draw 2: .*underflowed"):
         pk.posteriorExcitation(ev, seq, dumpPath=path_e, engine=engine)
     assert len(open(path_e).read().strip().split("\n")) == 3
+
+
+def test_excitation_row_windows_against_oracle_and_batch(engine):
+    """Excitation split with the trigger sums by row windows (ω = 200/day:
+    709/ω = 3.5 days, shorter than every tile) against the oracle; then MH
+    draws moving ω and h -- trigger-only evaluations fused into finalize --
+    through the batched posterior path, bitwise equal to single calls."""
+    ev = pk.generateBenchmarkCloud(3000, pk.SimWindow(0, 8, 0, 8, 400), 12)
+    p = pk.Params(0.7, 1.1, 6.0, 0.4, 200.0, 0.3)
+    ex = pk.excitationProbabilities(ev, p, engine=engine)
+    assert engine.stats()["trigger_rows"] == 1
+    mu, xi, pi = _oracle_split(ev, p)
+    assert np.allclose(ex.mu, mu, rtol=1e-12, atol=0)
+    assert np.all(np.abs(ex.xi - xi) <= 1e-12 * (np.abs(xi) + 1e-300) + 1e-300)
+    assert np.all(np.abs(ex.pi - pi) <= 1e-12)
+    rng = np.random.default_rng(8)
+    draws, q = [], [0.7, 1.1, 6.0, 0.4, 200.0, 0.3]
+    for _ in range(12):
+        k = [0, 3, 4, 5][int(rng.integers(4))]
+        q = list(q)
+        q[k] *= float(np.exp(0.05 * rng.standard_normal()))
+        draws.append(pk.Params(*q))
+    post = pk.posteriorExcitation(ev, draws, thinTo=12, engine=engine)
+    rows = [pk.excitationProbabilities(ev, d, engine=engine).pi for d in draws]
+    assert np.array_equal(post.perDraw, np.array(rows))
