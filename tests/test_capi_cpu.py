@@ -73,3 +73,26 @@ def test_eventset_first_failure_in_reference_order():
         pk.EventSet([0, float("inf"), 2], [0, 1, 2], [1.0, 0.5, 0.2])
     with pytest.raises(ValueError, match="negative time at index 1"):
         pk.EventSet([0, 1], [0, 1], [1.0, -1.0])
+
+
+def test_stats_struct_layout_matches_header(tmp_path):
+    """The Python mirror of sthk_stats (ctypes) has the C header's size and
+    field offsets: compiled here with gcc against include/sthk.h."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    fields = [f for f, _ in _lib.StatsStruct._fields_]
+    src = ["#include <stddef.h>", "#include <stdio.h>", '#include "sthk.h"', "int main(void) {",
+           '  printf("%zu\\n", sizeof(sthk_stats));']
+    src += ['  printf("%%zu\\n", offsetof(sthk_stats, %s));' % f for f in fields]
+    src += ["  return 0;", "}"]
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)], check=True)
+    out = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    assert out[0] == ctypes.sizeof(_lib.StatsStruct)
+    for f, off in zip(fields, out[1:]):
+        assert getattr(_lib.StatsStruct, f).offset == off, f
