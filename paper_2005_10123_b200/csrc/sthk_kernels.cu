@@ -1818,34 +1818,63 @@ __device__ __forceinline__ void final_sum_block(const double* __restrict__ bp, i
 // trigger-only, cached or not, any shard count, dense or culled -- takes this
 // path, so those stay bitwise identical.
 // ---------------------------------------------------------------------------
-constexpr int kTrigRowsThreads = 128;
+constexpr int kTrigRowsThreads = 256;
+// sources a row's window can reach before its block's first row: a window
+// holds at most 254 events (every tile spans more than it), plus the one
+// just outside that ends the walk
+constexpr int kTrigRowsBack = 256;
+
+// Where trig_row_sums reads the events: global memory through L1 (the fused
+// finalize), or a shared-memory copy of [base, ...) with the exp table
+// (trig_rows_kernel: it runs beside the near kernel, whose shared-memory
+// carveout leaves little L1). Same values either way, so the same bits.
+struct RowSrcGlobal {
+  const double* t;
+  const double* x;
+  const double* y;
+  __device__ __forceinline__ double tt(int64_t j) const { return __ldg(t + j); }
+  __device__ __forceinline__ double xx(int64_t j) const { return __ldg(x + j); }
+  __device__ __forceinline__ double yy(int64_t j) const { return __ldg(y + j); }
+  __device__ __forceinline__ const uint2* tab() const { return kExpTable; }
+};
+struct RowSrcShared {
+  const double* t;
+  const double* x;
+  const double* y;
+  int64_t base;
+  const uint2* table;
+  __device__ __forceinline__ double tt(int64_t j) const { return t[j - base]; }
+  __device__ __forceinline__ double xx(int64_t j) const { return x[j - base]; }
+  __device__ __forceinline__ double yy(int64_t j) const { return y[j - base]; }
+  __device__ __forceinline__ const uint2* tab() const { return table; }
+};
 
 // Row i's trigger sums (S_T, and for GRAD S_Tt, S_Tr') over its window,
 // written to trow; returns the pairs evaluated. Shared by trig_rows_kernel
 // and the fused trigger-only finalize, so both produce the same bits.
-template <bool GRAD>
-__device__ __forceinline__ unsigned long long trig_row_sums(const TrigRowsArgs& a, int64_t i,
-                                                            double (&st)[GRAD ? 3 : 1]) {
+template <bool GRAD, class Src>
+__device__ __forceinline__ unsigned long long trig_row_sums(const TrigRowsArgs& a, const Src& src,
+                                                            int64_t i, double (&st)[GRAD ? 3 : 1]) {
   unsigned long long pairs = 0;
-  const double ti = a.t[i], xi = a.xs[i], yi = a.ys[i];
+  const double ti = src.tt(i), xi = src.xx(i), yi = src.yy(i);
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   // two sources per step (j, j - 1), their exps in lockstep; a source outside
   // the window or tied with t_i adds an exact 0 (s + 0 == s: every sum >= 0),
   // so the sums are those of the one-at-a-time loop, bit for bit
   for (int64_t j = i - 1; j >= 0; j -= 2) {
     const int64_t j1 = j >= 1 ? j - 1 : j;
-    const double tj0 = __ldg(a.t + j);
-    const double tj1 = j >= 1 ? __ldg(a.t + j1) : ti;  // (no second source: dt 0, masked)
+    const double tj0 = src.tt(j);
+    const double tj1 = j >= 1 ? src.tt(j1) : ti;  // (no second source: dt 0, masked)
     const double dt0 = ti - tj0, dt1 = ti - tj1;
     if (dt0 > a.dT) break;
     const bool v0 = dt0 > 0.0;  // ties: strict t_j < t_i
     const bool v1 = dt1 > 0.0 && dt1 <= a.dT;
-    const double dx0 = xi - __ldg(a.xs + j), dy0 = yi - __ldg(a.ys + j);
-    const double dx1 = xi - __ldg(a.xs + j1), dy1 = yi - __ldg(a.ys + j1);
+    const double dx0 = xi - src.xx(j), dy0 = yi - src.yy(j);
+    const double dx1 = xi - src.xx(j1), dy1 = yi - src.yy(j1);
     const double r20 = fma(dx0, dx0, dy0 * dy0), r21 = fma(dx1, dx1, dy1 * dy1);
     const double x[2] = {fma(a.nomL, dt0, a.chS * r20), fma(a.nomL, dt1, a.chS * r21)};
     double e[2];
-    exp_l_batch<true, 2>(x, e, kExpTable);
+    exp_l_batch<true, 2>(x, e, src.tab());
     const double e0 = v0 ? e[0] : 0.0, e1 = v1 ? e[1] : 0.0;
     s0 += e0;
     s0 += e1;
@@ -1877,11 +1906,29 @@ __global__ void __launch_bounds__(kTrigRowsThreads) trig_rows_kernel(const TrigR
     stamp_min(a.tstamp, 0);
     stamp_min(a.tstamp, 2);
   }
-  const int64_t i = static_cast<int64_t>(a.row0) + static_cast<int64_t>(blockIdx.x) * kTrigRowsThreads + tid;
+  // stage the exp table and the events [first - kTrigRowsBack, last] of this
+  // block's rows (coalesced), then walk the windows in shared memory
+  extern __shared__ __align__(128) uint2 s_rtab[];  // kExpTableSize (dynamic)
+  __shared__ double s_rt[kTrigRowsBack + kTrigRowsThreads];
+  __shared__ double s_rx[kTrigRowsBack + kTrigRowsThreads];
+  __shared__ double s_ry[kTrigRowsBack + kTrigRowsThreads];
+  const int64_t first = static_cast<int64_t>(a.row0) + static_cast<int64_t>(blockIdx.x) * kTrigRowsThreads;
+  const int64_t last = min(first + kTrigRowsThreads, static_cast<int64_t>(a.row1)) - 1;
+  const int64_t base = max(first - kTrigRowsBack, int64_t{0});
+  const int cnt = static_cast<int>(last + 1 - base);
+  for (int k = tid; k < kExpTableSize; k += kTrigRowsThreads) s_rtab[k] = kExpTable[k];
+  for (int k = tid; k < cnt; k += kTrigRowsThreads) {
+    s_rt[k] = a.t[base + k];
+    s_rx[k] = a.xs[base + k];
+    s_ry[k] = a.ys[base + k];
+  }
+  __syncthreads();
+  const int64_t i = first + tid;
   unsigned long long pairs = 0;
-  if (i < a.row1) {
+  if (i <= last) {
     double st[GRAD ? 3 : 1];
-    pairs = trig_row_sums<GRAD>(a, i, st);
+    const RowSrcShared src{s_rt, s_rx, s_ry, base, s_rtab};
+    pairs = trig_row_sums<GRAD>(a, src, i, st);
   }
   if (a.pair_counts) {
 #pragma unroll
@@ -1971,7 +2018,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
       }
     };
     if constexpr (ROWS) {
-      rows_pairs = trig_row_sums<GRAD>(a.rows, r, st);
+      rows_pairs = trig_row_sums<GRAD>(a.rows, RowSrcGlobal{a.rows.t, a.rows.xs, a.rows.ys}, r, st);
     } else if (a.trow) {  // (trig_rows_kernel: one sum per row)
 #pragma unroll
       for (int k = 0; k < NT; ++k) st[k] = a.trow[static_cast<size_t>(k) * a.npad + r];
@@ -2235,8 +2282,8 @@ cudaError_t launch_finalize(const FinArgs& a, bool grad, cudaStream_t stream) {
 cudaError_t launch_trig_rows(const TrigRowsArgs& a, bool grad, cudaStream_t stream) {
   const int nblocks = (a.row1 - a.row0 + kTrigRowsThreads - 1) / kTrigRowsThreads;
   if (nblocks <= 0) return cudaSuccess;
-  return grad ? launch_one(trig_rows_kernel<true>, dim3(nblocks), dim3(kTrigRowsThreads), 0, stream, a)
-              : launch_one(trig_rows_kernel<false>, dim3(nblocks), dim3(kTrigRowsThreads), 0, stream, a);
+  return grad ? launch_one(trig_rows_kernel<true>, dim3(nblocks), dim3(kTrigRowsThreads), kTabBytes, stream, a)
+              : launch_one(trig_rows_kernel<false>, dim3(nblocks), dim3(kTrigRowsThreads), kTabBytes, stream, a);
 }
 
 cudaError_t launch_final_sum(const double* block_partial, int nblocks, double* out,
