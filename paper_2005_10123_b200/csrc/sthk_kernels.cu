@@ -1547,6 +1547,8 @@ __global__ void tile_load_kernel(const double* __restrict__ sx, const double* __
                                  double* __restrict__ y, double* __restrict__ t, int64_t n,
                                  int64_t npad, double4* box, double2* trange,
                                  double* __restrict__ piv, unsigned long long* bad, bool tiles) {
+  // (tile_stats_kernel is launched programmatically behind this one)
+  asm volatile("griddepcontrol.launch_dependents;");
   const bool copy = sx != x;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid < npad - n) {  // pad tail [n, npad): never read as sources
@@ -1621,6 +1623,9 @@ __global__ void tile_stats_kernel(const double* __restrict__ x, const double* __
                                   unsigned long long* bad, unsigned int* done,
                                   unsigned long long* h_bad, double* h_stats,
                                   unsigned long long* __restrict__ dstats) {
+  // (launched programmatically: wait for tile_load_kernel's device copy,
+  // boxes and time ranges -- its launch latency is hidden)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ unsigned long long s_st[kLoadStats];
   for (int q = threadIdx.x; q < kLoadStats; q += blockDim.x) {
     s_st[q] = q < 3 ? 0ULL : 0x7ff0000000000000ULL;
@@ -2188,8 +2193,24 @@ cudaError_t launch_tile_boxes(const double* sx, const double* sy, const double* 
   const unsigned blocks = static_cast<unsigned>((ntiles + 7) / 8);
   tile_load_kernel<<<blocks, 256, 0, stream>>>(sx, sy, st, x, y, t, n, npad, box, trange, piv, bad,
                                                tile_pivots);
-  tile_stats_kernel<<<blocks, 256, 0, stream>>>(x, y, t, n, box, trange, piv, tile_pivots, bad, done,
-                                                h_bad, h_stats, dstats);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  const double* cx = x;
+  const double* cy = y;
+  const double* ct = t;
+  const double4* cbox = box;
+  const double2* ctr = trange;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tile_stats_kernel, cx, cy, ct, n, cbox, ctr, piv,
+                                           tile_pivots, bad, done, h_bad, h_stats, dstats);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
