@@ -1753,6 +1753,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     pa.sym = sym ? 1 : 0;
     pa.trig_only = cached ? 1 : 0;
     pa.sc = pl.sc;
+    pa.tile_order = tr_rows ? 1 : 0;
     pa.sc_far = pl.sc_far;
     pa.nchunks = pl.nchunks;
     pa.ranges = s.ranges;
@@ -1785,7 +1786,8 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       pa.n_items_far = s.scalars + 6;
       pa.work_counter_far = s.scalars + 7;
     }
-    const int key[7] = {tile0, tile1, pl.sc, pa.dense, pa.sym, pa.trig_only, bg_split ? bg_adj : 0};  // (-1: bg_all)
+    const int key[7] = {tile0, tile1, pl.sc, pa.dense, pa.sym, pa.trig_only + 2 * pa.tile_order,
+                        bg_split ? bg_adj : 0};  // (-1: bg_all)
     const bool plan_hit = e.bg_cache && s.plan_valid && s.plan_dB == pa.dB &&
                           s.plan_dT == pa.dT && s.plan_tfar == pa.tfar && s.plan_dfar == pa.dFar &&
                           std::equal(key, key + 7, s.plan_key);

@@ -350,6 +350,55 @@ __device__ __forceinline__ void plan_lists(const PlanArgs& a, const PlanList (&p
   }
 }
 
+// Small sets with no trigger term in the near lists (row-window trigger sums:
+// every item one background stage, equal work) and at most 1024 tiles: the
+// lists in tile order -- the size order buys nothing -- by one block-wide
+// scan of the per-tile item counts (two barriers instead of the histogram's
+// five). (With trigger stages, whose items cost more, the sorted placement
+// stays: measured 36.5 -> 39.4 us at 10k events, Θ_init, in tile order.)
+__device__ __forceinline__ void plan_lists_tile_order(const PlanArgs& a, const PlanList (&pl)[kPlanLists],
+                                                      const bool (&on)[kPlanLists],
+                                                      const int2 (&my_cr)[kPlanLists],
+                                                      int (*s_warp)[32]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ntiles = a.tile1 - a.tile0;
+  int cnt[kPlanLists], incl[kPlanLists];
+  _Pragma("unroll") for (int l = 0; l < kPlanLists; ++l) {
+    cnt[l] = 0;
+    if (on[l] && tid < ntiles && my_cr[l].y >= my_cr[l].x) cnt[l] = my_cr[l].y - my_cr[l].x + 1;
+    incl[l] = cnt[l];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl[l], off);
+      if (lane >= off) incl[l] += u;
+    }
+    if (lane == 31) s_warp[l][warp] = incl[l];
+  }
+  __syncthreads();
+  if (warp < kPlanLists && on[warp]) {  // warp l scans list l's 32 warp totals
+    int w = s_warp[warp][lane];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += u;
+    }
+    s_warp[warp][lane] = w;
+  }
+  __syncthreads();
+  _Pragma("unroll") for (int l = 0; l < kPlanLists; ++l) {
+    if (!on[l]) continue;
+    const int end = incl[l] + (warp > 0 ? s_warp[l][warp - 1] : 0);
+    if (tid == 1023) {
+      *pl[l].n_items = end;
+      *pl[l].work_counter = 0;
+    }
+    int pos = end - cnt[l];
+    for (int c = my_cr[l].x; c <= my_cr[l].y && cnt[l] > 0; ++c) {
+      pl[l].items[pos++] = make_int2(a.tile0 + tid, c);
+    }
+  }
+}
+
 // Single CTA: per-tile near / far ranges, then each work list ordered by
 // decreasing item size, so the persistent pair kernels hand out the long
 // items first and end on short ones (less idle time in the tail); resets the
@@ -416,7 +465,13 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   const bool on[kPlanLists] = {true, a.ranges_far != nullptr, a.ranges_bg != nullptr};
   const int2 mrg[kPlanLists] = {my[0], my[2], my[4]};
   const int2 mcr[kPlanLists] = {my[1], my[3], my[5]};
-  plan_lists(a, pl, on, mrg, mcr, s_hist, s_warp);
+  const int nt = a.tile1 - a.tile0;
+  if (a.tile_order && nt <= 1024 && a.sc == kTS && (!on[1] || a.sc_far == kTS) &&
+      (!on[2] || a.sc_bg == kTS)) {
+    plan_lists_tile_order(a, pl, on, mcr, s_warp);
+  } else {
+    plan_lists(a, pl, on, mrg, mcr, s_hist, s_warp);
+  }
   if (a.trace && tid == 0) trace_cta(a.trace, a.trace_cap, 4, trace_t0);
 }
 

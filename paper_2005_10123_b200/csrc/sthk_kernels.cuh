@@ -92,6 +92,7 @@ struct PlanArgs {
   // list for the trigger-free FP64 kernel; nullptr: off
   int tile_pivots;      // piv holds tile last times (see use_tile_pivots), else strided times
   int bg_adj;           // near stages kept with the tile for the general kernel (>= 1)
+  int tile_order;       // equal one-stage items (no near trigger term): lists in tile order
   int bg_all;           // no near trigger term (trig_rows_kernel): every near stage,
                         // the diagonal one included, to the trigger-free list
   int sc_bg;            // sources per chunk of the background-only list (multiple of kTS)
