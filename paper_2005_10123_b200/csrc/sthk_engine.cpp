@@ -367,6 +367,11 @@ constexpr double kFarRowBound = 1e-13;    // bound on the far tier's error, rela
 constexpr double kFarCoordMax = 4096.0;
 constexpr int kMaxAdj = sthk::kLoadAdj;  // trigger-free split: at most 16 stages kept with the tile
 constexpr int64_t kBgSplitMinEvents = 36 * 1024;  // trigger-free split only from 36k events
+// plan + prep as one grid up to this many events (graph mode): whole
+// evaluation Θ_post / Θ_init, two kernels -> one grid: 1.5k 22.6 -> 20.8 /
+// 30.3 -> 27.3 us, 10k 26.4 -> 26.2 / 36.6 -> 32.3 us; at 20k-24k Θ_post
+// turns slower (the prep blocks take longer than the plan)
+constexpr int64_t kPlanPrepMaxEvents = 16 * 1024;
 
 void set_dev(const Slot& s) { ck(cudaSetDevice(s.dev), "cudaSetDevice"); }
 
@@ -1791,9 +1796,28 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     const bool plan_hit = e.bg_cache && s.plan_valid && s.plan_dB == pa.dB &&
                           s.plan_dT == pa.dT && s.plan_tfar == pa.tfar && s.plan_dfar == pa.dFar &&
                           std::equal(key, key + 7, s.plan_key);
-    if (!plan_hit) {  // (the work counters are re-armed by the last pair CTAs)
-      ck(sthk::launch_plan(pa, st), "plan");
+    // Small sets in graph mode: plan and prep as one grid, so the pair kernel's
+    // programmatic edge from it holds (a second predecessor on another stream
+    // makes it a full edge) -- development knob STHK_PLAN_PREP=0 disables
+    static const bool plan_prep_knob = [] {
+      const char* v = std::getenv("STHK_PLAN_PREP");
+      return !v || *v != '0';
+    }();
+    // (the symmetric kernel waits for its programmatic predecessor; the row
+    // kernel does not, so it keeps the two-kernel structure)
+    const bool plan_prep = plan_prep_knob && graph_mode && sym && !plan_hit && prep_unlaunched &&
+                           !bg_split && e.n <= kPlanPrepMaxEvents;
+    if (plan_prep) {
+      ck(sthk::launch_plan_prep(pa, pr, st), "plan + prep");
       e.launches += 1;
+      ck(op_record(e, s.prepped, st), "event");
+      prep_unlaunched = false;
+    }
+    if (!plan_hit) {  // (the work counters are re-armed by the last pair CTAs)
+      if (!plan_prep) {
+        ck(sthk::launch_plan(pa, st), "plan");
+        e.launches += 1;
+      }
       s.plan_valid = e.bg_cache;
       s.plan_dB = pa.dB;
       s.plan_dT = pa.dT;
@@ -1804,7 +1828,9 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
     launch_prep_now();
     const bool rows_forked = tr_rows && !cached;
     if (rows_forked) {  // beside the pair kernels, after prep (scaled coordinates)
-      if (!prep_pending) {
+      if (plan_prep) {
+        ck(op_wait(e, s.stream2, s.prepped), "wait");
+      } else if (!prep_pending) {
         ck(op_record(e, s.fork, st), "event");
         ck(op_wait(e, s.stream2, s.fork), "wait");
       }
@@ -1884,6 +1910,7 @@ void enqueue_eval_body(sthk_engine& e, bool grad, bool want_pe, bool want_ex, bo
       if (bg_all) return;
       ck(sthk::launch_pairs(qa, grad, e.mode, grid, st), "pair kernel");
       e.launches += 1;
+      if (plan_prep) mark_last_kernel(e, 1);  // (programmatic edge from plan + prep)
     };
     // ev[1] (pair-phase start) is recorded whether or not timing is on: a
     // timing event here, between the prep join and the far fork, measurably

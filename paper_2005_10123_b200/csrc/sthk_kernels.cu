@@ -405,7 +405,7 @@ __device__ __forceinline__ void plan_lists_tile_order(const PlanArgs& a, const P
 // kernels' work counters. The order only affects scheduling: every partial
 // has a fixed destination and integer (fixed-point) accumulation, so results
 // do not depend on it.
-__global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
+__device__ __forceinline__ void plan_body(const PlanArgs& a) {
   __shared__ int s_hist[kPlanLists][kPlanBins];
   __shared__ int s_warp[kPlanLists][32];
   __shared__ __align__(8) uint64_t s_bar;
@@ -474,6 +474,8 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   }
   if (a.trace && tid == 0) trace_cta(a.trace, a.trace_cap, 4, trace_t0);
 }
+
+__global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) { plan_body(a); }
 
 // ---------------------------------------------------------------------------
 // Pair kernel
@@ -1782,8 +1784,7 @@ __device__ __forceinline__ void comp_terms(double ti, double window_end, double 
   c[3] = D * exp(-omega * D);
 }
 
-__global__ void prep_kernel(const PrepArgs a) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void prep_body(const PrepArgs& a, int64_t i) {
   if (i >= a.npad) return;
   const unsigned long long trace_t0 = (a.trace && threadIdx.x == 0) ? global_ns() : 0ULL;
   if (threadIdx.x == 0) stamp_min(a.tstamp, 0);
@@ -1809,6 +1810,23 @@ __global__ void prep_kernel(const PrepArgs a) {
     for (int k = 0; k < 4; ++k) a.comp[static_cast<size_t>(k) * a.npad + i] = c[k];
   }
   if (a.trace && threadIdx.x == 0) trace_cta(a.trace, a.trace_cap, 5, trace_t0);
+}
+
+__global__ void prep_kernel(const PrepArgs a) {
+  prep_body(a, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
+}
+
+// Small sets, graph mode: the plan and the prep pass as one grid (block 0
+// plans, the others prepare 1024 events each), so the pair kernel has a
+// single predecessor and its programmatic edge holds: its CTAs launch while
+// this grid runs and wait for it (griddepcontrol.wait).
+__global__ void __launch_bounds__(1024) plan_prep_kernel(const PlanPrepArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (blockIdx.x == 0) {
+    plan_body(a.plan);
+    return;
+  }
+  prep_body(a.prep, static_cast<int64_t>(blockIdx.x - 1) * 1024 + threadIdx.x);
 }
 
 // exp_l on a vector of natural-unit exponents (accuracy tests; the argument
@@ -2286,6 +2304,12 @@ cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
   return launch_one(plan_kernel, dim3(1), dim3(1024), kPivots * sizeof(double), stream, a);
 }
 
+cudaError_t launch_plan_prep(const PlanArgs& plan, const PrepArgs& prep, cudaStream_t stream) {
+  const PlanPrepArgs a{plan, prep};
+  const unsigned nb = 1u + static_cast<unsigned>((prep.npad + 1023) / 1024);
+  return launch_one(plan_prep_kernel, dim3(nb), dim3(1024), kPivots * sizeof(double), stream, a);
+}
+
 // The exp table (pair kernels) and the search pivots (plan) live in dynamic
 // shared memory (static + dynamic > 48 KB needs the opt-in attribute); set
 // once per device before the first launch.
@@ -2306,6 +2330,10 @@ cudaError_t prepare_pair_kernels() {
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(kPivots * sizeof(double)));
   if (e != cudaSuccess) err = e;
+  const cudaError_t e2 = cudaFuncSetAttribute(reinterpret_cast<const void*>(&plan_prep_kernel),
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(kPivots * sizeof(double)));
+  if (e2 != cudaSuccess) err = e2;
   // Kernels that run beside the pair kernels (or just before them) ask for
   // the pair kernels' shared-memory carveout: an SM changes its L1 / shared
   // split only when idle, so a small kernel configured for the largest L1

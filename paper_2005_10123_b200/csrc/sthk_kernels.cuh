@@ -348,6 +348,12 @@ struct PrepArgs {
 };
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
+// plan + prep as one grid (block 0 plans, the rest prepare; small sets)
+struct PlanPrepArgs {
+  PlanArgs plan;
+  PrepArgs prep;
+};
+cudaError_t launch_plan_prep(const PlanArgs& plan, const PrepArgs& prep, cudaStream_t stream);
 cudaError_t launch_exp_probe(const double* x, int64_t n, double* out, cudaStream_t stream);
 cudaError_t launch_pairs(const PairArgs& a, bool grad, int mode, int grid, cudaStream_t stream);
 // Trigger-free symmetric FP64 kernel over the background-only list (PairArgs'
