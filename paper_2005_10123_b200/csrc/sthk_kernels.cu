@@ -1897,6 +1897,9 @@ __device__ __forceinline__ void final_sum_block(const double* __restrict__ bp, i
 // path, so those stay bitwise identical.
 // ---------------------------------------------------------------------------
 constexpr int kTrigRowsThreads = 256;
+#ifndef STHK_TRIG_ROWS_W
+#define STHK_TRIG_ROWS_W 4  // sources per step of the row-window walk
+#endif
 // sources a row's window can reach before its block's first row: a window
 // holds at most 254 events (every tile spans more than it), plus the one
 // just outside that ends the walk
@@ -1936,34 +1939,37 @@ __device__ __forceinline__ unsigned long long trig_row_sums(const TrigRowsArgs& 
   unsigned long long pairs = 0;
   const double ti = src.tt(i), xi = src.xx(i), yi = src.yy(i);
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  // two sources per step (j, j - 1), their exps in lockstep; a source outside
-  // the window or tied with t_i adds an exact 0 (s + 0 == s: every sum >= 0),
-  // so the sums are those of the one-at-a-time loop, bit for bit
-  for (int64_t j = i - 1; j >= 0; j -= 2) {
-    const int64_t j1 = j >= 1 ? j - 1 : j;
-    const double tj0 = src.tt(j);
-    const double tj1 = j >= 1 ? src.tt(j1) : ti;  // (no second source: dt 0, masked)
-    const double dt0 = ti - tj0, dt1 = ti - tj1;
-    if (dt0 > a.dT) break;
-    const bool v0 = dt0 > 0.0;  // ties: strict t_j < t_i
-    const bool v1 = dt1 > 0.0 && dt1 <= a.dT;
-    const double dx0 = xi - src.xx(j), dy0 = yi - src.yy(j);
-    const double dx1 = xi - src.xx(j1), dy1 = yi - src.yy(j1);
-    const double r20 = fma(dx0, dx0, dy0 * dy0), r21 = fma(dx1, dx1, dy1 * dy1);
-    const double x[2] = {fma(a.nomL, dt0, a.chS * r20), fma(a.nomL, dt1, a.chS * r21)};
-    double e[2];
-    exp_l_batch<true, 2>(x, e, src.tab());
-    const double e0 = v0 ? e[0] : 0.0, e1 = v1 ? e[1] : 0.0;
-    s0 += e0;
-    s0 += e1;
-    if constexpr (GRAD) {
-      s1 = fma(e0, dt0, s1);
-      s1 = fma(e1, dt1, s1);
-      s2 = fma(e0, r20, s2);
-      s2 = fma(e1, r21, s2);
+  // kW sources per step (j, j - 1, ...), their exps in lockstep; a source
+  // outside the window, tied with t_i or before index 0 adds an exact 0
+  // (s + 0 == s: every sum >= 0), so the sums are those of the one-at-a-time
+  // loop, bit for bit
+  constexpr int kW = STHK_TRIG_ROWS_W;
+  for (int64_t j = i - 1; j >= 0; j -= kW) {
+    double dt[kW], r2[kW], x[kW], e[kW];
+    bool v[kW];
+#pragma unroll
+    for (int w = 0; w < kW; ++w) {
+      const int64_t jw = j - w >= 0 ? j - w : j;  // (no source: dt 0, masked)
+      const double tj = j - w >= 0 ? src.tt(jw) : ti;
+      dt[w] = ti - tj;
+      v[w] = dt[w] > 0.0 && dt[w] <= a.dT;  // ties: strict t_j < t_i
+      const double dx = xi - src.xx(jw), dy = yi - src.yy(jw);
+      r2[w] = fma(dx, dx, dy * dy);
+      x[w] = fma(a.nomL, dt[w], a.chS * r2[w]);
     }
-    pairs += static_cast<unsigned long long>(v0) + static_cast<unsigned long long>(v1);
-    if (!(dt1 <= a.dT)) break;  // (time-sorted: every earlier source is outside too)
+    if (dt[0] > a.dT) break;
+    exp_l_batch<true, kW>(x, e, src.tab());
+#pragma unroll
+    for (int w = 0; w < kW; ++w) {
+      const double ew = v[w] ? e[w] : 0.0;
+      s0 += ew;
+      if constexpr (GRAD) {
+        s1 = fma(ew, dt[w], s1);
+        s2 = fma(ew, r2[w], s2);
+      }
+      pairs += static_cast<unsigned long long>(v[w]);
+    }
+    if (!(dt[kW - 1] <= a.dT)) break;  // (time-sorted: every earlier source is outside too)
   }
   st[0] = s0;
   a.trow[i] = s0;
